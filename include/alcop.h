@@ -1,0 +1,210 @@
+/*
+ * alcop.h — C ABI of the B200-native pipelined load-and-use hot path
+ * (ALCOP, arXiv 2210.16691) re-implemented for sm_100a.
+ *
+ * The reference ("pipec", /root/reference/proj/include/pipec) is a header-only
+ * C++20 library with no FFI; its operator surface is the C++ namespace
+ * `pipec`.  Every entry point below replaces one reference interface and
+ * cites it as file:line relative to /root/reference.  Plain pointers and
+ * sizes only: no torch or C++ types cross this boundary, no exceptions
+ * cross it, and the library never allocates device memory on a call path
+ * (the caller owns buffers and the stream).
+ *
+ * Return codes follow the reference CLI exit-code map
+ * (proj/include/pipec/cli.hpp:23-25) plus ALCOP_ERR_CUDA.  After a non-zero
+ * return, alcop_last_error() (thread-local) holds "<RuleTag>: message",
+ * reusing the reference rule tags (pipeline_pass.hpp:191-322,
+ * schedule.hpp:113-308).
+ */
+#ifndef ALCOP_H_
+#define ALCOP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes: pipec/cli.hpp:23-25 (kOk..kConfig) + CUDA ---------- */
+#define ALCOP_OK 0
+#define ALCOP_ERR_PARSE 2       /* ParseError        (common.hpp:43)  */
+#define ALCOP_ERR_VALIDATE 3    /* ValidationError   (common.hpp:51)  */
+#define ALCOP_ERR_ANALYSIS 4    /* AnalysisError/InterpError (common.hpp:57,67) */
+#define ALCOP_ERR_EQUIVALENCE 5 /* equivalence failure (cli.hpp:296-298) */
+#define ALCOP_ERR_CONFIG 6      /* ConfigError       (common.hpp:63)  */
+#define ALCOP_ERR_CUDA 7        /* CUDA runtime / launch failure (new) */
+
+/* ---- element types.  The reference has names only (f16 = 2 bytes,
+ * schedule.hpp:341-349); bf16 is added because B200 computes in it. ----- */
+typedef enum {
+  ALCOP_F16 = 0,
+  ALCOP_BF16 = 1,
+  ALCOP_F32 = 2
+} alcop_dtype;
+
+/* B operand layout.  The reference lowers B as [K,N] row-major
+ * (schedule.hpp:389) = MN-major for tcgen05; NK is the K-major variant. */
+typedef enum {
+  ALCOP_B_KN = 0,
+  ALCOP_B_NK = 1
+} alcop_b_layout;
+
+/* Pipeline emission mode.
+ *  WRAP  : bit-faithful to the pass output (pipeline_pass.hpp:482-552,
+ *          622-748): per output tile an n_stage-1 chunk prologue, steady
+ *          loads of chunk (v+s-1)%E into slot (v+s-1)%s, consumer slot v%s,
+ *          and s-1 drain wait/release pairs after the k loop.
+ *  FUSED : the paper's holistic pipeline applied to the persistent tile
+ *          loop: lookahead crosses into the next tile's chunks, so no
+ *          redundant wrapped loads and no per-tile drains. */
+typedef enum {
+  ALCOP_MODE_WRAP = 0,
+  ALCOP_MODE_FUSED = 1
+} alcop_mode;
+
+/* Problem descriptor.  Mirrors pipec::WorkloadDesc (schedule.hpp:15-19)
+ * plus the layout facts the reference fixes implicitly (row-major A[b,M,K],
+ * B[b,K,N], C[b,M,N], schedule.hpp:388-390).  Leading dims / batch strides
+ * are in elements; 0 means packed. */
+typedef struct {
+  int64_t M, N, K, batch;
+  int32_t in_dtype;  /* alcop_dtype: F16 or BF16 */
+  int32_t out_dtype; /* alcop_dtype: F32, F16 or BF16 */
+  int32_t b_layout;  /* alcop_b_layout */
+  int32_t reserved0;
+  int64_t lda, ldb, ldc;
+  int64_t stride_a, stride_b, stride_c;
+} alcop_gemm_desc;
+
+/* Schedule.  Mirrors the per-buffer pipelining hints (BufferDecl::
+ * pipelineStages, ir.hpp:12-26; mark_pipeline, schedule.hpp:258-268), the
+ * tile splits (tile, schedule.hpp:141-193) and perf::ScheduleParams
+ * (perf_model.hpp:32-38).  n_stage 1 = "no hint" (not pipelined): the
+ * reference cannot express it (stages >= 2, schedule.hpp:261), here it is
+ * the in-run baseline variant (one slot: load -> wait -> use -> release). */
+typedef struct {
+  int64_t tileM, tileN, tileK; /* CTA tile; tileM 128 (cta_group 1)     */
+  int32_t n_stage_smem_A;      /* A_shared ring depth (outer level)     */
+  int32_t n_stage_smem_B;      /* B_shared ring depth (outer level)     */
+  int32_t n_stage_inner;       /* A_reg/B_reg level -> TMEM accumulator buffers (1|2) */
+  int32_t cta_group;           /* 1 (2 reserved)                         */
+  int32_t mode;                /* alcop_mode                             */
+  int32_t num_ctas;            /* persistent grid; 0 = #SMs              */
+  int32_t raster;              /* reserved (tile rasterisation), 0       */
+  int32_t reserved1;
+} alcop_schedule;
+
+/* Implicit-GEMM conv2d descriptor (no reference form: SPEC.md:218).
+ * x: NHWC, w: KRSC, y: NPQK. */
+typedef struct {
+  int64_t N, H, W, C, K, R, S;
+  int32_t stride_h, stride_w, pad_h, pad_w;
+  int32_t in_dtype, out_dtype;
+} alcop_conv_desc;
+
+/* Hardware spec for the analytical model (perf::HardwareSpec,
+ * perf_model.hpp:14-30), B200 defaults via alcop_hw_default_b200(). */
+typedef struct {
+  int32_t numSM;
+  double throughputSM; /* FLOP / cycle / SM (dense f16/bf16) */
+  double bwLLC;        /* bytes / cycle, device-wide L2 -> SM */
+  double bwDRAM;       /* bytes / cycle */
+  double bwDRAMWrite;  /* bytes / cycle */
+  double latLLCRead, latDRAMRead, latDRAMWrite; /* cycles */
+  double bwSmem, latSmem;
+  int64_t smemPerSM, regsPerSM;
+  int32_t maxThreadblkPerSM, maxWarpsPerSM, utilKneeWarps;
+  int32_t tmemColsPerSM; /* 512 (new: TMEM capacity) */
+  double clockGHz;       /* cycles -> seconds */
+} alcop_hw;
+
+/* perf::LatencyBreakdown (perf_model.hpp:40-47); field names follow
+ * json_io.hpp:95-114. */
+typedef struct {
+  double tKernel, tThreadblk, tInit, tMainLoop, tEpilogue;
+  double tSmemLoad, tRegLoad, tSmemUse, tCompute;
+  int64_t nThreadblkBatch, nThreadblkPerSM, nThreadblkPerBatch;
+  int64_t nSmemLoop, nRegLoop;
+  int64_t bytesOneSmemLoop, bytesWorkset, bytesOutputTile;
+  int64_t flopsOneRegLoop;
+  double seconds; /* tKernel / clock (new) */
+} alcop_breakdown;
+
+/* One pipeline bookkeeping event (host enumerator and device trace).
+ * kind: 0 producer_acquire+commit (a load), 1 consumer_wait,
+ *       2 consumer_release.  buf: 0 = A_shared, 1 = B_shared.
+ * Counters follow interp.hpp:87-94 / TraceEvent (interp.hpp:20-26). */
+typedef struct {
+  int32_t kind, buf, tile, slot, chunk, parity;
+  int32_t acquired, committed, waited, released;
+} alcop_event;
+
+/* ---- library ---------------------------------------------------------- */
+const char* alcop_version(void);
+/* thread-local "<RuleTag>: message" of the last failing call */
+const char* alcop_last_error(void);
+
+/* ---- schedule surface ------------------------------------------------- */
+void alcop_schedule_default(alcop_schedule* out);
+
+/* Applies a reference schedule script (apply_script, schedule.hpp:590-646:
+ * `cache_read`, `tile C i0=.. i1=.. j0=.. j1=.. ko=.. ki=..`, `pipeline
+ * <buf> <n>`, `inline S2`) to gemm_schedule(w) (schedule.hpp:73-86) with the
+ * reference eligibility rules (check_eligibility, schedule.hpp:198-254) and
+ * rule tags, and maps the result to an alcop_schedule.  Buffers left without
+ * a hint get n_stage 1.  `warnings` (may be NULL) receives the
+ * SyncPositionConflict refusal text (schedule.hpp:625-637). */
+int alcop_parse_schedule_script(const alcop_gemm_desc* w, const char* script, alcop_schedule* out,
+                                char* warnings, size_t warnings_len);
+
+/* params_valid analogue (perf_model.hpp:129-142) for the B200 kernel:
+ * tile shape, stage counts vs 227 KB shared memory, TMEM columns,
+ * LookaheadExceedsOuter (pipeline_pass.hpp:305-313), alignment. */
+int alcop_validate(const alcop_gemm_desc* w, const alcop_schedule* s);
+/* dynamic shared memory bytes the kernel will request for (w, s) */
+int64_t alcop_smem_bytes(const alcop_gemm_desc* w, const alcop_schedule* s);
+
+/* ---- host bookkeeping enumerator (pipeline_pass.hpp:482-748 index
+ * algebra + interp.hpp:375-418 counters): the event sequence one CTA
+ * executes for `num_tiles` output tiles of E = ceil(K/tileK) chunks.
+ * role 0 = producer events, role 1 = consumer events.  Writes at most
+ * `cap` events, sets *count to the full length. */
+int alcop_enumerate_pipeline(int64_t num_tiles, int64_t E, int32_t sA, int32_t sB, int32_t mode,
+                             int32_t role, alcop_event* out, int64_t cap, int64_t* count);
+
+/* ---- compute entry points (device pointers, caller-owned stream) ------ */
+/* Pipelined matmul: gemm_schedule -> lower -> transform -> run
+ * (schedule.hpp:73,357; pipeline_pass.hpp:753; interp.hpp:440) as one
+ * sm_100a kernel launch.  batch > 1 is the batched GEMM (schedule.hpp:384-390). */
+int alcop_gemm(const alcop_gemm_desc* w, const alcop_schedule* s, const void* A, const void* B, void* C,
+               void* stream);
+
+/* Same launch with the device debug trace: each CTA's producer and MMA
+ * threads log their events.  trace must hold
+ * num_ctas * 2 * events_per_role_cap alcop_event records. */
+int alcop_gemm_traced(const alcop_gemm_desc* w, const alcop_schedule* s, const void* A, const void* B,
+                      void* C, alcop_event* trace_dev, int64_t events_per_role_cap, void* stream);
+
+/* End-to-end call with HOST buffers: H2D of A,B (pinned host recommended),
+ * the kernel, D2H of C, all on `stream`; `workspace` is caller-owned device
+ * memory of at least alcop_gemm_workspace_bytes(w) bytes. Synchronous. */
+int64_t alcop_gemm_workspace_bytes(const alcop_gemm_desc* w);
+int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
+                    void* hC, void* workspace, void* stream);
+
+/* Implicit-GEMM conv2d (new; the reference excludes it). */
+int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
+                 void* stream);
+
+/* ---- analytical model (perf_model.hpp:157-187, tuner.hpp:68-80) -------- */
+void alcop_hw_default_b200(alcop_hw* hw);
+void alcop_hw_default_a100_reference(alcop_hw* hw); /* perf_model.hpp:14-30 defaults */
+int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
+                  alcop_breakdown* out);
+int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALCOP_H_ */

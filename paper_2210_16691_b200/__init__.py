@@ -1,0 +1,348 @@
+"""paper_2210_16691_b200 — B200-native pipelined load-and-use GEMM / BMM /
+implicit-GEMM conv (ALCOP, arXiv 2210.16691), behind the reference's schedule
+surface.
+
+The product is ``libalcop.so`` (C ABI in ``include/alcop.h``: sm_100a kernels +
+C++ host code).  This module is a thin ctypes binding over that ABI so tests,
+``bench.py`` and ``__graft_entry__`` can drive it with torch-allocated device
+memory; it mirrors the reference's operator/schedule API names
+(``gemm_schedule``/``apply_script``/``mark_pipeline`` hints,
+``pipec::perf::predict``, ``tune::analytical_rank``) and its error classes.
+
+There is no CPU fallback: every compute call goes through the CUDA kernels and
+raises if the extension or a GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libalcop.so")
+
+ALCOP_OK = 0
+ALCOP_ERR_PARSE = 2
+ALCOP_ERR_VALIDATE = 3
+ALCOP_ERR_ANALYSIS = 4
+ALCOP_ERR_EQUIVALENCE = 5
+ALCOP_ERR_CONFIG = 6
+ALCOP_ERR_CUDA = 7
+
+F16, BF16, F32 = 0, 1, 2
+B_KN, B_NK = 0, 1
+MODE_WRAP, MODE_FUSED = 0, 1
+
+# every symbol include/alcop.h declares
+EXPORTED_SYMBOLS = [
+    "alcop_version", "alcop_last_error", "alcop_schedule_default", "alcop_parse_schedule_script",
+    "alcop_validate", "alcop_smem_bytes", "alcop_enumerate_pipeline", "alcop_gemm", "alcop_gemm_traced",
+    "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_conv2d", "alcop_hw_default_b200",
+    "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule",
+]
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64), ("batch", ctypes.c_int64),
+                ("in_dtype", ctypes.c_int32), ("out_dtype", ctypes.c_int32), ("b_layout", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64),
+                ("ldc", ctypes.c_int64), ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
+                ("stride_c", ctypes.c_int64)]
+
+
+class Schedule(ctypes.Structure):
+    _fields_ = [("tileM", ctypes.c_int64), ("tileN", ctypes.c_int64), ("tileK", ctypes.c_int64),
+                ("n_stage_smem_A", ctypes.c_int32), ("n_stage_smem_B", ctypes.c_int32),
+                ("n_stage_inner", ctypes.c_int32), ("cta_group", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("num_ctas", ctypes.c_int32), ("raster", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("reserved")}
+
+    def __repr__(self):
+        d = self.as_dict()
+        return ("Schedule(tile=%dx%dx%d, stages A/B=%d/%d, inner=%d, mode=%s)"
+                % (d["tileM"], d["tileN"], d["tileK"], d["n_stage_smem_A"], d["n_stage_smem_B"],
+                   d["n_stage_inner"], "FUSED" if d["mode"] == MODE_FUSED else "WRAP"))
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("N", "H", "W", "C", "K", "R", "S")] + \
+               [(n, ctypes.c_int32) for n in ("stride_h", "stride_w", "pad_h", "pad_w", "in_dtype", "out_dtype")]
+
+
+class HW(ctypes.Structure):
+    _fields_ = [("numSM", ctypes.c_int32), ("throughputSM", ctypes.c_double), ("bwLLC", ctypes.c_double),
+                ("bwDRAM", ctypes.c_double), ("bwDRAMWrite", ctypes.c_double), ("latLLCRead", ctypes.c_double),
+                ("latDRAMRead", ctypes.c_double), ("latDRAMWrite", ctypes.c_double), ("bwSmem", ctypes.c_double),
+                ("latSmem", ctypes.c_double), ("smemPerSM", ctypes.c_int64), ("regsPerSM", ctypes.c_int64),
+                ("maxThreadblkPerSM", ctypes.c_int32), ("maxWarpsPerSM", ctypes.c_int32),
+                ("utilKneeWarps", ctypes.c_int32), ("tmemColsPerSM", ctypes.c_int32), ("clockGHz", ctypes.c_double)]
+
+
+class Breakdown(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("tKernel", "tThreadblk", "tInit", "tMainLoop", "tEpilogue",
+                                                "tSmemLoad", "tRegLoad", "tSmemUse", "tCompute")] + \
+               [(n, ctypes.c_int64) for n in ("nThreadblkBatch", "nThreadblkPerSM", "nThreadblkPerBatch",
+                                               "nSmemLoop", "nRegLoop", "bytesOneSmemLoop", "bytesWorkset",
+                                               "bytesOutputTile", "flopsOneRegLoop")] + [("seconds", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Event(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("kind", "buf", "tile", "slot", "chunk", "parity", "acquired",
+                                               "committed", "waited", "released")]
+
+
+EVENT_FIELDS = [f for f, _ in Event._fields_]
+
+
+class AlcopError(RuntimeError):
+    """Raised on a non-zero ABI return; .code is the reference exit code, .rule the rule tag."""
+
+    def __init__(self, code, message):
+        self.code = code
+        self.rule = message.split(":", 1)[0] if ":" in message else ""
+        super().__init__("[%d] %s" % (code, message))
+
+
+_lib = None
+
+
+def load_library(path: str | None = None):
+    """Loads libalcop.so; raises (no fallback) if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise ImportError("libalcop.so not built (%s); run __graft_entry__.build()" % p)
+    lib = ctypes.CDLL(p)
+    P = ctypes.POINTER
+    lib.alcop_version.restype = ctypes.c_char_p
+    lib.alcop_last_error.restype = ctypes.c_char_p
+    lib.alcop_schedule_default.argtypes = [P(Schedule)]
+    lib.alcop_schedule_default.restype = None
+    lib.alcop_parse_schedule_script.argtypes = [P(GemmDesc), ctypes.c_char_p, P(Schedule), ctypes.c_char_p,
+                                                ctypes.c_size_t]
+    lib.alcop_validate.argtypes = [P(GemmDesc), P(Schedule)]
+    lib.alcop_smem_bytes.argtypes = [P(GemmDesc), P(Schedule)]
+    lib.alcop_smem_bytes.restype = ctypes.c_int64
+    lib.alcop_enumerate_pipeline.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_int32, ctypes.c_int32, P(Event), ctypes.c_int64,
+                                             P(ctypes.c_int64)]
+    lib.alcop_gemm.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p]
+    lib.alcop_gemm_traced.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+    lib.alcop_gemm_workspace_bytes.argtypes = [P(GemmDesc)]
+    lib.alcop_gemm_workspace_bytes.restype = ctypes.c_int64
+    lib.alcop_gemm_host.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p]
+    lib.alcop_conv2d.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_void_p]
+    lib.alcop_hw_default_b200.argtypes = [P(HW)]
+    lib.alcop_hw_default_b200.restype = None
+    lib.alcop_hw_default_a100_reference.argtypes = [P(HW)]
+    lib.alcop_hw_default_a100_reference.restype = None
+    lib.alcop_predict.argtypes = [P(GemmDesc), P(Schedule), P(HW), P(Breakdown)]
+    lib.alcop_choose_schedule.argtypes = [P(GemmDesc), P(HW), P(Schedule)]
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc != ALCOP_OK:
+        raise AlcopError(rc, load_library().alcop_last_error().decode())
+
+
+def version() -> str:
+    return load_library().alcop_version().decode()
+
+
+# ---------------------------------------------------------------- descriptors
+_TORCH_DT = {}
+
+
+def _dtype_code(dt) -> int:
+    import torch
+    m = {torch.float16: F16, torch.bfloat16: BF16, torch.float32: F32}
+    if dt not in m:
+        raise TypeError("unsupported dtype %s" % dt)
+    return m[dt]
+
+
+def gemm_desc(M, N, K, batch=1, in_dtype=BF16, out_dtype=BF16, b_layout=B_KN, **kw) -> GemmDesc:
+    """WorkloadDesc (schedule.hpp:15-19) + the layouts lower() fixes (schedule.hpp:388-390)."""
+    d = GemmDesc()
+    d.M, d.N, d.K, d.batch = M, N, K, batch
+    d.in_dtype, d.out_dtype, d.b_layout = in_dtype, out_dtype, b_layout
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+def default_schedule(**kw) -> Schedule:
+    s = Schedule()
+    load_library().alcop_schedule_default(ctypes.byref(s))
+    for k, v in kw.items():
+        setattr(s, k, v)
+    return s
+
+
+def make_schedule(tileN=256, tileK=64, n_stage=4, n_stage_inner=2, mode=MODE_FUSED, n_stage_B=None,
+                  num_ctas=0) -> Schedule:
+    return default_schedule(tileN=tileN, tileK=tileK, n_stage_smem_A=n_stage,
+                            n_stage_smem_B=n_stage if n_stage_B is None else n_stage_B,
+                            n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas)
+
+
+def apply_script(desc: GemmDesc, script: str):
+    """apply_script (schedule.hpp:590-646) on gemm_schedule(desc), mapped to a
+    B200 Schedule.  Returns (schedule, warnings)."""
+    s = Schedule()
+    buf = ctypes.create_string_buffer(4096)
+    _check(load_library().alcop_parse_schedule_script(ctypes.byref(desc), script.encode(), ctypes.byref(s), buf,
+                                                      len(buf)))
+    warns = [w for w in buf.value.decode().split("\n") if w]
+    return s, warns
+
+
+def validate(desc: GemmDesc, sched: Schedule):
+    _check(load_library().alcop_validate(ctypes.byref(desc), ctypes.byref(sched)))
+
+
+def smem_bytes(desc: GemmDesc, sched: Schedule) -> int:
+    return load_library().alcop_smem_bytes(ctypes.byref(desc), ctypes.byref(sched))
+
+
+def enumerate_pipeline(num_tiles, E, sA, sB, mode, role):
+    """Host bookkeeping enumerator: list of event dicts for one CTA."""
+    lib = load_library()
+    n = ctypes.c_int64(0)
+    _check(lib.alcop_enumerate_pipeline(num_tiles, E, sA, sB, mode, role, None, 0, ctypes.byref(n)))
+    arr = (Event * max(1, n.value))()
+    _check(lib.alcop_enumerate_pipeline(num_tiles, E, sA, sB, mode, role, arr, n.value, ctypes.byref(n)))
+    return [{f: getattr(arr[i], f) for f in EVENT_FIELDS} for i in range(n.value)]
+
+
+def hw_b200() -> HW:
+    h = HW()
+    load_library().alcop_hw_default_b200(ctypes.byref(h))
+    return h
+
+
+def hw_a100_reference() -> HW:
+    h = HW()
+    load_library().alcop_hw_default_a100_reference(ctypes.byref(h))
+    return h
+
+
+def predict(desc: GemmDesc, sched: Schedule, hw: HW | None = None) -> dict:
+    b = Breakdown()
+    _check(load_library().alcop_predict(ctypes.byref(desc), ctypes.byref(sched), ctypes.byref(hw or hw_b200()),
+                                        ctypes.byref(b)))
+    return b.as_dict()
+
+
+def choose_schedule(desc: GemmDesc, hw: HW | None = None) -> Schedule:
+    s = Schedule()
+    _check(load_library().alcop_choose_schedule(ctypes.byref(desc), ctypes.byref(hw or hw_b200()),
+                                                ctypes.byref(s)))
+    return s
+
+
+# ---------------------------------------------------------------- compute
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise RuntimeError("alcop compute entry points take CUDA tensors (no CPU fallback)")
+
+
+def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, out=None, stream=None):
+    """Pipelined matmul C = A @ B (or batched) through alcop_gemm.
+
+    A: [M,K] or [b,M,K]; B: [K,N] / [b,K,N] (b_layout B_KN, the reference
+    layout) or [N,K] / [b,N,K] (B_NK).  fp16/bf16 in, fp32 accumulate."""
+    import torch
+    _require_cuda(A, B)
+    batched = A.dim() == 3
+    M, K = A.shape[-2], A.shape[-1]
+    N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
+    batch = A.shape[0] if batched else 1
+    out_dtype = out_dtype or A.dtype
+    if out is None:
+        out = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, device=A.device)
+    A = A.contiguous()
+    B = B.contiguous()
+    d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout)
+    s = sched if sched is not None else choose_schedule(d)
+    _check(load_library().alcop_gemm(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
+                                     ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                     _stream_ptr(stream)))
+    return out
+
+
+def matmul_traced(A, B, sched: Schedule, out_dtype=None, b_layout=B_KN, events_cap=None):
+    """matmul with the device debug trace; returns (C, trace[cta][role] -> list of event dicts)."""
+    import torch
+    _require_cuda(A, B)
+    batched = A.dim() == 3
+    M, K = A.shape[-2], A.shape[-1]
+    N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
+    batch = A.shape[0] if batched else 1
+    out_dtype = out_dtype or A.dtype
+    out = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, device=A.device)
+    d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout)
+    tiles = -(-M // 128) * -(-N // sched.tileN) * batch
+    sms = torch.cuda.get_device_properties(A.device).multi_processor_count
+    ctas = min(tiles, sched.num_ctas if sched.num_ctas > 0 else sms)
+    E = -(-K // sched.tileK)
+    per_cta = -(-tiles // ctas)
+    cap = events_cap or (per_cta * (E + 32) * 4 + 64)
+    tr = torch.full((ctas, 2, cap, len(EVENT_FIELDS)), -7, dtype=torch.int32, device=A.device)
+    _check(load_library().alcop_gemm_traced(ctypes.byref(d), ctypes.byref(sched), ctypes.c_void_p(A.data_ptr()),
+                                            ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            ctypes.c_void_p(tr.data_ptr()), cap, _stream_ptr()))
+    torch.cuda.synchronize()
+    host = tr.cpu().numpy()
+    traces = []
+    for c in range(ctas):
+        roles = []
+        for r in range(2):
+            rows = host[c, r]
+            valid = rows[:, 0] != -7
+            roles.append([dict(zip(EVENT_FIELDS, map(int, row))) for row in rows[valid]])
+        traces.append(roles)
+    return out, traces
+
+
+def matmul_host(A_host, B_host, sched: Schedule, out_dtype, b_layout=B_KN, C_host=None, workspace=None,
+                stream=None):
+    """End-to-end call with HOST (pinned) tensors through alcop_gemm_host:
+    H2D copies, kernel, D2H copy, synchronous.  Returns C_host."""
+    import torch
+    batched = A_host.dim() == 3
+    M, K = A_host.shape[-2], A_host.shape[-1]
+    N = B_host.shape[-1] if b_layout == B_KN else B_host.shape[-2]
+    batch = A_host.shape[0] if batched else 1
+    d = gemm_desc(M, N, K, batch, _dtype_code(A_host.dtype), _dtype_code(out_dtype), b_layout)
+    if C_host is None:
+        C_host = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, pin_memory=True)
+    if workspace is None:
+        workspace = torch.empty(load_library().alcop_gemm_workspace_bytes(ctypes.byref(d)), dtype=torch.uint8,
+                                device="cuda")
+    _check(load_library().alcop_gemm_host(ctypes.byref(d), ctypes.byref(sched),
+                                          ctypes.c_void_p(A_host.data_ptr()), ctypes.c_void_p(B_host.data_ptr()),
+                                          ctypes.c_void_p(C_host.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+                                          _stream_ptr(stream)))
+    return C_host

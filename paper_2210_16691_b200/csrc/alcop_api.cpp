@@ -1,0 +1,200 @@
+// alcop_api.cpp — the C-ABI front end: error reporting, schedule
+// validation (the params_valid analogue, perf_model.hpp:129-142, plus the
+// pass's LookaheadExceedsOuter rule, pipeline_pass.hpp:305-313), and the
+// compute entry points.  No exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "alcop_internal.h"
+
+namespace alcop {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int set_error(int code, const std::string& tag, const std::string& msg) {
+  g_last_error = tag + ": " + msg;
+  return code;
+}
+void clear_error() { g_last_error.clear(); }
+
+int64_t round_up_pow2_cols(int64_t cols) {
+  int64_t c = 32;
+  while (c < cols) c <<= 1;
+  return c;
+}
+
+int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  (void)w;
+  const int64_t a_stage = kTileM * s.tileK * 2;
+  const int64_t b_stage = s.tileN * s.tileK * 2;
+  const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;
+  return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + bars;
+}
+
+static int dtype_bytes(int32_t dt) { return dt == ALCOP_F32 ? 4 : 2; }
+
+int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  if (w.M < 1 || w.N < 1 || w.K < 1 || w.batch < 1)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "M, N, K and batch must be >= 1");
+  if (w.M > INT32_MAX || w.N > INT32_MAX || w.K > INT32_MAX)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "M, N, K must fit in int32");
+  if (w.in_dtype != ALCOP_F16 && w.in_dtype != ALCOP_BF16)
+    return set_error(ALCOP_ERR_CONFIG, "BadDtype", "input dtype must be F16 or BF16 (tcgen05 kind::f16)");
+  if (w.out_dtype != ALCOP_F32 && w.out_dtype != ALCOP_F16 && w.out_dtype != ALCOP_BF16)
+    return set_error(ALCOP_ERR_CONFIG, "BadDtype", "output dtype must be F32, F16 or BF16");
+  if (w.b_layout != ALCOP_B_KN && w.b_layout != ALCOP_B_NK)
+    return set_error(ALCOP_ERR_CONFIG, "BadLayout", "b_layout must be KN or NK");
+  if (s.cta_group != 1)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "only cta_group 1 is implemented");
+  if (s.tileM != kTileM)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileM must be 128 (UMMA M with cta_group::1)");
+  if (s.tileN != 64 && s.tileN != 128 && s.tileN != 192 && s.tileN != 256)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256");
+  if (s.tileK != 32 && s.tileK != 64 && s.tileK != 128)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileK must be one of 32, 64, 128");
+  if (s.n_stage_smem_A < 1 || s.n_stage_smem_B < 1 || s.n_stage_smem_A > kMaxStages ||
+      s.n_stage_smem_B > kMaxStages)
+    return set_error(ALCOP_ERR_CONFIG, "BadStages", "shared-memory stages must be in [1, 16]");
+  if (s.n_stage_inner < 1 || s.n_stage_inner > 2)
+    return set_error(ALCOP_ERR_CONFIG, "BadStages", "inner (TMEM accumulator) stages must be 1 or 2");
+  if (s.mode != ALCOP_MODE_WRAP && s.mode != ALCOP_MODE_FUSED)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "mode must be WRAP or FUSED");
+  // The inner pipeline of the reference (A_reg/B_reg, F = tileK/regK k-steps
+  // per chunk) may not look further ahead than the outer one covers
+  // (LookaheadExceedsOuter, pipeline_pass.hpp:305-313; params_valid,
+  // perf_model.hpp:139-140).  On tcgen05 F = tileK/16.
+  const int64_t F = s.tileK / 16;
+  const int32_t s_outer = std::min(s.n_stage_smem_A, s.n_stage_smem_B);
+  if (static_cast<int64_t>(s.n_stage_inner - 1) > static_cast<int64_t>(s_outer - 1) * F && s_outer > 1)
+    return set_error(ALCOP_ERR_ANALYSIS, "LookaheadExceedsOuter",
+                     "inner pipeline looks ahead further than the outer pipeline covers");
+  const int64_t acc_stride = round_up_pow2_cols(s.tileN);
+  if (acc_stride * s.n_stage_inner > kTmemCols)
+    return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner * tileN exceeds 512 TMEM columns");
+  const int64_t smem = gemm_smem_bytes(w, s);
+  if (smem > kMaxSmemBytes)
+    return set_error(ALCOP_ERR_CONFIG, "SmemCapacity",
+                     "pipeline ring needs " + std::to_string(smem) + " B shared memory, more than 232448");
+  const int64_t lda = w.lda ? w.lda : w.K;
+  const int64_t ldb = w.ldb ? w.ldb : (w.b_layout == ALCOP_B_KN ? w.N : w.K);
+  const int64_t ldc = w.ldc ? w.ldc : w.N;
+  if ((lda * 2) % 16 || (ldb * 2) % 16)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "A/B row pitch must be a multiple of 16 bytes (TMA)");
+  if ((ldc * dtype_bytes(w.out_dtype)) % 16)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "C row pitch must be a multiple of 16 bytes");
+  if (w.stride_a % 8 || w.stride_b % 8 || w.stride_c % 8)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "batch strides must be multiples of 16 bytes");
+  return ALCOP_OK;
+}
+
+static int check_ptr_alignment(const void* A, const void* B, const void* C) {
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "A, B and C must be 16-byte aligned");
+  return ALCOP_OK;
+}
+
+}  // namespace alcop
+
+using namespace alcop;
+
+extern "C" {
+
+const char* alcop_version(void) { return "alcop-b200 0.1.0 (sm_100a)"; }
+
+const char* alcop_last_error(void) { return g_last_error.c_str(); }
+
+void alcop_schedule_default(alcop_schedule* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof(*out));
+  out->tileM = 128;
+  out->tileN = 256;
+  out->tileK = 64;
+  out->n_stage_smem_A = 4;
+  out->n_stage_smem_B = 4;
+  out->n_stage_inner = 2;
+  out->cta_group = 1;
+  out->mode = ALCOP_MODE_FUSED;
+}
+
+int alcop_validate(const alcop_gemm_desc* w, const alcop_schedule* s) {
+  if (!w || !s) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "descriptor is NULL");
+  clear_error();
+  return validate_gemm(*w, *s);
+}
+
+int64_t alcop_smem_bytes(const alcop_gemm_desc* w, const alcop_schedule* s) {
+  if (!w || !s) return -1;
+  return gemm_smem_bytes(*w, *s);
+}
+
+int alcop_gemm(const alcop_gemm_desc* w, const alcop_schedule* s, const void* A, const void* B, void* C,
+               void* stream) {
+  if (!w || !s || !A || !B || !C) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  int rc = validate_gemm(*w, *s);
+  if (rc) return rc;
+  rc = check_ptr_alignment(A, B, C);
+  if (rc) return rc;
+  return launch_gemm(*w, *s, A, B, C, nullptr, 0, stream);
+}
+
+int alcop_gemm_traced(const alcop_gemm_desc* w, const alcop_schedule* s, const void* A, const void* B, void* C,
+                      alcop_event* trace_dev, int64_t events_per_role_cap, void* stream) {
+  if (!w || !s || !A || !B || !C || !trace_dev)
+    return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  int rc = validate_gemm(*w, *s);
+  if (rc) return rc;
+  rc = check_ptr_alignment(A, B, C);
+  if (rc) return rc;
+  return launch_gemm(*w, *s, A, B, C, trace_dev, events_per_role_cap, stream);
+}
+
+int64_t alcop_gemm_workspace_bytes(const alcop_gemm_desc* w) {
+  if (!w) return -1;
+  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+  const int64_t ob = w->out_dtype == ALCOP_F32 ? 4 : 2;
+  return al(w->batch * w->M * w->K * 2) + al(w->batch * w->K * w->N * 2) + al(w->batch * w->M * w->N * ob);
+}
+
+int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB, void* hC,
+                    void* workspace, void* stream) {
+  if (!w || !s || !hA || !hB || !hC || !workspace)
+    return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  if (w->lda || w->ldb || w->ldc || w->stride_a || w->stride_b || w->stride_c)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "host-buffer entry point takes packed tensors only");
+  int rc = validate_gemm(*w, *s);
+  if (rc) return rc;
+  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+  const int64_t ob = w->out_dtype == ALCOP_F32 ? 4 : 2;
+  const int64_t bytesA = w->batch * w->M * w->K * 2, bytesB = w->batch * w->K * w->N * 2,
+                bytesC = w->batch * w->M * w->N * ob;
+  char* dA = static_cast<char*>(workspace);
+  char* dB = dA + al(bytesA);
+  char* dC = dB + al(bytesB);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dA, hA, bytesA, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, bytesB, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  rc = launch_gemm(*w, *s, dA, dB, dC, nullptr, 0, stream);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(hC, dC, bytesC, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  return ALCOP_OK;
+}
+
+int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* wt, void* y,
+                 void* stream) {
+  if (!d || !s || !x || !wt || !y) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  return launch_conv2d(*d, *s, x, wt, y, stream);
+}
+
+}  // extern "C"

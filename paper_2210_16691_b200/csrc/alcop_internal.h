@@ -1,0 +1,32 @@
+// alcop_internal.h — shared declarations between the C-ABI front end
+// (alcop_api.cpp, schedule.cpp, model.cpp) and the sm_100a kernels (*.cu).
+#pragma once
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/alcop.h"
+
+namespace alcop {
+
+// Sets the thread-local "<RuleTag>: message" and returns `code`.
+int set_error(int code, const std::string& tag, const std::string& msg);
+void clear_error();
+
+// Kernel limits of the cta_group::1 pipelined GEMM.
+constexpr int kTileM = 128;
+constexpr int kMaxStages = 16;
+constexpr int kMaxSmemBytes = 232448;  // 227 KB opt-in per CTA on sm_100
+constexpr int kTmemCols = 512;
+
+int64_t round_up_pow2_cols(int64_t cols);
+int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s);
+int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s);
+// Launch (validated) — implemented in gemm_sm100.cu.
+int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,
+                alcop_event* trace, int64_t trace_cap, void* stream);
+int device_sm_count();
+int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt, void* y,
+                  void* stream);
+
+}  // namespace alcop

@@ -1,0 +1,523 @@
+// gemm_sm100.cu — the output of ALCOP's pipelining pass as an sm_100a kernel.
+//
+// Reference: the pass rewrites the lowered load-and-use nest
+// (schedule.hpp:551-578) into the pipelined nest (pipeline_pass.hpp:753-764):
+//   expand_buffers          (pipeline_pass.hpp:392-437) -> an s-slot smem ring per buffer
+//   shift_and_wrap_indices  (pipeline_pass.hpp:482-552) -> producer loads chunk (v+s-1)%E
+//                                                          into slot (v+s-1)%s, consumer slot v%s
+//   inject_prologues        (pipeline_pass.hpp:627-682) -> s-1 chunk prologue
+//   inject_sync             (pipeline_pass.hpp:689-748) -> four primitives + s-1 drains
+// and the four primitives' semantics (interp.hpp:375-418) become mbarriers:
+//   producer_acquire  = wait empty[slot]           (slot free: previous use released)
+//   producer_commit   = arrive.expect_tx full[slot] + TMA bulk-tensor copies
+//   consumer_wait     = wait full[slot]            (bytes landed -> visible)
+//   consumer_release  = tcgen05.commit -> empty[slot] (arrives when the MMAs retire)
+// The inner (shared->register) level of the paper is re-expressed for
+// tcgen05: the "register load" of k-step u of chunk v is the smem descriptor
+// (slot v%s, k-offset u) handed to tcgen05.mma, and the register double
+// buffer becomes a ring of n_stage_inner TMEM accumulators rotating per
+// output tile, so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// Warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 2-5 = epilogue (TMEM -> regs ->
+// global).  Persistent: one CTA per SM walks tiles blockIdx.x + i*gridDim.x.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "alcop_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace alcop {
+
+struct GemmKParams {
+  int32_t M, N, K, batch;
+  int32_t BN, BK;
+  int32_t num_m, num_n, num_tiles;
+  int32_t E;  // chunks (k blocks) per output tile = pipelined loop extent
+  int32_t sA, sB, tacc;
+  int32_t mode;
+  int32_t b_mn_major;
+  uint32_t idesc;
+  uint32_t a_stage_bytes, b_stage_bytes;
+  uint32_t acc_stride;  // TMEM columns between accumulator buffers
+  uint32_t tmem_cols;
+  void* C;
+  int64_t ldc, stride_c;
+  alcop_event* trace;
+  int32_t trace_cap;
+};
+
+namespace {
+
+constexpr int kThreads = 192;
+
+struct TileCoord {
+  int b, mb, nb;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const GemmKParams& p, int tile_id) {
+  TileCoord t;
+  int per_batch = p.num_m * p.num_n;
+  t.b = tile_id / per_batch;
+  int r = tile_id - t.b * per_batch;
+  t.nb = r / p.num_m;  // m fastest: a wave of CTAs shares B columns
+  t.mb = r - t.nb * p.num_m;
+  return t;
+}
+
+__device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n, int kind, int buf, int tile,
+                                          int slot, int chunk, int parity, int c0, int c1, int c2, int c3) {
+  if (p.trace == nullptr) return;
+  if (n < p.trace_cap) {
+    alcop_event* e = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap + n;
+    e->kind = kind;
+    e->buf = buf;
+    e->tile = tile;
+    e->slot = slot;
+    e->chunk = chunk;
+    e->parity = parity;
+    e->acquired = c0;
+    e->committed = c1;
+    e->waited = c2;
+    e->released = c3;
+  }
+  ++n;
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_row_chunk(OutT* dst, const uint32_t (&r)[32], int valid);
+
+template <>
+__device__ __forceinline__ void store_row_chunk<float>(float* dst, const uint32_t (&r)[32], int valid) {
+  if (valid >= 32) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i] = __uint_as_float(r[i]);
+  }
+}
+
+template <>
+__device__ __forceinline__ void store_row_chunk<__nv_bfloat16>(__nv_bfloat16* dst, const uint32_t (&r)[32],
+                                                               int valid) {
+  uint32_t packed[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    packed[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  if (valid >= 32) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i] = __float2bfloat16_rn(__uint_as_float(r[i]));
+  }
+}
+
+template <>
+__device__ __forceinline__ void store_row_chunk<__half>(__half* dst, const uint32_t (&r)[32], int valid) {
+  uint32_t packed[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    __half2 h = __floats2half2_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    packed[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  if (valid >= 32) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i] = __float2half_rn(__uint_as_float(r[i]));
+  }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                const GemmKParams p) {
+  using namespace ptx;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B swizzle atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t ringA = smem_u32(smem);
+  const uint32_t ringB = ringA + p.sA * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * p.a_stage_bytes + p.sB * p.b_stage_bytes);
+  uint64_t* fullA = bars;
+  uint64_t* emptyA = fullA + p.sA;
+  uint64_t* fullB = emptyA + p.sA;
+  uint64_t* emptyB = fullB + p.sB;
+  uint64_t* tfull = emptyB + p.sB;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < p.sA; ++i) {
+        mbar_init(smem_u32(&fullA[i]), 1);
+        mbar_init(smem_u32(&emptyA[i]), 1);
+      }
+      for (int i = 0; i < p.sB; ++i) {
+        mbar_init(smem_u32(&fullB[i]), 1);
+        mbar_init(smem_u32(&emptyB[i]), 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(smem_u32(&tfull[i]), 1);
+        mbar_init(smem_u32(&tempty[i]), 4);
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int grid = gridDim.x;
+  const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
+  const int E = p.E;
+  const bool wrap = (p.mode == ALCOP_MODE_WRAP);
+
+  if (warp == 0 && lane == 0) {
+    // ======================= producer (TMA) =======================
+    uint32_t phA = 0, phB = 0;  // per-slot phase bits
+    int slotA = 0, slotB = 0;
+    int acqA = 0, acqB = 0;
+    int nev = 0;
+    const int a_atoms = p.BK >= 64 ? p.BK / 64 : 1;
+    const int a_box_k = p.BK >= 64 ? 64 : p.BK;
+    const uint32_t a_atom_bytes = 128u * 128u;
+    auto loadA = [&](int tl, int chunk) {
+      const uint32_t slot = slotA;
+      const uint32_t par = ((phA >> slot) & 1u) ^ 1u;
+      mbar_wait(smem_u32(&emptyA[slot]), par);  // producer_acquire
+      phA ^= 1u << slot;
+      ++acqA;
+      const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
+      const uint32_t fb = smem_u32(&fullA[slot]);
+      mbar_arrive_expect_tx(fb, p.a_stage_bytes);  // producer_commit
+      const uint32_t dst = ringA + slot * p.a_stage_bytes;
+      for (int a = 0; a < a_atoms; ++a)
+        tma_load_3d(dst + a * a_atom_bytes, &tmA, fb, chunk * p.BK + a * a_box_k, tc.mb * kTileM, tc.b);
+      log_event(p, 0, nev, 0, 0, tl, slot, chunk, par, acqA, acqA, -1, -1);
+      slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
+    };
+    auto loadB = [&](int tl, int chunk) {
+      const uint32_t slot = slotB;
+      const uint32_t par = ((phB >> slot) & 1u) ^ 1u;
+      mbar_wait(smem_u32(&emptyB[slot]), par);
+      phB ^= 1u << slot;
+      ++acqB;
+      const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
+      const uint32_t fb = smem_u32(&fullB[slot]);
+      mbar_arrive_expect_tx(fb, p.b_stage_bytes);
+      const uint32_t dst = ringB + slot * p.b_stage_bytes;
+      if (p.b_mn_major) {
+        // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
+        const int atoms = p.BN / 64;
+        for (int a = 0; a < atoms; ++a)
+          tma_load_3d(dst + a * (p.BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * p.BK, tc.b);
+      } else {
+        // B[N,K] row-major: K-major like A with BN rows
+        const int atoms = p.BK >= 64 ? p.BK / 64 : 1;
+        const int box_k = p.BK >= 64 ? 64 : p.BK;
+        for (int a = 0; a < atoms; ++a)
+          tma_load_3d(dst + a * (p.BN * 128), &tmB, fb, chunk * p.BK + a * box_k, tc.nb * p.BN, tc.b);
+      }
+      log_event(p, 0, nev, 0, 1, tl, slot, chunk, par, acqB, acqB, -1, -1);
+      slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
+    };
+
+    if (wrap) {
+      // reference-faithful: per tile, prologue chunks 0..s-2 into slots 0..s-2
+      // (pipeline_pass.hpp:647-656), then steady loads of chunk (v+s-1)%E
+      // (pipeline_pass.hpp:501-509); the s-1 tail loads wrap to chunks 0..
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        slotA = 0;
+        slotB = 0;
+        for (int i = 0; i < p.sA - 1; ++i) loadA(tl, i % E);
+        for (int i = 0; i < p.sB - 1; ++i) loadB(tl, i % E);
+        for (int v = 0; v < E; ++v) {
+          loadA(tl, (v + p.sA - 1) % E);
+          loadB(tl, (v + p.sB - 1) % E);
+        }
+      }
+    } else {
+      // fused: one lookahead window over the flattened (tile, chunk) stream
+      const int total = my_tiles * E;
+      for (int i = 0; i < p.sA - 1 && i < total; ++i) loadA(i / E, i % E);
+      for (int i = 0; i < p.sB - 1 && i < total; ++i) loadB(i / E, i % E);
+      for (int v = 0; v < total; ++v) {
+        const int ja = v + p.sA - 1, jb = v + p.sB - 1;
+        if (ja < total) loadA(ja / E, ja % E);
+        if (jb < total) loadB(jb / E, jb % E);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ======================= MMA issuer =======================
+    uint32_t phA = 0, phB = 0;
+    int slotA = 0, slotB = 0;
+    int waitA = 0, relA = 0, waitB = 0, relB = 0;
+    int nev = 0;
+    const int ksteps = p.BK / 16;
+    const bool a_sw64 = p.BK < 64;
+    const uint32_t a_sbo = a_sw64 ? 512u : 1024u;
+    const uint32_t a_layout = a_sw64 ? kLayoutSW64 : kLayoutSW128;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int acc = tl % p.tacc;
+      const uint32_t acc_par = ((tl / p.tacc) & 1) ^ 1;
+      mbar_wait(smem_u32(&tempty[acc]), acc_par);  // accumulator drained by the epilogue
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
+      if (wrap) {
+        slotA = 0;
+        slotB = 0;
+      }
+      for (int v = 0; v < E; ++v) {
+        const uint32_t sa = slotA, sb = slotB;
+        const uint32_t pa = (phA >> sa) & 1u, pb = (phB >> sb) & 1u;
+        mbar_wait(smem_u32(&fullA[sa]), pa);  // consumer_wait A
+        phA ^= 1u << sa;
+        ++waitA;
+        log_event(p, 1, nev, 1, 0, tl, sa, v, pa, -1, -1, waitA, relA);
+        mbar_wait(smem_u32(&fullB[sb]), pb);  // consumer_wait B
+        phB ^= 1u << sb;
+        ++waitB;
+        log_event(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, waitB, relB);
+        tc_fence_after();
+        const uint32_t a_base = ringA + sa * p.a_stage_bytes;
+        const uint32_t b_base = ringB + sb * p.b_stage_bytes;
+        for (int u = 0; u < ksteps; ++u) {
+          // inner level: step u of chunk v reads slot v%s at k offset u*16
+          const uint32_t a_addr = a_sw64 ? a_base + u * 32 : a_base + (u >> 2) * (128 * 128) + (u & 3) * 32;
+          const uint64_t adesc = make_smem_desc(a_addr, 16, a_sbo, a_layout);
+          uint64_t bdesc;
+          if (p.b_mn_major) {
+            bdesc = make_smem_desc(b_base + u * 2048, p.BK * 128, 1024, kLayoutSW128);
+          } else {
+            const uint32_t b_addr =
+                a_sw64 ? b_base + u * 32 : b_base + (u >> 2) * (p.BN * 128) + (u & 3) * 32;
+            bdesc = make_smem_desc(b_addr, 16, a_sbo, a_layout);
+          }
+          umma_f16_ss(d_tmem, adesc, bdesc, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
+        }
+        umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
+        ++relA;
+        log_event(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, waitA, relA);
+        umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
+        ++relB;
+        log_event(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, waitB, relB);
+        slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
+        slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
+      }
+      umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+      if (wrap) {
+        // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
+        // groups of each buffer, A's then B's, without MMA.
+        for (int d = 0; d < p.sA - 1; ++d) {
+          const uint32_t sa = slotA, pa = (phA >> sa) & 1u;
+          mbar_wait(smem_u32(&fullA[sa]), pa);
+          phA ^= 1u << sa;
+          ++waitA;
+          log_event(p, 1, nev, 1, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
+          mbar_arrive(smem_u32(&emptyA[sa]));
+          ++relA;
+          log_event(p, 1, nev, 2, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
+          slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
+        }
+        for (int d = 0; d < p.sB - 1; ++d) {
+          const uint32_t sb = slotB, pb = (phB >> sb) & 1u;
+          mbar_wait(smem_u32(&fullB[sb]), pb);
+          phB ^= 1u << sb;
+          ++waitB;
+          log_event(p, 1, nev, 1, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
+          mbar_arrive(smem_u32(&emptyB[sb]));
+          ++relB;
+          log_event(p, 1, nev, 2, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
+          slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
+        }
+      }
+    }
+  } else if (warp >= 2) {
+    // ======================= epilogue =======================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    OutT* C = reinterpret_cast<OutT*>(p.C);
+    const int nchunks = p.BN / 32;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int acc = tl % p.tacc;
+      mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
+      tc_fence_after();
+      const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
+      const int row = tc.mb * kTileM + q * 32 + lane;
+      OutT* crow = C + static_cast<int64_t>(tc.b) * p.stride_c + static_cast<int64_t>(row) * p.ldc;
+      const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_addr + c * 32, r);
+        tmem_wait_ld();
+        if (c == nchunks - 1) {
+          // all TMEM reads of this accumulator done: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+        }
+        const int col = tc.nb * p.BN + c * 32;
+        if (row < p.M && col < p.N) store_row_chunk<OutT>(crow + col, r, min(32, p.N - col));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+int encode_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+              uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+              CUtensorMapSwizzle swz, const char* what) {
+  auto enc = get_encode_tiled();
+  if (!enc) return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(ALCOP_ERR_CUDA, "CudaError",
+                     std::string("cuTensorMapEncodeTiled failed for ") + what + " (CUresult " + std::to_string(r) + ")");
+  return ALCOP_OK;
+}
+
+template <typename OutT>
+int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const GemmKParams& kp, int grid, int smem,
+                 cudaStream_t st) {
+  auto kern = alcop_pipelined_gemm_kernel<OutT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  kern<<<grid, kThreads, smem, st>>>(ta, tb, kp);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  return ALCOP_OK;
+}
+
+}  // namespace
+
+int device_sm_count() {
+  static int sms = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) sms = v;
+  });
+  return sms;
+}
+
+int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,
+                alcop_event* trace, int64_t trace_cap, void* stream) {
+  const int64_t lda = w.lda ? w.lda : w.K;
+  const int64_t ldb = w.ldb ? w.ldb : (w.b_layout == ALCOP_B_KN ? w.N : w.K);
+  const int64_t ldc = w.ldc ? w.ldc : w.N;
+  const int64_t sa = w.stride_a ? w.stride_a : w.M * lda;
+  const int64_t sb = w.stride_b ? w.stride_b : (w.b_layout == ALCOP_B_KN ? w.K * ldb : w.N * ldb);
+  const int64_t sc = w.stride_c ? w.stride_c : w.M * ldc;
+  const CUtensorMapDataType dt =
+      w.in_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int BN = static_cast<int>(s.tileN), BK = static_cast<int>(s.tileK);
+  const CUtensorMapSwizzle kswz = BK >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const uint32_t kbox = BK >= 64 ? 64 : BK;
+
+  CUtensorMap ta, tb;
+  int rc = encode_3d(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
+  if (rc) return rc;
+  if (w.b_layout == ALCOP_B_KN)
+    rc = encode_3d(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
+  else
+    rc = encode_3d(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN, kswz, "B");
+  if (rc) return rc;
+
+  GemmKParams kp{};
+  kp.M = static_cast<int32_t>(w.M);
+  kp.N = static_cast<int32_t>(w.N);
+  kp.K = static_cast<int32_t>(w.K);
+  kp.batch = static_cast<int32_t>(w.batch);
+  kp.BN = BN;
+  kp.BK = BK;
+  kp.num_m = static_cast<int32_t>((w.M + kTileM - 1) / kTileM);
+  kp.num_n = static_cast<int32_t>((w.N + BN - 1) / BN);
+  kp.num_tiles = static_cast<int32_t>(kp.num_m * kp.num_n * w.batch);
+  kp.E = static_cast<int32_t>((w.K + BK - 1) / BK);
+  kp.sA = s.n_stage_smem_A;
+  kp.sB = s.n_stage_smem_B;
+  kp.tacc = s.n_stage_inner;
+  kp.mode = s.mode;
+  kp.b_mn_major = w.b_layout == ALCOP_B_KN ? 1 : 0;
+  kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM, BN);
+  kp.a_stage_bytes = static_cast<uint32_t>(kTileM * BK * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>(BN * BK * 2);
+  kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
+  kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
+  kp.C = C;
+  kp.ldc = ldc;
+  kp.stride_c = sc;
+  kp.trace = trace;
+  kp.trace_cap = static_cast<int32_t>(trace_cap);
+
+  int sms = device_sm_count();
+  if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
+  int grid = s.num_ctas > 0 ? s.num_ctas : sms;
+  if (grid > kp.num_tiles) grid = kp.num_tiles;
+  const int smem = static_cast<int>(gemm_smem_bytes(w, s));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (w.out_dtype) {
+    case ALCOP_F32: return launch_typed<float>(ta, tb, kp, grid, smem, st);
+    case ALCOP_BF16: return launch_typed<__nv_bfloat16>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F16: return launch_typed<__half>(ta, tb, kp, grid, smem, st);
+  }
+  return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
+}
+
+}  // namespace alcop

@@ -1,0 +1,154 @@
+"""GPU parity of the sm_100a pipelined GEMM/BMM kernels (through the C ABI).
+
+D-int inputs (SplitMix64 range(-8,8), the reference generator) are exact in
+fp16/bf16 and every fp32 partial sum is an integer < 2^24, so the kernel's
+fp32 output must equal the exact integer product bit-for-bit, and bf16/f16
+output must equal its round-to-nearest-even value bit-for-bit.  D-float
+inputs are checked against a float64 reference with the tolerance stated in
+SURVEY §8(d): |d| <= 2 ulp(out)*|ref| + 2^-20*sqrt(K)  (rel. Frobenius 1e-5
+for fp32 out).
+"""
+import numpy as np
+import pytest
+
+from oracle.splitmix import gemm_inputs, uniform_tensor
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _exact(a, b, batched):
+    a = a.astype(np.int64)
+    b = b.astype(np.int64)
+    return np.matmul(a, b)
+
+
+def _run(alcop, M, N, K, batch=1, in_dt=None, out_dt=None, b_layout=0, sched=None, seed=0):
+    in_dt = in_dt or torch.bfloat16
+    out_dt = out_dt or torch.float32
+    a, b = gemm_inputs(M, N, K, batch, seed=seed)
+    exact = _exact(a, b, batch > 1)
+    A = torch.from_numpy(a).to(in_dt).cuda()
+    Bt = torch.from_numpy(b).to(in_dt)
+    if b_layout == alcop.B_NK:
+        Bt = Bt.transpose(-1, -2).contiguous()
+    B = Bt.cuda()
+    C = alcop.matmul(A, B, sched, out_dtype=out_dt, b_layout=b_layout)
+    torch.cuda.synchronize()
+    return C.cpu(), exact
+
+
+def _assert_exact(C, exact, out_dt):
+    ref = torch.from_numpy(exact.astype(np.float64))
+    if out_dt == torch.float32:
+        ref = ref.to(torch.float32)
+    else:
+        ref = ref.to(torch.float32).to(out_dt)  # exact int -> fp32 exact -> RNE to out dtype
+    if not torch.equal(C, ref):
+        diff = (C.float() - ref.float()).abs()
+        idx = torch.nonzero(diff)[:5]
+        raise AssertionError("mismatch at %s: got %s want %s (n=%d)" %
+                             (idx.tolist(), [C[tuple(i)].item() for i in idx],
+                              [ref[tuple(i)].item() for i in idx], int((diff != 0).sum())))
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["wrap", "fused"])
+def test_config1_fp16_512_exact(alcop, mode):
+    """BASELINE config 1: fp16 512^3, tile 128x128x32, 2 smem + 2 inner stages."""
+    s = alcop.make_schedule(tileN=128, tileK=32, n_stage=2, n_stage_inner=2, mode=mode)
+    C, exact = _run(alcop, 512, 512, 512, in_dt=torch.float16, out_dt=torch.float32, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("tileN", [64, 128, 192, 256])
+@pytest.mark.parametrize("tileK", [32, 64, 128])
+def test_tiles_exact(alcop, tileN, tileK):
+    stage_bytes = (128 + tileN) * tileK * 2
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=min(3, 220000 // stage_bytes), n_stage_inner=2)
+    C, exact = _run(alcop, 256, 3 * 192 if tileN == 192 else 512, 384, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("sA,sB,inner", [(1, 1, 1), (2, 2, 1), (1, 3, 2), (4, 2, 2), (5, 5, 2), (6, 6, 2), (8, 7, 2)])
+@pytest.mark.parametrize("mode", [0, 1], ids=["wrap", "fused"])
+def test_stages_exact(alcop, sA, sB, inner, mode):
+    s = alcop.make_schedule(tileN=128, tileK=64 if max(sA, sB) < 7 else 32, n_stage=sA, n_stage_B=sB, n_stage_inner=inner, mode=mode)
+    C, exact = _run(alcop, 384, 384, 640, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("out_dt", ["bf16", "f16"])
+def test_half_output_rne(alcop, out_dt):
+    odt = torch.bfloat16 if out_dt == "bf16" else torch.float16
+    idt = torch.bfloat16 if out_dt == "bf16" else torch.float16
+    s = alcop.make_schedule(tileN=256, tileK=64, n_stage=4)
+    C, exact = _run(alcop, 512, 768, 768, in_dt=idt, out_dt=odt, sched=s)
+    _assert_exact(C, exact, odt)
+
+
+def test_b_layout_nk(alcop):
+    for tk in (32, 64, 128):
+        s = alcop.make_schedule(tileN=128, tileK=tk, n_stage=3)
+        C, exact = _run(alcop, 256, 256, 512, b_layout=alcop.B_NK, sched=s)
+        _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["wrap", "fused"])
+def test_batched_exact(alcop, mode):
+    s = alcop.make_schedule(tileN=128, tileK=64, n_stage=3, mode=mode)
+    C, exact = _run(alcop, 256, 128, 192, batch=5, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+def test_ragged_shapes(alcop):
+    # M, N not multiples of the tile; K not a multiple of tileK (TMA zero fill)
+    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=3)
+    C, exact = _run(alcop, 300, 200, 104, sched=s)
+    _assert_exact(C, exact, torch.float32)
+    s = alcop.make_schedule(tileN=128, tileK=32, n_stage=2)
+    C, exact = _run(alcop, 130, 136, 40, batch=3, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+def test_single_tile_many_ctas(alcop):
+    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=2)
+    C, exact = _run(alcop, 128, 64, 64, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+def test_float_inputs_tolerance(alcop):
+    M, N, K = 1024, 768, 3072
+    a = uniform_tensor(M * K, 11).reshape(M, K)
+    b = uniform_tensor(K * N, 12).reshape(K, N)
+    A = torch.from_numpy(a).to(torch.bfloat16)
+    B = torch.from_numpy(b).to(torch.bfloat16)
+    ref = A.double() @ B.double()
+    s = alcop.make_schedule(tileN=256, tileK=64, n_stage=4)
+    C32 = alcop.matmul(A.cuda(), B.cuda(), s, out_dtype=torch.float32).cpu().double()
+    rel = (C32 - ref).norm() / ref.norm()
+    assert rel < 1e-5, rel
+    Cb = alcop.matmul(A.cuda(), B.cuda(), s, out_dtype=torch.bfloat16).cpu().double()
+    ulp = 2.0 ** -7
+    tol = 2 * ulp * ref.abs() + 2.0 ** -20 * np.sqrt(K)
+    assert bool(((Cb - ref).abs() <= tol).all())
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["wrap", "fused"])
+@pytest.mark.parametrize("sA,sB", [(2, 2), (3, 2), (1, 4)])
+def test_device_trace_matches_enumerator(alcop, mode, sA, sB):
+    """Bit-exact stage bookkeeping: every CTA's producer and MMA-thread event
+    stream equals the host enumerator (which tests/test_bookkeeping.py pins to
+    the reference pass + interpreter)."""
+    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=sA, n_stage_B=sB, n_stage_inner=2, mode=mode, num_ctas=3)
+    M, N, K = 256, 256, 320  # 8 tiles over 3 CTAs, E = 5
+    a, b = gemm_inputs(M, N, K)
+    A = torch.from_numpy(a).to(torch.bfloat16).cuda()
+    B = torch.from_numpy(b).to(torch.bfloat16).cuda()
+    C, traces = alcop.matmul_traced(A, B, s, out_dtype=torch.float32)
+    _assert_exact(C.cpu(), _exact(a, b, False), torch.float32)
+    tiles = 8
+    for cta, (prod, cons) in enumerate(traces):
+        my = (tiles - cta + 2) // 3
+        assert prod == alcop.enumerate_pipeline(my, 5, sA, sB, mode, 0), cta
+        assert cons == alcop.enumerate_pipeline(my, 5, sA, sB, mode, 1), cta
