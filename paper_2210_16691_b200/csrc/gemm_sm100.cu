@@ -147,11 +147,17 @@ __device__ __forceinline__ void store_row_chunk<__half>(__half* dst, const uint3
   }
 }
 
-template <typename OutT>
+template <typename OutT, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const GemmKParams p) {
   using namespace ptx;
+  constexpr int kSteps = BK / 16;             // tcgen05 k-steps per chunk (the inner loop, F)
+  constexpr int kBoxK = BK >= 64 ? 64 : BK;   // K extent of one K-major swizzle atom
+  constexpr int kKAtoms = BK / kBoxK;
+  constexpr uint32_t kKSbo = BK >= 64 ? 1024u : 512u;  // 8 rows x swizzle width
+  constexpr uint32_t kKLayout = BK >= 64 ? kLayoutSW128 : kLayoutSW64;
+
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -166,15 +172,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && elect_one()) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
   if (warp == 1) {
-    if (lane == 0) {
+    if (elect_one()) {
       for (int i = 0; i < p.sA; ++i) {
         mbar_init(smem_u32(&fullA[i]), 1);
         mbar_init(smem_u32(&emptyA[i]), 1);
@@ -203,28 +209,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int E = p.E;
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
 
-  if (warp == 0 && lane == 0) {
-    // ======================= producer (TMA) =======================
+  if (warp == 0) {
+    // ======================= producer (TMA), whole warp, one issuing lane =======================
     uint32_t phA = 0, phB = 0;  // per-slot phase bits
     int slotA = 0, slotB = 0;
     int acqA = 0, acqB = 0;
     int nev = 0;
-    const int a_atoms = p.BK >= 64 ? p.BK / 64 : 1;
-    const int a_box_k = p.BK >= 64 ? 64 : p.BK;
-    const uint32_t a_atom_bytes = 128u * 128u;
+    int tlA = -1, tlB = -1;
+    TileCoord tcA{0, 0, 0}, tcB{0, 0, 0};
     auto loadA = [&](int tl, int chunk) {
       const uint32_t slot = slotA;
       const uint32_t par = ((phA >> slot) & 1u) ^ 1u;
       mbar_wait(smem_u32(&emptyA[slot]), par);  // producer_acquire
       phA ^= 1u << slot;
       ++acqA;
-      const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
-      const uint32_t fb = smem_u32(&fullA[slot]);
-      mbar_arrive_expect_tx(fb, p.a_stage_bytes);  // producer_commit
-      const uint32_t dst = ringA + slot * p.a_stage_bytes;
-      for (int a = 0; a < a_atoms; ++a)
-        tma_load_3d(dst + a * a_atom_bytes, &tmA, fb, chunk * p.BK + a * a_box_k, tc.mb * kTileM, tc.b);
-      log_event(p, 0, nev, 0, 0, tl, slot, chunk, par, acqA, acqA, -1, -1);
+      if (tl != tlA) {
+        tlA = tl;
+        tcA = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
+      }
+      if (elect_one()) {
+        const uint32_t fb = smem_u32(&fullA[slot]);
+        mbar_arrive_expect_tx(fb, p.a_stage_bytes);  // producer_commit
+        const uint32_t dst = ringA + slot * p.a_stage_bytes;
+#pragma unroll
+        for (int a = 0; a < kKAtoms; ++a)
+          tma_load_3d(dst + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK, tcA.mb * kTileM, tcA.b);
+        log_event(p, 0, nev, 0, 0, tl, slot, chunk, par, acqA, acqA, -1, -1);
+      }
+      __syncwarp();
       slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
     };
     auto loadB = [&](int tl, int chunk) {
@@ -233,23 +245,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(&emptyB[slot]), par);
       phB ^= 1u << slot;
       ++acqB;
-      const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
-      const uint32_t fb = smem_u32(&fullB[slot]);
-      mbar_arrive_expect_tx(fb, p.b_stage_bytes);
-      const uint32_t dst = ringB + slot * p.b_stage_bytes;
-      if (p.b_mn_major) {
-        // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
-        const int atoms = p.BN / 64;
-        for (int a = 0; a < atoms; ++a)
-          tma_load_3d(dst + a * (p.BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * p.BK, tc.b);
-      } else {
-        // B[N,K] row-major: K-major like A with BN rows
-        const int atoms = p.BK >= 64 ? p.BK / 64 : 1;
-        const int box_k = p.BK >= 64 ? 64 : p.BK;
-        for (int a = 0; a < atoms; ++a)
-          tma_load_3d(dst + a * (p.BN * 128), &tmB, fb, chunk * p.BK + a * box_k, tc.nb * p.BN, tc.b);
+      if (tl != tlB) {
+        tlB = tl;
+        tcB = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
       }
-      log_event(p, 0, nev, 0, 1, tl, slot, chunk, par, acqB, acqB, -1, -1);
+      if (elect_one()) {
+        const uint32_t fb = smem_u32(&fullB[slot]);
+        mbar_arrive_expect_tx(fb, p.b_stage_bytes);
+        const uint32_t dst = ringB + slot * p.b_stage_bytes;
+        if (p.b_mn_major) {
+          // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
+          const int atoms = p.BN >> 6;
+          for (int a = 0; a < atoms; ++a)
+            tma_load_3d(dst + a * (BK * 128), &tmB, fb, tcB.nb * p.BN + a * 64, chunk * BK, tcB.b);
+        } else {
+          // B[N,K] row-major: K-major like A with BN rows
+#pragma unroll
+          for (int a = 0; a < kKAtoms; ++a)
+            tma_load_3d(dst + a * (p.BN * 128), &tmB, fb, chunk * BK + a * kBoxK, tcB.nb * p.BN, tcB.b);
+        }
+        log_event(p, 0, nev, 0, 1, tl, slot, chunk, par, acqB, acqB, -1, -1);
+      }
+      __syncwarp();
       slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
     };
 
@@ -262,32 +279,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         slotB = 0;
         for (int i = 0; i < p.sA - 1; ++i) loadA(tl, i % E);
         for (int i = 0; i < p.sB - 1; ++i) loadB(tl, i % E);
+        int ca = (p.sA - 1) % E, cb = (p.sB - 1) % E;
         for (int v = 0; v < E; ++v) {
-          loadA(tl, (v + p.sA - 1) % E);
-          loadB(tl, (v + p.sB - 1) % E);
+          loadA(tl, ca);
+          loadB(tl, cb);
+          ca = (ca + 1 == E) ? 0 : ca + 1;
+          cb = (cb + 1 == E) ? 0 : cb + 1;
         }
       }
     } else {
       // fused: one lookahead window over the flattened (tile, chunk) stream
       const int total = my_tiles * E;
-      for (int i = 0; i < p.sA - 1 && i < total; ++i) loadA(i / E, i % E);
-      for (int i = 0; i < p.sB - 1 && i < total; ++i) loadB(i / E, i % E);
+      int ta = 0, ca = 0, tb = 0, cb = 0;  // (tile, chunk) of the next A / B load
+      auto nextA = [&] { if (++ca == E) { ca = 0; ++ta; } };
+      auto nextB = [&] { if (++cb == E) { cb = 0; ++tb; } };
+      for (int i = 0; i < p.sA - 1 && i < total; ++i) { loadA(ta, ca); nextA(); }
+      for (int i = 0; i < p.sB - 1 && i < total; ++i) { loadB(tb, cb); nextB(); }
       for (int v = 0; v < total; ++v) {
-        const int ja = v + p.sA - 1, jb = v + p.sB - 1;
-        if (ja < total) loadA(ja / E, ja % E);
-        if (jb < total) loadB(jb / E, jb % E);
+        if (v + p.sA - 1 < total) { loadA(ta, ca); nextA(); }
+        if (v + p.sB - 1 < total) { loadB(tb, cb); nextB(); }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ======================= MMA issuer =======================
+  } else if (warp == 1) {
+    // ======================= MMA issuer, whole warp, one issuing lane =======================
     uint32_t phA = 0, phB = 0;
     int slotA = 0, slotB = 0;
     int waitA = 0, relA = 0, waitB = 0, relB = 0;
     int nev = 0;
-    const int ksteps = p.BK / 16;
-    const bool a_sw64 = p.BK < 64;
-    const uint32_t a_sbo = a_sw64 ? 512u : 1024u;
-    const uint32_t a_layout = a_sw64 ? kLayoutSW64 : kLayoutSW128;
+    // descriptor bases (start address advances in 16-byte units in the low word)
+    const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
+    uint64_t bdesc0;
+    uint32_t b_big, b_small;  // B k-step advance: (u>>2)*b_big + (u&3)*b_small, in 16 B units
+    if (p.b_mn_major) {
+      bdesc0 = make_smem_desc(ringB, BK * 128, 1024, kLayoutSW128);
+      b_small = 2048 / 16;
+      b_big = 4 * b_small;
+    } else {
+      bdesc0 = make_smem_desc(ringB, 16, kKSbo, kKLayout);
+      b_small = 2;
+      b_big = static_cast<uint32_t>(p.BN) * 128 / 16;
+    }
+    const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int acc = tl % p.tacc;
       const uint32_t acc_par = ((tl / p.tacc) & 1) ^ 1;
@@ -302,40 +334,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sa = slotA, sb = slotB;
         const uint32_t pa = (phA >> sa) & 1u, pb = (phB >> sb) & 1u;
         mbar_wait(smem_u32(&fullA[sa]), pa);  // consumer_wait A
-        phA ^= 1u << sa;
-        ++waitA;
-        log_event(p, 1, nev, 1, 0, tl, sa, v, pa, -1, -1, waitA, relA);
         mbar_wait(smem_u32(&fullB[sb]), pb);  // consumer_wait B
+        phA ^= 1u << sa;
         phB ^= 1u << sb;
+        ++waitA;
         ++waitB;
-        log_event(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, waitB, relB);
         tc_fence_after();
-        const uint32_t a_base = ringA + sa * p.a_stage_bytes;
-        const uint32_t b_base = ringB + sb * p.b_stage_bytes;
-        for (int u = 0; u < ksteps; ++u) {
-          // inner level: step u of chunk v reads slot v%s at k offset u*16
-          const uint32_t a_addr = a_sw64 ? a_base + u * 32 : a_base + (u >> 2) * (128 * 128) + (u & 3) * 32;
-          const uint64_t adesc = make_smem_desc(a_addr, 16, a_sbo, a_layout);
-          uint64_t bdesc;
-          if (p.b_mn_major) {
-            bdesc = make_smem_desc(b_base + u * 2048, p.BK * 128, 1024, kLayoutSW128);
-          } else {
-            const uint32_t b_addr =
-                a_sw64 ? b_base + u * 32 : b_base + (u >> 2) * (p.BN * 128) + (u & 3) * 32;
-            bdesc = make_smem_desc(b_addr, 16, a_sbo, a_layout);
+        if (elect_one()) {
+          log_event(p, 1, nev, 1, 0, tl, sa, v, pa, -1, -1, waitA, relA);
+          log_event(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, waitB, relB);
+          const uint64_t ad = adesc0 + sa * a_stage16;
+          const uint64_t bd = bdesc0 + sb * b_stage16;
+#pragma unroll
+          for (int u = 0; u < kSteps; ++u) {
+            // inner level: k-step u of chunk v reads slot v%s at k offset 16u
+            const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
+            const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
+            umma_f16_ss(d_tmem, ad + a_off, bd + b_off, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
           }
-          umma_f16_ss(d_tmem, adesc, bdesc, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
+          umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
+          umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
+          log_event(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, waitA, relA + 1);
+          log_event(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, waitB, relB + 1);
         }
-        umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
+        __syncwarp();
         ++relA;
-        log_event(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, waitA, relA);
-        umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
         ++relB;
-        log_event(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, waitB, relB);
         slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
         slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
       }
-      umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+      if (elect_one()) umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+      __syncwarp();
       if (wrap) {
         // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
         // groups of each buffer, A's then B's, without MMA.
@@ -344,10 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(&fullA[sa]), pa);
           phA ^= 1u << sa;
           ++waitA;
-          log_event(p, 1, nev, 1, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
-          mbar_arrive(smem_u32(&emptyA[sa]));
+          if (elect_one()) {
+            log_event(p, 1, nev, 1, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
+            mbar_arrive(smem_u32(&emptyA[sa]));
+            log_event(p, 1, nev, 2, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA + 1);
+          }
+          __syncwarp();
           ++relA;
-          log_event(p, 1, nev, 2, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
           slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
         }
         for (int d = 0; d < p.sB - 1; ++d) {
@@ -355,16 +387,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(&fullB[sb]), pb);
           phB ^= 1u << sb;
           ++waitB;
-          log_event(p, 1, nev, 1, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
-          mbar_arrive(smem_u32(&emptyB[sb]));
+          if (elect_one()) {
+            log_event(p, 1, nev, 1, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
+            mbar_arrive(smem_u32(&emptyB[sb]));
+            log_event(p, 1, nev, 2, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB + 1);
+          }
+          __syncwarp();
           ++relB;
-          log_event(p, 1, nev, 2, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
           slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
         }
       }
     }
-  } else if (warp >= 2) {
-    // ======================= epilogue =======================
+  } else {
+    // ======================= epilogue (warps 2-5) =======================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     OutT* C = reinterpret_cast<OutT*>(p.C);
     const int nchunks = p.BN / 32;
@@ -430,10 +465,10 @@ int encode_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
   return ALCOP_OK;
 }
 
-template <typename OutT>
+template <typename OutT, int BK>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const GemmKParams& kp, int grid, int smem,
                  cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_kernel<OutT>;
+  auto kern = alcop_pipelined_gemm_kernel<OutT, BK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   kern<<<grid, kThreads, smem, st>>>(ta, tb, kp);
@@ -512,10 +547,16 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   if (grid > kp.num_tiles) grid = kp.num_tiles;
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  switch (w.out_dtype) {
-    case ALCOP_F32: return launch_typed<float>(ta, tb, kp, grid, smem, st);
-    case ALCOP_BF16: return launch_typed<__nv_bfloat16>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F16: return launch_typed<__half>(ta, tb, kp, grid, smem, st);
+  switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
+    case ALCOP_F32 * 4 + 0: return launch_typed<float, 32>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 1: return launch_typed<float, 64>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 2: return launch_typed<float, 128>(ta, tb, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 0: return launch_typed<__nv_bfloat16, 32>(ta, tb, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 1: return launch_typed<__nv_bfloat16, 64>(ta, tb, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 2: return launch_typed<__nv_bfloat16, 128>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 0: return launch_typed<__half, 32>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 1: return launch_typed<__half, 64>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 2: return launch_typed<__half, 128>(ta, tb, kp, grid, smem, st);
   }
   return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
 }
