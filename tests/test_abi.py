@@ -1,0 +1,74 @@
+"""The drop-in boundary: libalcop.so loads without a GPU, exports every
+function include/alcop.h declares, and rejects bad schedules with the
+reference's exit-code numbering (cli.hpp:23-25) and rule tags."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "alcop.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(alcop_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(alcop):
+    lib = alcop.load_library()
+    names = header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(alcop.EXPORTED_SYMBOLS)
+
+
+def test_version_and_error_string(alcop):
+    assert "sm_100a" in alcop.version()
+
+
+@pytest.mark.parametrize("field,value,rule", [
+    ("tileM", 64, "BadTile"), ("tileN", 96, "BadTile"), ("tileK", 16, "BadTile"),
+    ("n_stage_smem_A", 0, "BadStages"), ("n_stage_inner", 3, "BadStages"), ("mode", 7, "BadSchedule"),
+    ("cta_group", 4, "BadSchedule"),
+])
+def test_validate_rejects(alcop, field, value, rule):
+    d = alcop.gemm_desc(1024, 1024, 1024)
+    s = alcop.make_schedule()
+    setattr(s, field, value)
+    with pytest.raises(alcop.AlcopError) as ei:
+        alcop.validate(d, s)
+    assert ei.value.code == alcop.ALCOP_ERR_CONFIG
+    assert ei.value.rule == rule
+
+
+def test_validate_capacity_and_lookahead(alcop):
+    d = alcop.gemm_desc(1024, 1024, 1024)
+    s = alcop.make_schedule(tileN=256, tileK=128, n_stage=4)
+    with pytest.raises(alcop.AlcopError) as ei:
+        alcop.validate(d, s)
+    assert ei.value.rule == "SmemCapacity"
+    s = alcop.make_schedule(tileN=256, tileK=64, n_stage=4, n_stage_inner=2)
+    alcop.validate(d, s)
+    assert alcop.smem_bytes(d, s) <= 232448
+    # TMA needs 16-byte row pitch
+    with pytest.raises(alcop.AlcopError) as ei:
+        alcop.validate(alcop.gemm_desc(128, 128, 100), s)
+    assert ei.value.rule == "Alignment"
+
+
+def test_null_arguments(alcop):
+    lib = alcop.load_library()
+    assert lib.alcop_gemm(None, None, None, None, None, None) == alcop.ALCOP_ERR_CONFIG
+    assert lib.alcop_last_error().decode().startswith("NullArgument")
+
+
+def test_host_entry_rejects_strided(alcop):
+    lib = alcop.load_library()
+    d = alcop.gemm_desc(128, 128, 128, ldc=256)
+    s = alcop.make_schedule()
+    dummy = ctypes.c_void_p(16)
+    rc = lib.alcop_gemm_host(ctypes.byref(d), ctypes.byref(s), dummy, dummy, dummy, dummy, None)
+    assert rc == alcop.ALCOP_ERR_CONFIG
