@@ -1,0 +1,495 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 pipelined load-and-use GEMM path.
+
+Workload (BASELINE.json configs[1]): the GEMMs of one BERT-base encoder layer
+at M = 4096 tokens, bf16 in / bf16 out, fp32 accumulate:
+    Q, K, V, O projections  4 x [4096 x 768] @ [768 x 768]
+    FFN1                    [4096 x 768]  @ [768 x 3072]
+    FFN2                    [4096 x 3072] @ [3072 x 768]
+B is the reference layout [K, N] row-major (schedule.hpp:389).  One "step" is
+one pass over those six GEMMs, each launched through the C ABI (alcop_gemm)
+with the schedule the analytical model picks (alcop_choose_schedule).  Inputs
+rotate over copies whose footprint exceeds 2x the 126 MB L2, so every step
+reads HBM.  Reported beside it, in the same run: the n_stage 1..5 sweep of
+each distinct shape (speedup vs the non-pipelined n_stage=1 variant), the
+model pick vs the best swept schedule, a large square GEMM, the roofline of
+the dominant kernel, the end-to-end number through the host-buffer ABI entry
+point, and the reference CPU path timed on the host cores.
+
+--impl reference times the reference's own CPU implementation (the pipec
+interpreter running the transformed program, oracle/_ref/ref_driver built
+from /root/reference) on a bounded sample of the same workload.
+
+Multi-GPU: the BERT GEMMs are replicas only — each rank runs
+the full step on its own GPU, no collective on the data path; value is the
+whole-job FLOP rate (N x per-GPU FLOPs / max-over-ranks time).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BERT_GEMMS = [  # (name, M, N, K)
+    ("q_proj", 4096, 768, 768), ("k_proj", 4096, 768, 768), ("v_proj", 4096, 768, 768),
+    ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768), ("ffn2", 4096, 768, 3072),
+]
+METRIC = "TFLOP/s (BERT-base layer GEMMs, M=4096, bf16)"
+UNIT = "TFLOP/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def step_flops():
+    return sum(2.0 * M * N * K for _, M, N, K in BERT_GEMMS)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d["bf16_tflops_sustained"],
+                "hbm_gbs": d["hbm_gbs"], "source": "measured"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------- CPU arms
+def _ref_driver():
+    p = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    return p if os.path.exists(p) else None
+
+
+REF_SAMPLE_COLS = 128  # one output sub-block per GEMM: rows x 128 columns, full K
+REF_NS_PER_MMA = 150e-9  # measured cost of one interpreted mma statement
+
+
+def ref_sample_rows(seconds_per_step):
+    """Rows of the sample block so the slowest job (FFN2, K=3072) takes ~seconds_per_step."""
+    kmax = max(K for _, _, _, K in BERT_GEMMS)
+    return max(1, min(128, int(seconds_per_step / (REF_NS_PER_MMA * REF_SAMPLE_COLS * kmax))))
+
+
+def _ref_sample_script(M, N, K):
+    # the reference's own config-1-style schedule for the sample block:
+    # one output tile, tileK = 32, 2-stage shared + 2-stage register pipeline
+    ko = K // 32
+    return ("cache_read A shared\ncache_read B shared\ncache_read A_shared register\n"
+            "cache_read B_shared register\ntile C i0=1 i1=%d j0=1 j1=%d ko=%d ki=32\n"
+            "pipeline A_shared 2\npipeline B_shared 2\npipeline A_reg 2\npipeline B_reg 2\n"
+            % (M, N, ko))
+
+
+def cpu_reference_step(rows):
+    """One step of the reference CPU path on a bounded sample: for every GEMM
+    of the layer, a REF_SAMPLE_ROWS x REF_SAMPLE_COLS output block with the
+    full K, interpreted by the reference (pipec::run on the transformed
+    program), the six samples run as concurrent processes on the host cores.
+    Returns (seconds, flops, kind, cores).  The block is a sub-problem of the
+    same GEMM: the interpreter's cost is linear in rows*cols*K."""
+    import tempfile
+    drv = _ref_driver()
+    jobs = []
+    tmp = tempfile.mkdtemp()
+    for name, M, N, K in BERT_GEMMS:
+        m, n = rows, REF_SAMPLE_COLS
+        sp = os.path.join(tmp, name + ".txt")
+        with open(sp, "w") as f:
+            f.write(_ref_sample_script(m, n, K))
+        jobs.append((name, m, n, K, sp))
+    flops = sum(2.0 * m * n * K for _, m, n, K, _ in jobs)
+    cores = os.cpu_count() or 1
+    if drv is not None:
+        t0 = time.perf_counter()
+        ps = [subprocess.Popen([drv, "time", "--M", str(m), "--N", str(n), "--K", str(K), "--script", sp,
+                                "--mode", "stale"], stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+              for _, m, n, K, sp in jobs]
+        outs = [p.communicate() for p in ps]
+        dt = time.perf_counter() - t0
+        for p, (o, e) in zip(ps, outs):
+            if p.returncode != 0:
+                raise RuntimeError("ref_driver failed: " + e)
+        return dt, flops, "reference", min(cores, len(jobs))
+    # port: the oracle's C restatement (fp32-accumulate GEMM, OpenMP on all cores)
+    import numpy as np
+    from oracle import coracle
+    t0 = time.perf_counter()
+    for _, m, n, K, _ in jobs:
+        A = coracle.to_dtype(np.ones((m, K), np.float32), "bf16")
+        B = coracle.to_dtype(np.ones((K, n), np.float32), "bf16")
+        coracle.gemm(A, B, "bf16", "bf16")
+    return time.perf_counter() - t0, flops, "port", cores
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    times = []
+    kind = cores = None
+    flops = 0.0
+    rows = ref_sample_rows(min(3.0, 150.0 / (args.warmup + args.steps)))
+    for i in range(args.warmup + args.steps):
+        dt, flops, kind, cores = cpu_reference_step(rows)
+        if i >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = flops * len(times) / total / 1e12
+    sample = ("per step: a %dx%d output block (full K) of each of the 6 BERT-layer GEMMs, pipec::run on the "
+              "transformed two-level program (tile %dx%dx32, 2+2 stages), 6 concurrent processes"
+              % (rows, REF_SAMPLE_COLS, rows, REF_SAMPLE_COLS))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (SplitMix64 range(-8,8), the reference generator)",
+            "config": {"workload": "bert_base_layer_gemms_sample", "M": 4096, "gemms": [g[1:] for g in BERT_GEMMS]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and clocks-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index, period_s=0.005):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+        self.period = period_s
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r) & ~0x1
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b], "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- GPU arm
+def main_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2210_16691_b200 as alcop
+    from paper_2210_16691_b200.timing import time_fn
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    alcop.load_library()
+    peaks = load_peaks()
+    stream = torch.cuda.current_stream()
+
+    # schedules: the analytical model's choice per distinct shape (alcop_choose_schedule)
+    shapes = sorted(set((M, N, K) for _, M, N, K in BERT_GEMMS))
+    sched = {}
+    for (M, N, K) in shapes:
+        d = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+        sched[(M, N, K)] = alcop.choose_schedule(d)
+
+    # rotating input sets so each step's operands come from HBM
+    set_bytes = sum((M * K + K * N + M * N) * 2 for _, M, N, K in BERT_GEMMS)
+    nsets = max(2, -(-2 * L2_BYTES // set_bytes))
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    def make_set():
+        out = []
+        for name, M, N, K in BERT_GEMMS:
+            A = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+            B = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+            C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+            out.append((A, B, C, sched[(M, N, K)]))
+        return out
+
+    sets = [make_set() for _ in range(nsets)]
+    lib = alcop.load_library()
+    import ctypes
+    descs = {s: alcop.gemm_desc(*s, 1, alcop.BF16, alcop.BF16, alcop.B_KN) for s in shapes}
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def launch(A, B, C, s, shape):
+        rc = lib.alcop_gemm(ctypes.byref(descs[shape]), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
+                            ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()), sp)
+        if rc:
+            raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+
+    state = {"i": 0}
+
+    def step():
+        st = sets[state["i"]]
+        state["i"] = (state["i"] + 1) % nsets
+        for (name, M, N, K), (A, B, C, s) in zip(BERT_GEMMS, st):
+            launch(A, B, C, s, (M, N, K))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- correctness spot check of this run's kernels (oracle-independent: exact-integer inputs)
+    for (M, N, K) in shapes:
+        a = torch.randint(-8, 9, (M, K), device=dev).to(torch.bfloat16)
+        b = torch.randint(-8, 9, (K, N), device=dev).to(torch.bfloat16)
+        c = torch.empty((M, N), device=dev, dtype=torch.float32)
+        d32 = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.F32, alcop.B_KN)
+        rc = lib.alcop_gemm(ctypes.byref(d32), ctypes.byref(sched[(M, N, K)]), ctypes.c_void_p(a.data_ptr()),
+                            ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(c.data_ptr()), sp)
+        assert rc == 0
+        ref = (a.double() @ b.double()).float()
+        assert torch.equal(c, ref), "kernel mismatch on %s" % ((M, N, K),)
+
+    # ---- warmup + timed region
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    # per-GEMM durations of the dominant kernel, on the launching stream
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    barrier()
+    t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops = step_flops()
+    value = world * flops * args.steps / (ms_max * 1e-3) / 1e12
+
+    # ---- per-GEMM times (events around each launch) -> dominant kernel roofline
+    per = {}
+    reps = max(5, min(50, args.steps // 4))
+    for (name, M, N, K) in BERT_GEMMS:
+        if name in ("k_proj", "v_proj", "o_proj"):
+            continue
+        j = [n for n, *_ in BERT_GEMMS].index(name)
+        st_i = {"i": 0}
+
+        def one():
+            A, B, C, s = sets[st_i["i"]][j]
+            st_i["i"] = (st_i["i"] + 1) % nsets
+            launch(A, B, C, s, (M, N, K))
+        ms = time_fn(one, iters=reps, warmup=3)
+        per[name] = {"ms": ms, "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12, "schedule": sched[(M, N, K)].as_dict()}
+    step_ms_est = sum(per["q_proj"]["ms"] if n in ("q_proj", "k_proj", "v_proj", "o_proj") else per[n]["ms"]
+                      for n, *_ in BERT_GEMMS)
+    dom = max(per, key=lambda n: per[n]["ms"] * (4 if n == "q_proj" else 1))
+    dM, dN, dK = [g[1:] for g in BERT_GEMMS if g[0] == dom][0]
+    dflops = 2.0 * dM * dN * dK
+    achieved = dflops / (per[dom]["ms"] * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_bench_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            traffic = pj.get("kernels", {}).get(dom, {}).get("dram_bytes")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "kernel": "alcop_pipelined_gemm_kernel (%s %dx%dx%d)" % (dom, dM, dN, dK),
+                "share_of_step": per[dom]["ms"] * (4 if dom == "q_proj" else 1) / step_ms_est,
+                "peak_source": peaks["source"] + " burst bf16 (MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": dflops}
+
+    extra = {}
+    if rank == 0 and not args.quick:
+        # ---- n_stage sweep 1..5 per distinct shape (same tile, same run) + model pick vs best
+        sweep = {}
+        for (M, N, K) in shapes:
+            base = sched[(M, N, K)]
+            rows = []
+            A = (torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16)
+            B = (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16)
+            C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+            best = None
+            cands = []
+            for st in range(1, 6):
+                for tn, tk in ((base.tileN, base.tileK), (128, 64), (256, 64), (128, 128), (256, 128), (192, 64)):
+                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, n_stage_inner=2 if st > 1 else 1)
+                    try:
+                        alcop.validate(descs[(M, N, K)], s)
+                    except alcop.AlcopError:
+                        continue
+                    cands.append((st, tn, tk, s))
+            for st, tn, tk, s in cands:
+                ms = time_fn(lambda: launch(A, B, C, s, (M, N, K)), iters=20, warmup=3)
+                tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
+                rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "tflops": round(tf, 1)})
+                if best is None or tf > best[0]:
+                    best = (tf, st, tn, tk)
+            ms_pick = time_fn(lambda: launch(A, B, C, base, (M, N, K)), iters=20, warmup=3)
+            tf_pick = 2.0 * M * N * K / (ms_pick * 1e-3) / 1e12
+            by_stage = {}
+            for r in rows:
+                if r["tileN"] == base.tileN and r["tileK"] == base.tileK:
+                    by_stage[r["n_stage"]] = r["tflops"]
+            s1 = max([r["tflops"] for r in rows if r["n_stage"] == 1] or [float("nan")])
+            sweep["%dx%dx%d" % (M, N, K)] = {
+                "tflops_by_n_stage_model_tile": by_stage,
+                "best_n_stage1_tflops": s1,
+                "best_swept": {"tflops": round(best[0], 1), "n_stage": best[1], "tileN": best[2], "tileK": best[3]},
+                "model_pick": {"tflops": round(tf_pick, 1), **{k: v for k, v in base.as_dict().items()
+                                                              if k in ("tileN", "tileK", "n_stage_smem_A")}},
+                "model_pick_over_best_time": round(best[0] / tf_pick, 3),
+                "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
+        extra["n_stage_sweep"] = sweep
+        # ---- large square GEMM (config 5 point): 8192^3 bf16
+        n = 8192
+        dsq = alcop.gemm_desc(n, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+        ssq = alcop.choose_schedule(dsq)
+        A = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
+        B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
+        C = torch.empty((n, n), device=dev, dtype=torch.bfloat16)
+        dsq_c = alcop.gemm_desc(n, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+        descs[(n, n, n)] = dsq_c
+        ms = time_fn(lambda: launch(A, B, C, ssq, (n, n, n)), iters=10, warmup=3)
+        tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+        extra["large_square_8192"] = {"tflops": round(tf, 1), "frac_of_peak": round(tf / peaks["bf16_tflops"], 3),
+                                      "schedule": ssq.as_dict()}
+        del A, B, C
+
+    # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)
+    host = []
+    for name, M, N, K in BERT_GEMMS:
+        A = (torch.rand((M, K)) * 2 - 1).to(torch.bfloat16).pin_memory()
+        B = (torch.rand((K, N)) * 2 - 1).to(torch.bfloat16).pin_memory()
+        C = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+        host.append((A, B, C))
+    ws_bytes = max(lib.alcop_gemm_workspace_bytes(ctypes.byref(descs[s])) for s in shapes)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+
+    def e2e_step():
+        for (name, M, N, K), (A, B, C) in zip(BERT_GEMMS, host):
+            rc = lib.alcop_gemm_host(ctypes.byref(descs[(M, N, K)]), ctypes.byref(sched[(M, N, K)]),
+                                     ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                     ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(ws.data_ptr()), sp)
+            if rc:
+                raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = world * flops * e2e_steps / float(te.item()) / 1e12
+    h2d = sum((M * K + K * N) * 2 for _, M, N, K in BERT_GEMMS)
+    d2h = sum(M * N * 2 for _, M, N, K in BERT_GEMMS)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            rows = ref_sample_rows(3.0)
+            dt, cflops, kind, cores = cpu_reference_step(rows)
+            cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": "a %dx%d output block (full K) of each of the 6 BERT-layer GEMMs through the "
+                             "reference interpreter (pipec::run, transformed program), %d concurrent processes; "
+                             "%.2f s wall" % (rows, REF_SAMPLE_COLS, len(BERT_GEMMS), dt)}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (uniform[-1,1) bf16; %d rotating input sets, %.0f MB > 2x L2)"
+                        % (nsets, nsets * set_bytes / 1e6),
+                "config": {"workload": "bert_base_layer_gemms", "M": 4096,
+                           "gemms": {n: [M, N, K] for n, M, N, K in BERT_GEMMS}, "b_layout": "KN (reference)",
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs rotated over copies > 2x L2", "schedule": "alcop_choose_schedule"},
+                "gpu_launches": len(BERT_GEMMS) * args.steps,
+                "clocks": clk.summary(),
+                "roofline": roofline,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "entry_point": "alcop_gemm_host (pinned host buffers, H2D + kernel + D2H per GEMM)"},
+                "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4)} for k, v in per.items()},
+                **extra}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="alcop", choices=["alcop", "reference"])
+    ap.add_argument("--quick", action="store_true", help="skip the n_stage sweep and the large square")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        main_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
