@@ -33,7 +33,8 @@ int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
   const int64_t a_stage = kTileM * s.tileK * 2;
   const int64_t b_stage = s.tileN * s.tileK * 2;
   const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;
-  return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + bars;
+  const int64_t staging = 4 * 2 * 32 * 128;  // epilogue TMA-store staging
+  return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + staging + bars;
 }
 
 static int dtype_bytes(int32_t dt) { return dt == ALCOP_F32 ? 4 : 2; }

@@ -51,11 +51,18 @@ struct GemmKParams {
   int64_t ldc, stride_c;
   alcop_event* trace;
   int32_t trace_cap;
+  uint64_t* stamps;  // debug timeline: 8 globaltimer stamps per CTA (nullptr = off)
 };
+
+// debug timeline buffer (set through alcop_debug_set_stamps)
+static uint64_t* g_stamps = nullptr;
+// programmatic dependent launch on (alcop_debug_set_pdl)
+static bool g_pdl = true;
 
 namespace {
 
 constexpr int kThreads = 192;
+constexpr int kStagingBytes = 4 * 2 * 32 * 128;
 
 struct TileCoord {
   int b, mb, nb;
@@ -69,6 +76,13 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmKParams& p, int tile_i
   t.nb = r / p.num_m;  // m fastest: a wave of CTAs shares B columns
   t.mb = r - t.nb * p.num_m;
   return t;
+}
+
+__device__ __forceinline__ void stamp(const GemmKParams& p, int i) {
+  if (p.stamps == nullptr) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.stamps[blockIdx.x * 8 + i] = t;
 }
 
 __device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n, int kind, int buf, int tile,
@@ -91,66 +105,22 @@ __device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n
 }
 
 template <typename OutT>
-__device__ __forceinline__ void store_row_chunk(OutT* dst, const uint32_t (&r)[32], int valid);
-
+__device__ __forceinline__ uint32_t pack2(uint32_t a, uint32_t b);
 template <>
-__device__ __forceinline__ void store_row_chunk<float>(float* dst, const uint32_t (&r)[32], int valid) {
-  if (valid >= 32) {
-    uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < valid) dst[i] = __uint_as_float(r[i]);
-  }
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(uint32_t a, uint32_t b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(a), __uint_as_float(b));
+  return *reinterpret_cast<uint32_t*>(&h);
 }
-
 template <>
-__device__ __forceinline__ void store_row_chunk<__nv_bfloat16>(__nv_bfloat16* dst, const uint32_t (&r)[32],
-                                                               int valid) {
-  uint32_t packed[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-    packed[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  if (valid >= 32) {
-    uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      d[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < valid) dst[i] = __float2bfloat16_rn(__uint_as_float(r[i]));
-  }
-}
-
-template <>
-__device__ __forceinline__ void store_row_chunk<__half>(__half* dst, const uint32_t (&r)[32], int valid) {
-  uint32_t packed[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    __half2 h = __floats2half2_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-    packed[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  if (valid >= 32) {
-    uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      d[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < valid) dst[i] = __float2half_rn(__uint_as_float(r[i]));
-  }
+__device__ __forceinline__ uint32_t pack2<__half>(uint32_t a, uint32_t b) {
+  __half2 h = __floats2half2_rn(__uint_as_float(a), __uint_as_float(b));
+  return *reinterpret_cast<uint32_t*>(&h);
 }
 
 template <typename OutT, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                                const GemmKParams p) {
+                                const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
   using namespace ptx;
   constexpr int kSteps = BK / 16;             // tcgen05 k-steps per chunk (the inner loop, F)
   constexpr int kBoxK = BK >= 64 ? 64 : BK;   // K extent of one K-major swizzle atom
@@ -163,7 +133,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t ringA = smem_u32(smem);
   const uint32_t ringB = ringA + p.sA * p.a_stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * p.a_stage_bytes + p.sB * p.b_stage_bytes);
+  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), 128B-swizzled for the TMA store
+  const uint32_t staging = ringB + p.sB * p.b_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * p.a_stage_bytes + p.sB * p.b_stage_bytes +
+                                               kStagingBytes);
   uint64_t* fullA = bars;
   uint64_t* emptyA = fullA + p.sA;
   uint64_t* fullB = emptyA + p.sA;
@@ -175,9 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
+  if (threadIdx.x == 0) stamp(p, 0);
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmC);
   }
   if (warp == 1) {
     if (elect_one()) {
@@ -203,6 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: the setup above overlapped the previous kernel's tail; from here on
+  // global memory is touched, so wait for it, and let the next kernel start
+  // its own setup as soon as SMs free up.
+  grid_dependency_wait();
+  grid_launch_dependents();
+  if (threadIdx.x == 0) stamp(p, 1);
 
   const int grid = gridDim.x;
   const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
@@ -235,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int a = 0; a < kKAtoms; ++a)
           tma_load_3d(dst + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK, tcA.mb * kTileM, tcA.b);
         log_event(p, 0, nev, 0, 0, tl, slot, chunk, par, acqA, acqA, -1, -1);
+        if (acqA == 1) stamp(p, 2);
       }
       __syncwarp();
       slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
@@ -341,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++waitB;
         tc_fence_after();
         if (elect_one()) {
+          if (waitA == 1) stamp(p, 3);
           log_event(p, 1, nev, 1, 0, tl, sa, v, pa, -1, -1, waitA, relA);
           log_event(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, waitB, relB);
           const uint64_t ad = adesc0 + sa * a_stage16;
@@ -363,7 +346,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
         slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
       }
-      if (elect_one()) umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+      if (elect_one()) {
+        umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+        if (tl == my_tiles - 1) stamp(p, 4);
+      }
       __syncwarp();
       if (wrap) {
         // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
@@ -400,31 +386,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ======================= epilogue (warps 2-5) =======================
+    // TMEM -> registers (tcgen05.ld) -> 128B-swizzled smem staging -> TMA
+    // bulk-tensor store; two staging buffers per warp so the store of one
+    // chunk overlaps the TMEM read of the next.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    OutT* C = reinterpret_cast<OutT*>(p.C);
-    const int nchunks = p.BN / 32;
+    const uint32_t stage_base = staging + (warp - 2) * 2 * 4096;
+    constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));  // 128 B of output per row
+    const int nchunks = p.BN / kChunkCols;
+    int buf = 0;
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
       tc_fence_after();
+      if (tl == 0 && warp == 2 && lane == 0) stamp(p, 5);
       const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
-      const int row = tc.mb * kTileM + q * 32 + lane;
-      OutT* crow = C + static_cast<int64_t>(tc.b) * p.stride_c + static_cast<int64_t>(row) * p.ldc;
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_addr + c * 32, r);
-        tmem_wait_ld();
+        uint32_t w[32];
+        if constexpr (sizeof(OutT) == 4) {
+          tmem_ld_32x32b_x32(t_addr + c * 32, w);
+          tmem_wait_ld();
+        } else {
+          uint32_t r0[32], r1[32];
+          tmem_ld_32x32b_x32(t_addr + c * 64, r0);
+          tmem_ld_32x32b_x32(t_addr + c * 64 + 32, r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack2<OutT>(r0[2 * i], r0[2 * i + 1]);
+            w[16 + i] = pack2<OutT>(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
         if (c == nchunks - 1) {
           // all TMEM reads of this accumulator done: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
         }
-        const int col = tc.nb * p.BN + c * 32;
-        if (row < p.M && col < p.N) store_row_chunk<OutT>(crow + col, r, min(32, p.N - col));
+        const uint32_t sbuf = stage_base + buf * 4096;
+        if (lane == 0) bulk_wait_group_read<1>();  // the store that last read sbuf is done
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                       w[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * kTileM + q * 32, tc.b);
+          bulk_commit_group();
+        }
+        buf ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_group<0>();
+    __syncwarp();
+    if (warp == 2 && lane == 0) stamp(p, 6);
   }
 
   tc_fence_before();
@@ -433,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
+  if (threadIdx.x == 0) stamp(p, 7);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
@@ -448,7 +466,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
   return fn;
 }
 
-int encode_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
               uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
               CUtensorMapSwizzle swz, const char* what) {
   auto enc = get_encode_tiled();
@@ -466,13 +484,23 @@ int encode_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
 }
 
 template <typename OutT, int BK>
-int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const GemmKParams& kp, int grid, int smem,
-                 cudaStream_t st) {
+int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
+                 int grid, int smem, cudaStream_t st) {
   auto kern = alcop_pipelined_gemm_kernel<OutT, BK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
-  kern<<<grid, kThreads, smem, st>>>(ta, tb, kp);
-  e = cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
 }
@@ -506,13 +534,23 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const uint32_t kbox = BK >= 64 ? 64 : BK;
 
   CUtensorMap ta, tb;
-  int rc = encode_3d(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
+  int rc = encode_3d_dt(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
   if (rc) return rc;
   if (w.b_layout == ALCOP_B_KN)
-    rc = encode_3d(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
+    rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
   else
-    rc = encode_3d(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN, kswz, "B");
+    rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN, kswz, "B");
   if (rc) return rc;
+  CUtensorMap tc;
+  {
+    const CUtensorMapDataType odt = w.out_dtype == ALCOP_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                    : w.out_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    const int ob = w.out_dtype == ALCOP_F32 ? 4 : 2;
+    rc = encode_3d_dt(&tc, odt, C, w.N, w.M, w.batch, ldc * ob, sc * ob, 128 / ob, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                      "C");
+    if (rc) return rc;
+  }
 
   GemmKParams kp{};
   kp.M = static_cast<int32_t>(w.M);
@@ -540,6 +578,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.stride_c = sc;
   kp.trace = trace;
   kp.trace_cap = static_cast<int32_t>(trace_cap);
+  kp.stamps = g_stamps;
 
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
@@ -548,17 +587,23 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
-    case ALCOP_F32 * 4 + 0: return launch_typed<float, 32>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 1: return launch_typed<float, 64>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 2: return launch_typed<float, 128>(ta, tb, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 0: return launch_typed<__nv_bfloat16, 32>(ta, tb, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 1: return launch_typed<__nv_bfloat16, 64>(ta, tb, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 2: return launch_typed<__nv_bfloat16, 128>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 0: return launch_typed<__half, 32>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 1: return launch_typed<__half, 64>(ta, tb, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 2: return launch_typed<__half, 128>(ta, tb, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 0: return launch_typed<float, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 1: return launch_typed<float, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 2: return launch_typed<float, 128>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 0: return launch_typed<__nv_bfloat16, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 1: return launch_typed<__nv_bfloat16, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 2: return launch_typed<__nv_bfloat16, 128>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 0: return launch_typed<__half, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 1: return launch_typed<__half, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 2: return launch_typed<__half, 128>(ta, tb, tc, kp, grid, smem, st);
   }
   return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
 }
 
 }  // namespace alcop
+
+// Debug-only: route an 8 x uint64 per-CTA globaltimer timeline of the next
+// launches into `dev` (device memory, >= 8 * grid entries); NULL turns it off.
+extern "C" void alcop_debug_set_stamps(void* dev) { alcop::g_stamps = static_cast<uint64_t*>(dev); }
+// Debug-only: programmatic dependent launch on (1, default) / off (0).
+extern "C" void alcop_debug_set_pdl(int on) { alcop::g_pdl = on != 0; }

@@ -1,0 +1,71 @@
+"""Exhaustive schedule sweep on the GPU: times every valid (tileN, tileK,
+n_stage, n_stage_inner, mode) point for a set of GEMM shapes and writes JSON
+(the "measured" side of the analytical model's calibration / model-pick check).
+
+python tools/sweep.py out.json [shape ...]   shape = MxNxK[xbatch]
+"""
+import itertools
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2210_16691_b200 as alcop
+from paper_2210_16691_b200.timing import Rotating, time_fn
+
+DEFAULT = ["4096x768x768", "4096x3072x768", "4096x768x3072", "4096x4096x4096", "8192x8192x8192",
+           "512x512x512", "512x512x64x192", "512x64x512x192", "16384x4096x4096"]
+
+
+def parse(s):
+    v = [int(x) for x in s.split("x")]
+    return v + [1] * (4 - len(v))
+
+
+def main():
+    out = sys.argv[1]
+    shapes = [parse(s) for s in (sys.argv[2:] or DEFAULT)]
+    res = []
+    for M, N, K, b in shapes:
+        bytes_set = (M * K + K * N + M * N) * 2 * b
+        shp = (b,) if b > 1 else ()
+
+        def mk(i):
+            A = (torch.rand(shp + (M, K), device="cuda") - 0.5).to(torch.bfloat16)
+            B = (torch.rand(shp + (K, N), device="cuda") - 0.5).to(torch.bfloat16)
+            C = torch.empty(shp + (M, N), device="cuda", dtype=torch.bfloat16)
+            return A, B, C
+        rot = Rotating(mk, bytes_set, max_sets=6)
+        d = alcop.gemm_desc(M, N, K, b, alcop.BF16, alcop.BF16, alcop.B_KN)
+        flops = 2.0 * M * N * K * b
+        iters = 3 if flops > 1e12 else (10 if flops > 1e11 else 30)
+        for tN, tK, st, inner, mode in itertools.product([64, 128, 192, 256], [32, 64, 128], range(1, 9), [1, 2],
+                                                         [alcop.MODE_FUSED, alcop.MODE_WRAP]):
+            s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode)
+            try:
+                alcop.validate(d, s)
+            except alcop.AlcopError:
+                continue
+            if mode == alcop.MODE_WRAP and inner == 1 and st > 1:
+                continue
+
+            def f():
+                A, B, C = rot.next()
+                alcop.matmul(A, B, s, out=C)
+            ms = time_fn(f, iters=iters, warmup=2)
+            pred = alcop.predict(d, s)["seconds"] * 1e3
+            res.append({"M": M, "N": N, "K": K, "batch": b, "tileN": tN, "tileK": tK, "stages": st, "inner": inner,
+                        "mode": mode, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12, "pred_ms": pred})
+        pick = alcop.choose_schedule(d)
+        best = min([r for r in res if (r["M"], r["N"], r["K"], r["batch"]) == (M, N, K, b)], key=lambda r: r["ms"])
+        print("%dx%dx%dx%d best %.1f TF (%s) pick %s" % (M, N, K, b, best["tflops"], best, pick), flush=True)
+        del rot
+        torch.cuda.empty_cache()
+    with open(out, "w") as f:
+        json.dump(res, f)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,53 @@
+"""Per-CTA globaltimer timeline of one pipelined-GEMM launch (debug tool).
+
+python tools/timeline.py M N K tileN tileK stages [inner] [mode]
+Stamps: 0 start, 1 setup done, 2 first TMA issued, 3 first full-wait passed,
+4 last accumulator commit, 5 epilogue got first accumulator, 6 epilogue done,
+7 CTA end.  Printed as microseconds after the earliest CTA start.
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2210_16691_b200 as alcop
+
+
+def main():
+    M, N, K, tN, tK, st = map(int, sys.argv[1:7])
+    inner = int(sys.argv[7]) if len(sys.argv) > 7 else 2
+    mode = int(sys.argv[8]) if len(sys.argv) > 8 else 1
+    lib = alcop.load_library()
+    lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode)
+    stamps = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        alcop.matmul(A, B, s, out=C)
+    torch.cuda.synchronize()
+    lib.alcop_debug_set_stamps(ctypes.c_void_p(stamps.data_ptr()))
+    res = []
+    for rep in range(5):
+        stamps.zero_()
+        alcop.matmul(A, B, s, out=C)
+        torch.cuda.synchronize()
+        t = stamps.view(148, 8).cpu().numpy().astype(np.int64)
+        t = t[t[:, 0] > 0]
+        t0 = t[:, 0].min()
+        res.append((t - t0) / 1000.0)
+    lib.alcop_debug_set_stamps(None)
+    names = ["start", "setup", "firstTMA", "firstFull", "lastCommit", "epiFirst", "epiDone", "end"]
+    r = np.stack(res)  # reps x ctas x 8
+    print("%s M=%d N=%d K=%d tile=128x%dx%d s=%d ctas=%d" % (s, M, N, K, tN, tK, st, r.shape[1]))
+    for i, n in enumerate(names):
+        col = r[:, :, i]
+        print("  %-10s mean %7.2f  min %7.2f  max %7.2f us" % (n, col.mean(), col.min(), col.max()))
+
+
+if __name__ == "__main__":
+    main()
