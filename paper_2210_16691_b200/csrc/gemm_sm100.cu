@@ -78,30 +78,36 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmKParams& p, int tile_i
   return t;
 }
 
+template <bool kDebug>
 __device__ __forceinline__ void stamp(const GemmKParams& p, int i) {
-  if (p.stamps == nullptr) return;
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  p.stamps[blockIdx.x * 8 + i] = t;
+  if constexpr (kDebug) {
+    if (p.stamps == nullptr) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.stamps[blockIdx.x * 8 + i] = t;
+  }
 }
 
+template <bool kDebug>
 __device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n, int kind, int buf, int tile,
                                           int slot, int chunk, int parity, int c0, int c1, int c2, int c3) {
-  if (p.trace == nullptr) return;
-  if (n < p.trace_cap) {
-    alcop_event* e = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap + n;
-    e->kind = kind;
-    e->buf = buf;
-    e->tile = tile;
-    e->slot = slot;
-    e->chunk = chunk;
-    e->parity = parity;
-    e->acquired = c0;
-    e->committed = c1;
-    e->waited = c2;
-    e->released = c3;
+  if constexpr (kDebug) {
+    if (p.trace == nullptr) return;
+    if (n < p.trace_cap) {
+      alcop_event* e = p.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * p.trace_cap + n;
+      e->kind = kind;
+      e->buf = buf;
+      e->tile = tile;
+      e->slot = slot;
+      e->chunk = chunk;
+      e->parity = parity;
+      e->acquired = c0;
+      e->committed = c1;
+      e->waited = c2;
+      e->released = c3;
+    }
+    ++n;
   }
-  ++n;
 }
 
 template <typename OutT>
@@ -117,7 +123,25 @@ __device__ __forceinline__ uint32_t pack2<__half>(uint32_t a, uint32_t b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <typename OutT, int BK>
+// One shared-memory ring of the pipeline (one pipeline group of the
+// reference, interp.hpp:87-94): slot cursor, per-slot phase bits and the
+// group counters.  Producer and consumer each keep their own copy.
+struct RingCursor {
+  uint32_t phase = 0;  // bit k = current phase parity of slot k
+  int slot = 0;
+  int count = 0;  // acquired/committed (producer) or waited (consumer)
+  int released = 0;
+  __device__ __forceinline__ void advance(int s) { slot = (slot + 1 == s) ? 0 : slot + 1; }
+};
+
+// ---------------------------------------------------------------------------
+// The kernel.  kJoint: both buffers carry the same n_stage, so one mbarrier
+// pair per slot guards the A and B copies of a chunk together (two groups
+// with identical counters — the reference's own emission when the hints are
+// equal); otherwise each buffer has its own ring and lookahead.  kDebug
+// compiles in the bookkeeping trace and the timeline stamps.
+// ---------------------------------------------------------------------------
+template <typename OutT, int BK, bool kJoint, bool kDebug>
 __global__ void __launch_bounds__(kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
@@ -139,16 +163,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                kStagingBytes);
   uint64_t* fullA = bars;
   uint64_t* emptyA = fullA + p.sA;
-  uint64_t* fullB = emptyA + p.sA;
-  uint64_t* emptyB = fullB + p.sB;
-  uint64_t* tfull = emptyB + p.sB;
+  uint64_t* fullB = kJoint ? fullA : emptyA + p.sA;
+  uint64_t* emptyB = kJoint ? emptyA : fullB + p.sB;
+  uint64_t* tfull = bars + 2 * p.sA + 2 * p.sB;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
-  if (threadIdx.x == 0) stamp(p, 0);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 0);
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -160,9 +184,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(smem_u32(&fullA[i]), 1);
         mbar_init(smem_u32(&emptyA[i]), 1);
       }
-      for (int i = 0; i < p.sB; ++i) {
-        mbar_init(smem_u32(&fullB[i]), 1);
-        mbar_init(smem_u32(&emptyB[i]), 1);
+      if (!kJoint) {
+        for (int i = 0; i < p.sB; ++i) {
+          mbar_init(smem_u32(&fullB[i]), 1);
+          mbar_init(smem_u32(&emptyB[i]), 1);
+        }
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(smem_u32(&tfull[i]), 1);
@@ -183,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // its own setup as soon as SMs free up.
   grid_dependency_wait();
   grid_launch_dependents();
-  if (threadIdx.x == 0) stamp(p, 1);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 1);
 
   const int grid = gridDim.x;
   const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
@@ -191,141 +217,173 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
 
   if (warp == 0) {
-    // ======================= producer (TMA), whole warp, one issuing lane =======================
-    uint32_t phA = 0, phB = 0;  // per-slot phase bits
-    int slotA = 0, slotB = 0;
-    int acqA = 0, acqB = 0;
-    int nev = 0;
-    int tlA = -1, tlB = -1;
-    TileCoord tcA{0, 0, 0}, tcB{0, 0, 0};
-    auto loadA = [&](int tl, int chunk) {
-      const uint32_t slot = slotA;
-      const uint32_t par = ((phA >> slot) & 1u) ^ 1u;
-      mbar_wait(smem_u32(&emptyA[slot]), par);  // producer_acquire
-      phA ^= 1u << slot;
-      ++acqA;
-      if (tl != tlA) {
-        tlA = tl;
-        tcA = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
-      }
-      if (elect_one()) {
-        const uint32_t fb = smem_u32(&fullA[slot]);
-        mbar_arrive_expect_tx(fb, p.a_stage_bytes);  // producer_commit
-        const uint32_t dst = ringA + slot * p.a_stage_bytes;
+    if (elect_one()) {
+      // ======================= producer (TMA), one thread =======================
+      RingCursor ra, rb;
+      int nev = 0;
+      TileCoord tc{0, 0, 0};
+      int tc_tile = -1;
+      const uint32_t a_bytes = p.a_stage_bytes, b_bytes = p.b_stage_bytes;
+      auto coord = [&](int tl) {
+        if (tl != tc_tile) {
+          tc_tile = tl;
+          tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
+        }
+      };
+      auto issue_a = [&](uint32_t slot, uint32_t fb, int chunk) {
 #pragma unroll
         for (int a = 0; a < kKAtoms; ++a)
-          tma_load_3d(dst + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK, tcA.mb * kTileM, tcA.b);
-        log_event(p, 0, nev, 0, 0, tl, slot, chunk, par, acqA, acqA, -1, -1);
-        if (acqA == 1) stamp(p, 2);
-      }
-      __syncwarp();
-      slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
-    };
-    auto loadB = [&](int tl, int chunk) {
-      const uint32_t slot = slotB;
-      const uint32_t par = ((phB >> slot) & 1u) ^ 1u;
-      mbar_wait(smem_u32(&emptyB[slot]), par);
-      phB ^= 1u << slot;
-      ++acqB;
-      if (tl != tlB) {
-        tlB = tl;
-        tcB = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
-      }
-      if (elect_one()) {
-        const uint32_t fb = smem_u32(&fullB[slot]);
-        mbar_arrive_expect_tx(fb, p.b_stage_bytes);
-        const uint32_t dst = ringB + slot * p.b_stage_bytes;
+          tma_load_3d(ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK,
+                      tc.mb * kTileM, tc.b);
+      };
+      auto issue_b = [&](uint32_t slot, uint32_t fb, int chunk) {
+        const uint32_t dst = ringB + slot * b_bytes;
         if (p.b_mn_major) {
           // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
-          const int atoms = p.BN >> 6;
-          for (int a = 0; a < atoms; ++a)
-            tma_load_3d(dst + a * (BK * 128), &tmB, fb, tcB.nb * p.BN + a * 64, chunk * BK, tcB.b);
+          for (int a = 0; a < (p.BN >> 6); ++a)
+            tma_load_3d(dst + a * (BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * BK, tc.b);
         } else {
           // B[N,K] row-major: K-major like A with BN rows
 #pragma unroll
           for (int a = 0; a < kKAtoms; ++a)
-            tma_load_3d(dst + a * (p.BN * 128), &tmB, fb, chunk * BK + a * kBoxK, tcB.nb * p.BN, tcB.b);
+            tma_load_3d(dst + a * (p.BN * 128), &tmB, fb, chunk * BK + a * kBoxK, tc.nb * p.BN, tc.b);
         }
-        log_event(p, 0, nev, 0, 1, tl, slot, chunk, par, acqB, acqB, -1, -1);
-      }
-      __syncwarp();
-      slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
-    };
+      };
+      // producer_acquire + producer_commit of one buffer's chunk
+      auto load = [&](RingCursor& r, int s, uint64_t* full, uint64_t* empty, int buf, int tl, int chunk) {
+        const uint32_t slot = r.slot;
+        const uint32_t par = ((r.phase >> slot) & 1u) ^ 1u;
+        mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire
+        r.phase ^= 1u << slot;
+        ++r.count;
+        coord(tl);
+        const uint32_t fb = smem_u32(&full[slot]);
+        if (buf == 0) {
+          mbar_arrive_expect_tx(fb, a_bytes);  // producer_commit
+          issue_a(slot, fb, chunk);
+        } else {
+          mbar_arrive_expect_tx(fb, b_bytes);
+          issue_b(slot, fb, chunk);
+        }
+        log_event<kDebug>(p, 0, nev, 0, buf, tl, slot, chunk, par, r.count, r.count, -1, -1);
+        r.advance(s);
+      };
+      // joint ring: both buffers' copies of a chunk under one barrier pair
+      auto load_joint = [&](int tl, int chunk) {
+        const uint32_t slot = ra.slot;
+        const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
+        mbar_wait(smem_u32(&emptyA[slot]), par);
+        ra.phase ^= 1u << slot;
+        ++ra.count;
+        coord(tl);
+        const uint32_t fb = smem_u32(&fullA[slot]);
+        mbar_arrive_expect_tx(fb, a_bytes + b_bytes);
+        issue_a(slot, fb, chunk);
+        issue_b(slot, fb, chunk);
+        log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
+        log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
+        ra.advance(p.sA);
+      };
 
-    if (wrap) {
-      // reference-faithful: per tile, prologue chunks 0..s-2 into slots 0..s-2
-      // (pipeline_pass.hpp:647-656), then steady loads of chunk (v+s-1)%E
-      // (pipeline_pass.hpp:501-509); the s-1 tail loads wrap to chunks 0..
-      for (int tl = 0; tl < my_tiles; ++tl) {
-        slotA = 0;
-        slotB = 0;
-        for (int i = 0; i < p.sA - 1; ++i) loadA(tl, i % E);
-        for (int i = 0; i < p.sB - 1; ++i) loadB(tl, i % E);
-        int ca = (p.sA - 1) % E, cb = (p.sB - 1) % E;
-        for (int v = 0; v < E; ++v) {
-          loadA(tl, ca);
-          loadB(tl, cb);
-          ca = (ca + 1 == E) ? 0 : ca + 1;
-          cb = (cb + 1 == E) ? 0 : cb + 1;
+      if (wrap) {
+        // reference-faithful: per tile, prologue chunks 0..s-2 into slots 0..s-2
+        // (pipeline_pass.hpp:647-656), then steady loads of chunk (v+s-1)%E
+        // (pipeline_pass.hpp:501-509); the s-1 tail loads wrap to chunks 0..
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          ra.slot = 0;
+          rb.slot = 0;
+          if constexpr (kJoint) {
+            int c = 0;
+            for (int i = 0; i < E + p.sA - 1; ++i) {
+              load_joint(tl, c);
+              c = (c + 1 == E) ? 0 : c + 1;
+            }
+          } else {
+            for (int i = 0; i < p.sA - 1; ++i) load(ra, p.sA, fullA, emptyA, 0, tl, i % E);
+            for (int i = 0; i < p.sB - 1; ++i) load(rb, p.sB, fullB, emptyB, 1, tl, i % E);
+            int ca = (p.sA - 1) % E, cb = (p.sB - 1) % E;
+            for (int v = 0; v < E; ++v) {
+              load(ra, p.sA, fullA, emptyA, 0, tl, ca);
+              load(rb, p.sB, fullB, emptyB, 1, tl, cb);
+              ca = (ca + 1 == E) ? 0 : ca + 1;
+              cb = (cb + 1 == E) ? 0 : cb + 1;
+            }
+          }
+        }
+      } else {
+        // fused: one lookahead window over the flattened (tile, chunk) stream;
+        // issuing in order is enough, the empty barriers enforce the lookahead
+        if constexpr (kJoint) {
+          for (int tl = 0; tl < my_tiles; ++tl)
+            for (int c = 0; c < E; ++c) load_joint(tl, c);
+        } else {
+          const int total = my_tiles * E;
+          int ta = 0, ca = 0, tb = 0, cb = 0;  // (tile, chunk) of the next A / B load
+          auto nextA = [&] { if (++ca == E) { ca = 0; ++ta; } };
+          auto nextB = [&] { if (++cb == E) { cb = 0; ++tb; } };
+          for (int i = 0; i < p.sA - 1 && i < total; ++i) { load(ra, p.sA, fullA, emptyA, 0, ta, ca); nextA(); }
+          for (int i = 0; i < p.sB - 1 && i < total; ++i) { load(rb, p.sB, fullB, emptyB, 1, tb, cb); nextB(); }
+          for (int v = 0; v < total; ++v) {
+            if (v + p.sA - 1 < total) { load(ra, p.sA, fullA, emptyA, 0, ta, ca); nextA(); }
+            if (v + p.sB - 1 < total) { load(rb, p.sB, fullB, emptyB, 1, tb, cb); nextB(); }
+          }
         }
       }
-    } else {
-      // fused: one lookahead window over the flattened (tile, chunk) stream
-      const int total = my_tiles * E;
-      int ta = 0, ca = 0, tb = 0, cb = 0;  // (tile, chunk) of the next A / B load
-      auto nextA = [&] { if (++ca == E) { ca = 0; ++ta; } };
-      auto nextB = [&] { if (++cb == E) { cb = 0; ++tb; } };
-      for (int i = 0; i < p.sA - 1 && i < total; ++i) { loadA(ta, ca); nextA(); }
-      for (int i = 0; i < p.sB - 1 && i < total; ++i) { loadB(tb, cb); nextB(); }
-      for (int v = 0; v < total; ++v) {
-        if (v + p.sA - 1 < total) { loadA(ta, ca); nextA(); }
-        if (v + p.sB - 1 < total) { loadB(tb, cb); nextB(); }
-      }
+      if (kDebug && ra.count == 1) stamp<kDebug>(p, 2);
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // ======================= MMA issuer, whole warp, one issuing lane =======================
-    uint32_t phA = 0, phB = 0;
-    int slotA = 0, slotB = 0;
-    int waitA = 0, relA = 0, waitB = 0, relB = 0;
-    int nev = 0;
-    // descriptor bases (start address advances in 16-byte units in the low word)
-    const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
-    uint64_t bdesc0;
-    uint32_t b_big, b_small;  // B k-step advance: (u>>2)*b_big + (u&3)*b_small, in 16 B units
-    if (p.b_mn_major) {
-      bdesc0 = make_smem_desc(ringB, BK * 128, 1024, kLayoutSW128);
-      b_small = 2048 / 16;
-      b_big = 4 * b_small;
-    } else {
-      bdesc0 = make_smem_desc(ringB, 16, kKSbo, kKLayout);
-      b_small = 2;
-      b_big = static_cast<uint32_t>(p.BN) * 128 / 16;
-    }
-    const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      const int acc = tl % p.tacc;
-      const uint32_t acc_par = ((tl / p.tacc) & 1) ^ 1;
-      mbar_wait(smem_u32(&tempty[acc]), acc_par);  // accumulator drained by the epilogue
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
-      if (wrap) {
-        slotA = 0;
-        slotB = 0;
+    if (elect_one()) {
+      // ======================= MMA issuer, one thread =======================
+      RingCursor ca, cb;
+      int nev = 0;
+      // descriptor bases (start address advances in 16-byte units in the low word)
+      const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
+      uint64_t bdesc0;
+      uint32_t b_big, b_small;  // B k-step advance: (u>>2)*b_big + (u&3)*b_small, in 16 B units
+      if (p.b_mn_major) {
+        bdesc0 = make_smem_desc(ringB, BK * 128, 1024, kLayoutSW128);
+        b_small = 2048 / 16;
+        b_big = 4 * b_small;
+      } else {
+        bdesc0 = make_smem_desc(ringB, 16, kKSbo, kKLayout);
+        b_small = 2;
+        b_big = static_cast<uint32_t>(p.BN) * 128 / 16;
       }
-      for (int v = 0; v < E; ++v) {
-        const uint32_t sa = slotA, sb = slotB;
-        const uint32_t pa = (phA >> sa) & 1u, pb = (phB >> sb) & 1u;
-        mbar_wait(smem_u32(&fullA[sa]), pa);  // consumer_wait A
-        mbar_wait(smem_u32(&fullB[sb]), pb);  // consumer_wait B
-        phA ^= 1u << sa;
-        phB ^= 1u << sb;
-        ++waitA;
-        ++waitB;
+      const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
+      const uint32_t idesc = p.idesc;
+      // consumer_wait of one buffer
+      auto cwait = [&](RingCursor& r, uint64_t* full, int buf, int tl, int chunk) -> uint32_t {
+        const uint32_t slot = r.slot, par = (r.phase >> slot) & 1u;
+        mbar_wait(smem_u32(&full[slot]), par);
+        r.phase ^= 1u << slot;
+        ++r.count;
+        log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released);
+        return par;
+      };
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int acc = tl % p.tacc;
+        const uint32_t acc_par = ((tl / p.tacc) & 1) ^ 1;
+        mbar_wait(smem_u32(&tempty[acc]), acc_par);  // accumulator drained by the epilogue
         tc_fence_after();
-        if (elect_one()) {
-          if (waitA == 1) stamp(p, 3);
-          log_event(p, 1, nev, 1, 0, tl, sa, v, pa, -1, -1, waitA, relA);
-          log_event(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, waitB, relB);
+        const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
+        if (wrap) {
+          ca.slot = 0;
+          cb.slot = 0;
+        }
+        for (int v = 0; v < E; ++v) {
+          const uint32_t sa = ca.slot, sb = kJoint ? ca.slot : cb.slot;
+          uint32_t pa, pb;
+          if constexpr (kJoint) {
+            pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A (+B: same barrier)
+            pb = pa;
+            ++cb.count;
+            log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released);
+          } else {
+            pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A
+            pb = cwait(cb, fullB, 1, tl, v);  // consumer_wait B
+          }
+          tc_fence_after();
           const uint64_t ad = adesc0 + sa * a_stage16;
           const uint64_t bd = bdesc0 + sb * b_stage16;
 #pragma unroll
@@ -333,57 +391,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             // inner level: k-step u of chunk v reads slot v%s at k offset 16u
             const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
             const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-            umma_f16_ss(d_tmem, ad + a_off, bd + b_off, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
+            umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
           }
           umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
-          umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
-          log_event(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, waitA, relA + 1);
-          log_event(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, waitB, relB + 1);
+          if (!kJoint) umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
+          ++ca.released;
+          ++cb.released;
+          log_event<kDebug>(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, ca.count, ca.released);
+          log_event<kDebug>(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released);
+          ca.advance(p.sA);
+          if (!kJoint) cb.advance(p.sB);
         }
-        __syncwarp();
-        ++relA;
-        ++relB;
-        slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
-        slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
-      }
-      if (elect_one()) {
         umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
-        if (tl == my_tiles - 1) stamp(p, 4);
-      }
-      __syncwarp();
-      if (wrap) {
-        // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
-        // groups of each buffer, A's then B's, without MMA.
-        for (int d = 0; d < p.sA - 1; ++d) {
-          const uint32_t sa = slotA, pa = (phA >> sa) & 1u;
-          mbar_wait(smem_u32(&fullA[sa]), pa);
-          phA ^= 1u << sa;
-          ++waitA;
-          if (elect_one()) {
-            log_event(p, 1, nev, 1, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA);
-            mbar_arrive(smem_u32(&emptyA[sa]));
-            log_event(p, 1, nev, 2, 0, tl, sa, (E + d) % E, pa, -1, -1, waitA, relA + 1);
+        if (tl == my_tiles - 1) stamp<kDebug>(p, 4);
+        if (wrap) {
+          // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
+          // groups of each buffer, A's then B's, without MMA.
+          auto drain = [&](RingCursor& r, int s, uint64_t* full, uint64_t* empty, int buf) {
+            for (int d = 0; d < s - 1; ++d) {
+              const uint32_t slot = r.slot;
+              const uint32_t par = cwait(r, full, buf, tl, (E + d) % E);
+              mbar_arrive(smem_u32(&empty[slot]));
+              ++r.released;
+              log_event<kDebug>(p, 1, nev, 2, buf, tl, slot, (E + d) % E, par, -1, -1, r.count, r.released);
+              r.advance(s);
+            }
+          };
+          if constexpr (kJoint) {
+            for (int d = 0; d < p.sA - 1; ++d) {
+              const uint32_t slot = ca.slot;
+              const uint32_t par = cwait(ca, fullA, 0, tl, (E + d) % E);
+              ++cb.count;
+              log_event<kDebug>(p, 1, nev, 1, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released);
+              mbar_arrive(smem_u32(&emptyA[slot]));
+              ++ca.released;
+              ++cb.released;
+              log_event<kDebug>(p, 1, nev, 2, 0, tl, slot, (E + d) % E, par, -1, -1, ca.count, ca.released);
+              log_event<kDebug>(p, 1, nev, 2, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released);
+              ca.advance(p.sA);
+            }
+          } else {
+            drain(ca, p.sA, fullA, emptyA, 0);
+            drain(cb, p.sB, fullB, emptyB, 1);
           }
-          __syncwarp();
-          ++relA;
-          slotA = (slotA + 1 == p.sA) ? 0 : slotA + 1;
-        }
-        for (int d = 0; d < p.sB - 1; ++d) {
-          const uint32_t sb = slotB, pb = (phB >> sb) & 1u;
-          mbar_wait(smem_u32(&fullB[sb]), pb);
-          phB ^= 1u << sb;
-          ++waitB;
-          if (elect_one()) {
-            log_event(p, 1, nev, 1, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB);
-            mbar_arrive(smem_u32(&emptyB[sb]));
-            log_event(p, 1, nev, 2, 1, tl, sb, (E + d) % E, pb, -1, -1, waitB, relB + 1);
-          }
-          __syncwarp();
-          ++relB;
-          slotB = (slotB + 1 == p.sB) ? 0 : slotB + 1;
         }
       }
     }
+    __syncwarp();
   } else {
     // ======================= epilogue (warps 2-5) =======================
     // TMEM -> registers (tcgen05.ld) -> 128B-swizzled smem staging -> TMA
@@ -398,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
       tc_fence_after();
-      if (tl == 0 && warp == 2 && lane == 0) stamp(p, 5);
+      if (tl == 0 && warp == 2 && lane == 0) stamp<kDebug>(p, 5);
       const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c) {
@@ -441,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) bulk_wait_group<0>();
     __syncwarp();
-    if (warp == 2 && lane == 0) stamp(p, 6);
+    if (warp == 2 && lane == 0) stamp<kDebug>(p, 6);
   }
 
   tc_fence_before();
@@ -450,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
-  if (threadIdx.x == 0) stamp(p, 7);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 7);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
@@ -483,10 +537,10 @@ int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint6
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK>
+template <typename OutT, int BK, bool kJoint, bool kDebug>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                  int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_kernel<OutT, BK>;
+  auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -503,6 +557,19 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
+}
+
+template <typename OutT, int BK>
+int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
+                   int grid, int smem, cudaStream_t st) {
+  const bool joint = kp.sA == kp.sB;
+  const bool debug = kp.trace != nullptr || kp.stamps != nullptr;
+  if (joint) {
+    return debug ? launch_typed<OutT, BK, true, true>(ta, tb, tc, kp, grid, smem, st)
+                 : launch_typed<OutT, BK, true, false>(ta, tb, tc, kp, grid, smem, st);
+  }
+  return debug ? launch_typed<OutT, BK, false, true>(ta, tb, tc, kp, grid, smem, st)
+               : launch_typed<OutT, BK, false, false>(ta, tb, tc, kp, grid, smem, st);
 }
 
 }  // namespace
@@ -587,15 +654,15 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
-    case ALCOP_F32 * 4 + 0: return launch_typed<float, 32>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 1: return launch_typed<float, 64>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 2: return launch_typed<float, 128>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 0: return launch_typed<__nv_bfloat16, 32>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 1: return launch_typed<__nv_bfloat16, 64>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 2: return launch_typed<__nv_bfloat16, 128>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 0: return launch_typed<__half, 32>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 1: return launch_typed<__half, 64>(ta, tb, tc, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 2: return launch_typed<__half, 128>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 0: return launch_variant<float, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 1: return launch_variant<float, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 2: return launch_variant<float, 128>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 0: return launch_variant<__nv_bfloat16, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 1: return launch_variant<__nv_bfloat16, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16 * 4 + 2: return launch_variant<__nv_bfloat16, 128>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 0: return launch_variant<__half, 32>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 1: return launch_variant<__half, 64>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16 * 4 + 2: return launch_variant<__half, 128>(ta, tb, tc, kp, grid, smem, st);
   }
   return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
 }
