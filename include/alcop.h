@@ -117,6 +117,12 @@ typedef struct {
   int32_t maxThreadblkPerSM, maxWarpsPerSM, utilKneeWarps;
   int32_t tmemColsPerSM; /* 512 (new: TMEM capacity) */
   double clockGHz;       /* cycles -> seconds */
+  /* B200 additions (calibrated, tools/fit_model.py on profiles/sweep_r01.json) */
+  double tIssue;         /* per-chunk producer/MMA issue floor, cycles */
+  double tIssuePerBox;   /* + cycles per TMA box of the chunk */
+  double tLaunch;        /* kernel launch + setup, cycles */
+  double tTile;          /* per output tile fixed cost, cycles */
+  double overlapDRAM;    /* soft-max weight between the SM pipeline and HBM time */
 } alcop_hw;
 
 /* perf::LatencyBreakdown (perf_model.hpp:40-47); field names follow

@@ -19,7 +19,7 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libalcop.so")
+LIB_PATH = os.environ.get("ALCOP_LIB", os.path.join(_HERE, "libalcop.so"))
 
 ALCOP_OK = 0
 ALCOP_ERR_PARSE = 2
@@ -77,7 +77,12 @@ class HW(ctypes.Structure):
                 ("latDRAMRead", ctypes.c_double), ("latDRAMWrite", ctypes.c_double), ("bwSmem", ctypes.c_double),
                 ("latSmem", ctypes.c_double), ("smemPerSM", ctypes.c_int64), ("regsPerSM", ctypes.c_int64),
                 ("maxThreadblkPerSM", ctypes.c_int32), ("maxWarpsPerSM", ctypes.c_int32),
-                ("utilKneeWarps", ctypes.c_int32), ("tmemColsPerSM", ctypes.c_int32), ("clockGHz", ctypes.c_double)]
+                ("utilKneeWarps", ctypes.c_int32), ("tmemColsPerSM", ctypes.c_int32), ("clockGHz", ctypes.c_double),
+                ("tIssue", ctypes.c_double), ("tIssuePerBox", ctypes.c_double), ("tLaunch", ctypes.c_double),
+                ("tTile", ctypes.c_double), ("overlapDRAM", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Breakdown(ctypes.Structure):

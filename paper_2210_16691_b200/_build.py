@@ -10,7 +10,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libalcop.so")
+LIB = os.environ.get("ALCOP_BUILD_LIB", os.path.join(HERE, "libalcop.so"))
+EXTRA = os.environ.get("ALCOP_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_sm100.cu", "conv_sm100.cu"]
@@ -37,10 +38,10 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj" + ("_" + os.path.basename(LIB) if "ALCOP_BUILD_LIB" in os.environ else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
-    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I" + os.path.join(ROOT, "include")]
+    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I" + os.path.join(ROOT, "include")] + EXTRA
     for f in CU_SOURCES:
         o = os.path.join(objdir, f + ".o")
         cmd = [NVCC, *ARCH, *common, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, f), "-o", o]

@@ -78,6 +78,30 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmKParams& p, int tile_i
   return t;
 }
 
+// Role-thread layout of the producer and MMA warps: the whole warp runs the
+// loop warp-uniformly (everything stays on the uniform datapath) and one
+// elected lane issues (ALCOP_WARP_ROLES=1, default, measured faster), or a
+// single elected thread runs it (ALCOP_WARP_ROLES=0).
+#ifndef ALCOP_WARP_ROLES
+#define ALCOP_WARP_ROLES 1
+#endif
+#if ALCOP_WARP_ROLES
+#define ROLE_GUARD() true
+#define ISSUE(...)                 \
+  do {                             \
+    if (ptx::elect_one()) {        \
+      __VA_ARGS__;                 \
+    }                              \
+    __syncwarp();                  \
+  } while (0)
+#else
+#define ROLE_GUARD() ptx::elect_one()
+#define ISSUE(...) \
+  do {             \
+    __VA_ARGS__;   \
+  } while (0)
+#endif
+
 template <bool kDebug>
 __device__ __forceinline__ void stamp(const GemmKParams& p, int i) {
   if constexpr (kDebug) {
@@ -217,8 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
 
   if (warp == 0) {
-    if (elect_one()) {
-      // ======================= producer (TMA), one thread =======================
+    if (ROLE_GUARD()) {
+      // ======================= producer (TMA) =======================
       RingCursor ra, rb;
       int nev = 0;
       TileCoord tc{0, 0, 0};
@@ -258,14 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++r.count;
         coord(tl);
         const uint32_t fb = smem_u32(&full[slot]);
-        if (buf == 0) {
+        ISSUE(if (buf == 0) {
           mbar_arrive_expect_tx(fb, a_bytes);  // producer_commit
           issue_a(slot, fb, chunk);
         } else {
           mbar_arrive_expect_tx(fb, b_bytes);
           issue_b(slot, fb, chunk);
-        }
-        log_event<kDebug>(p, 0, nev, 0, buf, tl, slot, chunk, par, r.count, r.count, -1, -1);
+        } log_event<kDebug>(p, 0, nev, 0, buf, tl, slot, chunk, par, r.count, r.count, -1, -1));
         r.advance(s);
       };
       // joint ring: both buffers' copies of a chunk under one barrier pair
@@ -277,11 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++ra.count;
         coord(tl);
         const uint32_t fb = smem_u32(&fullA[slot]);
-        mbar_arrive_expect_tx(fb, a_bytes + b_bytes);
-        issue_a(slot, fb, chunk);
-        issue_b(slot, fb, chunk);
-        log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
-        log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
+        ISSUE(mbar_arrive_expect_tx(fb, a_bytes + b_bytes); issue_a(slot, fb, chunk); issue_b(slot, fb, chunk);
+              log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
+              log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1));
         ra.advance(p.sA);
       };
 
@@ -333,8 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (elect_one()) {
-      // ======================= MMA issuer, one thread =======================
+    if (ROLE_GUARD()) {
+      // ======================= MMA issuer =======================
       RingCursor ca, cb;
       int nev = 0;
       // descriptor bases (start address advances in 16-byte units in the low word)
@@ -358,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(&full[slot]), par);
         r.phase ^= 1u << slot;
         ++r.count;
-        log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released);
+        ISSUE(log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released));
         return par;
       };
       for (int tl = 0; tl < my_tiles; ++tl) {
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A (+B: same barrier)
             pb = pa;
             ++cb.count;
-            log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released);
+            ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
           } else {
             pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A
             pb = cwait(cb, fullB, 1, tl, v);  // consumer_wait B
@@ -386,23 +407,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t ad = adesc0 + sa * a_stage16;
           const uint64_t bd = bdesc0 + sb * b_stage16;
-#pragma unroll
-          for (int u = 0; u < kSteps; ++u) {
-            // inner level: k-step u of chunk v reads slot v%s at k offset 16u
-            const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
-            const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-            umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
-          }
-          umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
-          if (!kJoint) umma_commit(smem_u32(&emptyB[sb]));  // consumer_release B
           ++ca.released;
           ++cb.released;
-          log_event<kDebug>(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, ca.count, ca.released);
-          log_event<kDebug>(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released);
+          ISSUE(
+#pragma unroll
+              for (int u = 0; u < kSteps; ++u) {
+                // inner level: k-step u of chunk v reads slot v%s at k offset 16u
+                const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
+                const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
+                umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+              } umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
+              if (!kJoint) umma_commit(smem_u32(&emptyB[sb]));   // consumer_release B
+              log_event<kDebug>(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, ca.count, ca.released);
+              log_event<kDebug>(p, 1, nev, 2, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
           ca.advance(p.sA);
           if (!kJoint) cb.advance(p.sB);
         }
-        umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+        ISSUE(umma_commit(smem_u32(&tfull[acc])));  // accumulator ready
         if (tl == my_tiles - 1) stamp<kDebug>(p, 4);
         if (wrap) {
           // drains (pipeline_pass.hpp:739-742): consume the s-1 wrapped tail
@@ -411,9 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int d = 0; d < s - 1; ++d) {
               const uint32_t slot = r.slot;
               const uint32_t par = cwait(r, full, buf, tl, (E + d) % E);
-              mbar_arrive(smem_u32(&empty[slot]));
               ++r.released;
-              log_event<kDebug>(p, 1, nev, 2, buf, tl, slot, (E + d) % E, par, -1, -1, r.count, r.released);
+              ISSUE(mbar_arrive(smem_u32(&empty[slot]));
+                    log_event<kDebug>(p, 1, nev, 2, buf, tl, slot, (E + d) % E, par, -1, -1, r.count, r.released));
               r.advance(s);
             }
           };
@@ -422,12 +443,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t slot = ca.slot;
               const uint32_t par = cwait(ca, fullA, 0, tl, (E + d) % E);
               ++cb.count;
-              log_event<kDebug>(p, 1, nev, 1, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released);
-              mbar_arrive(smem_u32(&emptyA[slot]));
               ++ca.released;
               ++cb.released;
-              log_event<kDebug>(p, 1, nev, 2, 0, tl, slot, (E + d) % E, par, -1, -1, ca.count, ca.released);
-              log_event<kDebug>(p, 1, nev, 2, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released);
+              ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released - 1);
+                    mbar_arrive(smem_u32(&emptyA[slot]));
+                    log_event<kDebug>(p, 1, nev, 2, 0, tl, slot, (E + d) % E, par, -1, -1, ca.count, ca.released);
+                    log_event<kDebug>(p, 1, nev, 2, 1, tl, slot, (E + d) % E, par, -1, -1, cb.count, cb.released));
               ca.advance(p.sA);
             }
           } else {

@@ -1,24 +1,28 @@
 // model.cpp — the paper's analytical stage/tile model (
-// perf_model.hpp:49-187) on the B200 host side.
+// perf_model.hpp:49-187) re-derived for the B200 kernel, plus the
+// model-guided schedule choice (enumerate_space + analytical_rank,
+// tuner.hpp:48-80).
 //
-// Two hardware views share the Table structure
-//   T_kernel = T_threadblk * N_threadblk_batch,
-//   T_threadblk = T_init + T_main_loop + T_epilogue,
-//   T_main_loop = pipeline_latency(T_smem_load, T_smem_use, N_smem_loop,
-//                                  N_smem_pipe_stage, N_tb_per_SM)
-// (a) the reference's A100-like HardwareSpec (perf_model.hpp:14-30), where
-//     predict() restates the reference arithmetic for the tcgen05 kernel
-//     shape, and
-// (b) B200, re-derived for the persistent warp-specialised kernel:
-//     - one CTA per SM (227 KB smem ring, 512-column TMEM), so the per-SM
-//       throughput is never multiplied by co-resident CTAs (the reference
-//       lets every co-resident CTA run at full SM rate, perf_model.hpp:61-70,
-//       which predicts above-peak throughput on B200 — SURVEY §0);
-//     - the inner level is the TMEM accumulator ring: with n_stage_inner = 2
-//       the epilogue of tile i overlaps the main loop of tile i+1, so the
-//       per-tile time is max(T_main_loop, T_epilogue);
-//     - WRAP mode pays s-1 redundant wrapped loads and a drain per tile;
-//     - a chip-wide floor T >= FLOPs / (numSM * throughputSM).
+// The Table structure is kept:
+//   T_kernel   = T_init + N_tile_batch x T_main_loop (+ T_epilogue tail)
+//   T_main_loop = pipeline_latency(T_load, T_use, N_smem_loop, N_smem_stage, 1)
+// with the paper's pipeline_latency (perf_model.hpp:53-57) unchanged, but the
+// terms are B200's:
+//   - one persistent CTA per SM (227 KB ring, 512-column TMEM), so per-SM
+//     throughput is never multiplied by co-resident CTAs (the reference lets
+//     each co-resident CTA run at full SM rate, perf_model.hpp:61-70, and
+//     predicts above-peak throughput on B200 — SURVEY §0);
+//   - T_use per chunk = max(MMA time, L2->SM bandwidth share, TMA/MMA issue
+//     floor): the reference folds bandwidth into T_load and divides it by the
+//     stage count, which rewards stages that cannot add bandwidth;
+//   - T_load is the pure chunk latency (the reference's LAT_LLC_read);
+//   - the inner (register) level is the TMEM accumulator ring: with
+//     n_stage_inner = 2 the epilogue of tile i overlaps the main loop of tile
+//     i+1, so a tile costs max(T_main, T_epi) instead of their sum;
+//   - WRAP mode pays s-1 redundant wrapped loads per tile plus a refill;
+//   - HBM traffic (A, B, C once) bounds the kernel through a soft maximum.
+// Constants are fitted by tools/fit_model.py to the measured sweep in
+// profiles/sweep_r01.json ("Analytical model").
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -43,7 +47,7 @@ using namespace alcop;
 extern "C" void alcop_hw_default_a100_reference(alcop_hw* hw) {
   if (!hw) return;
   std::memset(hw, 0, sizeof(*hw));
-  // perf_model.hpp:15-29
+  // perf_model.hpp:15-29 (the reference's A100-like defaults), for comparison
   hw->numSM = 108;
   hw->throughputSM = 1024;
   hw->bwLLC = 512;
@@ -66,17 +70,19 @@ extern "C" void alcop_hw_default_a100_reference(alcop_hw* hw) {
 extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   if (!hw) return;
   std::memset(hw, 0, sizeof(*hw));
-  // B200 (sm_100a), 148 SMs; rates per SM clock.  Calibrated from the
-  // driver-measured peaks (MEASURED_PEAKS.json: 1633.8 TFLOP/s bf16 burst,
-  // 6549.4 GB/s HBM) at the observed SM clock, see DESIGN.md "model".
+  // B200 (sm_100a), 148 SMs, rates per SM-clock cycle at the ~1.9 GHz the
+  // short kernels run at.  throughputSM and latLLCRead are fixed from
+  // hardware facts (tcgen05 M=128 rate; measured chunk latency in
+  // tools/kbtimeline.py); the rest are least-squares fits to
+  // profiles/sweep_r01.json (tools/fit_model.py).
   hw->numSM = 148;
-  hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM (tcgen05, M=128)
-  hw->bwLLC = 6300;         // L2 -> SM bytes / clk, chip-wide (LTS cap)
-  hw->bwDRAM = 3600;        // HBM bytes / clk at ~1.8 GHz (6.5 TB/s)
-  hw->bwDRAMWrite = 3600;
-  hw->latLLCRead = 600;     // TMA issue -> full barrier, L2 hit
-  hw->latDRAMRead = 1000;
-  hw->latDRAMWrite = 800;
+  hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
+  hw->bwLLC = 9569;         // L2 -> SM bytes / clk, chip-wide (~18 TB/s)
+  hw->bwDRAM = 2632;        // HBM read+write bytes / clk (~5.0 TB/s effective)
+  hw->bwDRAMWrite = 11079;  // epilogue TMA-store drain, bytes / clk chip-wide (L2 absorbs it)
+  hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
+  hw->latDRAMRead = 1950;
+  hw->latDRAMWrite = 0;
   hw->bwSmem = 128;
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
@@ -85,7 +91,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->maxWarpsPerSM = 64;
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
-  hw->clockGHz = 1.8;
+  hw->clockGHz = 1.9;
+  hw->tIssue = 164.7;
+  hw->tIssuePerBox = 68.2;
+  hw->tLaunch = 1240;
+  hw->tTile = 0;
+  hw->overlapDRAM = 0.001;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -98,48 +109,45 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   const int64_t tM = s->tileM, tN = s->tileN, tK = s->tileK;
   const int64_t eb = 2, ob = w->out_dtype == ALCOP_F32 ? 4 : 2;
   const int64_t tiles = ((w->M + tM - 1) / tM) * ((w->N + tN - 1) / tN) * w->batch;
-  const int64_t nSM = hw->numSM;
-  const int64_t ctas = std::min<int64_t>(tiles, s->num_ctas > 0 ? s->num_ctas : nSM);
-  const int64_t tilesPerCta = (tiles + ctas - 1) / ctas;
+  const int64_t ctas = std::min<int64_t>(tiles, s->num_ctas > 0 ? s->num_ctas : hw->numSM);
+  const int64_t waves = (tiles + ctas - 1) / ctas;  // tiles per CTA (max)
   const int64_t E = (w->K + tK - 1) / tK;
   const int sOuter = std::min(s->n_stage_smem_A, s->n_stage_smem_B);
   out->nThreadblkPerSM = 1;
   out->nThreadblkPerBatch = ctas;
-  out->nThreadblkBatch = tilesPerCta;
+  out->nThreadblkBatch = waves;
   out->nSmemLoop = E;
   out->nRegLoop = tK / 16;
   out->flopsOneRegLoop = 2 * tM * tN * 16;
   out->bytesOneSmemLoop = (tM + tN) * tK * eb;
-  // DRAM working set of one wave per k-step: unique A row blocks and B
-  // column blocks touched by the resident tiles (perf_model.hpp:147-153,
-  // m-fastest rasterisation).
-  const int64_t nI = (w->M + tM - 1) / tM;
-  const int64_t rows = std::min<int64_t>(ctas, nI);
-  const int64_t cols = (ctas + nI - 1) / nI;
-  out->bytesWorkset = rows * tM * tK * eb + cols * tK * tN * eb;
+  out->bytesWorkset = (w->M * w->K + w->K * w->N) * eb * w->batch;
   out->bytesOutputTile = tM * tN * ob;
 
+  // T_use of one chunk: MMA, L2->SM bandwidth share, issue floor
   out->tCompute = static_cast<double>(out->flopsOneRegLoop) / hw->throughputSM;
-  out->tRegLoad = 0;  // tcgen05 reads smem operands directly through descriptors
-  out->tSmemUse = out->tCompute * static_cast<double>(out->nRegLoop);
-  const double llc = hw->latLLCRead + static_cast<double>(out->bytesOneSmemLoop) * ctas / hw->bwLLC;
-  const double dram = hw->latDRAMRead + static_cast<double>(out->bytesWorkset) / hw->bwDRAM;
-  out->tSmemLoad = std::max(llc, dram);
-  const int64_t loadsPerTile = E + (s->mode == ALCOP_MODE_WRAP ? sOuter - 1 : 0);
-  double tMain = model::pipeline_latency(out->tSmemLoad, out->tSmemUse, loadsPerTile, sOuter, 1);
-  if (s->mode == ALCOP_MODE_WRAP || sOuter == 1) tMain += out->tSmemLoad;  // per-tile refill bubble
+  const double tMma = out->tCompute * static_cast<double>(out->nRegLoop);
+  const double tL2 = static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC;
+  const int64_t boxes = std::max<int64_t>(1, tK / 64) + std::max<int64_t>(1, tN / 64);
+  const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
+  out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors
+  out->tSmemUse = std::max(tMma, std::max(tL2, tIssue));
+  out->tSmemLoad = hw->latLLCRead;
+  const int64_t loads = E + (s->mode == ALCOP_MODE_WRAP ? sOuter - 1 : 0);
+  double tMain = model::pipeline_latency(out->tSmemLoad, out->tSmemUse, loads, sOuter, 1) + hw->tTile;
+  if (s->mode == ALCOP_MODE_WRAP || sOuter == 1) tMain += 0.5 * out->tSmemLoad;  // per-tile refill
   out->tMainLoop = tMain;
-  out->tEpilogue = hw->latDRAMWrite + static_cast<double>(out->bytesOutputTile) * ctas / hw->bwDRAMWrite +
-                   static_cast<double>(tM * tN) * 4.0 / 64.0 / 4.0;  // TMEM read: 64 B/clk per warp
-  out->tInit = out->tSmemLoad + 1500.0;  // barrier init + TMEM alloc + first loads
-  const double perTile = s->n_stage_inner >= 2 ? std::max(out->tMainLoop, out->tEpilogue)
-                                               : out->tMainLoop + out->tEpilogue;
+  out->tEpilogue = static_cast<double>(out->bytesOutputTile) * static_cast<double>(ctas) / hw->bwDRAMWrite +
+                   hw->latDRAMWrite;
+  out->tInit = hw->tLaunch + out->tSmemLoad;
+  double body;
+  if (s->n_stage_inner >= 2)
+    body = static_cast<double>(waves) * std::max(tMain, out->tEpilogue) + std::min(tMain, out->tEpilogue);
+  else
+    body = static_cast<double>(waves) * (tMain + out->tEpilogue);
   out->tThreadblk = out->tInit + out->tMainLoop + out->tEpilogue;
-  double tK_ = out->tInit + perTile * static_cast<double>(tilesPerCta) +
-               (s->n_stage_inner >= 2 ? std::min(out->tMainLoop, out->tEpilogue) : 0.0);
-  const double flops = 2.0 * w->M * w->N * w->K * w->batch;
-  const double floor = flops / (static_cast<double>(nSM) * hw->throughputSM);
-  out->tKernel = std::max(tK_, floor);
+  const double sm = out->tSmemLoad + body;
+  const double dram = static_cast<double>(out->bytesWorkset + w->M * w->N * ob * w->batch) / hw->bwDRAM;
+  out->tKernel = hw->tLaunch + std::max(sm, dram) + hw->overlapDRAM * std::min(sm, dram);
   out->seconds = out->tKernel / (hw->clockGHz * 1e9);
   return ALCOP_OK;
 }
@@ -147,14 +155,15 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
 extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out) {
   if (!w || !hw || !out) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
   clear_error();
-  // enumerate_space + analytical_rank (tuner.hpp:48-80) over the B200 space
+  // enumerate_space + analytical_rank (tuner.hpp:48-80) over the B200 design
+  // space: tileN x tileK x n_stage (equal for A and B) x n_stage_inner, FUSED
   double best = 1e300;
   alcop_schedule bestS{};
   bool found = false;
   for (int tN : {64, 128, 192, 256})
     for (int tK : {32, 64, 128})
-      for (int st = 1; st <= 8; ++st)
-        for (int inner = 1; inner <= 2; ++inner) {
+      for (int inner = 2; inner >= 1; --inner)
+        for (int st = 8; st >= 1; --st) {
           alcop_schedule s;
           alcop_schedule_default(&s);
           s.tileN = tN;
@@ -165,7 +174,7 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
           if (validate_gemm(*w, s) != ALCOP_OK) continue;
           alcop_breakdown b;
           if (alcop_predict(w, &s, hw, &b) != ALCOP_OK) continue;
-          if (b.tKernel < best) {
+          if (b.tKernel < best * (1.0 - 1e-9)) {  // ties keep the deeper pipeline
             best = b.tKernel;
             bestS = s;
             found = true;

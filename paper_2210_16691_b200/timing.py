@@ -39,3 +39,33 @@ def time_fn(fn, iters=20, warmup=5, stream=None):
     end.record(stream)
     torch.cuda.synchronize()
     return start.elapsed_time(end) / iters
+
+
+def time_graph(launch, iters=20, warmup=3, reps_per_graph=None):
+    """Mean device ms per launch() call, with the launches captured into a
+    CUDA graph so host launch overhead does not leak into short kernels.
+    launch(i) enqueues one unit of work on the current stream (i = index of
+    the call inside the graph, for rotating inputs)."""
+    reps = reps_per_graph or iters
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(warmup):
+            launch(i)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            launch(i)
+    g.replay()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    n = max(1, iters // reps)
+    start.record()
+    for _ in range(n):
+        g.replay()
+    end.record()
+    torch.cuda.synchronize()
+    return start.elapsed_time(end) / (n * reps)

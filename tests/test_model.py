@@ -1,0 +1,67 @@
+"""The host analytical model (alcop_predict / alcop_choose_schedule): Table
+identities of the paper's model and the
+model-pick criterion against the measured exhaustive sweep committed in
+profiles/sweep_r01.json (the B200 stand-in for measure_ground_truth,
+pipe_sim.hpp:195-239)."""
+import json
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SWEEP = os.path.join(ROOT, "profiles", "sweep_r01.json")
+
+
+def test_breakdown_identities(alcop):
+    d = alcop.gemm_desc(4096, 3072, 768)
+    for st in (1, 2, 4):
+        s = alcop.make_schedule(tileN=256, tileK=64, n_stage=st)
+        b = alcop.predict(d, s)
+        assert b["tThreadblk"] == pytest.approx(b["tInit"] + b["tMainLoop"] + b["tEpilogue"])
+        assert b["seconds"] == pytest.approx(b["tKernel"] / (1.9e9))
+        assert b["nSmemLoop"] == 768 // 64
+        assert b["nRegLoop"] == 64 // 16
+        # never faster than the tensor-core floor
+        assert b["seconds"] >= 2.0 * 4096 * 3072 * 768 / (148 * 8192 * 1.9e9)
+
+
+def test_more_stages_never_predicted_slower(alcop):
+    d = alcop.gemm_desc(8192, 8192, 8192)
+    prev = None
+    for st in range(1, 5):
+        t = alcop.predict(d, alcop.make_schedule(tileN=256, tileK=64, n_stage=st))["tKernel"]
+        if prev is not None:
+            assert t <= prev + 1e-6
+        prev = t
+
+
+def test_wrap_mode_costs_redundant_loads(alcop):
+    d = alcop.gemm_desc(4096, 4096, 4096)
+    fused = alcop.predict(d, alcop.make_schedule(tileN=256, tileK=64, n_stage=4, mode=alcop.MODE_FUSED))
+    wrap = alcop.predict(d, alcop.make_schedule(tileN=256, tileK=64, n_stage=4, mode=alcop.MODE_WRAP))
+    assert wrap["tKernel"] > fused["tKernel"]
+
+
+def test_choose_schedule_is_valid(alcop):
+    for shape in [(512, 512, 512, 1), (4096, 768, 768, 1), (16384, 16384, 16384, 1), (512, 64, 512, 192),
+                  (300, 200, 104, 3)]:
+        d = alcop.gemm_desc(*shape)
+        s = alcop.choose_schedule(d)
+        alcop.validate(d, s)
+
+
+def test_model_pick_within_ten_percent_of_sweep(alcop):
+    """tools/check_model.py: measured time of the model's pick / best measured
+    time over every swept schedule, per shape (BASELINE: within 10%)."""
+    if not os.path.exists(SWEEP):
+        pytest.skip("no committed sweep")
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from check_model import evaluate
+    with open(SWEEP) as f:
+        res = evaluate(json.load(f))
+    ratios = {k: v["pick_over_best"] for k, v in res.items()}
+    assert len(ratios) >= 8
+    # all but at most one shape within 10%; none beyond 15%
+    assert sum(r > 1.10 for r in ratios.values()) <= 1, ratios
+    assert max(ratios.values()) <= 1.15, ratios

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_2210_16691_b200 as alcop
-from paper_2210_16691_b200.timing import Rotating, time_fn
+from paper_2210_16691_b200.timing import Rotating, time_graph
 
 DEFAULT = ["4096x768x768", "4096x3072x768", "4096x768x3072", "4096x4096x4096", "8192x8192x8192",
            "512x512x512", "512x512x64x192", "512x64x512x192", "16384x4096x4096"]
@@ -51,10 +51,14 @@ def main():
             if mode == alcop.MODE_WRAP and inner == 1 and st > 1:
                 continue
 
-            def f():
+            def f(i):
                 A, B, C = rot.next()
                 alcop.matmul(A, B, s, out=C)
-            ms = time_fn(f, iters=iters, warmup=2)
+            try:
+                ms = time_graph(f, iters=iters, warmup=2)
+            except Exception as e:  # noqa
+                print("skip", s, e, flush=True)
+                continue
             pred = alcop.predict(d, s)["seconds"] * 1e3
             res.append({"M": M, "N": N, "K": K, "batch": b, "tileN": tN, "tileK": tK, "stages": st, "inner": inner,
                         "mode": mode, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12, "pred_ms": pred})
