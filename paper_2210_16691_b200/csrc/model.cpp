@@ -77,13 +77,13 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   // profiles/sweep_r01.json (tools/fit_model.py).
   hw->numSM = 148;
   hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
-  hw->bwLLC = 9569;         // L2 -> SM bytes / clk, chip-wide (~18 TB/s)
-  hw->bwDRAM = 2632;        // HBM read+write bytes / clk (~5.0 TB/s effective)
-  hw->bwDRAMWrite = 11079;  // epilogue TMA-store drain, bytes / clk chip-wide (L2 absorbs it)
+  hw->bwLLC = 20000;        // L2 -> SM bytes / clk, chip-wide (not binding in the fit)
+  hw->bwDRAM = 2600;        // HBM read+write bytes / clk (~4.9 TB/s effective)
+  hw->bwDRAMWrite = 20000;  // epilogue TMA-store drain, chip-wide (L2 absorbs it; not binding)
   hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
   hw->latDRAMRead = 1950;
   hw->latDRAMWrite = 0;
-  hw->bwSmem = 128;
+  hw->bwSmem = 62.24;       // per-SM L2 -> shared-memory TMA fill, bytes / clk
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
   hw->regsPerSM = 262144;
@@ -92,11 +92,11 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
   hw->clockGHz = 1.9;
-  hw->tIssue = 164.7;
-  hw->tIssuePerBox = 68.2;
-  hw->tLaunch = 1240;
+  hw->tIssue = 166.8;
+  hw->tIssuePerBox = 70.8;
+  hw->tLaunch = 774;
   hw->tTile = 0;
-  hw->overlapDRAM = 0.001;
+  hw->overlapDRAM = 0.01;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -126,7 +126,9 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // T_use of one chunk: MMA, L2->SM bandwidth share, issue floor
   out->tCompute = static_cast<double>(out->flopsOneRegLoop) / hw->throughputSM;
   const double tMma = out->tCompute * static_cast<double>(out->nRegLoop);
-  const double tL2 = static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC;
+  // L2 -> SM: the chip-wide share and the per-SM TMA fill rate
+  const double tL2 = std::max(static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC,
+                              static_cast<double>(out->bytesOneSmemLoop) / hw->bwSmem);
   const int64_t boxes = std::max<int64_t>(1, tK / 64) + std::max<int64_t>(1, tN / 64);
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors

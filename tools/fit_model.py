@@ -33,7 +33,7 @@ def predict_cycles(r, P):
     E = math.ceil(K / BK)
     bytes_kb = (128 + BN) * BK * 2
     t_mma = 2 * 128 * BN * BK / P["tp"]
-    t_l2 = bytes_kb * ctas / P["bwL2"]
+    t_l2 = max(bytes_kb * ctas / P["bwL2"], bytes_kb / P["bwSM"])
     boxes = max(1, BK // 64) + max(1, BN // 64)
     t_kb = max(t_mma, t_l2, P["t_issue"] + P["t_issue_b"] * boxes)
     loads = E + (s - 1 if mode == 0 else 0)
@@ -51,9 +51,9 @@ def predict_cycles(r, P):
     return P["launch"] + max(t, dram) + P["ovl"] * min(t, dram)
 
 
-KEYS = ["tp", "bwL2", "t_issue", "t_issue_b", "lat", "bwW", "epi0", "launch", "bwD", "tile0", "ovl"]
+KEYS = ["tp", "bwL2", "t_issue", "t_issue_b", "lat", "bwW", "epi0", "launch", "bwD", "tile0", "ovl", "bwSM"]
 INIT = {"tp": 8192.0, "bwL2": 6500.0, "t_issue": 250.0, "t_issue_b": 20.0, "lat": 1800.0, "bwW": 3000.0,
-        "epi0": 800.0, "launch": 3000.0, "bwD": 3300.0, "tile0": 300.0, "ovl": 0.2}
+        "epi0": 800.0, "launch": 3000.0, "bwD": 3300.0, "tile0": 300.0, "ovl": 0.2, "bwSM": 80.0}
 CLOCK = 1.9e9
 PICK_W = 0.0
 
