@@ -351,3 +351,56 @@ def matmul_host(A_host, B_host, sched: Schedule, out_dtype, b_layout=B_KN, C_hos
                                           ctypes.c_void_p(C_host.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
                                           _stream_ptr(stream)))
     return C_host
+
+
+def conv_desc(N, H, W, C, K, R, S, stride=(1, 1), pad=(0, 0), in_dtype=BF16, out_dtype=BF16) -> ConvDesc:
+    d = ConvDesc()
+    d.N, d.H, d.W, d.C, d.K, d.R, d.S = N, H, W, C, K, R, S
+    d.stride_h, d.stride_w = stride
+    d.pad_h, d.pad_w = pad
+    d.in_dtype, d.out_dtype = in_dtype, out_dtype
+    return d
+
+
+def conv_out_hw(H, W, R, S, stride, pad):
+    return (H + 2 * pad[0] - R) // stride[0] + 1, (W + 2 * pad[1] - S) // stride[1] + 1
+
+
+def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_dtype=None, out=None, stream=None):
+    """Implicit-GEMM conv2d through alcop_conv2d: x NHWC, w KRSC -> y NPQK
+    (fp16/bf16 in, fp32 accumulate).  Default schedule: the model's pick for
+    the GEMM view (M=N*P*Q, N=K, K=R*S*C) with tileK 64."""
+    import torch
+    _require_cuda(x, w)
+    N, H, W, C = x.shape
+    K, R, S, _ = w.shape
+    P, Q = conv_out_hw(H, W, R, S, stride, pad)
+    out_dtype = out_dtype or x.dtype
+    if out is None:
+        out = torch.empty((N, P, Q, K), dtype=out_dtype, device=x.device)
+    d = conv_desc(N, H, W, C, K, R, S, stride, pad, _dtype_code(x.dtype), _dtype_code(out_dtype))
+    if sched is None:
+        g = gemm_desc(N * P * Q, K, R * S * C, 1, _dtype_code(x.dtype), _dtype_code(out_dtype), B_NK)
+        sched = choose_conv_schedule(g)
+    _check(load_library().alcop_conv2d(ctypes.byref(d), ctypes.byref(sched), ctypes.c_void_p(x.contiguous().data_ptr()),
+                                       ctypes.c_void_p(w.contiguous().data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                       _stream_ptr(stream)))
+    return out
+
+
+def choose_conv_schedule(gview: GemmDesc, hw: HW | None = None) -> Schedule:
+    """Model pick restricted to the conv kernel's space (tileK 64, equal stages)."""
+    best, best_s = None, None
+    for tn in (64, 128, 192, 256):
+        for st in range(8, 0, -1):
+            for inner in (2, 1):
+                s = make_schedule(tileN=tn, tileK=64, n_stage=st, n_stage_inner=inner)
+                try:
+                    t = predict(gview, s, hw)["tKernel"]
+                except AlcopError:
+                    continue
+                if best is None or t < best * (1 - 1e-9):
+                    best, best_s = t, s
+    if best_s is None:
+        raise AlcopError(ALCOP_ERR_CONFIG, "Unschedulable: no conv schedule")
+    return best_s

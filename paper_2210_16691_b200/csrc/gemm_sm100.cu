@@ -52,6 +52,10 @@ struct GemmKParams {
   alcop_event* trace;
   int32_t trace_cap;
   uint64_t* stamps;  // debug timeline: 8 globaltimer stamps per CTA (nullptr = off)
+  // implicit-GEMM conv2d (kConv): output pixels m = (n, p, q) row-major,
+  // reduction chunk = (r, s, channel block) matching the KRSC filter layout
+  int32_t conv_P, conv_Q, conv_S, conv_Cb;
+  int32_t conv_sh, conv_sw, conv_ph, conv_pw;
 };
 
 // debug timeline buffer (set through alcop_debug_set_stamps)
@@ -165,7 +169,7 @@ struct RingCursor {
 // equal); otherwise each buffer has its own ring and lookahead.  kDebug
 // compiles in the bookkeeping trace and the timeline stamps.
 // ---------------------------------------------------------------------------
-template <typename OutT, int BK, bool kJoint, bool kDebug>
+template <typename OutT, int BK, bool kJoint, bool kDebug, bool kConv = false>
 __global__ void __launch_bounds__(kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
@@ -254,11 +258,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
         }
       };
+      // conv: origin of the tile's first output pixel in input coordinates
+      int cv_n = 0, cv_h = 0, cv_w = 0, cv_tile = -1;
       auto issue_a = [&](uint32_t slot, uint32_t fb, int chunk) {
+        if constexpr (kConv) {
+          if (tc_tile != cv_tile) {
+            cv_tile = tc_tile;
+            const int m0 = tc.mb * kTileM;
+            const int pq = p.conv_P * p.conv_Q;
+            cv_n = m0 / pq;
+            const int rem = m0 - cv_n * pq;
+            const int pp = rem / p.conv_Q;
+            cv_h = pp * p.conv_sh - p.conv_ph;
+            cv_w = (rem - pp * p.conv_Q) * p.conv_sw - p.conv_pw;
+          }
+          const int cb = chunk % p.conv_Cb;
+          const int rs = chunk / p.conv_Cb;
+          const int fs = rs % p.conv_S;
+          const int fr = rs / p.conv_S;
+          tma_load_im2col_4d(ringA + slot * a_bytes, &tmA, fb, cb * 64, cv_w, cv_h, cv_n,
+                             static_cast<uint16_t>(fs), static_cast<uint16_t>(fr));
+        } else {
 #pragma unroll
-        for (int a = 0; a < kKAtoms; ++a)
-          tma_load_3d(ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK,
-                      tc.mb * kTileM, tc.b);
+          for (int a = 0; a < kKAtoms; ++a)
+            tma_load_3d(ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb, chunk * BK + a * kBoxK,
+                        tc.mb * kTileM, tc.b);
+        }
       };
       auto issue_b = [&](uint32_t slot, uint32_t fb, int chunk) {
         const uint32_t dst = ringB + slot * b_bytes;
@@ -580,6 +605,28 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   return ALCOP_OK;
 }
 
+template <typename OutT, bool kDebug>
+int launch_typed_conv(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
+                      int grid, int smem, cudaStream_t st) {
+  auto kern = alcop_pipelined_gemm_kernel<OutT, 64, true, kDebug, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  return ALCOP_OK;
+}
+
 template <typename OutT, int BK>
 int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                    int grid, int smem, cudaStream_t st) {
@@ -591,6 +638,14 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   }
   return debug ? launch_typed<OutT, BK, false, true>(ta, tb, tc, kp, grid, smem, st)
                : launch_typed<OutT, BK, false, false>(ta, tb, tc, kp, grid, smem, st);
+}
+
+template <typename OutT>
+int launch_conv_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
+                      int grid, int smem, cudaStream_t st) {
+  if (kp.trace != nullptr || kp.stamps != nullptr)
+    return launch_typed_conv<OutT, true>(ta, tb, tc, kp, grid, smem, st);
+  return launch_typed_conv<OutT, false>(ta, tb, tc, kp, grid, smem, st);
 }
 
 }  // namespace
@@ -684,6 +739,127 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
     case ALCOP_F16 * 4 + 0: return launch_variant<__half, 32>(ta, tb, tc, kp, grid, smem, st);
     case ALCOP_F16 * 4 + 1: return launch_variant<__half, 64>(ta, tb, tc, kp, grid, smem, st);
     case ALCOP_F16 * 4 + 2: return launch_variant<__half, 128>(ta, tb, tc, kp, grid, smem, st);
+  }
+  return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 get_encode_im2col() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(ptr);
+  });
+  return fn;
+}
+
+// Implicit-GEMM conv2d (K3): x NHWC, w KRSC, y NPQK.  GEMM view
+// M = N*P*Q output pixels, N = K filters, K = R*S*C in the filter's own order.
+// A tiles come from the im2col-mode tensor map of x (window origin per
+// output pixel, filter-tap offsets, zero fill at the padding), B from w
+// viewed as [K, R*S*C] (K-major), C goes to y viewed as [N*P*Q, K].
+int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt, void* y,
+                  void* stream) {
+  if (d.N < 1 || d.H < 1 || d.W < 1 || d.C < 1 || d.K < 1 || d.R < 1 || d.S < 1 || d.stride_h < 1 ||
+      d.stride_w < 1 || d.pad_h < 0 || d.pad_w < 0)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "conv dimensions must be positive, padding >= 0");
+  if (d.C % 64)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "implicit-GEMM conv needs C to be a multiple of 64");
+  if (d.stride_h > 8 || d.stride_w > 8 || d.pad_h > 127 || d.pad_w > 127 || d.R > 128 || d.S > 128)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "stride <= 8 and padding/filter within TMA im2col range");
+  if (s.tileK != 64 || s.n_stage_smem_A != s.n_stage_smem_B)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "conv needs tileK 64 and equal A/B stage counts");
+  const int64_t P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
+  const int64_t Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
+  if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  alcop_gemm_desc g{};
+  g.M = d.N * P * Q;
+  g.N = d.K;
+  g.K = d.R * d.S * d.C;
+  g.batch = 1;
+  g.in_dtype = d.in_dtype;
+  g.out_dtype = d.out_dtype;
+  g.b_layout = ALCOP_B_NK;
+  int rc = validate_gemm(g, s);
+  if (rc) return rc;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wt) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "x, w and y must be 16-byte aligned");
+  const CUtensorMapDataType dt =
+      d.in_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  auto enc = get_encode_im2col();
+  if (!enc) return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col unavailable");
+  CUtensorMap ta, tb, tc;
+  {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(d.W), static_cast<cuuint64_t>(d.H),
+                          static_cast<cuuint64_t>(d.N)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.C * 2), static_cast<cuuint64_t>(d.W * d.C * 2),
+                             static_cast<cuuint64_t>(d.H * d.W * d.C * 2)};
+    // bounding box of window origins, per spatial dim in tensor order (W, H)
+    int lower[2] = {-d.pad_w, -d.pad_h};
+    int upper[2] = {static_cast<int>(d.pad_w - (d.S - 1)), static_cast<int>(d.pad_h - (d.R - 1))};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(d.stride_w), static_cast<cuuint32_t>(d.stride_h), 1};
+    CUresult r = enc(&ta, dt, 4, const_cast<void*>(x), dims, strides, lower, upper, 64, kTileM, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(r) + ")");
+  }
+  const int BN = static_cast<int>(s.tileN);
+  rc = encode_3d_dt(&tb, dt, wt, g.K, g.N, 1, g.K * 2, g.N * g.K * 2, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B, "w");
+  if (rc) return rc;
+  const CUtensorMapDataType odt = d.out_dtype == ALCOP_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : d.out_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
+  rc = encode_3d_dt(&tc, odt, y, g.N, g.M, 1, g.N * ob, g.M * g.N * ob, 128 / ob, 32, CU_TENSOR_MAP_SWIZZLE_128B, "y");
+  if (rc) return rc;
+
+  GemmKParams kp{};
+  kp.M = static_cast<int32_t>(g.M);
+  kp.N = static_cast<int32_t>(g.N);
+  kp.K = static_cast<int32_t>(g.K);
+  kp.batch = 1;
+  kp.BN = BN;
+  kp.BK = 64;
+  kp.num_m = static_cast<int32_t>((g.M + kTileM - 1) / kTileM);
+  kp.num_n = static_cast<int32_t>((g.N + BN - 1) / BN);
+  kp.num_tiles = kp.num_m * kp.num_n;
+  kp.E = static_cast<int32_t>(g.K / 64);
+  kp.sA = s.n_stage_smem_A;
+  kp.sB = s.n_stage_smem_B;
+  kp.tacc = s.n_stage_inner;
+  kp.mode = s.mode;
+  kp.b_mn_major = 0;
+  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, BN);
+  kp.a_stage_bytes = static_cast<uint32_t>(kTileM * 64 * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>(BN * 64 * 2);
+  kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
+  kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
+  kp.C = y;
+  kp.ldc = g.N;
+  kp.stride_c = g.M * g.N;
+  kp.stamps = g_stamps;
+  kp.conv_P = static_cast<int32_t>(P);
+  kp.conv_Q = static_cast<int32_t>(Q);
+  kp.conv_S = static_cast<int32_t>(d.S);
+  kp.conv_Cb = static_cast<int32_t>(d.C / 64);
+  kp.conv_sh = d.stride_h;
+  kp.conv_sw = d.stride_w;
+  kp.conv_ph = d.pad_h;
+  kp.conv_pw = d.pad_w;
+  const int sms = device_sm_count();
+  if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
+  int grid = s.num_ctas > 0 ? s.num_ctas : sms;
+  if (grid > kp.num_tiles) grid = kp.num_tiles;
+  const int smem = static_cast<int>(gemm_smem_bytes(g, s));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (d.out_dtype) {
+    case ALCOP_F32: return launch_conv_typed<float>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_BF16: return launch_conv_typed<__nv_bfloat16>(ta, tb, tc, kp, grid, smem, st);
+    case ALCOP_F16: return launch_conv_typed<__half>(ta, tb, tc, kp, grid, smem, st);
   }
   return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
 }
