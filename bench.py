@@ -41,6 +41,22 @@ BERT_GEMMS = [  # (name, M, N, K)
     ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768), ("ffn2", 4096, 768, 3072),
 ]
 METRIC = "TFLOP/s (BERT-base layer GEMMs, M=4096, bf16)"
+# ResNet-50 v1.5 convolutions at batch 256 (BASELINE configs[3]); conv1 (C=3) is
+# outside the implicit-GEMM kernel's C % 64 == 0 support and is not counted.
+# (name, H_in, C, K, R, stride, pad, repeats)
+RESNET50_CONVS = [
+    ("l1_1x1_64_64", 56, 64, 64, 1, 1, 0, 1), ("l1_3x3_64_64", 56, 64, 64, 3, 1, 1, 3),
+    ("l1_1x1_64_256", 56, 64, 256, 1, 1, 0, 4), ("l1_1x1_256_64", 56, 256, 64, 1, 1, 0, 2),
+    ("l2_1x1_256_128", 56, 256, 128, 1, 1, 0, 1), ("l2_3x3s2_128", 56, 128, 128, 3, 2, 1, 1),
+    ("l2_3x3_128", 28, 128, 128, 3, 1, 1, 3), ("l2_1x1_128_512", 28, 128, 512, 1, 1, 0, 4),
+    ("l2_ds_256_512", 56, 256, 512, 1, 2, 0, 1), ("l2_1x1_512_128", 28, 512, 128, 1, 1, 0, 3),
+    ("l3_1x1_512_256", 28, 512, 256, 1, 1, 0, 1), ("l3_3x3s2_256", 28, 256, 256, 3, 2, 1, 1),
+    ("l3_3x3_256", 14, 256, 256, 3, 1, 1, 5), ("l3_1x1_256_1024", 14, 256, 1024, 1, 1, 0, 6),
+    ("l3_ds_512_1024", 28, 512, 1024, 1, 2, 0, 1), ("l3_1x1_1024_256", 14, 1024, 256, 1, 1, 0, 5),
+    ("l4_1x1_1024_512", 14, 1024, 512, 1, 1, 0, 1), ("l4_3x3s2_512", 14, 512, 512, 3, 2, 1, 1),
+    ("l4_3x3_512", 7, 512, 512, 3, 1, 1, 2), ("l4_1x1_512_2048", 7, 512, 2048, 1, 1, 0, 3),
+    ("l4_ds_1024_2048", 14, 1024, 2048, 1, 2, 0, 1), ("l4_1x1_2048_512", 7, 2048, 512, 1, 1, 0, 2),
+]
 UNIT = "TFLOP/s"
 L2_BYTES = 126 * 1024 * 1024
 
@@ -414,6 +430,40 @@ def main_gpu(args, rank, world, local_rank):
         extra["large_square_8192"] = {"tflops": round(tf, 1), "frac_of_peak": round(tf / peaks["bf16_tflops"], 3),
                                       "schedule": ssq.as_dict()}
         del A, B, C
+
+    # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
+    if not args.quick:
+        from paper_2210_16691_b200.sharded import shard_range
+        sh = shard_range(256, rank, world)
+        nloc = sh.size
+        conv_rows = []
+        tot_flops = 0.0
+        tot_ms = 0.0
+        for (name, H, C, K, R, st, pd, rep) in RESNET50_CONVS:
+            P, Q = alcop.conv_out_hw(H, H, R, R, (st, st), (pd, pd))
+            g = alcop.gemm_desc(nloc * P * Q, K, R * R * C, 1, alcop.BF16, alcop.BF16, alcop.B_NK)
+            cs = alcop.choose_conv_schedule(g)
+            X = (torch.rand((nloc, H, H, C), device=dev) - 0.5).to(torch.bfloat16)
+            Wf = (torch.rand((K, R, R, C), device=dev) - 0.5).to(torch.bfloat16)
+            Y = torch.empty((nloc, P, Q, K), device=dev, dtype=torch.bfloat16)
+            ms = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=cs, out=Y), iters=6, warmup=2)
+            s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
+            ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=s1, out=Y), iters=4, warmup=1)
+            fl = 2.0 * nloc * P * Q * K * R * R * C
+            tot_flops += fl * rep
+            tot_ms += ms * rep
+            conv_rows.append({"layer": name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+                              "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN,
+                              "n_stage": cs.n_stage_smem_A})
+            del X, Wf, Y
+        tt = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        extra["resnet50_convs_b256"] = {
+            "tflops_aggregate": round(world * tot_flops / (float(tt.item()) * 1e-3) / 1e12, 1),
+            "images_per_gpu": nloc, "sharding": "batch", "layers": conv_rows,
+            "note": "sum over the 52 conv layers except conv1 (C=3); per-layer CUDA-graph timing, model schedules"}
+        torch.cuda.empty_cache()
 
     # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)
     host = []
