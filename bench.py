@@ -285,16 +285,21 @@ def main_gpu(args, rank, world, local_rank):
             step_set(i)
     stream.wait_stream(cs)
     torch.cuda.synchronize()
+    use_graphs = os.environ.get("ALCOP_BENCH_GRAPHS", "1") != "0"  # 0: direct launches (profiling)
     graphs = []
-    for i in range(nsets):
-        g_ = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_):
-            step_set(i)
-        graphs.append(g_)
+    if use_graphs:
+        for i in range(nsets):
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                step_set(i)
+            graphs.append(g_)
     state = {"i": 0}
 
     def step():
-        graphs[state["i"]].replay()
+        if use_graphs:
+            graphs[state["i"]].replay()
+        else:
+            step_set(state["i"])
         state["i"] = (state["i"] + 1) % nsets
 
     def barrier():

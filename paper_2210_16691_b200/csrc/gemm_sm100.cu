@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -60,8 +61,11 @@ struct GemmKParams {
 
 // debug timeline buffer (set through alcop_debug_set_stamps)
 static uint64_t* g_stamps = nullptr;
-// programmatic dependent launch on (alcop_debug_set_pdl)
-static bool g_pdl = true;
+// programmatic dependent launch on (alcop_debug_set_pdl; env ALCOP_PDL=0 turns it off)
+static bool g_pdl = [] {
+  const char* e = std::getenv("ALCOP_PDL");
+  return !(e && e[0] == '0');
+}();
 
 namespace {
 

@@ -46,6 +46,14 @@ def time_graph(launch, iters=20, warmup=3, reps_per_graph=None):
     CUDA graph so host launch overhead does not leak into short kernels.
     launch(i) enqueues one unit of work on the current stream (i = index of
     the call inside the graph, for rotating inputs)."""
+    import os
+    if os.environ.get("ALCOP_BENCH_GRAPHS", "1") == "0":  # profiling: plain launches
+        cnt = {"i": 0}
+
+        def f():
+            launch(cnt["i"])
+            cnt["i"] += 1
+        return time_fn(f, iters=iters, warmup=warmup)
     reps = reps_per_graph or iters
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
