@@ -84,11 +84,11 @@ typedef struct {
  * reference cannot express it (stages >= 2, schedule.hpp:261), here it is
  * the in-run baseline variant (one slot: load -> wait -> use -> release). */
 typedef struct {
-  int64_t tileM, tileN, tileK; /* CTA tile; tileM 128 (cta_group 1)     */
+  int64_t tileM, tileN, tileK; /* tile; tileM = 128 x cta_group           */
   int32_t n_stage_smem_A;      /* A_shared ring depth (outer level)     */
   int32_t n_stage_smem_B;      /* B_shared ring depth (outer level)     */
   int32_t n_stage_inner;       /* A_reg/B_reg level -> TMEM accumulator buffers (1|2) */
-  int32_t cta_group;           /* 1 (2 reserved)                         */
+  int32_t cta_group;           /* 1, or 2 = CTA pair (tcgen05 cta_group::2, tileM 256) */
   int32_t mode;                /* alcop_mode                             */
   int32_t num_ctas;            /* persistent grid; 0 = #SMs              */
   int32_t raster;              /* reserved (tile rasterisation), 0       */
@@ -123,6 +123,7 @@ typedef struct {
   double tLaunch;        /* kernel launch + setup, cycles */
   double tTile;          /* per output tile fixed cost, cycles */
   double overlapDRAM;    /* soft-max weight between the SM pipeline and HBM time */
+  double tPair;          /* fixed extra cycles of a cta_group::2 (CTA-pair) launch */
 } alcop_hw;
 
 /* perf::LatencyBreakdown (perf_model.hpp:40-47); field names follow

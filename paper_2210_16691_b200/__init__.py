@@ -61,9 +61,10 @@ class Schedule(ctypes.Structure):
 
     def __repr__(self):
         d = self.as_dict()
-        return ("Schedule(tile=%dx%dx%d, stages A/B=%d/%d, inner=%d, mode=%s)"
+        return ("Schedule(tile=%dx%dx%d, stages A/B=%d/%d, inner=%d, mode=%s%s)"
                 % (d["tileM"], d["tileN"], d["tileK"], d["n_stage_smem_A"], d["n_stage_smem_B"],
-                   d["n_stage_inner"], "FUSED" if d["mode"] == MODE_FUSED else "WRAP"))
+                   d["n_stage_inner"], "FUSED" if d["mode"] == MODE_FUSED else "WRAP",
+                   ", cta_group=2" if d["cta_group"] == 2 else ""))
 
 
 class ConvDesc(ctypes.Structure):
@@ -79,7 +80,7 @@ class HW(ctypes.Structure):
                 ("maxThreadblkPerSM", ctypes.c_int32), ("maxWarpsPerSM", ctypes.c_int32),
                 ("utilKneeWarps", ctypes.c_int32), ("tmemColsPerSM", ctypes.c_int32), ("clockGHz", ctypes.c_double),
                 ("tIssue", ctypes.c_double), ("tIssuePerBox", ctypes.c_double), ("tLaunch", ctypes.c_double),
-                ("tTile", ctypes.c_double), ("overlapDRAM", ctypes.c_double)]
+                ("tTile", ctypes.c_double), ("overlapDRAM", ctypes.c_double), ("tPair", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -199,10 +200,10 @@ def default_schedule(**kw) -> Schedule:
 
 
 def make_schedule(tileN=256, tileK=64, n_stage=4, n_stage_inner=2, mode=MODE_FUSED, n_stage_B=None,
-                  num_ctas=0) -> Schedule:
-    return default_schedule(tileN=tileN, tileK=tileK, n_stage_smem_A=n_stage,
+                  num_ctas=0, cta_group=1) -> Schedule:
+    return default_schedule(tileM=128 * cta_group, tileN=tileN, tileK=tileK, n_stage_smem_A=n_stage,
                             n_stage_smem_B=n_stage if n_stage_B is None else n_stage_B,
-                            n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas)
+                            n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas, cta_group=cta_group)
 
 
 def apply_script(desc: GemmDesc, script: str):

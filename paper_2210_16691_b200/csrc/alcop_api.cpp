@@ -30,8 +30,9 @@ int64_t round_up_pow2_cols(int64_t cols) {
 
 int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
   (void)w;
-  const int64_t a_stage = kTileM * s.tileK * 2;
-  const int64_t b_stage = s.tileN * s.tileK * 2;
+  const int64_t cg = s.cta_group == 2 ? 2 : 1;
+  const int64_t a_stage = kTileM * s.tileK * 2;         // per CTA: 128 rows of A
+  const int64_t b_stage = s.tileN / cg * s.tileK * 2;   // per CTA: tileN/cta_group columns of B
   const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;
   const int64_t staging = 4 * 2 * 32 * 128;  // epilogue TMA-store staging
   return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + staging + bars;
@@ -50,12 +51,16 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadDtype", "output dtype must be F32, F16 or BF16");
   if (w.b_layout != ALCOP_B_KN && w.b_layout != ALCOP_B_NK)
     return set_error(ALCOP_ERR_CONFIG, "BadLayout", "b_layout must be KN or NK");
-  if (s.cta_group != 1)
-    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "only cta_group 1 is implemented");
-  if (s.tileM != kTileM)
-    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileM must be 128 (UMMA M with cta_group::1)");
+  if (s.cta_group != 1 && s.cta_group != 2)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "cta_group must be 1 or 2");
+  if (s.tileM != kTileM * s.cta_group)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileM must be 128 x cta_group (UMMA M 128 / 256)");
   if (s.tileN != 64 && s.tileN != 128 && s.tileN != 192 && s.tileN != 256)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256");
+  if (s.cta_group == 2 && s.tileN != 128 && s.tileN != 256)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "cta_group 2 needs tileN 128 or 256 (B split in halves of 64k)");
+  if (s.cta_group == 2 && s.n_stage_smem_A != s.n_stage_smem_B)
+    return set_error(ALCOP_ERR_CONFIG, "BadStages", "cta_group 2 uses one joint A+B ring: equal stage counts");
   if (s.tileK != 32 && s.tileK != 64 && s.tileK != 128)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileK must be one of 32, 64, 128");
   if (s.n_stage_smem_A < 1 || s.n_stage_smem_B < 1 || s.n_stage_smem_A > kMaxStages ||

@@ -557,6 +557,249 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) stamp<kDebug>(p, 7);
 }
 
+// ---------------------------------------------------------------------------
+// cta_group::2 variant: a cluster of two CTAs on one TPC computes a
+// 256 x BN output tile with tcgen05.mma.cta_group::2 (M = 256).  Each CTA
+// stages its 128 rows of A and half (BN/2) of B's columns per chunk, so the
+// per-SM TMA fill per FLOP drops by (128+BN)/(128+BN/2).  Both CTAs' copies
+// complete on the leader's full barrier (leader arms it with both CTAs'
+// bytes); the leader's single MMA thread consumes the chunk from both shared
+// memories and its tcgen05.commit multicasts the release to both CTAs'
+// empty barriers — the four primitives of the pass, now spanning a CTA pair.
+// Each CTA's TMEM holds its 128 rows x BN columns; the epilogue is per CTA
+// and hands the accumulator back on the leader's tmem_empty (8 arrivals).
+// Joint A+B ring only (n_stage_A == n_stage_B).
+// ---------------------------------------------------------------------------
+template <typename OutT, int BK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                     const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
+  using namespace ptx;
+  constexpr int kSteps = BK / 16;
+  constexpr int kBoxK = BK >= 64 ? 64 : BK;
+  constexpr int kKAtoms = BK / kBoxK;
+  constexpr uint32_t kKSbo = BK >= 64 ? 1024u : 512u;
+  constexpr uint32_t kKLayout = BK >= 64 ? kLayoutSW128 : kLayoutSW64;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t ringA = smem_u32(smem);
+  const uint32_t ringB = ringA + p.sA * p.a_stage_bytes;
+  const uint32_t staging = ringB + p.sA * p.b_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * (p.a_stage_bytes + p.b_stage_bytes) + kStagingBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + p.sA;
+  uint64_t* tfull = empty + p.sA;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int half_n = p.BN / 2;
+
+  if (warp == 0 && elect_one()) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmC);
+  }
+  if (warp == 1) {
+    if (elect_one()) {
+      for (int i = 0; i < p.sA; ++i) {
+        mbar_init(smem_u32(&full[i]), 1);
+        mbar_init(smem_u32(&empty[i]), 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(smem_u32(&tfull[i]), 1);
+        mbar_init(smem_u32(&tempty[i]), 8);  // 4 epilogue warps x 2 CTAs
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc_pair(smem_u32(tmem_slot), p.tmem_cols);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers initialised before any remote arrive / complete_tx
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  grid_dependency_wait();
+  grid_launch_dependents();
+
+  const int cluster_id = static_cast<int>(blockIdx.x) >> 1;
+  const int nclusters = static_cast<int>(gridDim.x) >> 1;
+  const int my_tiles = (p.num_tiles - cluster_id + nclusters - 1) / nclusters;
+  const int E = p.E;
+  const bool wrap = (p.mode == ALCOP_MODE_WRAP);
+
+  if (warp == 0) {
+    if (ROLE_GUARD()) {
+      // ======================= producer (both CTAs) =======================
+      RingCursor ra;
+      TileCoord tc{0, 0, 0};
+      int tc_tile = -1;
+      const uint32_t a_bytes = p.a_stage_bytes, b_bytes = p.b_stage_bytes;
+      const uint32_t pair_bytes = 2 * (a_bytes + b_bytes);
+      auto load = [&](int tl, int chunk) {
+        const uint32_t slot = ra.slot;
+        const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
+        mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire (own slot, released by the pair's MMA)
+        ra.phase ^= 1u << slot;
+        if (tl != tc_tile) {
+          tc_tile = tl;
+          tc = tile_coord(p, cluster_id + tl * nclusters);
+        }
+        const uint32_t fb_local = smem_u32(&full[slot]);
+        const uint32_t fb_leader = mapa_shared(fb_local, 0);
+        ISSUE(if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
+#pragma unroll
+              for (int a = 0; a < kKAtoms; ++a) tma_load_3d_pair(
+                  ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
+                  tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
+              const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
+              if (p.b_mn_major) {
+                for (int a = 0; a < (half_n >> 6); ++a)
+                  tma_load_3d_pair(dst + a * (BK * 128), &tmB, fb_leader, n0 + a * 64, chunk * BK, tc.b);
+              } else {
+#pragma unroll
+                for (int a = 0; a < kKAtoms; ++a)
+                  tma_load_3d_pair(dst + a * (half_n * 128), &tmB, fb_leader, chunk * BK + a * kBoxK, n0, tc.b);
+              });
+        ra.advance(p.sA);
+      };
+      if (wrap) {
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          ra.slot = 0;
+          int c = 0;
+          for (int i = 0; i < E + p.sA - 1; ++i) {
+            load(tl, c);
+            c = (c + 1 == E) ? 0 : c + 1;
+          }
+        }
+      } else {
+        for (int tl = 0; tl < my_tiles; ++tl)
+          for (int c = 0; c < E; ++c) load(tl, c);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && ROLE_GUARD()) {
+      // ======================= MMA issuer (leader CTA only) =======================
+      RingCursor ca;
+      const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
+      uint64_t bdesc0;
+      uint32_t b_big, b_small;
+      if (p.b_mn_major) {
+        bdesc0 = make_smem_desc(ringB, BK * 128, 1024, kLayoutSW128);
+        b_small = 2048 / 16;
+        b_big = 4 * b_small;
+      } else {
+        bdesc0 = make_smem_desc(ringB, 16, kKSbo, kKLayout);
+        b_small = 2;
+        b_big = static_cast<uint32_t>(half_n) * 128 / 16;
+      }
+      const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
+      const uint32_t idesc = p.idesc;
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int acc = tl % p.tacc;
+        mbar_wait(smem_u32(&tempty[acc]), ((tl / p.tacc) & 1) ^ 1);  // both CTAs drained it
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
+        if (wrap) ca.slot = 0;
+        for (int v = 0; v < E; ++v) {
+          const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
+          mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
+          ca.phase ^= 1u << slot;
+          tc_fence_after();
+          const uint64_t ad = adesc0 + slot * a_stage16;
+          const uint64_t bd = bdesc0 + slot * b_stage16;
+          ISSUE(
+#pragma unroll
+              for (int u = 0; u < kSteps; ++u) {
+                const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
+                const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
+                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+              } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
+          ca.advance(p.sA);
+        }
+        ISSUE(umma_commit_pair_multicast(smem_u32(&tfull[acc]), 0x3));
+        if (wrap) {
+          // drain the s-1 wrapped tail groups (no MMA): release both CTAs' slots
+          for (int d = 0; d < p.sA - 1; ++d) {
+            const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
+            mbar_wait(smem_u32(&full[slot]), par);
+            ca.phase ^= 1u << slot;
+            ISSUE(mbar_arrive(smem_u32(&empty[slot])); mbar_arrive_cluster(mapa_shared(smem_u32(&empty[slot]), 1)));
+            ca.advance(p.sA);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= epilogue (both CTAs) =======================
+    const int q = warp & 3;
+    const uint32_t stage_base = staging + (warp - 2) * 2 * 4096;
+    constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
+    const int nchunks = p.BN / kChunkCols;
+    int buf = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int acc = tl % p.tacc;
+      mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
+      tc_fence_after();
+      const TileCoord tc = tile_coord(p, cluster_id + tl * nclusters);
+      const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t w[32];
+        if constexpr (sizeof(OutT) == 4) {
+          tmem_ld_32x32b_x32(t_addr + c * 32, w);
+          tmem_wait_ld();
+        } else {
+          uint32_t r0[32], r1[32];
+          tmem_ld_32x32b_x32(t_addr + c * 64, r0);
+          tmem_ld_32x32b_x32(t_addr + c * 64 + 32, r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack2<OutT>(r0[2 * i], r0[2 * i + 1]);
+            w[16 + i] = pack2<OutT>(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
+        if (c == nchunks - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        }
+        const uint32_t sbuf = stage_base + buf * 4096;
+        if (lane == 0) bulk_wait_group_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                       w[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols,
+                       tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM + q * 32, tc.b);
+          bulk_commit_group();
+        }
+        buf ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait_group<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still signal it or read its smem
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, p.tmem_cols);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -591,6 +834,28 @@ template <typename OutT, int BK, bool kJoint, bool kDebug>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                  int grid, int smem, cudaStream_t st) {
   auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  return ALCOP_OK;
+}
+
+template <typename OutT, int BK>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
+                int smem, cudaStream_t st) {
+  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -677,6 +942,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const CUtensorMapDataType dt =
       w.in_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const int BN = static_cast<int>(s.tileN), BK = static_cast<int>(s.tileK);
+  const int cg = s.cta_group == 2 ? 2 : 1;
   const CUtensorMapSwizzle kswz = BK >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   const uint32_t kbox = BK >= 64 ? 64 : BK;
 
@@ -686,7 +952,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   if (w.b_layout == ALCOP_B_KN)
     rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
   else
-    rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN, kswz, "B");
+    rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN / cg, kswz, "B");
   if (rc) return rc;
   CUtensorMap tc;
   {
@@ -706,7 +972,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.batch = static_cast<int32_t>(w.batch);
   kp.BN = BN;
   kp.BK = BK;
-  kp.num_m = static_cast<int32_t>((w.M + kTileM - 1) / kTileM);
+  kp.num_m = static_cast<int32_t>((w.M + kTileM * cg - 1) / (kTileM * cg));
   kp.num_n = static_cast<int32_t>((w.N + BN - 1) / BN);
   kp.num_tiles = static_cast<int32_t>(kp.num_m * kp.num_n * w.batch);
   kp.E = static_cast<int32_t>((w.K + BK - 1) / BK);
@@ -715,9 +981,9 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.tacc = s.n_stage_inner;
   kp.mode = s.mode;
   kp.b_mn_major = w.b_layout == ALCOP_B_KN ? 1 : 0;
-  kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM, BN);
+  kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM * cg, BN);
   kp.a_stage_bytes = static_cast<uint32_t>(kTileM * BK * 2);
-  kp.b_stage_bytes = static_cast<uint32_t>(BN * BK * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>(BN / cg * BK * 2);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
   kp.C = C;
@@ -730,9 +996,27 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
-  if (grid > kp.num_tiles) grid = kp.num_tiles;
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cg == 2) {
+    if (trace != nullptr)
+      return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the device trace is implemented for cta_group 1");
+    grid = (grid / 2) * 2;
+    if (grid > 2 * kp.num_tiles) grid = 2 * kp.num_tiles;
+    switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
+      case ALCOP_F32 * 4 + 0: return launch_pair<float, 32>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F32 * 4 + 1: return launch_pair<float, 64>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F32 * 4 + 2: return launch_pair<float, 128>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 0: return launch_pair<__nv_bfloat16, 32>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 1: return launch_pair<__nv_bfloat16, 64>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 2: return launch_pair<__nv_bfloat16, 128>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 0: return launch_pair<__half, 32>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 1: return launch_pair<__half, 64>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 2: return launch_pair<__half, 128>(ta, tb, tc, kp, grid, smem, st);
+    }
+    return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
+  }
+  if (grid > kp.num_tiles) grid = kp.num_tiles;
   switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
     case ALCOP_F32 * 4 + 0: return launch_variant<float, 32>(ta, tb, tc, kp, grid, smem, st);
     case ALCOP_F32 * 4 + 1: return launch_variant<float, 64>(ta, tb, tc, kp, grid, smem, st);

@@ -77,13 +77,13 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   // profiles/sweep_r01.json (tools/fit_model.py).
   hw->numSM = 148;
   hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
-  hw->bwLLC = 20000;        // L2 -> SM bytes / clk, chip-wide (not binding in the fit)
-  hw->bwDRAM = 2600;        // HBM read+write bytes / clk (~4.9 TB/s effective)
-  hw->bwDRAMWrite = 20000;  // epilogue TMA-store drain, chip-wide (L2 absorbs it; not binding)
+  hw->bwLLC = 1e9;          // L2 -> SM bytes / clk, chip-wide (not binding in the fit)
+  hw->bwDRAM = 2273;        // HBM read+write bytes / clk (~4.3 TB/s effective)
+  hw->bwDRAMWrite = 11335;  // epilogue TMA-store drain, bytes / clk chip-wide
   hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
   hw->latDRAMRead = 1950;
   hw->latDRAMWrite = 0;
-  hw->bwSmem = 62.24;       // per-SM L2 -> shared-memory TMA fill, bytes / clk
+  hw->bwSmem = 55.43;       // per-SM L2 -> shared-memory TMA fill, bytes / clk
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
   hw->regsPerSM = 262144;
@@ -92,11 +92,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
   hw->clockGHz = 1.9;
-  hw->tIssue = 166.8;
-  hw->tIssuePerBox = 70.8;
-  hw->tLaunch = 774;
+  hw->tIssue = 268.1;
+  hw->tIssuePerBox = 49.24;
+  hw->tLaunch = 160.8;
   hw->tTile = 0;
-  hw->overlapDRAM = 0.01;
+  hw->overlapDRAM = 0.02;
+  hw->tPair = 3878;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -106,11 +107,14 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   int rc = validate_gemm(*w, *s);
   if (rc) return rc;
   std::memset(out, 0, sizeof(*out));
+  const int64_t cg = s->cta_group == 2 ? 2 : 1;
   const int64_t tM = s->tileM, tN = s->tileN, tK = s->tileK;
   const int64_t eb = 2, ob = w->out_dtype == ALCOP_F32 ? 4 : 2;
   const int64_t tiles = ((w->M + tM - 1) / tM) * ((w->N + tN - 1) / tN) * w->batch;
-  const int64_t ctas = std::min<int64_t>(tiles, s->num_ctas > 0 ? s->num_ctas : hw->numSM);
-  const int64_t waves = (tiles + ctas - 1) / ctas;  // tiles per CTA (max)
+  // CTAs (cta_group 1) or CTA pairs (cta_group 2) working concurrently
+  const int64_t units = std::min<int64_t>(tiles, (s->num_ctas > 0 ? s->num_ctas : hw->numSM) / cg);
+  const int64_t ctas = units * cg;
+  const int64_t waves = (tiles + units - 1) / units;  // tiles per CTA (pair), max
   const int64_t E = (w->K + tK - 1) / tK;
   const int sOuter = std::min(s->n_stage_smem_A, s->n_stage_smem_B);
   out->nThreadblkPerSM = 1;
@@ -118,10 +122,10 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   out->nThreadblkBatch = waves;
   out->nSmemLoop = E;
   out->nRegLoop = tK / 16;
-  out->flopsOneRegLoop = 2 * tM * tN * 16;
-  out->bytesOneSmemLoop = (tM + tN) * tK * eb;
+  out->flopsOneRegLoop = 2 * (tM / cg) * tN * 16;            // per SM (each CTA owns 128 rows)
+  out->bytesOneSmemLoop = (tM / cg + tN / cg) * tK * eb;      // per CTA: 128 rows of A + tileN/cg of B
   out->bytesWorkset = (w->M * w->K + w->K * w->N) * eb * w->batch;
-  out->bytesOutputTile = tM * tN * ob;
+  out->bytesOutputTile = (tM / cg) * tN * ob;
 
   // T_use of one chunk: MMA, L2->SM bandwidth share, issue floor
   out->tCompute = static_cast<double>(out->flopsOneRegLoop) / hw->throughputSM;
@@ -129,7 +133,7 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // L2 -> SM: the chip-wide share and the per-SM TMA fill rate
   const double tL2 = std::max(static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC,
                               static_cast<double>(out->bytesOneSmemLoop) / hw->bwSmem);
-  const int64_t boxes = std::max<int64_t>(1, tK / 64) + std::max<int64_t>(1, tN / 64);
+  const int64_t boxes = std::max<int64_t>(1, tK / 64) + std::max<int64_t>(1, tN / cg / 64);
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors
   out->tSmemUse = std::max(tMma, std::max(tL2, tIssue));
@@ -147,7 +151,7 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   else
     body = static_cast<double>(waves) * (tMain + out->tEpilogue);
   out->tThreadblk = out->tInit + out->tMainLoop + out->tEpilogue;
-  const double sm = out->tSmemLoad + body;
+  const double sm = out->tSmemLoad + body + (cg == 2 ? hw->tPair : 0.0);
   const double dram = static_cast<double>(out->bytesWorkset + w->M * w->N * ob * w->batch) / hw->bwDRAM;
   out->tKernel = hw->tLaunch + std::max(sm, dram) + hw->overlapDRAM * std::min(sm, dram);
   out->seconds = out->tKernel / (hw->clockGHz * 1e9);
@@ -158,16 +162,19 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
   if (!w || !hw || !out) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
   clear_error();
   // enumerate_space + analytical_rank (tuner.hpp:48-80) over the B200 design
-  // space: tileN x tileK x n_stage (equal for A and B) x n_stage_inner, FUSED
+  // space: cta_group x tileN x tileK x n_stage (equal for A and B) x n_stage_inner, FUSED
   double best = 1e300;
   alcop_schedule bestS{};
   bool found = false;
+  for (int cg = 1; cg <= 2; ++cg)
   for (int tN : {64, 128, 192, 256})
     for (int tK : {32, 64, 128})
       for (int inner = 2; inner >= 1; --inner)
         for (int st = 8; st >= 1; --st) {
           alcop_schedule s;
           alcop_schedule_default(&s);
+          s.cta_group = cg;
+          s.tileM = 128 * cg;
           s.tileN = tN;
           s.tileK = tK;
           s.n_stage_smem_A = s.n_stage_smem_B = st;

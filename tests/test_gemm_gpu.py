@@ -158,3 +158,21 @@ def test_device_trace_matches_enumerator(alcop, mode, sA, sB):
             want_c = [e for e in alcop.enumerate_pipeline(my, 5, sA, sB, mode, 1) if e["buf"] == b]
             assert [e for e in prod if e["buf"] == b] == want_p, (cta, b)
             assert [e for e in cons if e["buf"] == b] == want_c, (cta, b)
+
+
+@pytest.mark.parametrize("tileN,tileK,st,mode,layout", [(256, 64, 4, 1, 0), (128, 64, 4, 0, 0), (256, 128, 2, 1, 1),
+                                                        (128, 32, 6, 1, 1), (256, 64, 1, 1, 0), (128, 64, 3, 0, 1)])
+def test_cta_pair_exact(alcop, tileN, tileK, st, mode, layout):
+    """cta_group::2: a CTA pair computes 256 x tileN tiles (M=256 tcgen05.mma)."""
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, n_stage_inner=2 if st > 1 else 1, mode=mode,
+                            cta_group=2)
+    C, exact = _run(alcop, 768, 512, 640, b_layout=layout, sched=s)
+    _assert_exact(C, exact, torch.float32)
+
+
+def test_cta_pair_ragged_batched(alcop):
+    s = alcop.make_schedule(tileN=128, tileK=64, n_stage=4, cta_group=2)
+    C, exact = _run(alcop, 300, 200, 136, batch=3, sched=s)
+    _assert_exact(C, exact, torch.float32)
+    C, exact = _run(alcop, 512, 768, 768, in_dt=torch.bfloat16, out_dt=torch.bfloat16, sched=s)
+    _assert_exact(C, exact, torch.bfloat16)

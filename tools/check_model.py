@@ -17,12 +17,12 @@ def evaluate(rows):
         d = alcop.gemm_desc(M, N, K, b, alcop.BF16, alcop.BF16, alcop.B_KN)
         best = min(v, key=lambda r: r["ms"])
         pick = alcop.choose_schedule(d)
-        meas = [r for r in v if (r["tileN"], r["tileK"], r["stages"], r["inner"], r["mode"]) ==
-                (pick.tileN, pick.tileK, pick.n_stage_smem_A, pick.n_stage_inner, pick.mode)]
+        meas = [r for r in v if (r["tileN"], r["tileK"], r["stages"], r["inner"], r["mode"], r.get("cg", 1)) ==
+                (pick.tileN, pick.tileK, pick.n_stage_smem_A, pick.n_stage_inner, pick.mode, pick.cta_group)]
         pm = meas[0]["ms"] if meas else float("nan")
         pred = alcop.predict(d, pick)["seconds"] * 1e3
-        out["%dx%dx%dx%d" % (M, N, K, b)] = {"best_ms": best["ms"], "best": [best["tileN"], best["tileK"], best["stages"], best["inner"], best["mode"]],
-                                              "pick_ms": pm, "pick": [pick.tileN, pick.tileK, pick.n_stage_smem_A, pick.n_stage_inner, pick.mode],
+        out["%dx%dx%dx%d" % (M, N, K, b)] = {"best_ms": best["ms"], "best": [best["tileN"], best["tileK"], best["stages"], best["inner"], best["mode"], best.get("cg", 1)],
+                                              "pick_ms": pm, "pick": [pick.tileN, pick.tileK, pick.n_stage_smem_A, pick.n_stage_inner, pick.mode, pick.cta_group],
                                               "pred_ms": pred, "pick_over_best": pm / best["ms"]}
     return out
 

@@ -27,14 +27,16 @@ def predict_cycles(r, P):
     """P = dict of constants (cycles / bytes-per-cycle)."""
     M, N, K, b = r["M"], r["N"], r["K"], r["batch"]
     BN, BK, s, inner, mode = r["tileN"], r["tileK"], r["stages"], r["inner"], r["mode"]
-    tiles = math.ceil(M / 128) * math.ceil(N / BN) * b
-    ctas = min(tiles, NSM)
-    waves = math.ceil(tiles / ctas)
+    cg = r.get("cg", 1)
+    tiles = math.ceil(M / (128 * cg)) * math.ceil(N / BN) * b
+    units = min(tiles, NSM // cg)   # CTAs (pairs) working at once
+    ctas = units * cg
+    waves = math.ceil(tiles / units)
     E = math.ceil(K / BK)
-    bytes_kb = (128 + BN) * BK * 2
+    bytes_kb = (128 + BN // cg) * BK * 2   # per CTA
     t_mma = 2 * 128 * BN * BK / P["tp"]
     t_l2 = max(bytes_kb * ctas / P["bwL2"], bytes_kb / P["bwSM"])
-    boxes = max(1, BK // 64) + max(1, BN // 64)
+    boxes = max(1, BK // 64) + max(1, (BN // cg) // 64)
     t_kb = max(t_mma, t_l2, P["t_issue"] + P["t_issue_b"] * boxes)
     loads = E + (s - 1 if mode == 0 else 0)
     main = pipeline_latency(P["lat"], t_kb, loads, s) + P["tile0"]
@@ -45,15 +47,15 @@ def predict_cycles(r, P):
         body = waves * max(main, epi) + min(main, epi)
     else:
         body = waves * (main + epi)
-    t = P["lat"] + body
+    t = P["lat"] + body + (P["pair0"] if cg == 2 else 0.0)
     dram = (M * K + K * N + M * N) * 2 * b / P["bwD"]
     # DRAM and the SM pipeline overlap imperfectly: soft maximum
     return P["launch"] + max(t, dram) + P["ovl"] * min(t, dram)
 
 
-KEYS = ["tp", "bwL2", "t_issue", "t_issue_b", "lat", "bwW", "epi0", "launch", "bwD", "tile0", "ovl", "bwSM"]
+KEYS = ["tp", "bwL2", "t_issue", "t_issue_b", "lat", "bwW", "epi0", "launch", "bwD", "tile0", "ovl", "bwSM", "pair0"]
 INIT = {"tp": 8192.0, "bwL2": 6500.0, "t_issue": 250.0, "t_issue_b": 20.0, "lat": 1800.0, "bwW": 3000.0,
-        "epi0": 800.0, "launch": 3000.0, "bwD": 3300.0, "tile0": 300.0, "ovl": 0.2, "bwSM": 80.0}
+        "epi0": 800.0, "launch": 3000.0, "bwD": 3300.0, "tile0": 300.0, "ovl": 0.2, "bwSM": 80.0, "pair0": 500.0}
 CLOCK = 1.9e9
 PICK_W = 0.0
 
@@ -95,10 +97,10 @@ def report(rows, P):
         ratio = pick["ms"] / best["ms"]
         worst = max(worst, ratio)
         pred_best = predict_cycles(best, P) / CLOCK * 1e3
-        print("%-22s best %.4f ms (%d,%d,s%d,t%d,m%d) pick %.4f ms (%d,%d,s%d,t%d,m%d) ratio %.3f  pred(best) %.4f"
+        print("%-22s best %.4f ms (%d,%d,s%d,t%d,m%d,cg%d) pick %.4f ms (%d,%d,s%d,t%d,m%d,cg%d) ratio %.3f  pred(best) %.4f"
               % (k, best["ms"], best["tileN"], best["tileK"], best["stages"], best["inner"], best["mode"],
-                 pick["ms"], pick["tileN"], pick["tileK"], pick["stages"], pick["inner"], pick["mode"], ratio,
-                 pred_best))
+                 best.get("cg", 1), pick["ms"], pick["tileN"], pick["tileK"], pick["stages"], pick["inner"],
+                 pick["mode"], pick.get("cg", 1), ratio, pred_best))
     print("worst pick/best:", round(worst, 3))
 
 

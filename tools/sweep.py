@@ -41,9 +41,9 @@ def main():
         d = alcop.gemm_desc(M, N, K, b, alcop.BF16, alcop.BF16, alcop.B_KN)
         flops = 2.0 * M * N * K * b
         iters = 3 if flops > 1e12 else (10 if flops > 1e11 else 30)
-        for tN, tK, st, inner, mode in itertools.product([64, 128, 192, 256], [32, 64, 128], range(1, 9), [1, 2],
-                                                         [alcop.MODE_FUSED, alcop.MODE_WRAP]):
-            s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode)
+        for cg, tN, tK, st, inner, mode in itertools.product([1, 2], [64, 128, 192, 256], [32, 64, 128], range(1, 9),
+                                                             [1, 2], [alcop.MODE_FUSED, alcop.MODE_WRAP]):
+            s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
             try:
                 alcop.validate(d, s)
             except alcop.AlcopError:
@@ -61,7 +61,7 @@ def main():
                 continue
             pred = alcop.predict(d, s)["seconds"] * 1e3
             res.append({"M": M, "N": N, "K": K, "batch": b, "tileN": tN, "tileK": tK, "stages": st, "inner": inner,
-                        "mode": mode, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12, "pred_ms": pred})
+                        "mode": mode, "cg": cg, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12, "pred_ms": pred})
         pick = alcop.choose_schedule(d)
         best = min([r for r in res if (r["M"], r["N"], r["K"], r["batch"]) == (M, N, K, b)], key=lambda r: r["ms"])
         print("%dx%dx%dx%d best %.1f TF (%s) pick %s" % (M, N, K, b, best["tflops"], best, pick), flush=True)
