@@ -391,33 +391,37 @@ def main_gpu(args, rank, world, local_rank):
                 launch(A, B, C, s, (M, N, K))
             best = None
             cands = []
-            for st in range(1, 6):
-                for tn, tk in ((base.tileN, base.tileK), (128, 64), (256, 64), (128, 128), (256, 128), (192, 64)):
-                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, n_stage_inner=2 if st > 1 else 1)
+            for st in range(1, 7):
+                for tn, tk, cg in ((base.tileN, base.tileK, base.cta_group), (128, 64, 1), (256, 64, 1),
+                                   (128, 128, 1), (256, 128, 1), (192, 64, 1), (256, 64, 2), (128, 64, 2)):
+                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, n_stage_inner=2 if st > 1 else 1,
+                                            cta_group=cg)
                     try:
                         alcop.validate(descs[(M, N, K)], s)
                     except alcop.AlcopError:
                         continue
-                    cands.append((st, tn, tk, s))
-            for st, tn, tk, s in cands:
+                    cands.append((st, tn, tk, cg, s))
+            for st, tn, tk, cg, s in cands:
                 ms = time_graph(lambda i, s=s: run_on(i, s), iters=24, warmup=3)
                 tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
-                rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "tflops": round(tf, 1)})
+                rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "cta_group": cg, "tflops": round(tf, 1)})
                 if best is None or tf > best[0]:
-                    best = (tf, st, tn, tk)
+                    best = (tf, st, tn, tk, cg)
             ms_pick = time_graph(lambda i: run_on(i, base), iters=24, warmup=3)
             tf_pick = 2.0 * M * N * K / (ms_pick * 1e-3) / 1e12
             by_stage = {}
             for r in rows:
-                if r["tileN"] == base.tileN and r["tileK"] == base.tileK:
-                    by_stage[r["n_stage"]] = r["tflops"]
+                if (r["tileN"], r["tileK"], r["cta_group"]) == (base.tileN, base.tileK, base.cta_group):
+                    by_stage[r["n_stage"]] = max(by_stage.get(r["n_stage"], 0), r["tflops"])
             s1 = max([r["tflops"] for r in rows if r["n_stage"] == 1] or [float("nan")])
             sweep["%dx%dx%d" % (M, N, K)] = {
                 "tflops_by_n_stage_model_tile": by_stage,
                 "best_n_stage1_tflops": s1,
-                "best_swept": {"tflops": round(best[0], 1), "n_stage": best[1], "tileN": best[2], "tileK": best[3]},
+                "best_swept": {"tflops": round(best[0], 1), "n_stage": best[1], "tileN": best[2], "tileK": best[3],
+                               "cta_group": best[4]},
                 "model_pick": {"tflops": round(tf_pick, 1), **{k: v for k, v in base.as_dict().items()
-                                                              if k in ("tileN", "tileK", "n_stage_smem_A")}},
+                                                              if k in ("tileN", "tileK", "n_stage_smem_A",
+                                                                       "cta_group")}},
                 "model_pick_over_best_time": round(best[0] / tf_pick, 3),
                 "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
         extra["n_stage_sweep"] = sweep

@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         buf ^= 1;
       }
     }
-    if (lane == 0) bulk_wait_group<0>();
+    if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
     __syncwarp();
     if (warp == 2 && lane == 0) stamp<kDebug>(p, 6);
   }
@@ -598,6 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
+  if (threadIdx.x == 0) stamp<true>(p, 0);
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tmA);
@@ -626,6 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   grid_dependency_wait();
   grid_launch_dependents();
+  if (threadIdx.x == 0) stamp<true>(p, 1);
 
   const int cluster_id = static_cast<int>(blockIdx.x) >> 1;
   const int nclusters = static_cast<int>(gridDim.x) >> 1;
@@ -712,6 +714,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
           ca.phase ^= 1u << slot;
           tc_fence_after();
+          if (tl == 0 && v == 0 && lane == 0) stamp<true>(p, 3);
           const uint64_t ad = adesc0 + slot * a_stage16;
           const uint64_t bd = bdesc0 + slot * b_stage16;
           ISSUE(
@@ -724,6 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ca.advance(p.sA);
         }
         ISSUE(umma_commit_pair_multicast(smem_u32(&tfull[acc]), 0x3));
+        if (tl == my_tiles - 1 && lane == 0) stamp<true>(p, 4);
         if (wrap) {
           // drain the s-1 wrapped tail groups (no MMA): release both CTAs' slots
           for (int d = 0; d < p.sA - 1; ++d) {
@@ -748,6 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
       tc_fence_after();
+      if (tl == 0 && warp == 2 && lane == 0) stamp<true>(p, 5);
       const TileCoord tc = tile_coord(p, cluster_id + tl * nclusters);
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c) {
@@ -788,8 +793,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         buf ^= 1;
       }
     }
-    if (lane == 0) bulk_wait_group<0>();
+    if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
     __syncwarp();
+    if (warp == 2 && lane == 0) stamp<true>(p, 6);
   }
 
   tc_fence_before();
@@ -798,6 +804,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, p.tmem_cols);
   }
+  if (threadIdx.x == 0) stamp<true>(p, 7);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {

@@ -20,12 +20,13 @@ def main():
     M, N, K, tN, tK, st = map(int, sys.argv[1:7])
     inner = int(sys.argv[7]) if len(sys.argv) > 7 else 2
     mode = int(sys.argv[8]) if len(sys.argv) > 8 else 1
+    cg = int(sys.argv[9]) if len(sys.argv) > 9 else 1
     lib = alcop.load_library()
     lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode)
+    s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
     stamps = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
     for _ in range(3):
         alcop.matmul(A, B, s, out=C)
