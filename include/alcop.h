@@ -180,6 +180,18 @@ int64_t alcop_smem_bytes(const alcop_gemm_desc* w, const alcop_schedule* s);
 int alcop_enumerate_pipeline(int64_t num_tiles, int64_t E, int32_t sA, int32_t sB, int32_t mode,
                              int32_t role, alcop_event* out, int64_t cap, int64_t* count);
 
+/* ---- reference IR front end ---------------------
+ * Parses a program in the reference's textual IR (the
+ * `pipec schedule` output = lower() with `stages` hints, schedule.hpp:357-584),
+ * recognises the lowered GEMM / batched-GEMM nest and returns the problem and
+ * schedule that run it on B200 (mode WRAP = the pass's own emission, f16 in,
+ * f32 out = the interpreter's exact sums).  Parse errors -> ALCOP_ERR_PARSE
+ * ("ParseError: ... (line L, col C)", parser.hpp:22-454); an already
+ * transformed program -> ALCOP_ERR_ANALYSIS "AlreadySynchronized"
+ * (pipeline_pass.hpp:191-196).  `info` (may be NULL) receives a summary. */
+int alcop_ir_to_gemm(const char* ir_text, alcop_gemm_desc* desc, alcop_schedule* sched, char* info,
+                     size_t info_len);
+
 /* ---- compute entry points (device pointers, caller-owned stream) ------ */
 /* Pipelined matmul: gemm_schedule -> lower -> transform -> run
  * (schedule.hpp:73,357; pipeline_pass.hpp:753; interp.hpp:440) as one

@@ -152,7 +152,7 @@ def gen_gemm(outdir):
         with tempfile.TemporaryDirectory() as tmp:
             run(["gemm", "--M", str(M), "--N", str(N), "--K", str(K), "--batch", str(batch), "--script",
                  os.path.join(d, "script.txt"), "--outdir", tmp, "--mode", mode, "--seed", "0"])
-            for f in ("plan.json", "run.json", "transformed.ir", "warnings.json"):
+            for f in ("plan.json", "run.json", "lowered.ir", "transformed.ir", "warnings.json"):
                 shutil.copy(os.path.join(tmp, f), os.path.join(d, f))
             big = M * N * K * batch > 1 << 20
             if not big:

@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = [
     "alcop_version", "alcop_last_error", "alcop_schedule_default", "alcop_parse_schedule_script",
     "alcop_validate", "alcop_smem_bytes", "alcop_enumerate_pipeline", "alcop_gemm", "alcop_gemm_traced",
     "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_conv2d", "alcop_hw_default_b200",
-    "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule",
+    "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
 ]
 
 
@@ -155,6 +155,7 @@ def load_library(path: str | None = None):
     lib.alcop_hw_default_a100_reference.restype = None
     lib.alcop_predict.argtypes = [P(GemmDesc), P(Schedule), P(HW), P(Breakdown)]
     lib.alcop_choose_schedule.argtypes = [P(GemmDesc), P(HW), P(Schedule)]
+    lib.alcop_ir_to_gemm.argtypes = [ctypes.c_char_p, P(GemmDesc), P(Schedule), ctypes.c_char_p, ctypes.c_size_t]
     if path is None:
         _lib = lib
     return lib
@@ -405,3 +406,29 @@ def choose_conv_schedule(gview: GemmDesc, hw: HW | None = None) -> Schedule:
     if best_s is None:
         raise AlcopError(ALCOP_ERR_CONFIG, "Unschedulable: no conv schedule")
     return best_s
+
+
+def ir_to_gemm(ir_text: str):
+    """Reference IR (`pipec schedule` output) -> (GemmDesc, Schedule, info)."""
+    d, s = GemmDesc(), Schedule()
+    buf = ctypes.create_string_buffer(512)
+    _check(load_library().alcop_ir_to_gemm(ir_text.encode(), ctypes.byref(d), ctypes.byref(s), buf, len(buf)))
+    return d, s, buf.value.decode()
+
+
+def run_ir(ir_text: str, inputs: dict, stream=None):
+    """The reference's `run` workflow on B200: inputs {"A": int/float array, "B": ...}
+    laid out as the IR declares them; returns {"C": float32 array} (exact for the
+    reference's integer inputs)."""
+    import numpy as np
+    import torch
+    d, s, _ = ir_to_gemm(ir_text)
+    A = torch.as_tensor(np.asarray(inputs["A"], dtype=np.float32)).to(torch.float16).cuda()
+    B = torch.as_tensor(np.asarray(inputs["B"], dtype=np.float32)).to(torch.float16).cuda()
+    shp = ((d.batch,) if d.batch > 1 else ()) + (d.M, d.N)
+    C = torch.empty(shp, dtype=torch.float32, device="cuda")
+    _check(load_library().alcop_gemm(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
+                                     ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                     _stream_ptr(stream)))
+    torch.cuda.synchronize()
+    return {"C": C.cpu().numpy()}
