@@ -72,7 +72,8 @@ typedef struct {
   int32_t in_dtype;  /* alcop_dtype: F16 or BF16 */
   int32_t out_dtype; /* alcop_dtype: F32, F16 or BF16 */
   int32_t b_layout;  /* alcop_b_layout */
-  int32_t reserved0;
+  int32_t pre_op;    /* 0, or 1 = gemm_schedule(w, preOp=true): the mma reads f(A) = 2A+1
+                        (the reference's "ew" tag, interp.hpp:363, schedule.hpp:73-86) */
   int64_t lda, ldb, ldc;
   int64_t stride_a, stride_b, stride_c;
 } alcop_gemm_desc;

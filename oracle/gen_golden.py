@@ -30,6 +30,19 @@ def script_text(split, hints, reg=False):
     return "\n".join(lines) + "\n"
 
 
+def preop_script(split, hints, inline=True, reg=False):
+    """gemm_schedule(w, preOp=true): S2 = ew(A) feeds the mma (schedule.hpp:73-86)."""
+    lines = ["cache_read S2 shared", "cache_read B shared"]
+    if reg:
+        lines += ["cache_read S2_shared register", "cache_read B_shared register"]
+    lines.append("tile C " + " ".join("%s=%d" % kv for kv in split))
+    for buf, n in hints:
+        lines.append("pipeline %s %d" % (buf, n))
+    if inline:
+        lines.append("inline S2")
+    return "\n".join(lines) + "\n"
+
+
 def split_of(M, N, K, tm, tn, ko, ki):
     return [("i0", M // tm), ("i1", tm), ("j0", N // tn), ("j1", tn), ("ko", ko), ("ki", ki)]
 
@@ -57,6 +70,15 @@ GEMM_CASES = [
     ("t_b2", 8, 8, 16, 2, 8, 8, 4, 4, 3, 3, 2, 2, "stale"),
     # BASELINE config 1 exactly: fp16 512^3, tile 128x128x32, 2 smem + 2 inner stages
     ("config1", 512, 512, 512, 1, 128, 128, 16, 32, 2, 2, 2, 2, "stale"),
+]
+
+# pre-op programs (name, M, N, K, batch, script, mode): inline case 2 (mma_ewa) and the
+# un-inlined (materialised S2) form
+PREOP_CASES = [
+    ("p8_inline", 8, 8, 8, 1, None, "strict"),
+    ("p16_inline_33", 16, 16, 16, 1, None, "strict"),
+    ("p16_materialised", 16, 16, 16, 1, None, "strict"),
+    ("p16_inline_b2", 16, 8, 16, 2, None, "strict"),
 ]
 
 # schedule-surface cases: (name, M, N, K, batch, script)
@@ -93,6 +115,23 @@ SCRIPT_CASES = [
     ("one_level_k", 64, 64, 64, 1, "cache_read A shared\ncache_read B shared\ntile C i0=2 i1=32 j0=2 j1=32 ko=8\n"
                                    "pipeline A_shared 4\npipeline B_shared 2\n"),
     ("reg_only_hint", 64, 64, 64, 1, script_text(split_of(64, 64, 64, 32, 32, 4, 16), [("A_reg", 2)], reg=True)),
+]
+# (name, M, N, K, batch, script) with gemm_schedule(w, preOp=true)
+PREOP_SCRIPT_CASES = [
+    ("pre_inline_after_pipeline", 64, 64, 64, 1,
+     preop_script(split_of(64, 64, 64, 32, 32, 4, 16), [("S2_shared", 3), ("B_shared", 3)])),
+    ("pre_inline_before_pipeline", 64, 64, 64, 1,
+     "cache_read S2 shared\ncache_read B shared\ntile C i0=2 i1=32 j0=2 j1=32 ko=4 ki=16\ninline S2\n"
+     "pipeline S2_shared 2\n"),
+    ("pre_materialised", 64, 64, 64, 1,
+     preop_script(split_of(64, 64, 64, 32, 32, 4, 16), [("S2_shared", 2), ("B_shared", 2)], inline=False)),
+    ("pre_inline_twice", 64, 64, 64, 1,
+     preop_script(split_of(64, 64, 64, 32, 32, 4, 16), [("S2_shared", 2)]) + "inline S2\n"),
+    ("pre_inline_no_consumer", 64, 64, 64, 1, "tile C i0=2 i1=32 j0=2 j1=32 ko=4 ki=16\ninline S2\n"),
+    ("pre_inline_binary", 64, 64, 64, 1, "inline C\n"),
+    ("pre_two_level", 64, 64, 64, 1,
+     preop_script(split_of(64, 64, 64, 32, 32, 4, 16), [("S2_shared", 3), ("B_shared", 3), ("S2_reg", 2),
+                                                         ("B_reg", 2)], reg=True)),
 ]
 
 # model queries (SPEC.md:438-475 examples, then a deterministic grid)
@@ -178,6 +217,38 @@ def gen_gemm(outdir):
         print("gemm", name, file=sys.stderr)
     with open(os.path.join(outdir, "index.json"), "w") as f:
         json.dump(index, f, indent=1)
+    pre = []
+    gen_preop(outdir, pre)
+    with open(os.path.join(outdir, "preop_index.json"), "w") as f:
+        json.dump(pre, f, indent=1)
+
+
+def _preop_text(name, M, N, K):
+    if name == "p8_inline":
+        return preop_script(split_of(M, N, K, 4, 4, 4, 2), [("S2_shared", 2), ("B_shared", 2)])
+    if name == "p16_inline_33":
+        return preop_script(split_of(M, N, K, 8, 8, 8, 2), [("S2_shared", 3), ("B_shared", 3)])
+    if name == "p16_materialised":
+        return preop_script(split_of(M, N, K, 8, 8, 8, 2), [("S2_shared", 3), ("B_shared", 3)], inline=False)
+    return preop_script(split_of(M, N, K, 8, 4, 4, 4), [("S2_shared", 2), ("B_shared", 2)])
+
+
+def gen_preop(outdir, index):
+    for (name, M, N, K, batch, _, mode) in PREOP_CASES:
+        text = _preop_text(name, M, N, K)
+        d = os.path.join(outdir, name)
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, "script.txt"), "w") as f:
+            f.write(text)
+        with tempfile.TemporaryDirectory() as tmp:
+            run(["gemm", "--M", str(M), "--N", str(N), "--K", str(K), "--batch", str(batch), "--script",
+                 os.path.join(d, "script.txt"), "--outdir", tmp, "--mode", mode, "--seed", "0", "--preop", "1"])
+            for f in ("plan.json", "run.json", "lowered.ir", "transformed.ir", "warnings.json", "walk.jsonl",
+                      "trace.jsonl"):
+                shutil.copy(os.path.join(tmp, f), os.path.join(d, f))
+            C = np.fromfile(os.path.join(tmp, "C.bin"), dtype=np.int64)
+            np.savez_compressed(os.path.join(d, "C.npz"), C=C.astype(np.int32))
+        index.append({"name": name, "M": M, "N": N, "K": K, "batch": batch, "preop": 1, "mode": mode, "seed": 0})
 
 
 def gen_scripts(path):
@@ -190,6 +261,15 @@ def gen_scripts(path):
             r = run(["script", "--M", str(M), "--N", str(N), "--K", str(K), "--batch", str(batch), "--script", p])
             res = json.loads(r.stdout)
             out.append({"name": name, "M": M, "N": N, "K": K, "batch": batch, "script": text, "result": res})
+        for (name, M, N, K, batch, text) in PREOP_SCRIPT_CASES:
+            p = os.path.join(tmp, name + ".txt")
+            with open(p, "w") as f:
+                f.write(text)
+            r = run(["script", "--M", str(M), "--N", str(N), "--K", str(K), "--batch", str(batch), "--script", p,
+                     "--preop", "1"])
+            res = json.loads(r.stdout)
+            out.append({"name": name, "M": M, "N": N, "K": K, "batch": batch, "script": text, "result": res,
+                        "preop": 1})
     with open(path, "w") as f:
         for o in out:
             f.write(json.dumps(o) + "\n")

@@ -197,9 +197,10 @@ int cmd_gemm(const std::map<std::string, std::string>& a) {
   uint64_t seed = a.count("seed") ? std::stoull(a.at("seed")) : 0;
   bool doRun = !a.count("no-run");
   ExecMode mode = (a.count("mode") && a.at("mode") == "stale") ? ExecMode::StaleRead : ExecMode::Strict;
+  const bool preOp = a.count("preop") && a.at("preop") == "1";
 
   std::vector<std::string> warnings;
-  ScheduleState st = apply_script(gemm_schedule(w, false), script, &warnings);
+  ScheduleState st = apply_script(gemm_schedule(w, preOp), script, &warnings);
   Program p = lower(st);
   PipelinePlan plan = analyze_pipelines(p);
   Program q = transform(p);
@@ -251,9 +252,10 @@ int cmd_script(const std::map<std::string, std::string>& a) {
   w.K = std::stoll(a.at("K"));
   w.batch = a.count("batch") ? std::stoll(a.at("batch")) : 1;
   std::string script = read_file(a.at("script"));
+  const bool preOp = a.count("preop") && a.at("preop") == "1";
   std::vector<std::string> warnings;
   try {
-    ScheduleState st = apply_script(gemm_schedule(w, false), script, &warnings);
+    ScheduleState st = apply_script(gemm_schedule(w, preOp), script, &warnings);
     Program p = lower(st);
     PipelinePlan plan = analyze_pipelines(p);
     Program q = transform(p);

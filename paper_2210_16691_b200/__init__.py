@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = [
 class GemmDesc(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64), ("batch", ctypes.c_int64),
                 ("in_dtype", ctypes.c_int32), ("out_dtype", ctypes.c_int32), ("b_layout", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64),
+                ("pre_op", ctypes.c_int32), ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64),
                 ("ldc", ctypes.c_int64), ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
                 ("stride_c", ctypes.c_int64)]
 
@@ -275,8 +275,10 @@ def _require_cuda(*ts):
             raise RuntimeError("alcop compute entry points take CUDA tensors (no CPU fallback)")
 
 
-def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, out=None, stream=None):
-    """Pipelined matmul C = A @ B (or batched) through alcop_gemm.
+def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, out=None, stream=None, pre_op=0):
+    """Pipelined matmul C = A @ B (or batched) through alcop_gemm; pre_op=1
+    computes C = (2A+1) @ B with f fused into the pipeline (the reference's
+    inlined elementwise pre-op).
 
     A: [M,K] or [b,M,K]; B: [K,N] / [b,K,N] (b_layout B_KN, the reference
     layout) or [N,K] / [b,N,K] (B_NK).  fp16/bf16 in, fp32 accumulate."""
@@ -291,8 +293,15 @@ def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, o
         out = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, device=A.device)
     A = A.contiguous()
     B = B.contiguous()
-    d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout)
-    s = sched if sched is not None else choose_schedule(d)
+    d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout, pre_op=pre_op)
+    if sched is not None:
+        s = sched
+    elif pre_op:
+        s = choose_schedule(gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout))
+        if s.cta_group == 2:
+            s = make_schedule(tileN=s.tileN, tileK=s.tileK, n_stage=s.n_stage_smem_A, n_stage_inner=s.n_stage_inner)
+    else:
+        s = choose_schedule(d)
     _check(load_library().alcop_gemm(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
                                      ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                      _stream_ptr(stream)))
@@ -411,7 +420,7 @@ def choose_conv_schedule(gview: GemmDesc, hw: HW | None = None) -> Schedule:
 def ir_to_gemm(ir_text: str):
     """Reference IR (`pipec schedule` output) -> (GemmDesc, Schedule, info)."""
     d, s = GemmDesc(), Schedule()
-    buf = ctypes.create_string_buffer(512)
+    buf = ctypes.create_string_buffer(512)  # noqa
     _check(load_library().alcop_ir_to_gemm(ir_text.encode(), ctypes.byref(d), ctypes.byref(s), buf, len(buf)))
     return d, s, buf.value.decode()
 

@@ -33,7 +33,7 @@ int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
   const int64_t cg = s.cta_group == 2 ? 2 : 1;
   const int64_t a_stage = kTileM * s.tileK * 2;         // per CTA: 128 rows of A
   const int64_t b_stage = s.tileN / cg * s.tileK * 2;   // per CTA: tileN/cta_group columns of B
-  const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;
+  const int64_t bars = 8 * (3 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;  // + ready[] (pre-op)
   const int64_t staging = 4 * 2 * 32 * 128;  // epilogue TMA-store staging
   return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + staging + bars;
 }
@@ -51,6 +51,10 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadDtype", "output dtype must be F32, F16 or BF16");
   if (w.b_layout != ALCOP_B_KN && w.b_layout != ALCOP_B_NK)
     return set_error(ALCOP_ERR_CONFIG, "BadLayout", "b_layout must be KN or NK");
+  if (w.pre_op != 0 && w.pre_op != 1)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "pre_op must be 0 or 1 (f(x) = 2x+1)");
+  if (w.pre_op && (s.cta_group != 1 || s.n_stage_smem_A != s.n_stage_smem_B))
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the fused pre-op needs cta_group 1 and equal stage counts");
   if (s.cta_group != 1 && s.cta_group != 2)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "cta_group must be 1 or 2");
   if (s.tileM != kTileM * s.cta_group)

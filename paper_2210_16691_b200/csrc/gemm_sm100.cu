@@ -57,6 +57,8 @@ struct GemmKParams {
   // reduction chunk = (r, s, channel block) matching the KRSC filter layout
   int32_t conv_P, conv_Q, conv_S, conv_Cb;
   int32_t conv_sh, conv_sw, conv_ph, conv_pw;
+  int32_t in_bf16;  // fused pre-op arithmetic type
+  int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
 };
 
 // debug timeline buffer (set through alcop_debug_set_stamps)
@@ -70,6 +72,7 @@ static bool g_pdl = [] {
 namespace {
 
 constexpr int kThreads = 192;
+constexpr int kThreadsPreOp = 192 + 128;  // + 4 transform warps for the fused pre-op
 constexpr int kStagingBytes = 4 * 2 * 32 * 128;
 
 struct TileCoord {
@@ -142,6 +145,20 @@ __device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n
   }
 }
 
+// f(x) = 2x + 1 on a packed pair of f16 / bf16 values (RNE back to the input type)
+__device__ __forceinline__ uint32_t pre_op_pair(uint32_t v, int bf16) {
+  if (bf16) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
+    float2 f = __bfloat1622float2(h);
+    __nv_bfloat162 r = __floats2bfloat162_rn(fmaf(2.f, f.x, 1.f), fmaf(2.f, f.y, 1.f));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+  __half2 h = *reinterpret_cast<__half2*>(&v);
+  float2 f = __half22float2(h);
+  __half2 r = __floats2half2_rn(fmaf(2.f, f.x, 1.f), fmaf(2.f, f.y, 1.f));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
 template <typename OutT>
 __device__ __forceinline__ uint32_t pack2(uint32_t a, uint32_t b);
 template <>
@@ -173,8 +190,8 @@ struct RingCursor {
 // equal); otherwise each buffer has its own ring and lookahead.  kDebug
 // compiles in the bookkeeping trace and the timeline stamps.
 // ---------------------------------------------------------------------------
-template <typename OutT, int BK, bool kJoint, bool kDebug, bool kConv = false>
-__global__ void __launch_bounds__(kThreads, 1)
+template <typename OutT, int BK, bool kJoint, bool kDebug, bool kConv = false, bool kPreOp = false>
+__global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
   using namespace ptx;
@@ -199,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* emptyB = kJoint ? emptyA : fullB + p.sB;
   uint64_t* tfull = bars + 2 * p.sA + 2 * p.sB;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // fused pre-op: transform warps turn full[slot] (raw A landed) into ready[slot] (f(A) in place)
+  uint64_t* ready = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + (kPreOp ? p.sA : 0));
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
@@ -226,6 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(smem_u32(&tfull[i]), 1);
         mbar_init(smem_u32(&tempty[i]), 4);
       }
+      if (kPreOp)
+        for (int i = 0; i < p.sA; ++i) mbar_init(smem_u32(&ready[i]), 4);
       fence_barrier_init();
     }
     __syncwarp();
@@ -425,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = ca.slot, sb = kJoint ? ca.slot : cb.slot;
           uint32_t pa, pb;
           if constexpr (kJoint) {
-            pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A (+B: same barrier)
+            pa = cwait(ca, kPreOp ? ready : fullA, 0, tl, v);  // consumer_wait A (+B: same barrier)
             pb = pa;
             ++cb.count;
             ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
@@ -470,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kJoint) {
             for (int d = 0; d < p.sA - 1; ++d) {
               const uint32_t slot = ca.slot;
-              const uint32_t par = cwait(ca, fullA, 0, tl, (E + d) % E);
+              const uint32_t par = cwait(ca, kPreOp ? ready : fullA, 0, tl, (E + d) % E);
               ++cb.count;
               ++ca.released;
               ++cb.released;
@@ -488,6 +509,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
+  } else if (kPreOp && warp >= 6) {
+    // ======================= fused elementwise pre-op (warps 6-9) =======================
+    // The reference's `inline S2` case 2 (schedule.hpp:275-314) turns the
+    // consumer into mma_ewa: acc + f(a)*b with f(x) = 2x+1 (interp.hpp:367-369).
+    // Here f is applied once per element, in place in the landed A slot,
+    // between consumer_wait (full) and the MMA (ready): elementwise, so the
+    // 128B swizzle of the slot does not matter.
+    const int tw = warp - 6;
+    RingCursor cr;
+    const uint32_t quarter = p.a_stage_bytes / 4;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      if (wrap) cr.slot = 0;
+      const int uses = E + (wrap ? p.sA - 1 : 0);
+      for (int i = 0; i < uses; ++i) {
+        const uint32_t slot = cr.slot, par = (cr.phase >> slot) & 1u;
+        mbar_wait(smem_u32(&fullA[slot]), par);
+        cr.phase ^= 1u << slot;
+        if (i < E) {
+          const uint32_t base = ringA + slot * p.a_stage_bytes + tw * quarter;
+          for (uint32_t off = lane * 16; off < quarter; off += 32 * 16) {
+            uint32_t v[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                         : "r"(base + off));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = pre_op_pair(v[j], p.in_bf16);
+            st_shared_v4(base + off, v[0], v[1], v[2], v[3]);
+          }
+          fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 (async proxy)
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&ready[slot]));
+        cr.advance(p.sA);
+      }
+    }
   } else {
     // ======================= epilogue (warps 2-5) =======================
     // TMEM -> registers (tcgen05.ld) -> 128B-swizzled smem staging -> TMA
@@ -837,15 +893,15 @@ int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint6
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK, bool kJoint, bool kDebug>
+template <typename OutT, int BK, bool kJoint, bool kDebug, bool kPreOp = false>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                  int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug>;
+  auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug, false, kPreOp>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kPreOp ? kThreadsPreOp : kThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -908,6 +964,12 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
                    int grid, int smem, cudaStream_t st) {
   const bool joint = kp.sA == kp.sB;
   const bool debug = kp.trace != nullptr || kp.stamps != nullptr;
+  if (kp.pre_op) {
+    if (!joint || debug)
+      return set_error(ALCOP_ERR_CONFIG, "Unsupported",
+                       "the fused pre-op needs equal A/B stage counts and no debug trace");
+    return launch_typed<OutT, BK, true, false, true>(ta, tb, tc, kp, grid, smem, st);
+  }
   if (joint) {
     return debug ? launch_typed<OutT, BK, true, true>(ta, tb, tc, kp, grid, smem, st)
                  : launch_typed<OutT, BK, true, false>(ta, tb, tc, kp, grid, smem, st);
@@ -999,6 +1061,8 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.trace = trace;
   kp.trace_cap = static_cast<int32_t>(trace_cap);
   kp.stamps = g_stamps;
+  kp.in_bf16 = w.in_dtype == ALCOP_BF16 ? 1 : 0;
+  kp.pre_op = w.pre_op;
 
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
@@ -1006,6 +1070,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cg == 2) {
+    if (w.pre_op) return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the fused pre-op runs with cta_group 1");
     if (trace != nullptr)
       return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the device trace is implemented for cta_group 1");
     grid = (grid / 2) * 2;

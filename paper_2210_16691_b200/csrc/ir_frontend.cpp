@@ -366,10 +366,11 @@ void recognise(Parser& P, alcop_gemm_desc& d, alcop_schedule& s, std::string& in
   if (f.sync)
     throw Err{ALCOP_ERR_ANALYSIS, "AlreadySynchronized",
               "program already contains pipeline synchronization (pass the hinted, untransformed nest)"};
-  bool fused = false;
-  for (const auto& t : f.tags) fused |= t == "mma_ewa";
-  if (fused)
-    throw Err{ALCOP_ERR_CONFIG, "Unsupported", "inline pre-op (mma_ewa) is not implemented on the B200 path yet"};
+  // elementwise pre-op: inlined into the consumer (mma_ewa) or materialised
+  // as S2 = ew(A) (schedule.hpp:393-407); both run as the fused pre-op
+  bool pre = false;
+  for (const auto& t : f.tags) pre |= (t == "mma_ewa" || t == "ew");
+  d.pre_op = pre ? 1 : 0;
   s = alcop_schedule{};
   alcop_schedule_default(&s);
   s.tileM = Creg.shape[0];
@@ -378,15 +379,17 @@ void recognise(Parser& P, alcop_gemm_desc& d, alcop_schedule& s, std::string& in
     auto it = P.bufs.find(n);
     return it == P.bufs.end() ? 0 : it->second.stages;
   };
-  auto it = P.bufs.find("A_shared");
+  const char* aSh = P.bufs.count("S2_shared") ? "S2_shared" : "A_shared";
+  const char* aReg = P.bufs.count("S2_reg") ? "S2_reg" : "A_reg";
+  auto it = P.bufs.find(aSh);
   if (it != P.bufs.end())
     s.tileK = it->second.shape[1];
   else if (f.loops.count("ko"))
     s.tileK = d.K / f.loops["ko"];
   else
     s.tileK = d.K;
-  const int sA = stages_of("A_shared"), sB = stages_of("B_shared");
-  const int tA = stages_of("A_reg"), tB = stages_of("B_reg");
+  const int sA = stages_of(aSh), sB = stages_of("B_shared");
+  const int tA = stages_of(aReg), tB = stages_of("B_reg");
   s.n_stage_smem_A = sA ? sA : 1;
   s.n_stage_smem_B = sB ? sB : 1;
   s.n_stage_inner = std::min(std::max({tA, tB, 1}), 2);
@@ -397,7 +400,7 @@ void recognise(Parser& P, alcop_gemm_desc& d, alcop_schedule& s, std::string& in
     if (ss >= 2 && tt >= 2 && static_cast<int64_t>(tt - 1) > static_cast<int64_t>(ss - 1) * F)
       throw Err{ALCOP_ERR_ANALYSIS, "LookaheadExceedsOuter",
                 "inner pipeline looks ahead " + std::to_string(tt - 1) + " steps, more than the outer pipeline covers"};
-  info = "GEMM M=" + std::to_string(d.M) + " N=" + std::to_string(d.N) + " K=" + std::to_string(d.K) +
+  info = std::string(d.pre_op ? "pre-op (2A+1) " : "") + "GEMM M=" + std::to_string(d.M) + " N=" + std::to_string(d.N) + " K=" + std::to_string(d.K) +
          " batch=" + std::to_string(d.batch) + " tile " + std::to_string(s.tileM) + "x" + std::to_string(s.tileN) +
          "x" + std::to_string(s.tileK) + " stages A/B " + std::to_string(s.n_stage_smem_A) + "/" +
          std::to_string(s.n_stage_smem_B) + " inner " + std::to_string(s.n_stage_inner);

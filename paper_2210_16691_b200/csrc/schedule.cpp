@@ -79,7 +79,7 @@ struct State {
   }
 };
 
-// gemm_schedule (schedule.hpp:73-86), preOp = false
+// gemm_schedule (schedule.hpp:73-86); preOp adds S2 = ew(A) feeding the mma
 State gemm_schedule(const alcop_gemm_desc& w) {
   State s;
   s.M = w.M;
@@ -88,7 +88,12 @@ State gemm_schedule(const alcop_gemm_desc& w) {
   s.batch = w.batch;
   s.graph.push_back({"A", Node::Producer::ExternalInput, "", {}, "", Scope::Global, {}, false, -1});
   s.graph.push_back({"B", Node::Producer::ExternalInput, "", {}, "", Scope::Global, {}, false, -1});
-  s.graph.push_back({"C", Node::Producer::ComputeFrom, "", {"A", "B"}, "mma", Scope::Global, {}, false, -1});
+  std::string aSide = "A";
+  if (w.pre_op) {
+    s.graph.push_back({"S2", Node::Producer::ComputeFrom, "", {"A"}, "ew", Scope::Global, {}, false, -1});
+    aSide = "S2";
+  }
+  s.graph.push_back({"C", Node::Producer::ComputeFrom, "", {aSide, "B"}, "mma", Scope::Global, {}, false, -1});
   return s;
 }
 
@@ -235,14 +240,43 @@ State mark_pipeline(const State& s, const std::string& buffer, int stages) {
   return out;
 }
 
+// inline_tensor (schedule.hpp:275-314): case 2 (the consumer buffer is already
+// pipelined) re-sources the buffer to the tensor's input and fuses the
+// elementwise op into its consumer (mma -> mma_ewa); otherwise classic
+// inlining makes the buffer compute-produced (and rule 1 rejects it later).
 State inline_tensor(const State& s, const std::string& tensor) {
   const Node* t = s.find(tensor);
   if (!t) analysis("NoSuchTensor", "inline: tensor '" + tensor + "' not found");
   if (t->producer != Node::Producer::ComputeFrom || t->computeSrcs.size() != 1)
     analysis("NotElementwise", "inline: '" + tensor + "' is not unary elementwise");
-  // the GEMM family here has no elementwise pre-op (preOp = false), so no
-  // reachable tensor passes the check above; kept for rule-tag parity.
-  analysis("NoRewrite", "inline: '" + tensor + "' has no cache-read consumer");
+  const std::string src = t->computeSrcs[0];
+  const std::string tag = t->opTag;
+  State out = s;
+  bool consumed = false;
+  for (auto& n : out.graph) {
+    if (n.producer == Node::Producer::AsyncCopyFrom && n.copySrc == tensor) {
+      consumed = true;
+      if (n.stages) {
+        if (n.fusedPreOp)
+          analysis("NoRewrite", "inline: buffer '" + n.name + "' already carries a fused elementwise op");
+        n.copySrc = src;
+        n.fusedPreOp = true;
+      } else {
+        n.producer = Node::Producer::ComputeFrom;
+        n.computeSrcs = {src};
+        n.opTag = tag;
+        n.copySrc.clear();
+      }
+    } else {
+      for (auto& cs : n.computeSrcs)
+        if (cs == tensor) analysis("NoRewrite", "inline: v1 requires '" + tensor + "' to feed cache-read buffers");
+    }
+  }
+  if (!consumed) analysis("NoRewrite", "inline: '" + tensor + "' has no cache-read consumer");
+  out.graph.erase(std::remove_if(out.graph.begin(), out.graph.end(),
+                                 [&](const Node& n) { return n.name == tensor; }),
+                  out.graph.end());
+  return out;
 }
 
 State apply_script(const State& start, const std::string& script, std::vector<std::string>* warnings) {

@@ -176,3 +176,17 @@ def test_cta_pair_ragged_batched(alcop):
     _assert_exact(C, exact, torch.float32)
     C, exact = _run(alcop, 512, 768, 768, in_dt=torch.bfloat16, out_dt=torch.bfloat16, sched=s)
     _assert_exact(C, exact, torch.bfloat16)
+
+
+
+@pytest.mark.parametrize("tileN,tileK,st,mode", [(128, 64, 4, 1), (256, 64, 4, 0), (64, 32, 3, 1), (192, 128, 2, 1),
+                                                 (128, 64, 1, 1)])
+def test_fused_preop_exact(alcop, tileN, tileK, st, mode):
+    """C = (2A+1) @ B with f applied in shared memory between the TMA landing
+    and the MMA (the reference's inline S2 case 2, mma_ewa)."""
+    M, N, K = 384, 3 * tileN if tileN == 192 else 512, 320
+    a, b = gemm_inputs(M, N, K, seed=4)
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, n_stage_inner=2 if st > 1 else 1, mode=mode)
+    C = alcop.matmul(torch.from_numpy(a).to(torch.bfloat16).cuda(), torch.from_numpy(b).to(torch.bfloat16).cuda(),
+                     s, out_dtype=torch.float32, pre_op=1)
+    _assert_exact(C.cpu(), _exact(2 * a + 1, b, False), torch.float32)

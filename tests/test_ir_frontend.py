@@ -10,6 +10,7 @@ from oracle.splitmix import random_tensor
 from tests import golden_util as G
 
 CASES = G.gemm_cases()
+PRE = G.preop_cases()
 
 
 def _lowered(name):
@@ -62,3 +63,26 @@ def test_ir_runs_on_gpu_equal_to_interpreter(alcop, case):
     C = alcop.matmul(At, Bt, s, out_dtype=torch.float32)
     got = C.cpu().numpy().astype(np.int64).reshape(-1)
     assert np.array_equal(got, G.output_c(case["name"]).reshape(-1))
+
+
+@pytest.mark.parametrize("case", PRE, ids=lambda c: c["name"])
+def test_ir_preop_programs(alcop, case):
+    d, s, info = alcop.ir_to_gemm(_lowered(case["name"]))
+    assert d.pre_op == 1 and "pre-op" in info
+    sd = alcop.gemm_desc(case["M"], case["N"], case["K"], case["batch"], pre_op=1)
+    s2, _ = alcop.apply_script(sd, open(G.case_dir(case["name"]) + "/script.txt").read())
+    for f in ("tileM", "tileN", "tileK", "n_stage_smem_A", "n_stage_smem_B", "n_stage_inner"):
+        assert getattr(s, f) == getattr(s2, f), f
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", PRE, ids=lambda c: c["name"])
+def test_ir_preop_runs_on_gpu(alcop, case):
+    import torch
+    d, _, _ = alcop.ir_to_gemm(_lowered(case["name"]))
+    b, M, N, K = case["batch"], case["M"], case["N"], case["K"]
+    A = random_tensor(b * M * K, 0).reshape((b, M, K) if b > 1 else (M, K))
+    B = random_tensor(b * K * N, 1).reshape((b, K, N) if b > 1 else (K, N))
+    C = alcop.matmul(torch.from_numpy(A).to(torch.float16).cuda(), torch.from_numpy(B).to(torch.float16).cuda(),
+                     alcop.make_schedule(tileN=64, tileK=32, n_stage=2), out_dtype=torch.float32, pre_op=1)
+    assert np.array_equal(C.cpu().numpy().astype(np.int64).reshape(-1), G.output_c(case["name"]).reshape(-1))

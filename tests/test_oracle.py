@@ -206,3 +206,13 @@ def test_conv_oracle_equals_gemm_for_1x1():
     A = x.reshape(-1, 16).astype(np.int64)
     B = w.reshape(8, 16).T.astype(np.int64)
     assert np.array_equal(y.reshape(-1, 8).astype(np.int64), coracle.gemm_i64(A, B))
+
+
+@pytest.mark.parametrize("case", G.preop_cases(), ids=lambda c: c["name"])
+def test_preop_outputs_match_interpreter(case):
+    """gemm_schedule(w, preOp=true): C = mma(S2, B) with S2 = ew(A) = 2A+1
+    (interp.hpp:363, 367-369), inlined (mma_ewa) or materialised."""
+    M, N, K, b = case["M"], case["N"], case["K"], case["batch"]
+    A = random_tensor(b * M * K, case["seed"] + 0).reshape((b, M, K) if b > 1 else (M, K))
+    B = random_tensor(b * K * N, case["seed"] + 1).reshape((b, K, N) if b > 1 else (K, N))
+    assert np.array_equal(coracle.gemm_i64(2 * A + 1, B).reshape(-1), G.output_c(case["name"]).reshape(-1))

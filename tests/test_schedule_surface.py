@@ -11,15 +11,16 @@ CASES = G.scripts()
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: c["name"])
 def test_script_matches_reference(alcop, case):
-    desc = alcop.gemm_desc(case["M"], case["N"], case["K"], case["batch"])
+    desc = alcop.gemm_desc(case["M"], case["N"], case["K"], case["batch"], pre_op=case.get("preop", 0))
     res = case["result"]
     if res["ok"]:
         s, warns = alcop.apply_script(desc, case["script"])
         assert warns == []
         plan = {p["buffer"]: p for p in res["plan"]}
         for side, field in (("A", "n_stage_smem_A"), ("B", "n_stage_smem_B")):
-            want = plan[side + "_shared"]["stages"] if side + "_shared" in plan else 1
-            assert getattr(s, field) == want
+            names = [side + "_shared"] + (["S2_shared"] if side == "A" else [])
+            hit = [plan[n]["stages"] for n in names if n in plan]
+            assert getattr(s, field) == (hit[0] if hit else 1)
         regs = [p["stages"] for b, p in plan.items() if b.endswith("_reg")]
         assert s.n_stage_inner == (min(max(regs), 2) if regs else 1)
         assert s.mode == alcop.MODE_WRAP
