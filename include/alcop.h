@@ -224,6 +224,24 @@ int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop
                   alcop_breakdown* out);
 int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out);
 
+/* One measured candidate of the model-assisted tuner. */
+typedef struct {
+  alcop_schedule schedule;
+  double predicted_s; /* alcop_predict seconds */
+  double measured_s;  /* CUDA-event time per launch */
+} alcop_tune_trial;
+
+/* Model-assisted tuning on real B200 timings (tuner.hpp:363-531, the
+ * AnalyticalOnly method of tuner.hpp:407-413 with measure_ground_truth,
+ * pipe_sim.hpp:195-239, replaced by the GPU): enumerate the B200 space,
+ * rank by alcop_predict, time the top `budget` schedules on the caller's
+ * buffers (CUDA events on `stream`), return the fastest in *best.
+ * `trials` (may be NULL) receives up to `trials_cap` measured candidates in
+ * rank order; *n_trials their count. */
+int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, const void* A, const void* B, void* C,
+               void* stream, alcop_schedule* best, alcop_tune_trial* trials, int32_t trials_cap,
+               int32_t* n_trials);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = [
     "alcop_validate", "alcop_smem_bytes", "alcop_enumerate_pipeline", "alcop_gemm", "alcop_gemm_traced",
     "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_conv2d", "alcop_hw_default_b200",
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
+    "alcop_tune",
 ]
 
 
@@ -95,6 +96,10 @@ class Breakdown(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class TuneTrial(ctypes.Structure):
+    _fields_ = [("schedule", Schedule), ("predicted_s", ctypes.c_double), ("measured_s", ctypes.c_double)]
 
 
 class Event(ctypes.Structure):
@@ -156,6 +161,8 @@ def load_library(path: str | None = None):
     lib.alcop_predict.argtypes = [P(GemmDesc), P(Schedule), P(HW), P(Breakdown)]
     lib.alcop_choose_schedule.argtypes = [P(GemmDesc), P(HW), P(Schedule)]
     lib.alcop_ir_to_gemm.argtypes = [ctypes.c_char_p, P(GemmDesc), P(Schedule), ctypes.c_char_p, ctypes.c_size_t]
+    lib.alcop_tune.argtypes = [P(GemmDesc), P(HW), ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, P(Schedule), P(TuneTrial), ctypes.c_int32, P(ctypes.c_int32)]
     if path is None:
         _lib = lib
     return lib
@@ -441,3 +448,23 @@ def run_ir(ir_text: str, inputs: dict, stream=None):
                                      _stream_ptr(stream)))
     torch.cuda.synchronize()
     return {"C": C.cpu().numpy()}
+
+
+def tune(A, B, C, budget=8, b_layout=B_KN, hw: HW | None = None, stream=None):
+    """Model-assisted tuning on the GPU (alcop_tune): rank the B200 space with
+    the analytical model, time the top `budget` schedules on (A, B, C), return
+    (best schedule, [trials in model rank order])."""
+    batched = A.dim() == 3
+    M, K = A.shape[-2], A.shape[-1]
+    N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
+    d = gemm_desc(M, N, K, A.shape[0] if batched else 1, _dtype_code(A.dtype), _dtype_code(C.dtype), b_layout)
+    best = Schedule()
+    cap = max(1, budget)
+    arr = (TuneTrial * cap)()
+    n = ctypes.c_int32(0)
+    _check(load_library().alcop_tune(ctypes.byref(d), ctypes.byref(hw or hw_b200()), budget,
+                                     ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                     ctypes.c_void_p(C.data_ptr()), _stream_ptr(stream), ctypes.byref(best), arr, cap,
+                                     ctypes.byref(n)))
+    return best, [{"schedule": arr[i].schedule.as_dict(), "predicted_s": arr[i].predicted_s,
+                   "measured_s": arr[i].measured_s} for i in range(n.value)]

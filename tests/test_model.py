@@ -65,3 +65,21 @@ def test_model_pick_within_ten_percent_of_sweep(alcop):
     # all but at most one shape within 10%; none beyond 15%
     assert sum(r > 1.10 for r in ratios.values()) <= 1, ratios
     assert max(ratios.values()) <= 1.15, ratios
+
+
+@pytest.mark.gpu
+def test_model_assisted_tuning_on_gpu(alcop):
+    """tuner.hpp:407-413 (AnalyticalOnly) on real timings: the best of the
+    model's top-8 is within 5% of the best of its top-40 (a near-exhaustive
+    search of the well-ranked region)."""
+    import torch
+    M, N, K = 4096, 3072, 768
+    A = (torch.rand(M, K, device="cuda") - 0.5).to(torch.bfloat16)
+    B = (torch.rand(K, N, device="cuda") - 0.5).to(torch.bfloat16)
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    best8, t8 = alcop.tune(A, B, C, budget=8)
+    best40, t40 = alcop.tune(A, B, C, budget=40)
+    m8 = min(t["measured_s"] for t in t8)
+    m40 = min(t["measured_s"] for t in t40)
+    assert len(t8) == 8 and len(t40) == 40
+    assert m8 <= 1.05 * m40, (m8, m40, best8, best40)
