@@ -92,7 +92,7 @@ typedef struct {
   int32_t cta_group;           /* 1, or 2 = CTA pair (tcgen05 cta_group::2, tileM 256) */
   int32_t mode;                /* alcop_mode                             */
   int32_t num_ctas;            /* persistent grid; 0 = #SMs              */
-  int32_t raster;              /* reserved (tile rasterisation), 0       */
+  int32_t raster;              /* tile rows per raster group; 0 = auto  */
   int32_t reserved1;
 } alcop_schedule;
 

@@ -208,10 +208,11 @@ def default_schedule(**kw) -> Schedule:
 
 
 def make_schedule(tileN=256, tileK=64, n_stage=4, n_stage_inner=2, mode=MODE_FUSED, n_stage_B=None,
-                  num_ctas=0, cta_group=1) -> Schedule:
+                  num_ctas=0, cta_group=1, raster=0) -> Schedule:
     return default_schedule(tileM=128 * cta_group, tileN=tileN, tileK=tileK, n_stage_smem_A=n_stage,
                             n_stage_smem_B=n_stage if n_stage_B is None else n_stage_B,
-                            n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas, cta_group=cta_group)
+                            n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas, cta_group=cta_group,
+                            raster=raster)
 
 
 def apply_script(desc: GemmDesc, script: str):

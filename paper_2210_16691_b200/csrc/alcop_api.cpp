@@ -61,12 +61,14 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileM must be 128 x cta_group (UMMA M 128 / 256)");
   if (s.tileN != 64 && s.tileN != 128 && s.tileN != 192 && s.tileN != 256)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256");
-  if (s.cta_group == 2 && s.tileN != 128 && s.tileN != 256)
-    return set_error(ALCOP_ERR_CONFIG, "BadTile", "cta_group 2 needs tileN 128 or 256 (B split in halves of 64k)");
+  if (s.cta_group == 2 && s.tileN == 64)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "cta_group 2 needs tileN 128, 192 or 256");
   if (s.cta_group == 2 && s.n_stage_smem_A != s.n_stage_smem_B)
     return set_error(ALCOP_ERR_CONFIG, "BadStages", "cta_group 2 uses one joint A+B ring: equal stage counts");
   if (s.tileK != 32 && s.tileK != 64 && s.tileK != 128)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileK must be one of 32, 64, 128");
+  if (s.raster < 0 || s.num_ctas < 0)
+    return set_error(ALCOP_ERR_CONFIG, "BadRaster", "raster group and num_ctas must be >= 0");
   if (s.n_stage_smem_A < 1 || s.n_stage_smem_B < 1 || s.n_stage_smem_A > kMaxStages ||
       s.n_stage_smem_B > kMaxStages)
     return set_error(ALCOP_ERR_CONFIG, "BadStages", "shared-memory stages must be in [1, 16]");

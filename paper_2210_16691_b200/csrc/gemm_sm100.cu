@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -40,6 +41,7 @@ struct GemmKParams {
   int32_t M, N, K, batch;
   int32_t BN, BK;
   int32_t num_m, num_n, num_tiles;
+  int32_t group_m;  // raster: tile rows per group (>= num_m: plain m-fastest order)
   int32_t E;  // chunks (k blocks) per output tile = pipelined loop extent
   int32_t sA, sB, tacc;
   int32_t mode;
@@ -84,8 +86,16 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmKParams& p, int tile_i
   int per_batch = p.num_m * p.num_n;
   t.b = tile_id / per_batch;
   int r = tile_id - t.b * per_batch;
-  t.nb = r / p.num_m;  // m fastest: a wave of CTAs shares B columns
-  t.mb = r - t.nb * p.num_m;
+  // grouped raster: m fastest inside a group of group_m tile rows, groups in
+  // order, so the tiles in flight at once share few A rows and B columns
+  // (their panels stay L2-resident instead of streaming A once per wave)
+  const int span = p.group_m * p.num_n;
+  const int g = r / span;
+  const int first = g * p.group_m;
+  const int gs = min(p.group_m, p.num_m - first);
+  const int w = r - g * span;
+  t.nb = w / gs;
+  t.mb = first + (w - t.nb * gs);
   return t;
 }
 
@@ -120,6 +130,15 @@ __device__ __forceinline__ void stamp(const GemmKParams& p, int i) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.stamps[blockIdx.x * 8 + i] = t;
+  }
+}
+
+// epilogue clock64 log of CTA 0, warp 2 (debug): [chunk][event]
+template <bool kDebug>
+__device__ __forceinline__ void epistamp(const GemmKParams& p, int warp, int lane, int c, int ev) {
+  if constexpr (kDebug) {
+    if (p.stamps == nullptr || blockIdx.x != 0 || warp != 2 || lane != 0 || c >= 16) return;
+    p.stamps[148 * 8 + c * 4 + ev] = clock64();
   }
 }
 
@@ -563,6 +582,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c) {
         uint32_t w[32];
+        epistamp<kDebug>(p, warp, lane, c, 0);
         if constexpr (sizeof(OutT) == 4) {
           tmem_ld_32x32b_x32(t_addr + c * 32, w);
           tmem_wait_ld();
@@ -583,9 +603,11 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
         }
+        epistamp<kDebug>(p, warp, lane, c, 1);
         const uint32_t sbuf = stage_base + buf * 4096;
         if (lane == 0) bulk_wait_group_read<1>();  // the store that last read sbuf is done
         __syncwarp();
+        epistamp<kDebug>(p, warp, lane, c, 2);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
@@ -596,6 +618,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
           tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * kTileM + q * 32, tc.b);
           bulk_commit_group();
         }
+        epistamp<kDebug>(p, warp, lane, c, 3);
         buf ^= 1;
       }
     }
@@ -654,6 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
+  const bool b_sw64 = (half_n & 63) != 0;  // BN = 192: N-major halves of 96 columns
   if (threadIdx.x == 0) stamp<true>(p, 0);
 
   if (warp == 0 && elect_one()) {
@@ -716,7 +740,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
                   tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
               const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
-              if (p.b_mn_major) {
+              if (p.b_mn_major && b_sw64) {
+                for (int a = 0; a < (half_n >> 5); ++a)  // 32-column SW64 atoms (half_n = 96)
+                  tma_load_3d_pair(dst + a * (BK * 64), &tmB, fb_leader, n0 + a * 32, chunk * BK, tc.b);
+              } else if (p.b_mn_major) {
                 for (int a = 0; a < (half_n >> 6); ++a)
                   tma_load_3d_pair(dst + a * (BK * 128), &tmB, fb_leader, n0 + a * 64, chunk * BK, tc.b);
               } else {
@@ -748,7 +775,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
       uint64_t bdesc0;
       uint32_t b_big, b_small;
-      if (p.b_mn_major) {
+      if (p.b_mn_major && b_sw64) {
+        // N-major B in 32-column SW64 atoms: LBO = next atom along N, SBO =
+        // next 8 K rows (512 B); one UMMA_K step = 16 K rows = 1024 B
+        bdesc0 = make_smem_desc(ringB, BK * 64, 512, kLayoutSW64);
+        b_small = 1024 / 16;
+        b_big = 4 * b_small;
+      } else if (p.b_mn_major) {
         bdesc0 = make_smem_desc(ringB, BK * 128, 1024, kLayoutSW128);
         b_small = 2048 / 16;
         b_big = 4 * b_small;
@@ -1000,6 +1033,19 @@ int device_sm_count() {
   return sms;
 }
 
+// Tile rows per raster group.  schedule.raster > 0 sets it; 0 picks the group
+// that minimises the distinct A-row + B-column panels touched by the tiles in
+// flight at once (W = CTAs / cg): G*BM + (W/G)*BN  ->  G = sqrt(W*BN/BM).
+static int32_t raster_group(const alcop_schedule& s, int num_m, int num_n, int BM, int BN, int cg) {
+  if (s.raster > 0) return s.raster;
+  const int ctas = s.num_ctas > 0 ? s.num_ctas : device_sm_count();
+  const int W = ctas / cg > 0 ? ctas / cg : 1;
+  if (num_m * num_n <= W) return num_m;  // a single wave: order does not matter
+  int g = static_cast<int>(std::sqrt(static_cast<double>(W) * BN / BM) + 0.5);
+  if (g < 1) g = 1;
+  return g < num_m ? g : num_m;
+}
+
 int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,
                 alcop_event* trace, int64_t trace_cap, void* stream) {
   const int64_t lda = w.lda ? w.lda : w.K;
@@ -1018,7 +1064,9 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   CUtensorMap ta, tb;
   int rc = encode_3d_dt(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
   if (rc) return rc;
-  if (w.b_layout == ALCOP_B_KN)
+  if (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0)  // pair, BN 192: 32-column SW64 boxes
+    rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 32, BK, CU_TENSOR_MAP_SWIZZLE_64B, "B");
+  else if (w.b_layout == ALCOP_B_KN)
     rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
   else
     rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN / cg, kswz, "B");
@@ -1044,6 +1092,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.num_m = static_cast<int32_t>((w.M + kTileM * cg - 1) / (kTileM * cg));
   kp.num_n = static_cast<int32_t>((w.N + BN - 1) / BN);
   kp.num_tiles = static_cast<int32_t>(kp.num_m * kp.num_n * w.batch);
+  kp.group_m = raster_group(s, kp.num_m, kp.num_n, kTileM * cg, BN, cg);
   kp.E = static_cast<int32_t>((w.K + BK - 1) / BK);
   kp.sA = s.n_stage_smem_A;
   kp.sB = s.n_stage_smem_B;
@@ -1187,6 +1236,7 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   kp.num_m = static_cast<int32_t>((g.M + kTileM - 1) / kTileM);
   kp.num_n = static_cast<int32_t>((g.N + BN - 1) / BN);
   kp.num_tiles = kp.num_m * kp.num_n;
+  kp.group_m = raster_group(s, kp.num_m, kp.num_n, kTileM, BN, 1);
   kp.E = static_cast<int32_t>(g.K / 64);
   kp.sA = s.n_stage_smem_A;
   kp.sB = s.n_stage_smem_B;

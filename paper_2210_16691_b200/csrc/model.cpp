@@ -133,7 +133,9 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // L2 -> SM: the chip-wide share and the per-SM TMA fill rate
   const double tL2 = std::max(static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC,
                               static_cast<double>(out->bytesOneSmemLoop) / hw->bwSmem);
-  const int64_t boxes = std::max<int64_t>(1, tK / 64) + std::max<int64_t>(1, tN / cg / 64);
+  const int64_t bN = tN / cg;  // B columns staged per CTA
+  const int64_t bBoxes = w->b_layout == ALCOP_B_KN ? ((bN % 64) ? bN / 32 : bN / 64) : std::max<int64_t>(1, tK / 64);
+  const int64_t boxes = std::max<int64_t>(1, tK / 64) + bBoxes;
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors
   out->tSmemUse = std::max(tMma, std::max(tL2, tIssue));

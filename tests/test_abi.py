@@ -32,6 +32,7 @@ def test_version_and_error_string(alcop):
 @pytest.mark.parametrize("field,value,rule", [
     ("tileM", 64, "BadTile"), ("tileN", 96, "BadTile"), ("tileK", 16, "BadTile"),
     ("n_stage_smem_A", 0, "BadStages"), ("n_stage_inner", 3, "BadStages"), ("mode", 7, "BadSchedule"),
+    ("raster", -1, "BadRaster"),
     ("cta_group", 4, "BadSchedule"),
 ])
 def test_validate_rejects(alcop, field, value, rule):

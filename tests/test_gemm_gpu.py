@@ -161,7 +161,9 @@ def test_device_trace_matches_enumerator(alcop, mode, sA, sB):
 
 
 @pytest.mark.parametrize("tileN,tileK,st,mode,layout", [(256, 64, 4, 1, 0), (128, 64, 4, 0, 0), (256, 128, 2, 1, 1),
-                                                        (128, 32, 6, 1, 1), (256, 64, 1, 1, 0), (128, 64, 3, 0, 1)])
+                                                        (128, 32, 6, 1, 1), (256, 64, 1, 1, 0), (128, 64, 3, 0, 1),
+                                                        (192, 64, 4, 1, 0), (192, 128, 2, 0, 0), (192, 32, 6, 1, 0),
+                                                        (192, 64, 4, 1, 1), (192, 32, 5, 0, 1)])
 def test_cta_pair_exact(alcop, tileN, tileK, st, mode, layout):
     """cta_group::2: a CTA pair computes 256 x tileN tiles (M=256 tcgen05.mma)."""
     s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, n_stage_inner=2 if st > 1 else 1, mode=mode,
@@ -176,6 +178,11 @@ def test_cta_pair_ragged_batched(alcop):
     _assert_exact(C, exact, torch.float32)
     C, exact = _run(alcop, 512, 768, 768, in_dt=torch.bfloat16, out_dt=torch.bfloat16, sched=s)
     _assert_exact(C, exact, torch.bfloat16)
+    s = alcop.make_schedule(tileN=192, tileK=64, n_stage=5, cta_group=2)
+    C, exact = _run(alcop, 1024, 768, 3072, in_dt=torch.bfloat16, out_dt=torch.bfloat16, sched=s)
+    _assert_exact(C, exact, torch.bfloat16)
+    C, exact = _run(alcop, 300, 200, 136, batch=3, sched=s)
+    _assert_exact(C, exact, torch.float32)
 
 
 
@@ -190,3 +197,13 @@ def test_fused_preop_exact(alcop, tileN, tileK, st, mode):
     C = alcop.matmul(torch.from_numpy(a).to(torch.bfloat16).cuda(), torch.from_numpy(b).to(torch.bfloat16).cuda(),
                      s, out_dtype=torch.float32, pre_op=1)
     _assert_exact(C.cpu(), _exact(2 * a + 1, b, False), torch.float32)
+
+
+@pytest.mark.parametrize("cg,raster,num_ctas", [(1, 3, 10), (1, 1, 7), (2, 3, 8), (2, 2, 6), (1, 0, 0), (2, 0, 0)])
+def test_grouped_raster_exact(alcop, cg, raster, num_ctas):
+    """Grouped tile rasterisation (raster rows per group, ragged last group)
+    with several tiles per persistent CTA: every tile is visited exactly once."""
+    s = alcop.make_schedule(tileN=128, tileK=64, n_stage=4, cta_group=cg, raster=raster, num_ctas=num_ctas)
+    M = 7 * 128 * cg + 40  # 8 tile rows, last one ragged
+    C, exact = _run(alcop, M, 5 * 128 - 24, 192, batch=2, sched=s)
+    _assert_exact(C, exact, torch.float32)

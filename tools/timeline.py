@@ -27,7 +27,7 @@ def main():
     B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
-    stamps = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    stamps = torch.zeros(148 * 8 + 64, dtype=torch.int64, device="cuda")
     for _ in range(3):
         alcop.matmul(A, B, s, out=C)
     torch.cuda.synchronize()
@@ -37,11 +37,18 @@ def main():
         stamps.zero_()
         alcop.matmul(A, B, s, out=C)
         torch.cuda.synchronize()
-        t = stamps.view(148, 8).cpu().numpy().astype(np.int64)
+        epi = stamps[148 * 8:].view(16, 4).cpu().numpy().astype(np.int64)
+        t = stamps[:148 * 8].view(148, 8).cpu().numpy().astype(np.int64)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         res.append((t - t0) / 1000.0)
     lib.alcop_debug_set_stamps(None)
+    nz = epi[epi[:, 0] > 0]
+    if len(nz):
+        base = nz[0, 0]
+        print("epilogue CTA0 warp2 per chunk (clk from first chunk start): ldstart, ld+pack done, staging free, store issued")
+        for row in nz:
+            print("   ", [int(x - base) for x in row])
     names = ["start", "setup", "firstTMA", "firstFull", "lastCommit", "epiFirst", "epiDone", "end"]
     r = np.stack(res)  # reps x ctas x 8
     print("%s M=%d N=%d K=%d tile=128x%dx%d s=%d ctas=%d" % (s, M, N, K, tN, tK, st, r.shape[1]))
