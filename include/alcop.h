@@ -242,6 +242,58 @@ int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, con
                void* stream, alcop_schedule* best, alcop_tune_trial* trials, int32_t trials_cap,
                int32_t* n_trials);
 
+/* ---- event-level pipeline simulation (pipe_sim.hpp:16-167) ------------ */
+/* SimConfig (pipe_sim.hpp:16-22): nMplx workers share one compute unit, each
+ * with nPipe chunk slots; loads take tLoad, uses tUse (serialised). */
+typedef struct {
+  double tLoad, tUse;
+  int64_t nLoop;
+  int32_t nPipe, nMplx;
+} alcop_sim_config;
+
+/* SimResult (pipe_sim.hpp:43-49) + comparable_worker_latency (:129-133). */
+typedef struct {
+  double makespan, firstComputeStart, busy, idleFraction;
+  double comparable; /* per-worker latency comparable with the closed form */
+} alcop_sim_result;
+
+/* SimEvent (pipe_sim.hpp:24-40): kind 0 loadIssue, 1 loadDone,
+ * 2 computeStart, 3 computeEnd. */
+typedef struct {
+  double time;
+  int32_t worker, kind;
+  int64_t iteration;
+} alcop_sim_event;
+
+/* simulate_pipeline (pipe_sim.hpp:55-127).  trace (may be NULL) receives up
+ * to trace_cap events sorted by time (stable); *n_events = the full count.
+ * Counts < 1 or negative times -> ALCOP_ERR_CONFIG "BadSimConfig". */
+int alcop_simulate_pipeline(const alcop_sim_config* cfg, alcop_sim_result* out, alcop_sim_event* trace,
+                            int64_t trace_cap, int64_t* n_events);
+/* simulate_two_level (pipe_sim.hpp:138-167): fused != 0 lets inner loads run
+ * ahead across outer chunks, 0 restarts the inner pipeline per outer chunk. */
+int alcop_simulate_two_level(const alcop_sim_config* outer, const alcop_sim_config* inner, int32_t fused,
+                             double* makespan);
+
+/* B200 two-level kernel simulation (the event-level analogue of
+ * alcop_predict, as measure_ground_truth is of perf::predict,
+ * pipe_sim.hpp:195-239): per persistent CTA (pair), the outer level is the
+ * n_stage smem ring (FUSED: loads run ahead across tiles; WRAP: the ring
+ * restarts per tile with s-1 drained wrap loads), the inner level is the
+ * n_stage_inner TMEM accumulator ring between the MMA issuer and the
+ * epilogue.  Chunk load/use and epilogue times come from alcop_predict. */
+typedef struct {
+  double tKernel;     /* cycles */
+  double seconds;
+  double tBody;       /* first load -> last epilogue end, one CTA (pair) */
+  double mmaBusy;     /* cycles the MMA issuer is busy */
+  double mmaIdleFraction;
+  double tMainLoopTile, tEpilogueTile, tLoadChunk, tUseChunk;
+  int64_t tilesPerUnit, loads;
+} alcop_sim_kernel;
+int alcop_simulate_kernel(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
+                          alcop_sim_kernel* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -165,6 +165,27 @@ def model_grid():
     return qs
 
 
+def sim_grid():
+    """pipe_sim.hpp:50-167: simulate_pipeline stats + traces and
+    simulate_two_level (fused and restart) on a deterministic grid, incl. the
+    ConfigError cases (counts < 1, negative times)."""
+    rng = np.random.RandomState(4321)
+    qs = ["sim 0 1 1 1 1", "sim 5 0 3 1 2", "sim 0 10 0 1 1", "sim -1 10 4 2 1", "sim 10 10 4 0 1",
+          "simtrace 30 10 6 2 1", "simtrace 10 10 5 2 3", "simtrace 0 4 4 1 2",
+          "sim2 100 10 8 2 5 10 4 2 1", "sim2 100 10 8 2 5 10 4 2 0", "sim2 0 10 0 2 5 10 4 2 1"]
+    for _ in range(150):
+        qs.append("sim %g %g %d %d %d" % (rng.randint(0, 400), rng.randint(0, 120), rng.randint(1, 40),
+                                          rng.randint(1, 7), rng.randint(1, 5)))
+    for _ in range(40):
+        qs.append("simtrace %g %g %d %d %d" % (rng.randint(0, 100), rng.randint(1, 50), rng.randint(1, 8),
+                                               rng.randint(1, 4), rng.randint(1, 4)))
+    for _ in range(150):
+        qs.append("sim2 %g %g %d %d %g %g %d %d %d" % (rng.randint(0, 2000), rng.randint(0, 50), rng.randint(1, 16),
+                                                       rng.randint(1, 6), rng.randint(0, 100), rng.randint(1, 60),
+                                                       rng.randint(1, 8), rng.randint(1, 4), rng.randint(0, 2)))
+    return qs
+
+
 def run(args, **kw):
     return subprocess.run([DRIVER] + args, check=True, capture_output=True, text=True, **kw)
 
@@ -276,7 +297,7 @@ def gen_scripts(path):
 
 
 def gen_model(path):
-    qs = MODEL_QUERIES + model_grid()
+    qs = MODEL_QUERIES + model_grid() + sim_grid()
     with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
         f.write("\n".join(qs) + "\n")
         qpath = f.name

@@ -12,7 +12,8 @@
 //   script    apply_script only: {"ok":..} or the exception class + rule tag
 //   model     perf:: functions on a JSON list of queries (SPEC examples and
 //             grids) -> predictions
-//   sim       sim::simulate_pipeline on a list of configs
+//   (model)   also sim / simtrace / sim2: sim::simulate_pipeline stats, its
+//             event trace, and sim::simulate_two_level (fused | restart)
 //   splitmix  first N draws / range(-8,8) values for a seed
 //   time      wall time of pipec::run on a lowered+transformed GEMM
 //
@@ -320,8 +321,30 @@ int cmd_model(const std::map<std::string, std::string>& a) {
     } else if (fn == "sim") {
       sim::SimConfig c;
       ls >> c.tLoad >> c.tUse >> c.nLoop >> c.nPipe >> c.nMplx;
-      auto r = sim::simulate_pipeline(c);
-      std::cout << r.makespan << "\n";
+      try {
+        auto r = sim::simulate_pipeline(c);
+        std::cout << r.makespan << " " << r.firstComputeStart << " " << r.busy << " " << r.idleFraction << " "
+                  << sim::comparable_worker_latency(r, c) << "\n";
+      } catch (const std::exception& e) {
+        std::cout << "error\n";
+      }
+    } else if (fn == "simtrace") {
+      sim::SimConfig c;
+      ls >> c.tLoad >> c.tUse >> c.nLoop >> c.nPipe >> c.nMplx;
+      auto r = sim::simulate_pipeline(c, true);
+      for (size_t i = 0; i < r.trace.size(); ++i)
+        std::cout << (i ? " " : "") << r.trace[i].time << ":" << r.trace[i].worker << ":"
+                  << sim::sim_event_name(r.trace[i].kind) << ":" << r.trace[i].iteration;
+      std::cout << "\n";
+    } else if (fn == "sim2") {
+      sim::SimConfig o, in;
+      int fused;
+      ls >> o.tLoad >> o.tUse >> o.nLoop >> o.nPipe >> in.tLoad >> in.tUse >> in.nLoop >> in.nPipe >> fused;
+      try {
+        std::cout << sim::simulate_two_level(o, in, fused != 0) << "\n";
+      } catch (const std::exception& e) {
+        std::cout << "error\n";
+      }
     } else {
       std::cout << "unknown\n";
     }

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = [
     "alcop_validate", "alcop_smem_bytes", "alcop_enumerate_pipeline", "alcop_gemm", "alcop_gemm_traced",
     "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_conv2d", "alcop_hw_default_b200",
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
-    "alcop_tune",
+    "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
 ]
 
 
@@ -93,6 +93,33 @@ class Breakdown(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("nThreadblkBatch", "nThreadblkPerSM", "nThreadblkPerBatch",
                                                "nSmemLoop", "nRegLoop", "bytesOneSmemLoop", "bytesWorkset",
                                                "bytesOutputTile", "flopsOneRegLoop")] + [("seconds", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class SimConfig(ctypes.Structure):
+    _fields_ = [("tLoad", ctypes.c_double), ("tUse", ctypes.c_double), ("nLoop", ctypes.c_int64),
+                ("nPipe", ctypes.c_int32), ("nMplx", ctypes.c_int32)]
+
+
+class SimResult(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("makespan", "firstComputeStart", "busy", "idleFraction",
+                                                "comparable")]
+
+
+class SimEvent(ctypes.Structure):
+    _fields_ = [("time", ctypes.c_double), ("worker", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("iteration", ctypes.c_int64)]
+
+
+SIM_EVENT_NAMES = ("loadIssue", "loadDone", "computeStart", "computeEnd")  # pipe_sim.hpp:31-39
+
+
+class SimKernel(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("tKernel", "seconds", "tBody", "mmaBusy", "mmaIdleFraction",
+                                                "tMainLoopTile", "tEpilogueTile", "tLoadChunk", "tUseChunk")] + \
+               [("tilesPerUnit", ctypes.c_int64), ("loads", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -163,6 +190,10 @@ def load_library(path: str | None = None):
     lib.alcop_ir_to_gemm.argtypes = [ctypes.c_char_p, P(GemmDesc), P(Schedule), ctypes.c_char_p, ctypes.c_size_t]
     lib.alcop_tune.argtypes = [P(GemmDesc), P(HW), ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p, P(Schedule), P(TuneTrial), ctypes.c_int32, P(ctypes.c_int32)]
+    lib.alcop_simulate_pipeline.argtypes = [P(SimConfig), P(SimResult), P(SimEvent), ctypes.c_int64,
+                                            P(ctypes.c_int64)]
+    lib.alcop_simulate_two_level.argtypes = [P(SimConfig), P(SimConfig), ctypes.c_int32, P(ctypes.c_double)]
+    lib.alcop_simulate_kernel.argtypes = [P(GemmDesc), P(Schedule), P(HW), P(SimKernel)]
     if path is None:
         _lib = lib
     return lib
@@ -268,6 +299,45 @@ def choose_schedule(desc: GemmDesc, hw: HW | None = None) -> Schedule:
     _check(load_library().alcop_choose_schedule(ctypes.byref(desc), ctypes.byref(hw or hw_b200()),
                                                 ctypes.byref(s)))
     return s
+
+
+def sim_config(tLoad, tUse, nLoop, nPipe=1, nMplx=1) -> SimConfig:
+    """SimConfig (pipe_sim.hpp:16-22)."""
+    return SimConfig(float(tLoad), float(tUse), int(nLoop), int(nPipe), int(nMplx))
+
+
+def simulate_pipeline(cfg: SimConfig, trace=False):
+    """simulate_pipeline (pipe_sim.hpp:55-127): a dict of the SimResult
+    fields (+ "comparable" = comparable_worker_latency); with trace=True also
+    "trace": [(time, worker, kind_name, iteration)] sorted by time."""
+    lib = load_library()
+    r = SimResult()
+    n = ctypes.c_int64(0)
+    cap = 4 * cfg.nLoop * cfg.nMplx if trace and cfg.nLoop > 0 and cfg.nMplx > 0 else 0
+    buf = (SimEvent * max(1, cap))() if trace else None
+    _check(lib.alcop_simulate_pipeline(ctypes.byref(cfg), ctypes.byref(r), buf, cap,
+                                       ctypes.byref(n) if trace else None))
+    out = {f: getattr(r, f) for f, _ in r._fields_}
+    if trace:
+        out["trace"] = [(e.time, e.worker, SIM_EVENT_NAMES[e.kind], e.iteration) for e in buf[:n.value]]
+    return out
+
+
+def simulate_two_level(outer: SimConfig, inner: SimConfig, fused=True) -> float:
+    """simulate_two_level (pipe_sim.hpp:138-167)."""
+    m = ctypes.c_double(0)
+    _check(load_library().alcop_simulate_two_level(ctypes.byref(outer), ctypes.byref(inner), 1 if fused else 0,
+                                                   ctypes.byref(m)))
+    return m.value
+
+
+def simulate_kernel(desc: GemmDesc, sched: Schedule, hw: HW | None = None) -> dict:
+    """B200 two-level kernel simulation: smem ring x TMEM accumulator ring per
+    persistent CTA, with alcop_predict's chunk and epilogue times."""
+    k = SimKernel()
+    _check(load_library().alcop_simulate_kernel(ctypes.byref(desc), ctypes.byref(sched), ctypes.byref(hw or hw_b200()),
+                                                ctypes.byref(k)))
+    return k.as_dict()
 
 
 # ---------------------------------------------------------------- compute

@@ -62,6 +62,7 @@ def test_model_pick_within_ten_percent_of_sweep(alcop):
         res = evaluate(json.load(f))
     ratios = {k: v["pick_over_best"] for k, v in res.items()}
     assert len(ratios) >= 8
+    assert all(r == r for r in ratios.values()), ("model pick not in the sweep", ratios)  # no NaN
     # all but at most one shape within 10%; none beyond 15%
     assert sum(r > 1.10 for r in ratios.values()) <= 1, ratios
     assert max(ratios.values()) <= 1.15, ratios
