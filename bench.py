@@ -45,6 +45,7 @@ METRIC = "TFLOP/s (BERT-base layer GEMMs, M=4096, bf16)"
 # outside the implicit-GEMM kernel's C % 64 == 0 support and is not counted.
 # (name, H_in, C, K, R, stride, pad, repeats)
 RESNET50_CONVS = [
+    ("conv1_7x7s2_3_64", 224, 3, 64, 7, 2, 3, 1),  # NHWC input padded to 8 channels (zero filter taps)
     ("l1_1x1_64_64", 56, 64, 64, 1, 1, 0, 1), ("l1_3x3_64_64", 56, 64, 64, 3, 1, 1, 3),
     ("l1_1x1_64_256", 56, 64, 256, 1, 1, 0, 4), ("l1_1x1_256_64", 56, 256, 64, 1, 1, 0, 2),
     ("l2_1x1_256_128", 56, 256, 128, 1, 1, 0, 1), ("l2_3x3s2_128", 56, 128, 128, 3, 2, 1, 1),
@@ -450,14 +451,22 @@ def main_gpu(args, rank, world, local_rank):
         tot_ms = 0.0
         for (name, H, C, K, R, st, pd, rep) in RESNET50_CONVS:
             P, Q = alcop.conv_out_hw(H, H, R, R, (st, st), (pd, pd))
-            g = alcop.gemm_desc(nloc * P * Q, K, R * R * C, 1, alcop.BF16, alcop.BF16, alcop.B_NK)
+            Cs = -(-C // 8) * 8  # stored channels (conv1: 3 -> 8, zero padded)
+            halo = R * Cs <= 64  # stem layer: network input stored with its padding halo (NHWC8)
+            hp = pd if halo else 0
+            g = alcop.gemm_desc(nloc * P * Q, K, R * 64 if halo else R * R * Cs, 1, alcop.BF16, alcop.BF16,
+                                alcop.B_NK)
             cs = alcop.choose_conv_schedule(g)
-            X = (torch.rand((nloc, H, H, C), device=dev) - 0.5).to(torch.bfloat16)
-            Wf = (torch.rand((K, R, R, C), device=dev) - 0.5).to(torch.bfloat16)
+            X = torch.zeros((nloc, H + 2 * hp, H + 2 * hp, Cs), device=dev, dtype=torch.bfloat16)
+            Wf = torch.zeros((K, R, R, Cs), device=dev, dtype=torch.bfloat16)
+            X[:, hp:hp + H, hp:hp + H, :C] = (torch.rand((nloc, H, H, C), device=dev) - 0.5).to(torch.bfloat16)
+            Wf[..., :C] = (torch.rand((K, R, R, C), device=dev) - 0.5).to(torch.bfloat16)
             Y = torch.empty((nloc, P, Q, K), device=dev, dtype=torch.bfloat16)
-            ms = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=cs, out=Y), iters=6, warmup=2)
+            ms = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=cs, out=Y, x_halo=halo),
+                            iters=6, warmup=2)
             s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
-            ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=s1, out=Y), iters=4, warmup=1)
+            ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=s1, out=Y, x_halo=halo),
+                             iters=4, warmup=1)
             fl = 2.0 * nloc * P * Q * K * R * R * C
             tot_flops += fl * rep
             tot_ms += ms * rep
@@ -471,7 +480,9 @@ def main_gpu(args, rank, world, local_rank):
         extra["resnet50_convs_b256"] = {
             "tflops_aggregate": round(world * tot_flops / (float(tt.item()) * 1e-3) / 1e12, 1),
             "images_per_gpu": nloc, "sharding": "batch", "layers": conv_rows,
-            "note": "sum over the 52 conv layers except conv1 (C=3); per-layer CUDA-graph timing, model schedules"}
+            "note": "sum over all 53 conv layers (conv1: stem kernel on the NHWC8 halo-padded input, C 3 -> 8 "
+                    "zero-padded, FLOPs counted at C=3); "
+                    "per-layer CUDA-graph timing, model schedules"}
         torch.cuda.empty_cache()
 
     # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)

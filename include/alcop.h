@@ -102,6 +102,10 @@ typedef struct {
   int64_t N, H, W, C, K, R, S;
   int32_t stride_h, stride_w, pad_h, pad_w;
   int32_t in_dtype, out_dtype;
+  int32_t x_halo;   /* 1: x is stored [N][H+2pad_h][W+2pad_w][C] with its zero
+                       padding halo (a network-input layout); enables the stem
+                       kernel (one TMA box per filter row) when S*C <= 64 */
+  int32_t reserved0;
 } alcop_conv_desc;
 
 /* Hardware spec for the analytical model (perf::HardwareSpec,

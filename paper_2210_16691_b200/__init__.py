@@ -70,7 +70,8 @@ class Schedule(ctypes.Structure):
 
 class ConvDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("N", "H", "W", "C", "K", "R", "S")] + \
-               [(n, ctypes.c_int32) for n in ("stride_h", "stride_w", "pad_h", "pad_w", "in_dtype", "out_dtype")]
+               [(n, ctypes.c_int32) for n in ("stride_h", "stride_w", "pad_h", "pad_w", "in_dtype", "out_dtype",
+                                               "x_halo", "reserved0")]
 
 
 class HW(ctypes.Structure):
@@ -455,21 +456,34 @@ def conv_out_hw(H, W, R, S, stride, pad):
     return (H + 2 * pad[0] - R) // stride[0] + 1, (W + 2 * pad[1] - S) // stride[1] + 1
 
 
-def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_dtype=None, out=None, stream=None):
+def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_dtype=None, out=None, stream=None,
+           x_halo=False):
     """Implicit-GEMM conv2d through alcop_conv2d: x NHWC, w KRSC -> y NPQK
     (fp16/bf16 in, fp32 accumulate).  Default schedule: the model's pick for
-    the GEMM view (M=N*P*Q, N=K, K=R*S*C) with tileK 64."""
+    the GEMM view (M=N*P*Q, N=K, K=R*S*C) with tileK 64.  x_halo=True: x is
+    stored with its zero padding halo, [N, H+2*pad_h, W+2*pad_w, C] (enables
+    the one-box-per-filter-row stem kernel when S*C <= 64)."""
     import torch
     _require_cuda(x, w)
+    if x.shape[-1] % 8:
+        # NHWC channel padding to the 16-byte TMA granule (ResNet-50 conv1: 3 -> 8); zero filter
+        # channels make the padded taps contribute nothing
+        padc = 8 - x.shape[-1] % 8
+        x = torch.nn.functional.pad(x, (0, padc))
+        w = torch.nn.functional.pad(w, (0, padc))
     N, H, W, C = x.shape
+    if x_halo:
+        H, W = H - 2 * pad[0], W - 2 * pad[1]
     K, R, S, _ = w.shape
     P, Q = conv_out_hw(H, W, R, S, stride, pad)
     out_dtype = out_dtype or x.dtype
     if out is None:
         out = torch.empty((N, P, Q, K), dtype=out_dtype, device=x.device)
     d = conv_desc(N, H, W, C, K, R, S, stride, pad, _dtype_code(x.dtype), _dtype_code(out_dtype))
+    d.x_halo = 1 if x_halo else 0
     if sched is None:
-        g = gemm_desc(N * P * Q, K, R * S * C, 1, _dtype_code(x.dtype), _dtype_code(out_dtype), B_NK)
+        kv = R * 64 if (x_halo and S * C <= 64) else R * S * C
+        g = gemm_desc(N * P * Q, K, kv, 1, _dtype_code(x.dtype), _dtype_code(out_dtype), B_NK)
         sched = choose_conv_schedule(g)
     _check(load_library().alcop_conv2d(ctypes.byref(d), ctypes.byref(sched), ctypes.c_void_p(x.contiguous().data_ptr()),
                                        ctypes.c_void_p(w.contiguous().data_ptr()), ctypes.c_void_p(out.data_ptr()),

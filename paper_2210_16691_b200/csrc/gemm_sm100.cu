@@ -57,7 +57,11 @@ struct GemmKParams {
   uint64_t* stamps;  // debug timeline: 8 globaltimer stamps per CTA (nullptr = off)
   // implicit-GEMM conv2d (kConv): output pixels m = (n, p, q) row-major,
   // reduction chunk = (r, s, channel block) matching the KRSC filter layout
-  int32_t conv_P, conv_Q, conv_S, conv_Cb;
+  int32_t conv_P, conv_Q, conv_S, conv_Cb;  // Cb: 64-channel blocks (kConv 1) / 8-channel groups (2)
+  int32_t conv_RS;                         // filter taps R*S
+  int32_t conv_small_c;                    // 1: C % 64 != 0 (kConv 2); 2: stem (kConv 3)
+  int32_t conv_Pb, conv_Qb;                // stem: 8-row x 16-column output blocks per image
+  int32_t conv_stem5;                      // stem A map is the 5-D strided view (stored H % stride_h == 0)
   int32_t conv_sh, conv_sw, conv_ph, conv_pw;
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
@@ -209,7 +213,16 @@ struct RingCursor {
 // equal); otherwise each buffer has its own ring and lookahead.  kDebug
 // compiles in the bookkeeping trace and the timeline stamps.
 // ---------------------------------------------------------------------------
-template <typename OutT, int BK, bool kJoint, bool kDebug, bool kConv = false, bool kPreOp = false>
+// kConv: 0 GEMM / BMM; 1 implicit-GEMM conv, C % 64 == 0 (one 128B-swizzled
+// im2col box per chunk); 2 small-channel conv, C % 8 == 0 (eight 16-byte-wide
+// im2col boxes per chunk, one per 8-channel group of a filter tap, in the
+// no-swizzle K-major core-matrix layout; ResNet-50 conv1 with C padded 3 -> 8);
+// 3 stem conv on a halo-padded input with S*C <= 64: one chunk = one filter
+// row, whose S taps x C channels are S*C contiguous elements of the input
+// row, so a tiled TMA box over an overlapping (pixel-stride) view of x loads
+// the whole 128 x 64 A chunk in one 128B-swizzled copy; output tiles are
+// 8 x 16 output-pixel blocks
+template <typename OutT, int BK, bool kJoint, bool kDebug, int kConv = 0, bool kPreOp = false>
 __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
@@ -316,12 +329,40 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
             cv_h = pp * p.conv_sh - p.conv_ph;
             cv_w = (rem - pp * p.conv_Q) * p.conv_sw - p.conv_pw;
           }
-          const int cb = chunk % p.conv_Cb;
-          const int rs = chunk / p.conv_Cb;
-          const int fs = rs % p.conv_S;
-          const int fr = rs / p.conv_S;
-          tma_load_im2col_4d(ringA + slot * a_bytes, &tmA, fb, cb * 64, cv_w, cv_h, cv_n,
-                             static_cast<uint16_t>(fs), static_cast<uint16_t>(fr));
+          if constexpr (kConv == 3) {
+            // tile = 8 output rows x 16 output columns of image n; chunk = filter row
+            const int per_img = p.conv_Pb * p.conv_Qb;
+            const int n = tc.mb / per_img;
+            const int rem = tc.mb - n * per_img;
+            const int pb = rem / p.conv_Qb;
+            const int qb = rem - pb * p.conv_Qb;
+            if (p.conv_stem5)  // {taps, q (stride sw px), p (stride sh rows), row parity, n}: no traversal strides
+              tma_load_5d(ringA + slot * a_bytes, &tmA, fb, 0, qb * 16, pb * 8 + chunk / p.conv_sh,
+                          chunk % p.conv_sh, n);
+            else
+              tma_load_4d(ringA + slot * a_bytes, &tmA, fb, 0, qb * 16 * p.conv_sw, pb * 8 * p.conv_sh + chunk, n);
+          } else if constexpr (kConv == 2) {
+            // K-group G = 8 channels of one filter tap; taps past R*S re-read
+            // tap 0 (their filter rows are zero-filled by the w map)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const int G = chunk * 8 + g;
+              int tap = G / p.conv_Cb;
+              const int cgrp = G - tap * p.conv_Cb;
+              if (tap >= p.conv_RS) tap = 0;
+              const int fs = tap % p.conv_S;
+              const int fr = tap / p.conv_S;
+              tma_load_im2col_4d(ringA + slot * a_bytes + g * (kTileM * 16), &tmA, fb, cgrp * 8, cv_w, cv_h, cv_n,
+                                 static_cast<uint16_t>(fs), static_cast<uint16_t>(fr));
+            }
+          } else {
+            const int cb = chunk % p.conv_Cb;
+            const int rs = chunk / p.conv_Cb;
+            const int fs = rs % p.conv_S;
+            const int fr = rs / p.conv_S;
+            tma_load_im2col_4d(ringA + slot * a_bytes, &tmA, fb, cb * 64, cv_w, cv_h, cv_n,
+                               static_cast<uint16_t>(fs), static_cast<uint16_t>(fr));
+          }
         } else {
 #pragma unroll
           for (int a = 0; a < kKAtoms; ++a)
@@ -331,7 +372,9 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
       };
       auto issue_b = [&](uint32_t slot, uint32_t fb, int chunk) {
         const uint32_t dst = ringB + slot * b_bytes;
-        if (p.b_mn_major) {
+        if (kConv == 3) {
+          tma_load_3d(dst, &tmB, fb, 0, chunk, tc.nb * p.BN);  // filter row `chunk`: S*C taps, zero-filled to 64
+        } else if (p.b_mn_major) {
           // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
           for (int a = 0; a < (p.BN >> 6); ++a)
             tma_load_3d(dst + a * (BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * BK, tc.b);
@@ -428,7 +471,10 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
       RingCursor ca, cb;
       int nev = 0;
       // descriptor bases (start address advances in 16-byte units in the low word)
-      const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
+      // small-channel conv A: no-swizzle core matrices (8 rows x 16 B), LBO =
+      // next 8 K (one 128-row x 16 B box), SBO = next 8 rows
+      const uint64_t adesc0 = kConv == 2 ? make_smem_desc(ringA, kTileM * 16, 128, kLayoutNone)
+                                         : make_smem_desc(ringA, 16, kKSbo, kKLayout);
       uint64_t bdesc0;
       uint32_t b_big, b_small;  // B k-step advance: (u>>2)*b_big + (u&3)*b_small, in 16 B units
       if (p.b_mn_major) {
@@ -482,7 +528,8 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
 #pragma unroll
               for (int u = 0; u < kSteps; ++u) {
                 // inner level: k-step u of chunk v reads slot v%s at k offset 16u
-                const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
+                const uint32_t a_off = kConv == 2 ? u * (2 * kTileM * 16 / 16)
+                                       : BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
                 umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
               } umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
@@ -615,7 +662,16 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * kTileM + q * 32, tc.b);
+          if constexpr (kConv == 3) {
+            // warp quarter q holds output rows 2q, 2q+1 of the 8 x 16 pixel block
+            const int per_img = p.conv_Pb * p.conv_Qb;
+            const int n = tc.mb / per_img;
+            const int rem = tc.mb - n * per_img;
+            const int pb = rem / p.conv_Qb;
+            tma_store_4d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, (rem - pb * p.conv_Qb) * 16, pb * 8 + q * 2, n);
+          } else {
+            tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * kTileM + q * 32, tc.b);
+          }
           bulk_commit_group();
         }
         epistamp<kDebug>(p, warp, lane, c, 3);
@@ -909,6 +965,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
   return fn;
 }
 
+// rank-D tiled map with traversal strides (stem conv: overlapping pixel-stride view)
+int encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int rank, const cuuint64_t* dims,
+                 const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr,
+                 CUtensorMapSwizzle swz, const char* what) {
+  auto enc = get_encode_tiled();
+  if (!enc) return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled unavailable");
+  CUresult r = enc(m, dt, rank, const_cast<void*>(base), dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(ALCOP_ERR_CUDA, "CudaError",
+                     std::string("cuTensorMapEncodeTiled failed for ") + what + " (CUresult " + std::to_string(r) + ")");
+  return ALCOP_OK;
+}
+
 int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
               uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
               CUtensorMapSwizzle swz, const char* what) {
@@ -970,10 +1040,10 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   return ALCOP_OK;
 }
 
-template <typename OutT, bool kDebug>
+template <typename OutT, bool kDebug, int kConv>
 int launch_typed_conv(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                       int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_kernel<OutT, 64, true, kDebug, true>;
+  auto kern = alcop_pipelined_gemm_kernel<OutT, 64, true, kDebug, kConv>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -1014,9 +1084,15 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
 template <typename OutT>
 int launch_conv_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                       int grid, int smem, cudaStream_t st) {
-  if (kp.trace != nullptr || kp.stamps != nullptr)
-    return launch_typed_conv<OutT, true>(ta, tb, tc, kp, grid, smem, st);
-  return launch_typed_conv<OutT, false>(ta, tb, tc, kp, grid, smem, st);
+  const bool dbg = kp.trace != nullptr || kp.stamps != nullptr;
+  if (kp.conv_small_c == 2)
+    return dbg ? launch_typed_conv<OutT, true, 3>(ta, tb, tc, kp, grid, smem, st)
+               : launch_typed_conv<OutT, false, 3>(ta, tb, tc, kp, grid, smem, st);
+  if (kp.conv_small_c)
+    return dbg ? launch_typed_conv<OutT, true, 2>(ta, tb, tc, kp, grid, smem, st)
+               : launch_typed_conv<OutT, false, 2>(ta, tb, tc, kp, grid, smem, st);
+  return dbg ? launch_typed_conv<OutT, true, 1>(ta, tb, tc, kp, grid, smem, st)
+             : launch_typed_conv<OutT, false, 1>(ta, tb, tc, kp, grid, smem, st);
 }
 
 }  // namespace
@@ -1175,8 +1251,21 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   if (d.N < 1 || d.H < 1 || d.W < 1 || d.C < 1 || d.K < 1 || d.R < 1 || d.S < 1 || d.stride_h < 1 ||
       d.stride_w < 1 || d.pad_h < 0 || d.pad_w < 0)
     return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "conv dimensions must be positive, padding >= 0");
-  if (d.C % 64)
-    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "implicit-GEMM conv needs C to be a multiple of 64");
+  if (d.C % 8)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported",
+                     "implicit-GEMM conv needs C to be a multiple of 8 (pad NHWC channels, e.g. conv1 3 -> 8)");
+  const bool small_c = (d.C % 64) != 0;  // 8-channel im2col boxes (no-swizzle core matrices)
+  const bool halo = d.x_halo != 0;
+  // stem kernel: a filter row's S*C taps are contiguous in the halo-padded input
+  const bool stem = halo && d.S * d.C <= 64 && d.stride_w * 16 <= 256 && d.stride_h * 8 <= 256;
+  const int64_t Hs = halo ? d.H + 2 * d.pad_h : d.H, Ws = halo ? d.W + 2 * d.pad_w : d.W;  // stored extents
+  const int ph = halo ? 0 : d.pad_h, pw = halo ? 0 : d.pad_w;  // padding the im2col map applies
+  // 5-D stem view unless disabled (ALCOP_STEM5=0) or the stored height is not a stride multiple
+  static const bool stem5_env = [] {
+    const char* e = std::getenv("ALCOP_STEM5");
+    return !(e && e[0] == '0');
+  }();
+  const bool stem5 = stem && stem5_env && (Hs % d.stride_h) == 0 && d.stride_w * d.C * 2 % 16 == 0;
   if (d.stride_h > 8 || d.stride_w > 8 || d.pad_h > 127 || d.pad_w > 127 || d.R > 128 || d.S > 128)
     return set_error(ALCOP_ERR_CONFIG, "Unsupported", "stride <= 8 and padding/filter within TMA im2col range");
   if (s.tileK != 64 || s.n_stage_smem_A != s.n_stage_smem_B)
@@ -1187,7 +1276,7 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   alcop_gemm_desc g{};
   g.M = d.N * P * Q;
   g.N = d.K;
-  g.K = d.R * d.S * d.C;
+  g.K = stem ? d.R * 64 : d.R * d.S * d.C;
   g.batch = 1;
   g.in_dtype = d.in_dtype;
   g.out_dtype = d.out_dtype;
@@ -1201,30 +1290,73 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   auto enc = get_encode_im2col();
   if (!enc) return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col unavailable");
   CUtensorMap ta, tb, tc;
-  {
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(d.W), static_cast<cuuint64_t>(d.H),
-                          static_cast<cuuint64_t>(d.N)};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.C * 2), static_cast<cuuint64_t>(d.W * d.C * 2),
-                             static_cast<cuuint64_t>(d.H * d.W * d.C * 2)};
-    // bounding box of window origins, per spatial dim in tensor order (W, H)
-    int lower[2] = {-d.pad_w, -d.pad_h};
-    int upper[2] = {static_cast<int>(d.pad_w - (d.S - 1)), static_cast<int>(d.pad_h - (d.R - 1))};
-    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(d.stride_w), static_cast<cuuint32_t>(d.stride_h), 1};
-    CUresult r = enc(&ta, dt, 4, const_cast<void*>(x), dims, strides, lower, upper, 64, kTileM, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(r) + ")");
-  }
   const int BN = static_cast<int>(s.tileN);
-  rc = encode_3d_dt(&tb, dt, wt, g.K, g.N, 1, g.K * 2, g.N * g.K * 2, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B, "w");
-  if (rc) return rc;
   const CUtensorMapDataType odt = d.out_dtype == ALCOP_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                   : d.out_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
-  rc = encode_3d_dt(&tc, odt, y, g.N, g.M, 1, g.N * ob, g.M * g.N * ob, 128 / ob, 32, CU_TENSOR_MAP_SWIZZLE_128B, "y");
-  if (rc) return rc;
+  if (stem) {
+    // A: {S*C taps of one filter row (elements 56..63 zero-filled), window
+    // origin pixel (stride C: overlapping view), row, image}; box 64 x 16 x 8
+    // output positions at traversal strides (1, stride_w, stride_h)
+    const cuuint32_t one[5] = {1, 1, 1, 1, 1};
+    if (stem5) {
+      // the strides folded into the view: q steps stride_w pixels, p steps
+      // stride_h rows, filter row r = (r / stride_h) p-steps + (r % stride_h) rows
+      const cuuint64_t adims[5] = {static_cast<cuuint64_t>(d.S * d.C), static_cast<cuuint64_t>(Q),
+                                   static_cast<cuuint64_t>(Hs / d.stride_h), static_cast<cuuint64_t>(d.stride_h),
+                                   static_cast<cuuint64_t>(d.N)};
+      const cuuint64_t astr[4] = {static_cast<cuuint64_t>(d.stride_w * d.C * 2),
+                                  static_cast<cuuint64_t>(d.stride_h * Ws * d.C * 2),
+                                  static_cast<cuuint64_t>(Ws * d.C * 2), static_cast<cuuint64_t>(Hs * Ws * d.C * 2)};
+      const cuuint32_t abox[5] = {64, 16, 8, 1, 1};
+      rc = encode_tiled(&ta, dt, x, 5, adims, astr, abox, one, CU_TENSOR_MAP_SWIZZLE_128B, "x (stem)");
+    } else {
+      const cuuint64_t adims[4] = {static_cast<cuuint64_t>(d.S * d.C), static_cast<cuuint64_t>(Ws - d.S + 1),
+                                   static_cast<cuuint64_t>(Hs), static_cast<cuuint64_t>(d.N)};
+      const cuuint64_t astr[3] = {static_cast<cuuint64_t>(d.C * 2), static_cast<cuuint64_t>(Ws * d.C * 2),
+                                  static_cast<cuuint64_t>(Hs * Ws * d.C * 2)};
+      const cuuint32_t abox[4] = {64, static_cast<cuuint32_t>(16 * d.stride_w),
+                                  static_cast<cuuint32_t>(8 * d.stride_h), 1};
+      const cuuint32_t aestr[4] = {1, static_cast<cuuint32_t>(d.stride_w), static_cast<cuuint32_t>(d.stride_h), 1};
+      rc = encode_tiled(&ta, dt, x, 4, adims, astr, abox, aestr, CU_TENSOR_MAP_SWIZZLE_128B, "x (stem)");
+    }
+    if (rc) return rc;
+    // B: filter row r = S*C contiguous taps of w[k][r][.][.], zero-filled to 64
+    const cuuint64_t bdims[3] = {static_cast<cuuint64_t>(d.S * d.C), static_cast<cuuint64_t>(d.R),
+                                 static_cast<cuuint64_t>(d.K)};
+    const cuuint64_t bstr[2] = {static_cast<cuuint64_t>(d.S * d.C * 2), static_cast<cuuint64_t>(d.R * d.S * d.C * 2)};
+    const cuuint32_t bbox[3] = {64, 1, static_cast<cuuint32_t>(BN)};
+    rc = encode_tiled(&tb, dt, wt, 3, bdims, bstr, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "w (stem)");
+    if (rc) return rc;
+    // y as {K, Q, P, N}: each epilogue warp stores 2 output rows x 16 columns
+    const cuuint64_t cdims[4] = {static_cast<cuuint64_t>(d.K), static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(P),
+                                 static_cast<cuuint64_t>(d.N)};
+    const cuuint64_t cstr[3] = {static_cast<cuuint64_t>(d.K * ob), static_cast<cuuint64_t>(Q * d.K * ob),
+                                static_cast<cuuint64_t>(P * Q * d.K * ob)};
+    const cuuint32_t cbox[4] = {static_cast<cuuint32_t>(128 / ob), 16, 2, 1};
+    rc = encode_tiled(&tc, odt, y, 4, cdims, cstr, cbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "y (stem)");
+    if (rc) return rc;
+  } else {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(Ws), static_cast<cuuint64_t>(Hs),
+                          static_cast<cuuint64_t>(d.N)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(d.C * 2), static_cast<cuuint64_t>(Ws * d.C * 2),
+                             static_cast<cuuint64_t>(Hs * Ws * d.C * 2)};
+    // bounding box of window origins, per spatial dim in tensor order (W, H)
+    int lower[2] = {-pw, -ph};
+    int upper[2] = {static_cast<int>(pw - (d.S - 1)), static_cast<int>(ph - (d.R - 1))};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(d.stride_w), static_cast<cuuint32_t>(d.stride_h), 1};
+    CUresult r = enc(&ta, dt, 4, const_cast<void*>(x), dims, strides, lower, upper, small_c ? 8 : 64, kTileM, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, small_c ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(r) + ")");
+    rc = encode_3d_dt(&tb, dt, wt, g.K, g.N, 1, g.K * 2, g.N * g.K * 2, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B, "w");
+    if (rc) return rc;
+    rc = encode_3d_dt(&tc, odt, y, g.N, g.M, 1, g.N * ob, g.M * g.N * ob, 128 / ob, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                      "y");
+    if (rc) return rc;
+  }
 
   GemmKParams kp{};
   kp.M = static_cast<int32_t>(g.M);
@@ -1233,11 +1365,15 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   kp.batch = 1;
   kp.BN = BN;
   kp.BK = 64;
-  kp.num_m = static_cast<int32_t>((g.M + kTileM - 1) / kTileM);
+  kp.conv_Pb = static_cast<int32_t>((P + 7) / 8);
+  kp.conv_Qb = static_cast<int32_t>((Q + 15) / 16);
+  kp.num_m = stem ? static_cast<int32_t>(d.N * kp.conv_Pb * kp.conv_Qb)
+                  : static_cast<int32_t>((g.M + kTileM - 1) / kTileM);
   kp.num_n = static_cast<int32_t>((g.N + BN - 1) / BN);
   kp.num_tiles = kp.num_m * kp.num_n;
   kp.group_m = raster_group(s, kp.num_m, kp.num_n, kTileM, BN, 1);
-  kp.E = static_cast<int32_t>(g.K / 64);
+  kp.E = static_cast<int32_t>((g.K + 63) / 64);  // small C: the last chunk's taps past R*S meet zero filter rows
+                                                 // stem: one chunk per filter row (g.K = R * 64)
   kp.sA = s.n_stage_smem_A;
   kp.sB = s.n_stage_smem_B;
   kp.tacc = s.n_stage_inner;
@@ -1255,11 +1391,14 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   kp.conv_P = static_cast<int32_t>(P);
   kp.conv_Q = static_cast<int32_t>(Q);
   kp.conv_S = static_cast<int32_t>(d.S);
-  kp.conv_Cb = static_cast<int32_t>(d.C / 64);
+  kp.conv_Cb = static_cast<int32_t>(small_c ? d.C / 8 : d.C / 64);
+  kp.conv_RS = static_cast<int32_t>(d.R * d.S);
+  kp.conv_small_c = stem ? 2 : small_c ? 1 : 0;
+  kp.conv_stem5 = stem5 ? 1 : 0;
   kp.conv_sh = d.stride_h;
   kp.conv_sw = d.stride_w;
-  kp.conv_ph = d.pad_h;
-  kp.conv_pw = d.pad_w;
+  kp.conv_ph = ph;
+  kp.conv_pw = pw;
   const int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
