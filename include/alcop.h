@@ -239,7 +239,8 @@ typedef struct {
  * AnalyticalOnly method of tuner.hpp:407-413 with measure_ground_truth,
  * pipe_sim.hpp:195-239, replaced by the GPU): enumerate the B200 space,
  * rank by alcop_predict, time the top `budget` schedules on the caller's
- * buffers (CUDA events on `stream`), return the fastest in *best.
+ * buffers (CUDA events on `stream`, each launch from a cold L2: a 256 MB
+ * scratch write precedes it), return the fastest in *best.
  * `trials` (may be NULL) receives up to `trials_cap` measured candidates in
  * rank order; *n_trials their count. */
 int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, const void* A, const void* B, void* C,

@@ -47,24 +47,39 @@ extern "C" int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t 
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
     return set_error(ALCOP_ERR_CUDA, "CudaError", "cudaEventCreate failed");
+  // each timed launch starts from a cold L2 (a 2 x L2 scratch write before
+  // it, outside the events), as the model was calibrated on rotating inputs
+  const size_t kFlush = size_t(256) << 20;
+  void* flush = nullptr;
+  if (cudaMalloc(&flush, kFlush) != cudaSuccess) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return set_error(ALCOP_ERR_CUDA, "CudaError", "tuning scratch allocation failed");
+  }
   double bestT = 1e300;
   int out = 0;
   int rc = ALCOP_OK;
   for (int i = 0; i < n && rc == ALCOP_OK; ++i) {
     const alcop_schedule& s = space[i].second;
     rc = launch_gemm(*w, s, A, B, C, nullptr, 0, stream);  // warm-up
-    const int reps = 3;
-    if (rc == ALCOP_OK) cudaEventRecord(e0, st);
-    for (int r = 0; r < reps && rc == ALCOP_OK; ++r) rc = launch_gemm(*w, s, A, B, C, nullptr, 0, stream);
-    if (rc != ALCOP_OK) break;
-    cudaEventRecord(e1, st);
-    if (cudaEventSynchronize(e1) != cudaSuccess) {
-      rc = set_error(ALCOP_ERR_CUDA, "CudaError", "kernel failed during tuning");
-      break;
+    const int reps = 5;
+    double sum = 0;
+    for (int r = 0; r < reps && rc == ALCOP_OK; ++r) {
+      cudaMemsetAsync(flush, r & 0xff, kFlush, st);
+      cudaEventRecord(e0, st);
+      rc = launch_gemm(*w, s, A, B, C, nullptr, 0, stream);
+      cudaEventRecord(e1, st);
+      if (rc != ALCOP_OK) break;
+      if (cudaEventSynchronize(e1) != cudaSuccess) {
+        rc = set_error(ALCOP_ERR_CUDA, "CudaError", "kernel failed during tuning");
+        break;
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      sum += ms;
     }
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    const double t = ms * 1e-3 / reps;
+    if (rc != ALCOP_OK) break;
+    const double t = sum * 1e-3 / reps;
     if (trials && out < trials_cap) trials[out] = alcop_tune_trial{s, space[i].first, t};
     ++out;
     if (t < bestT) {
@@ -72,6 +87,7 @@ extern "C" int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t 
       *best = s;
     }
   }
+  cudaFree(flush);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (n_trials) *n_trials = out;
