@@ -146,6 +146,16 @@ __device__ __forceinline__ void epistamp(const GemmKParams& p, int warp, int lan
   }
 }
 
+// per-chunk clock64 log of CTA 0 (debug): role 0 = producer after
+// producer_acquire, 1 = MMA after consumer_wait; chunks 0..63 of the stream
+template <bool kDebug>
+__device__ __forceinline__ void chunkstamp(const GemmKParams& p, int role, int i) {
+  if constexpr (kDebug) {
+    if (p.stamps == nullptr || blockIdx.x != 0 || i >= 64) return;
+    p.stamps[148 * 8 + 64 + role * 64 + i] = clock64();
+  }
+}
+
 template <bool kDebug>
 __device__ __forceinline__ void log_event(const GemmKParams& p, int role, int& n, int kind, int buf, int tile,
                                           int slot, int chunk, int parity, int c0, int c1, int c2, int c3) {
@@ -409,6 +419,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&emptyA[slot]), par);
         ra.phase ^= 1u << slot;
+        if (lane == 0) chunkstamp<kDebug>(p, 0, ra.count);
         ++ra.count;
         coord(tl);
         const uint32_t fb = smem_u32(&fullA[slot]);
@@ -512,6 +523,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
           uint32_t pa, pb;
           if constexpr (kJoint) {
             pa = cwait(ca, kPreOp ? ready : fullA, 0, tl, v);  // consumer_wait A (+B: same barrier)
+            if (lane == 0) chunkstamp<kDebug>(p, 1, ca.count - 1);
             pb = pa;
             ++cb.count;
             ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
@@ -784,6 +796,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire (own slot, released by the pair's MMA)
         ra.phase ^= 1u << slot;
+        if (lane == 0) chunkstamp<true>(p, 0, ra.count++);
         if (tl != tc_tile) {
           tc_tile = tl;
           tc = tile_coord(p, cluster_id + tl * nclusters);
@@ -858,6 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
           mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
           ca.phase ^= 1u << slot;
+          if (lane == 0) chunkstamp<true>(p, 1, ca.count++);
           tc_fence_after();
           if (tl == 0 && v == 0 && lane == 0) stamp<true>(p, 3);
           const uint64_t ad = adesc0 + slot * a_stage16;

@@ -27,7 +27,7 @@ def main():
     B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
-    stamps = torch.zeros(148 * 8 + 64, dtype=torch.int64, device="cuda")
+    stamps = torch.zeros(148 * 8 + 64 + 128, dtype=torch.int64, device="cuda")
     for _ in range(3):
         alcop.matmul(A, B, s, out=C)
     torch.cuda.synchronize()
@@ -37,12 +37,19 @@ def main():
         stamps.zero_()
         alcop.matmul(A, B, s, out=C)
         torch.cuda.synchronize()
-        epi = stamps[148 * 8:].view(16, 4).cpu().numpy().astype(np.int64)
+        epi = stamps[148 * 8:148 * 8 + 64].view(16, 4).cpu().numpy().astype(np.int64)
+        ch = stamps[148 * 8 + 64:].view(2, 64).cpu().numpy().astype(np.int64)
         t = stamps[:148 * 8].view(148, 8).cpu().numpy().astype(np.int64)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         res.append((t - t0) / 1000.0)
     lib.alcop_debug_set_stamps(None)
+    n = int((ch[1] > 0).sum())
+    if n:
+        base = ch[0, 0]
+        print("CTA0 chunks (clk from first producer_acquire): acquire / consumer_wait passed")
+        print("   acq ", [int(x - base) for x in ch[0, :n]])
+        print("   wait", [int(x - base) for x in ch[1, :n]])
     nz = epi[epi[:, 0] > 0]
     if len(nz):
         base = nz[0, 0]
