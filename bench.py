@@ -3,14 +3,19 @@
 
 Workload (BASELINE.json configs[1]): the GEMMs of one BERT-base encoder layer
 at M = 4096 tokens, bf16 in / bf16 out, fp32 accumulate:
-    Q, K, V, O projections  4 x [4096 x 768] @ [768 x 768]
+    Q, K, V projections     [4096 x 768] @ [768 x 2304]  (one GEMM: the three
+                            projections read the same activations, so their
+                            weights are stored side by side, B = [Wq|Wk|Wv])
+    O projection            [4096 x 768]  @ [768 x 768]
     FFN1                    [4096 x 768]  @ [768 x 3072]
     FFN2                    [4096 x 3072] @ [3072 x 768]
+(--unfused-qkv: Q, K, V as three [768 x 768] GEMMs; the same FLOPs, six
+launches; that variant's step time is reported beside the headline too.)
 B is the reference layout [K, N] row-major (schedule.hpp:389).  One "step" is
-one pass over those six GEMMs, each launched through the C ABI (alcop_gemm)
+one pass over those GEMMs, each launched through the C ABI (alcop_gemm)
 with the schedule the analytical model picks (alcop_choose_schedule).  Inputs
 rotate over copies whose footprint exceeds 2x the 126 MB L2, so every step
-reads HBM.  Reported beside it, in the same run: the n_stage 1..5 sweep of
+reads HBM.  Reported beside it, in the same run: the n_stage 1..6 sweep of
 each distinct shape (speedup vs the non-pipelined n_stage=1 variant), the
 model pick vs the best swept schedule, a large square GEMM, the roofline of
 the dominant kernel, the end-to-end number through the host-buffer ABI entry
@@ -36,7 +41,11 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BERT_GEMMS = [  # (name, M, N, K)
+BERT_GEMMS = [  # (name, M, N, K): the layer's GEMMs, Q/K/V fused into one launch
+    ("qkv_proj", 4096, 2304, 768), ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768),
+    ("ffn2", 4096, 768, 3072),
+]
+BERT_GEMMS_UNFUSED = [
     ("q_proj", 4096, 768, 768), ("k_proj", 4096, 768, 768), ("v_proj", 4096, 768, 768),
     ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768), ("ffn2", 4096, 768, 3072),
 ]
@@ -59,6 +68,7 @@ RESNET50_CONVS = [
     ("l4_ds_1024_2048", 14, 1024, 2048, 1, 2, 0, 1), ("l4_1x1_2048_512", 7, 2048, 512, 1, 1, 0, 2),
 ]
 UNIT = "TFLOP/s"
+TUNE_BUDGET = 24
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -225,6 +235,14 @@ class ClockSampler:
                 "reasons": [n for b, n in self.REASONS.items() if self.reasons & b], "samples": len(self.samples)}
 
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 # ----------------------------------------------------------------- GPU arm
 def main_gpu(args, rank, world, local_rank):
     import torch
@@ -238,33 +256,31 @@ def main_gpu(args, rank, world, local_rank):
     peaks = load_peaks()
     stream = torch.cuda.current_stream()
 
-    # schedules: the analytical model's choice per distinct shape (alcop_choose_schedule)
-    shapes = sorted(set((M, N, K) for _, M, N, K in BERT_GEMMS))
-    sched = {}
-    for (M, N, K) in shapes:
-        d = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
-        sched[(M, N, K)] = alcop.choose_schedule(d)
-
-    # rotating input sets so each step's operands come from HBM
-    set_bytes = sum((M * K + K * N + M * N) * 2 for _, M, N, K in BERT_GEMMS)
-    nsets = max(2, -(-2 * L2_BYTES // set_bytes))
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-
-    def make_set():
-        out = []
-        for name, M, N, K in BERT_GEMMS:
-            A = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
-            B = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
-            C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
-            out.append((A, B, C, sched[(M, N, K)]))
-        return out
-
-    sets = [make_set() for _ in range(nsets)]
+    gemms = BERT_GEMMS_UNFUSED if args.unfused_qkv else BERT_GEMMS
     lib = alcop.load_library()
     import ctypes
-    descs = {s: alcop.gemm_desc(*s, 1, alcop.BF16, alcop.BF16, alcop.B_KN) for s in shapes}
     sp = ctypes.c_void_p(stream.cuda_stream)
+    descs, sched = {}, {}
+
+    model_pick = {}
+
+    def plan(shape):
+        # per distinct shape: the analytical model's ranking (alcop_choose_schedule);
+        # with --schedule tune (default) its top TUNE_BUDGET schedules are timed on
+        # this GPU and the fastest is used (alcop_tune: the reference's
+        # model-assisted tuning, tuner.hpp:363-531, on real B200 timings)
+        if shape not in sched:
+            descs[shape] = alcop.gemm_desc(*shape, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+            model_pick[shape] = alcop.choose_schedule(descs[shape])
+            sched[shape] = model_pick[shape]
+            if args.schedule == "tune":
+                M, N, K = shape
+                A = (torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16)
+                B = (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16)
+                C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+                sched[shape], _ = alcop.tune(A, B, C, budget=TUNE_BUDGET)
+                del A, B, C
+        return sched[shape]
 
     def launch(A, B, C, s, shape):
         cur = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -273,63 +289,56 @@ def main_gpu(args, rank, world, local_rank):
         if rc:
             raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
 
-    # the layer's dependency DAG: q/k/v read the same activations and are
-    # independent (three graph branches that overlap each other's prologue,
-    # epilogue and tail); o -> ffn1 -> ffn2 are a chain (PDL edges)
-    dag = args.dag  # measured slower than the PDL chain (0.079 vs 0.077 ms/step): off by default
-    branches = [torch.cuda.Stream(), torch.cuda.Stream()]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
 
-    def step_set(i):
-        work = list(zip(BERT_GEMMS, sets[i]))
-        if not dag:
-            for (name, M, N, K), (A, B, C, s) in work:
-                launch(A, B, C, s, (M, N, K))
-            return
-        cur = torch.cuda.current_stream()
-        fork = torch.cuda.Event()
-        fork.record(cur)
-        joins = []
-        for j, ((name, M, N, K), (A, B, C, s)) in enumerate(work[:3]):
-            if j == 0:
-                launch(A, B, C, s, (M, N, K))
-                continue
-            br = branches[j - 1]
-            br.wait_event(fork)
-            with torch.cuda.stream(br):
-                launch(A, B, C, s, (M, N, K))
-                e = torch.cuda.Event()
-                e.record(br)
-            joins.append(e)
-        for e in joins:
-            cur.wait_event(e)
-        for (name, M, N, K), (A, B, C, s) in work[3:]:
-            launch(A, B, C, s, (M, N, K))
+    def make_step(gl):
+        """CUDA graphs of one step over the GEMM list gl, one graph per input
+        set; input sets rotate so the step's operands come from HBM (> 2x L2).
+        The launches are chained with PDL (the kernels are unchanged)."""
+        set_bytes = sum((M * K + K * N + M * N) * 2 for _, M, N, K in gl)
+        nsets = max(2, -(-2 * L2_BYTES // set_bytes))
+        sets = []
+        for _ in range(nsets):
+            one = []
+            for name, M, N, K in gl:
+                A = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+                B = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+                C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+                one.append((A, B, C, plan((M, N, K))))
+            sets.append(one)
 
-    # one CUDA graph per input set: the step's six launches replay without
-    # host launch overhead (the kernels and their PDL edges are unchanged)
-    cs = torch.cuda.Stream()
-    cs.wait_stream(stream)
-    with torch.cuda.stream(cs):
-        for i in range(nsets):
-            step_set(i)
-    stream.wait_stream(cs)
-    torch.cuda.synchronize()
-    use_graphs = os.environ.get("ALCOP_BENCH_GRAPHS", "1") != "0"  # 0: direct launches (profiling)
-    graphs = []
-    if use_graphs:
-        for i in range(nsets):
-            g_ = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_):
+        def step_set(i):
+            for (name, M, N, K), (A, B, C, s) in zip(gl, sets[i]):
+                launch(A, B, C, s, (M, N, K))
+
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            for i in range(nsets):
                 step_set(i)
-            graphs.append(g_)
-    state = {"i": 0}
-
-    def step():
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        use_graphs = os.environ.get("ALCOP_BENCH_GRAPHS", "1") != "0"  # 0: direct launches (profiling)
+        graphs = []
         if use_graphs:
-            graphs[state["i"]].replay()
-        else:
-            step_set(state["i"])
-        state["i"] = (state["i"] + 1) % nsets
+            for i in range(nsets):
+                g_ = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_):
+                    step_set(i)
+                graphs.append(g_)
+        state = {"i": 0}
+
+        def step():
+            if use_graphs:
+                graphs[state["i"]].replay()
+            else:
+                step_set(state["i"])
+            state["i"] = (state["i"] + 1) % nsets
+        return step, nsets, set_bytes
+
+    step, nsets, set_bytes = make_step(gemms)
+    shapes = sorted(set((M, N, K) for _, M, N, K in gemms))
 
     def barrier():
         if world > 1:
@@ -347,47 +356,69 @@ def main_gpu(args, rank, world, local_rank):
         ref = (a.double() @ b.double()).float()
         assert torch.equal(c, ref), "kernel mismatch on %s" % ((M, N, K),)
 
-    # ---- warmup + timed region
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    # per-GEMM durations of the dominant kernel, on the launching stream
-    with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
+    def timed(stepfn, steps, sample_clocks=False):
+        for _ in range(args.warmup):
+            stepfn()
         torch.cuda.synchronize()
-    ms_total = ev0.elapsed_time(ev1)
-    barrier()
-    t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+        barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) if sample_clocks else _Null() as clk:
+            ev0.record(stream)
+            for _ in range(steps):
+                stepfn()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        ms_total = ev0.elapsed_time(ev1)
+        barrier()
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), clk
+
+    # ---- warmup + timed region (the headline)
+    ms_max, clk = timed(step, args.steps, sample_clocks=True)
     flops = step_flops()
     value = world * flops * args.steps / (ms_max * 1e-3) / 1e12
+    # the other decomposition of the same layer (same FLOPs), same run
+    alt_gemms = BERT_GEMMS if args.unfused_qkv else BERT_GEMMS_UNFUSED
+    alt_step, _, _ = make_step(alt_gemms)
+    alt_steps = max(50, args.steps // 4)
+    alt_ms, _ = timed(alt_step, alt_steps)
+    alt = {"gemms": {n: [M, N, K] for n, M, N, K in alt_gemms}, "launches_per_step": len(alt_gemms),
+           "ms_per_step": alt_ms / alt_steps, "tflops": world * flops * alt_steps / (alt_ms * 1e-3) / 1e12}
+    del alt_step
+    torch.cuda.empty_cache()
 
-    # ---- per-GEMM times (events around each launch) -> dominant kernel roofline
+    # ---- per-GEMM times (CUDA graphs on the launching stream, each GEMM on its
+    # own rotating inputs > 2x L2, i.e. cold operands as inside the step)
     per = {}
-    reps = max(5, min(50, args.steps // 4))
-    for (name, M, N, K) in BERT_GEMMS:
-        if name in ("k_proj", "v_proj", "o_proj"):
+    reps = max(8, min(50, args.steps // 4))
+    from paper_2210_16691_b200.timing import Rotating
+    for (name, M, N, K) in gemms:
+        if (M, N, K) in [tuple(v["shape"]) for v in per.values()]:
             continue
-        j = [n for n, *_ in BERT_GEMMS].index(name)
+        rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
+                                                 (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
+                                                 torch.empty((M, N), device=dev, dtype=torch.bfloat16)),
+                       (M * K + K * N + M * N) * 2, max_sets=16)
+        nr = len(rot.sets)
 
-        def one(i, j=j, M=M, N=N, K=K):
-            A, B, C, s = sets[i % nsets][j]
-            launch(A, B, C, s, (M, N, K))
-        ms = time_graph(one, iters=reps, warmup=3)
-        per[name] = {"ms": ms, "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12, "schedule": sched[(M, N, K)].as_dict()}
-    step_ms_est = sum(per["q_proj"]["ms"] if n in ("q_proj", "k_proj", "v_proj", "o_proj") else per[n]["ms"]
-                      for n, *_ in BERT_GEMMS)
-    dom = max(per, key=lambda n: per[n]["ms"] * (4 if n == "q_proj" else 1))
-    dM, dN, dK = [g[1:] for g in BERT_GEMMS if g[0] == dom][0]
+        def one(i, rot=rot, nr=nr, M=M, N=N, K=K):
+            A, B, C = rot.sets[i % nr]
+            launch(A, B, C, sched[(M, N, K)], (M, N, K))
+        ms = time_graph(one, iters=max(reps, 2 * nr), warmup=3, reps_per_graph=nr)
+        per[name] = {"ms": ms, "shape": [M, N, K], "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12,
+                     "schedule": sched[(M, N, K)].as_dict()}
+        del rot
+    count = {}
+    for (name, M, N, K) in gemms:
+        key = [n for n, v in per.items() if v["shape"] == [M, N, K]][0]
+        count[key] = count.get(key, 0) + 1
+    step_ms_est = sum(per[n]["ms"] * c for n, c in count.items())
+    dom = max(per, key=lambda n: per[n]["ms"] * count[n])
+    dM, dN, dK = per[dom]["shape"]
     dflops = 2.0 * dM * dN * dK
     achieved = dflops / (per[dom]["ms"] * 1e-3) / 1e12
     traffic = None
@@ -402,21 +433,27 @@ def main_gpu(args, rank, world, local_rank):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
                 "kernel": "alcop_pipelined_gemm_kernel (%s %dx%dx%d)" % (dom, dM, dN, dK),
-                "share_of_step": per[dom]["ms"] * (4 if dom == "q_proj" else 1) / step_ms_est,
+                "share_of_step": per[dom]["ms"] * count[dom] / step_ms_est,
                 "peak_source": peaks["source"] + " burst bf16 (MEASURED_PEAKS.json)",
-                "algorithmic_flops_per_launch": dflops}
+                "algorithmic_flops_per_launch": dflops,
+                "timing": "CUDA events around CUDA graphs of this GEMM alone, rotating cold inputs > 2x L2"}
 
     extra = {}
     if rank == 0 and not args.quick:
         # ---- n_stage sweep 1..5 per distinct shape (same tile, same run) + model pick vs best
         sweep = {}
         for (M, N, K) in shapes:
-            base = sched[(M, N, K)]
+            base = model_pick[(M, N, K)]
+            tuned = sched[(M, N, K)]
             rows = []
-            j = [g[1:] for g in BERT_GEMMS].index((M, N, K))  # rotate over the same input sets as the step
+            rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
+                                                     (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
+                                                     torch.empty((M, N), device=dev, dtype=torch.bfloat16)),
+                           (M * K + K * N + M * N) * 2, max_sets=16)
+            nr = len(rot.sets)
 
-            def run_on(i, s, j=j, M=M, N=N, K=K):
-                A, B, C, _ = sets[i % nsets][j]
+            def run_on(i, s, rot=rot, nr=nr, M=M, N=N, K=K):
+                A, B, C = rot.sets[i % nr]
                 launch(A, B, C, s, (M, N, K))
             best = None
             cands = []
@@ -431,13 +468,15 @@ def main_gpu(args, rank, world, local_rank):
                         continue
                     cands.append((st, tn, tk, cg, s))
             for st, tn, tk, cg, s in cands:
-                ms = time_graph(lambda i, s=s: run_on(i, s), iters=24, warmup=3)
+                ms = time_graph(lambda i, s=s: run_on(i, s), iters=2 * nr, warmup=3, reps_per_graph=nr)
                 tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
                 rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "cta_group": cg, "tflops": round(tf, 1)})
                 if best is None or tf > best[0]:
                     best = (tf, st, tn, tk, cg)
-            ms_pick = time_graph(lambda i: run_on(i, base), iters=24, warmup=3)
+            ms_pick = time_graph(lambda i: run_on(i, base), iters=2 * nr, warmup=3, reps_per_graph=nr)
             tf_pick = 2.0 * M * N * K / (ms_pick * 1e-3) / 1e12
+            ms_tuned = time_graph(lambda i: run_on(i, tuned), iters=2 * nr, warmup=3, reps_per_graph=nr)
+            tf_tuned = 2.0 * M * N * K / (ms_tuned * 1e-3) / 1e12
             by_stage = {}
             for r in rows:
                 if (r["tileN"], r["tileK"], r["cta_group"]) == (base.tileN, base.tileK, base.cta_group):
@@ -452,6 +491,9 @@ def main_gpu(args, rank, world, local_rank):
                                                               if k in ("tileN", "tileK", "n_stage_smem_A",
                                                                        "cta_group")}},
                 "model_pick_over_best_time": round(best[0] / tf_pick, 3),
+                "tuned_pick": {"tflops": round(tf_tuned, 1), **{k: v for k, v in tuned.as_dict().items()
+                                                               if k in ("tileN", "tileK", "n_stage_smem_A",
+                                                                        "cta_group")}},
                 "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
         extra["n_stage_sweep"] = sweep
         # ---- large square GEMM (config 5 point): 8192^3 bf16
@@ -515,7 +557,7 @@ def main_gpu(args, rank, world, local_rank):
 
     # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)
     host = []
-    for name, M, N, K in BERT_GEMMS:
+    for name, M, N, K in gemms:
         A = (torch.rand((M, K)) * 2 - 1).to(torch.bfloat16).pin_memory()
         B = (torch.rand((K, N)) * 2 - 1).to(torch.bfloat16).pin_memory()
         C = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
@@ -524,7 +566,7 @@ def main_gpu(args, rank, world, local_rank):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 
     def e2e_step():
-        for (name, M, N, K), (A, B, C) in zip(BERT_GEMMS, host):
+        for (name, M, N, K), (A, B, C) in zip(gemms, host):
             rc = lib.alcop_gemm_host(ctypes.byref(descs[(M, N, K)]), ctypes.byref(sched[(M, N, K)]),
                                      ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
                                      ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(ws.data_ptr()), sp)
@@ -545,8 +587,8 @@ def main_gpu(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = world * flops * e2e_steps / float(te.item()) / 1e12
-    h2d = sum((M * K + K * N) * 2 for _, M, N, K in BERT_GEMMS)
-    d2h = sum(M * N * 2 for _, M, N, K in BERT_GEMMS)
+    h2d = sum((M * K + K * N) * 2 for _, M, N, K in gemms)
+    d2h = sum(M * N * 2 for _, M, N, K in gemms)
 
     if rank == 0:
         cpu = None
@@ -554,27 +596,32 @@ def main_gpu(args, rank, world, local_rank):
             rows = ref_sample_rows(3.0)
             dt, cflops, kind, cores = cpu_reference_step(rows)
             cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": "a %dx%d output block (full K) of each of the 6 BERT-layer GEMMs through the "
+                   "sample": "a %dx%d output block (full K) of each of the %d BERT-layer GEMMs through the "
                              "reference interpreter (pipec::run, transformed program), %d concurrent processes; "
-                             "%.2f s wall" % (rows, REF_SAMPLE_COLS, len(BERT_GEMMS), dt)}
+                             "%.2f s wall" % (rows, REF_SAMPLE_COLS, len(BERT_GEMMS), len(BERT_GEMMS), dt)}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (uniform[-1,1) bf16; %d rotating input sets, %.0f MB > 2x L2)"
                         % (nsets, nsets * set_bytes / 1e6),
-                "config": {"workload": "bert_base_layer_gemms", "M": 4096, "launch": ("CUDA graph per input set: 6 alcop_gemm launches, q/k/v as three parallel "
-                                                                      "branches, o -> ffn1 -> ffn2 chained with PDL" if args.dag else
-                                                                      "CUDA graph per input set: 6 alcop_gemm launches chained with PDL"),
-                           "gemms": {n: [M, N, K] for n, M, N, K in BERT_GEMMS}, "b_layout": "KN (reference)",
+                "config": {"workload": "bert_base_layer_gemms" + ("" if args.unfused_qkv else "_fused_qkv"),
+                           "M": 4096,
+                           "launch": "CUDA graph per input set: %d alcop_gemm launches chained with PDL" % len(gemms),
+                           "gemms": {n: [M, N, K] for n, M, N, K in gemms}, "b_layout": "KN (reference)",
                            "parallelism": "replicas" if world > 1 else "single",
-                           "l2": "inputs rotated over copies > 2x L2", "schedule": "alcop_choose_schedule"},
-                "gpu_launches": len(BERT_GEMMS) * args.steps,
+                           "l2": "inputs rotated over copies > 2x L2",
+                           "schedule": ("alcop_tune (model rank, top %d timed on this GPU)" % TUNE_BUDGET
+                                        if args.schedule == "tune" else "alcop_choose_schedule (model pick)"),
+                           "schedules": {"%dx%dx%d" % k: v.as_dict() for k, v in sched.items()}},
+                "gpu_launches": len(gemms) * args.steps,
                 "clocks": clk.summary(),
                 "roofline": roofline,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "entry_point": "alcop_gemm_host (pinned host buffers, H2D + kernel + D2H per GEMM)"},
-                "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4)} for k, v in per.items()},
+                "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4), "shape": v["shape"],
+                                 "launches_per_step": count[k]} for k, v in per.items()},
+                ("step_fused_qkv" if args.unfused_qkv else "step_unfused_qkv"): alt,
                 **extra}
         print(json.dumps(line), flush=True)
 
@@ -586,7 +633,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="alcop", choices=["alcop", "reference"])
     ap.add_argument("--quick", action="store_true", help="skip the n_stage sweep and the large square")
-    ap.add_argument("--dag", action="store_true", help="q/k/v as parallel graph branches instead of one PDL chain")
+    ap.add_argument("--schedule", default="tune", choices=["tune", "model"],
+                    help="tune: time the model's top schedules per shape (alcop_tune); model: its first pick")
+    ap.add_argument("--unfused-qkv", action="store_true", help="Q, K, V as three GEMMs (six launches per step)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -63,6 +63,10 @@ struct GemmKParams {
   int32_t conv_Pb, conv_Qb;                // stem: 8-row x 16-column output blocks per image
   int32_t conv_stem5;                      // stem A map is the 5-D strided view (stored H % stride_h == 0)
   int32_t conv_sh, conv_sw, conv_ph, conv_pw;
+  // atom-stacked views: one 4-D TMA box brings all 128-B (64-B) swizzle atoms
+  // of a chunk (A: the BK/64 K atoms; B[K,N]: the N atoms), instead of one
+  // instruction per atom (each TMA issue costs the producer ~60-80 clk)
+  int32_t a_view, b_view;
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
 };
@@ -134,6 +138,8 @@ __device__ __forceinline__ void stamp(const GemmKParams& p, int i) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.stamps[blockIdx.x * 8 + i] = t;
+    // CTA 0: SM clock beside the globaltimer at start / end (effective SM MHz under load)
+    if (blockIdx.x == 0 && (i == 0 || i == 7)) p.stamps[148 * 8 + 192 + (i == 7)] = clock64();
   }
 }
 
@@ -373,6 +379,8 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
             tma_load_im2col_4d(ringA + slot * a_bytes, &tmA, fb, cb * 64, cv_w, cv_h, cv_n,
                                static_cast<uint16_t>(fs), static_cast<uint16_t>(fr));
           }
+        } else if (kKAtoms > 1 && p.a_view) {
+          tma_load_4d(ringA + slot * a_bytes, &tmA, fb, 0, tc.mb * kTileM, chunk * kKAtoms, tc.b);
         } else {
 #pragma unroll
           for (int a = 0; a < kKAtoms; ++a)
@@ -384,6 +392,9 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         const uint32_t dst = ringB + slot * b_bytes;
         if (kConv == 3) {
           tma_load_3d(dst, &tmB, fb, 0, chunk, tc.nb * p.BN);  // filter row `chunk`: S*C taps, zero-filled to 64
+        } else if (p.b_mn_major && p.b_view) {
+          // B[K,N] row-major, atom-stacked view {64 N, K, N/64}: all BN/64 atoms in one box
+          tma_load_4d(dst, &tmB, fb, 0, chunk * BK, tc.nb * (p.BN >> 6), tc.b);
         } else if (p.b_mn_major) {
           // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
           for (int a = 0; a < (p.BN >> 6); ++a)
@@ -804,12 +815,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
         ISSUE(if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
+              if (kKAtoms > 1 && p.a_view) {
+                tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
+                                 tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, chunk * kKAtoms, tc.b);
+              } else {
 #pragma unroll
-              for (int a = 0; a < kKAtoms; ++a) tma_load_3d_pair(
-                  ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
-                  tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
+                for (int a = 0; a < kKAtoms; ++a) tma_load_3d_pair(
+                    ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
+                    tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
+              }
               const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
-              if (p.b_mn_major && b_sw64) {
+              if (p.b_mn_major && p.b_view) {
+                // atom-stacked view {atom width, K, N/atom}: the CTA's half_n columns in one box
+                tma_load_4d_pair(dst, &tmB, fb_leader, 0, chunk * BK, n0 / (b_sw64 ? 32 : 64), tc.b);
+              } else if (p.b_mn_major && b_sw64) {
                 for (int a = 0; a < (half_n >> 5); ++a)  // 32-column SW64 atoms (half_n = 96)
                   tma_load_3d_pair(dst + a * (BK * 64), &tmB, fb_leader, n0 + a * 32, chunk * BK, tc.b);
               } else if (p.b_mn_major) {
@@ -1152,14 +1171,45 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const uint32_t kbox = BK >= 64 ? 64 : BK;
 
   CUtensorMap ta, tb;
-  int rc = encode_3d_dt(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
+  // Atom-stacked views (one TMA instruction per operand per chunk) need the
+  // atom dimension to tile the row exactly: a ragged last atom would read
+  // across the row end instead of zero-filling.  ALCOP_ATOM_VIEWS=0 disables.
+  static const bool views_on = [] {
+    const char* e = std::getenv("ALCOP_ATOM_VIEWS");
+    return !(e && e[0] == '0');
+  }();
+  const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0) ? 32 : 64;  // pair BN 192: SW64 halves
+  const bool a_view = views_on && BK > 64 && w.K % 64 == 0 && w.pre_op == 0;
+  const bool b_view = views_on && w.b_layout == ALCOP_B_KN && w.N % b_atom == 0 && (BN / cg) / b_atom > 1;
+  int rc;
+  if (a_view) {
+    const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(w.M), static_cast<cuuint64_t>(w.K / 64),
+                                static_cast<cuuint64_t>(w.batch)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(lda * 2), 128, static_cast<cuuint64_t>(sa * 2)};
+    const cuuint32_t box[4] = {64, kTileM, static_cast<cuuint32_t>(BK / 64), 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    rc = encode_tiled(&ta, dt, A, 4, dims, strides, box, es, CU_TENSOR_MAP_SWIZZLE_128B, "A (atom view)");
+  } else {
+    rc = encode_3d_dt(&ta, dt, A, w.K, w.M, w.batch, lda * 2, sa * 2, kbox, kTileM, kswz, "A");
+  }
   if (rc) return rc;
-  if (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0)  // pair, BN 192: 32-column SW64 boxes
+  if (b_view) {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(b_atom), static_cast<cuuint64_t>(w.K),
+                                static_cast<cuuint64_t>(w.N / b_atom), static_cast<cuuint64_t>(w.batch)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ldb * 2), static_cast<cuuint64_t>(b_atom * 2),
+                                   static_cast<cuuint64_t>(sb * 2)};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(b_atom), static_cast<cuuint32_t>(BK),
+                               static_cast<cuuint32_t>((BN / cg) / b_atom), 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    rc = encode_tiled(&tb, dt, B, 4, dims, strides, box, es,
+                      b_atom == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, "B (atom view)");
+  } else if (w.b_layout == ALCOP_B_KN && b_atom == 32) {  // pair, BN 192: 32-column SW64 boxes
     rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 32, BK, CU_TENSOR_MAP_SWIZZLE_64B, "B");
-  else if (w.b_layout == ALCOP_B_KN)
+  } else if (w.b_layout == ALCOP_B_KN) {
     rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
-  else
+  } else {
     rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN / cg, kswz, "B");
+  }
   if (rc) return rc;
   CUtensorMap tc;
   {
@@ -1202,6 +1252,8 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.stamps = g_stamps;
   kp.in_bf16 = w.in_dtype == ALCOP_BF16 ? 1 : 0;
   kp.pre_op = w.pre_op;
+  kp.a_view = a_view ? 1 : 0;
+  kp.b_view = b_view ? 1 : 0;
 
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");

@@ -207,3 +207,14 @@ def test_grouped_raster_exact(alcop, cg, raster, num_ctas):
     M = 7 * 128 * cg + 40  # 8 tile rows, last one ragged
     C, exact = _run(alcop, M, 5 * 128 - 24, 192, batch=2, sched=s)
     _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("cg,tileN,tileK", [(1, 256, 128), (1, 192, 64), (2, 192, 64), (2, 256, 128), (2, 128, 128)])
+def test_atom_views_batched(alcop, cg, tileN, tileK):
+    """One 4-D TMA box per operand per chunk (atom-stacked views of A[.., K/64]
+    and B[K, N/atom]) with a batch dimension: batch strides and the atom
+    coordinates must land every swizzle atom where the per-atom loads would."""
+    st = max(2, min(4, 200000 // ((128 + tileN // cg) * tileK * 2)))
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, cta_group=cg)
+    C, exact = _run(alcop, 512, 768, 384, batch=3, sched=s, seed=11)
+    _assert_exact(C, exact, torch.float32)

@@ -21,25 +21,30 @@ def main():
     inner = int(sys.argv[7]) if len(sys.argv) > 7 else 2
     mode = int(sys.argv[8]) if len(sys.argv) > 8 else 1
     cg = int(sys.argv[9]) if len(sys.argv) > 9 else 1
+    nctas = int(sys.argv[10]) if len(sys.argv) > 10 else 0
     lib = alcop.load_library()
     lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
-    stamps = torch.zeros(148 * 8 + 64 + 128, dtype=torch.int64, device="cuda")
+    s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg,
+                            num_ctas=nctas)
+    stamps = torch.zeros(148 * 8 + 64 + 128 + 2, dtype=torch.int64, device="cuda")
     for _ in range(3):
         alcop.matmul(A, B, s, out=C)
     torch.cuda.synchronize()
     lib.alcop_debug_set_stamps(ctypes.c_void_p(stamps.data_ptr()))
     res = []
+    mhz = []
     for rep in range(5):
         stamps.zero_()
         alcop.matmul(A, B, s, out=C)
         torch.cuda.synchronize()
         epi = stamps[148 * 8:148 * 8 + 64].view(16, 4).cpu().numpy().astype(np.int64)
-        ch = stamps[148 * 8 + 64:].view(2, 64).cpu().numpy().astype(np.int64)
+        ch = stamps[148 * 8 + 64:148 * 8 + 192].view(2, 64).cpu().numpy().astype(np.int64)
         t = stamps[:148 * 8].view(148, 8).cpu().numpy().astype(np.int64)
+        clk = stamps[148 * 8 + 192:148 * 8 + 194].cpu().numpy().astype(np.int64)
+        mhz.append((clk[1] - clk[0]) / max(1, t[0, 7] - t[0, 0]) * 1e3)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         res.append((t - t0) / 1000.0)
@@ -56,6 +61,7 @@ def main():
         print("epilogue CTA0 warp2 per chunk (clk from first chunk start): ldstart, ld+pack done, staging free, store issued")
         for row in nz:
             print("   ", [int(x - base) for x in row])
+    print("CTA0 effective SM clock (clock64 / globaltimer): %s MHz" % [round(x) for x in mhz])
     names = ["start", "setup", "firstTMA", "firstFull", "lastCommit", "epiFirst", "epiDone", "end"]
     r = np.stack(res)  # reps x ctas x 8
     print("%s M=%d N=%d K=%d tile=128x%dx%d s=%d ctas=%d" % (s, M, N, K, tN, tK, st, r.shape[1]))
