@@ -29,10 +29,13 @@ int64_t round_up_pow2_cols(int64_t cols) {
 }
 
 int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
-  (void)w;
   const int64_t cg = s.cta_group == 2 ? 2 : 1;
   const int64_t a_stage = kTileM * s.tileK * 2;         // per CTA: 128 rows of A
-  const int64_t b_stage = s.tileN / cg * s.tileK * 2;   // per CTA: tileN/cta_group columns of B
+  // per CTA: tileN/cta_group columns of B (a CTA pair with B[K,N] and 96-column
+  // halves stages two 64-column 128B-swizzled atoms, see gemm_sm100.cu b_pad)
+  const int64_t half = s.tileN / cg;
+  const int64_t b_cols = (cg == 2 && w.b_layout == ALCOP_B_KN && half % 64 != 0) ? (half + 63) / 64 * 64 : half;
+  const int64_t b_stage = b_cols * s.tileK * 2;
   const int64_t bars = 8 * (3 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;  // + ready[] (pre-op)
   const int64_t staging = 4 * 2 * 32 * 128;  // epilogue TMA-store staging
   return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + staging + bars;

@@ -67,6 +67,13 @@ struct GemmKParams {
   // of a chunk (A: the BK/64 K atoms; B[K,N]: the N atoms), instead of one
   // instruction per atom (each TMA issue costs the producer ~60-80 clk)
   int32_t a_view, b_view;
+  // timing experiments only (env ALCOP_DEBUG_SKIP, results are garbage):
+  // bit 0 = no TMA loads (producer arrives on full without bytes), bit 1 = no MMAs
+  int32_t dbg_skip;
+  // CTA pair, B[K,N] with BN/2 % 64 != 0 (BN 192: halves of 96 columns): load
+  // each half as two 128B-swizzled 64-column atoms (over-fetching 32 columns
+  // that the MMA never reads) instead of three 64B-swizzled 32-column atoms
+  int32_t b_pad;
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
 };
@@ -434,7 +441,11 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         ++ra.count;
         coord(tl);
         const uint32_t fb = smem_u32(&fullA[slot]);
-        ISSUE(mbar_arrive_expect_tx(fb, a_bytes + b_bytes); issue_a(slot, fb, chunk); issue_b(slot, fb, chunk);
+        ISSUE(if (p.dbg_skip & 1) mbar_arrive(fb); else {
+          mbar_arrive_expect_tx(fb, a_bytes + b_bytes);
+          issue_a(slot, fb, chunk);
+          issue_b(slot, fb, chunk);
+        };
               log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
               log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1));
         ra.advance(p.sA);
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
                 const uint32_t a_off = kConv == 2 ? u * (2 * kTileM * 16 / 16)
                                        : BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+                if (!(p.dbg_skip & 2)) umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
               } umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
               if (!kJoint) umma_commit(smem_u32(&emptyB[sb]));   // consumer_release B
               log_event<kDebug>(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, ca.count, ca.released);
@@ -756,7 +767,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
-  const bool b_sw64 = (half_n & 63) != 0;  // BN = 192: N-major halves of 96 columns
+  const bool b_sw64 = (half_n & 63) != 0 && !p.b_pad;  // BN = 192: N-major halves of 96 columns
   if (threadIdx.x == 0) stamp<true>(p, 0);
 
   if (warp == 0 && elect_one()) {
@@ -814,6 +825,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
+        if (p.dbg_skip & 1) {
+          ISSUE(if (leader) mbar_arrive(fb_local));
+          ra.advance(p.sA);
+          return;
+        }
         ISSUE(if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
               if (kKAtoms > 1 && p.a_view) {
                 tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
@@ -825,7 +841,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
               }
               const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
-              if (p.b_mn_major && p.b_view) {
+              if (p.b_mn_major && p.b_pad) {
+                tma_load_3d_pair(dst, &tmB, fb_leader, n0, chunk * BK, tc.b);
+                tma_load_3d_pair(dst + BK * 128, &tmB, fb_leader, n0 + 64, chunk * BK, tc.b);
+              } else if (p.b_mn_major && p.b_view) {
                 // atom-stacked view {atom width, K, N/atom}: the CTA's half_n columns in one box
                 tma_load_4d_pair(dst, &tmB, fb_leader, 0, chunk * BK, n0 / (b_sw64 ? 32 : 64), tc.b);
               } else if (p.b_mn_major && b_sw64) {
@@ -900,7 +919,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int u = 0; u < kSteps; ++u) {
                 const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+                if (!(p.dbg_skip & 2)) umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
           ca.advance(p.sA);
         }
@@ -1178,9 +1197,14 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
     const char* e = std::getenv("ALCOP_ATOM_VIEWS");
     return !(e && e[0] == '0');
   }();
-  const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0) ? 32 : 64;  // pair BN 192: SW64 halves
+  static const bool pad_on = [] {
+    const char* e = std::getenv("ALCOP_PAIR_B_PAD");
+    return !(e && e[0] == '0');
+  }();
+  const bool b_pad = pad_on && cg == 2 && w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0;
+  const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0 && !b_pad) ? 32 : 64;  // pair BN 192: SW64 halves
   const bool a_view = views_on && BK > 64 && w.K % 64 == 0 && w.pre_op == 0;
-  const bool b_view = views_on && w.b_layout == ALCOP_B_KN && w.N % b_atom == 0 && (BN / cg) / b_atom > 1;
+  const bool b_view = views_on && !b_pad && w.b_layout == ALCOP_B_KN && w.N % b_atom == 0 && (BN / cg) / b_atom > 1;
   int rc;
   if (a_view) {
     const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(w.M), static_cast<cuuint64_t>(w.K / 64),
@@ -1241,7 +1265,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.b_mn_major = w.b_layout == ALCOP_B_KN ? 1 : 0;
   kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM * cg, BN);
   kp.a_stage_bytes = static_cast<uint32_t>(kTileM * BK * 2);
-  kp.b_stage_bytes = static_cast<uint32_t>(BN / cg * BK * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>((b_pad ? (BN / cg + 63) / 64 * 64 : BN / cg) * BK * 2);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
   kp.C = C;
@@ -1252,8 +1276,16 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.stamps = g_stamps;
   kp.in_bf16 = w.in_dtype == ALCOP_BF16 ? 1 : 0;
   kp.pre_op = w.pre_op;
+  kp.b_pad = b_pad ? 1 : 0;
   kp.a_view = a_view ? 1 : 0;
   kp.b_view = b_view ? 1 : 0;
+  {
+    static const int skip = [] {
+      const char* e = std::getenv("ALCOP_DEBUG_SKIP");
+      return e ? std::atoi(e) : 0;
+    }();
+    kp.dbg_skip = skip;
+  }
 
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");

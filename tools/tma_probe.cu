@@ -28,7 +28,7 @@
 using namespace alcop::ptx;
 
 struct Params {
-  int box_rows, box_w, nbox, stages, chunks, share, csize, rows, cols, spin;
+  int box_rows, box_w, nbox, stages, chunks, share, csize, rows, cols, spin, mc;
   long long* cycles;
   long long* trace;  // [3][64] per-chunk clocks of CTA 0 (nullptr = off)
 };
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
         mbar_arrive_expect_tx(fb, chunk_bytes);
         if (p.trace && blockIdx.x == 0 && i < 64) p.trace[256 + i] = clock64() - t0;
         const int cb = (i + group) % ncb;
-        if (p.csize > 1) {
+        if (p.csize > 1 && p.mc) {
           for (int b = crank; b < p.nbox; b += p.csize)
             tma_load_2d_mc(ring + slot * chunk_bytes + b * box_bytes, &tm, fb, cb * p.box_w,
                            (rb * p.nbox + b) * p.box_rows, static_cast<uint16_t>((1u << p.csize) - 1));
@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
         if (p.trace && blockIdx.x == 0 && i < 64) p.trace[128 + i] = clock64() - t0;
         if (p.csize > 1) {
           for (uint32_t r = 0; r < static_cast<uint32_t>(p.csize); ++r)
-            mbar_arrive_cluster(mapa_shared(smem_u32(&empty[slot]), r));
+            asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                             mapa_shared(smem_u32(&empty[slot]), r))
+                         : "memory");
         } else {
           mbar_arrive(smem_u32(&empty[slot]));
         }
@@ -192,8 +194,16 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   // configs: {grid, box_rows, box_w, nbox, stages, share, csize}
   // configs: {grid, box_rows, box_w, nbox, stages, share, csize, spin}
+  // configs: {grid, box_rows, box_w, nbox, stages, share, csize, spin, multicast}
   std::vector<std::vector<int>> cfgs = {
-      {1, 128, 64, 1, 8, 1, 1, 0},  {1, 128, 64, 1, 8, 1, 1, 2}, {1, 128, 64, 2, 4, 1, 1, 2},
+      {148, 128, 64, 2, 4, 1, 1, 0, 0},  // unicast, no cluster (baseline)
+      {148, 128, 64, 2, 4, 2, 2, 0, 0},  // clusters of 2, same chunk, unicast, cross-CTA empties
+      {148, 128, 64, 2, 4, 2, 2, 0, 1},  // clusters of 2, multicast halves
+      {148, 128, 64, 4, 3, 4, 4, 0, 0},  // clusters of 4, unicast (64 KB chunks)
+      {148, 128, 64, 4, 3, 4, 4, 0, 1},  // clusters of 4, multicast quarters
+      {148, 128, 64, 4, 3, 1, 1, 0, 0},  // 64 KB chunks, no cluster
+      {8, 128, 64, 2, 4, 2, 2, 0, 1},    // few CTAs: multicast at low load
+      {8, 128, 64, 2, 4, 1, 1, 0, 0},
   };
   printf("grid box_rows box_w nbox stages share csize | chunkKB  GB/s_total  B/clk_chip  B/clk_SM  rows/clk_chip  clk/chunk\n");
   for (auto& c : cfgs) {
@@ -206,6 +216,7 @@ int main(int argc, char** argv) {
     p.share = c[5];
     p.csize = c[6];
     p.spin = c[7];
+    p.mc = c[8];
     p.rows = rows;
     p.cols = cols;
     p.chunks = 4000;
