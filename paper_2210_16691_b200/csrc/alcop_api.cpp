@@ -28,7 +28,7 @@ int64_t round_up_pow2_cols(int64_t cols) {
   return c;
 }
 
-int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
+static int64_t gemm_smem_base(const alcop_gemm_desc& w, const alcop_schedule& s) {
   const int64_t cg = s.cta_group == 2 ? 2 : 1;
   const int64_t a_stage = kTileM * s.tileK * 2;         // per CTA: 128 rows of A
   // per CTA: tileN/cta_group columns of B (a CTA pair with B[K,N] and 96-column
@@ -37,8 +37,19 @@ int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
   const int64_t b_cols = (cg == 2 && w.b_layout == ALCOP_B_KN && half % 64 != 0) ? (half + 63) / 64 * 64 : half;
   const int64_t b_stage = b_cols * s.tileK * 2;
   const int64_t bars = 8 * (3 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;  // + ready[] (pre-op)
-  const int64_t staging = 4 * 2 * 32 * 128;  // epilogue TMA-store staging
-  return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + staging + bars;
+  return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + bars;
+}
+
+// Epilogue TMA-store staging: two 4 KB buffers per epilogue warp (the store of
+// one chunk overlaps the TMEM read of the next) when they fit beside the ring,
+// else one — shared memory goes to pipeline stages first (one more stage of
+// lookahead is worth more than the store overlap).
+int32_t gemm_staging_bufs(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  return gemm_smem_base(w, s) + 4 * 2 * 32 * 128 <= kMaxSmemBytes ? 2 : 1;
+}
+
+int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  return gemm_smem_base(w, s) + 4 * gemm_staging_bufs(w, s) * 32 * 128;
 }
 
 static int dtype_bytes(int32_t dt) { return dt == ALCOP_F32 ? 4 : 2; }

@@ -74,6 +74,7 @@ struct GemmKParams {
   // each half as two 128B-swizzled 64-column atoms (over-fetching 32 columns
   // that the MMA never reads) instead of three 64B-swizzled 32-column atoms
   int32_t b_pad;
+  int32_t stage_bufs;  // epilogue staging buffers per warp (1 or 2), gemm_staging_bufs
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
 };
@@ -90,7 +91,7 @@ namespace {
 
 constexpr int kThreads = 192;
 constexpr int kThreadsPreOp = 192 + 128;  // + 4 transform warps for the fused pre-op
-constexpr int kStagingBytes = 4 * 2 * 32 * 128;
+constexpr int kStagingBytesPerBuf = 4 * 32 * 128;  // 4 epilogue warps x 32 rows x 128 B
 
 struct TileCoord {
   int b, mb, nb;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), 128B-swizzled for the TMA store
   const uint32_t staging = ringB + p.sB * p.b_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * p.a_stage_bytes + p.sB * p.b_stage_bytes +
-                                               kStagingBytes);
+                                               kStagingBytesPerBuf * p.stage_bufs);
   uint64_t* fullA = bars;
   uint64_t* emptyA = fullA + p.sA;
   uint64_t* fullB = kJoint ? fullA : emptyA + p.sA;
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
     // bulk-tensor store; two staging buffers per warp so the store of one
     // chunk overlaps the TMEM read of the next.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const uint32_t stage_base = staging + (warp - 2) * 2 * 4096;
+    const uint32_t stage_base = staging + (warp - 2) * p.stage_bufs * 4096;
     constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));  // 128 B of output per row
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
@@ -686,7 +687,12 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         }
         epistamp<kDebug>(p, warp, lane, c, 1);
         const uint32_t sbuf = stage_base + buf * 4096;
-        if (lane == 0) bulk_wait_group_read<1>();  // the store that last read sbuf is done
+        if (lane == 0) {  // the store that last read sbuf is done
+          if (p.stage_bufs == 2)
+            bulk_wait_group_read<1>();
+          else
+            bulk_wait_group_read<0>();
+        }
         __syncwarp();
         epistamp<kDebug>(p, warp, lane, c, 2);
 #pragma unroll
@@ -709,7 +715,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
           bulk_commit_group();
         }
         epistamp<kDebug>(p, warp, lane, c, 3);
-        buf ^= 1;
+        buf ^= p.stage_bufs - 1;
       }
     }
     if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
@@ -755,7 +761,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t ringA = smem_u32(smem);
   const uint32_t ringB = ringA + p.sA * p.a_stage_bytes;
   const uint32_t staging = ringB + p.sA * p.b_stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * (p.a_stage_bytes + p.b_stage_bytes) + kStagingBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * (p.a_stage_bytes + p.b_stage_bytes) +
+                                               kStagingBytesPerBuf * p.stage_bufs);
   uint64_t* full = bars;
   uint64_t* empty = full + p.sA;
   uint64_t* tfull = empty + p.sA;
@@ -941,7 +948,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     // ======================= epilogue (both CTAs) =======================
     const int q = warp & 3;
-    const uint32_t stage_base = staging + (warp - 2) * 2 * 4096;
+    const uint32_t stage_base = staging + (warp - 2) * p.stage_bufs * 4096;
     constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
@@ -974,7 +981,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
         const uint32_t sbuf = stage_base + buf * 4096;
-        if (lane == 0) bulk_wait_group_read<1>();
+        if (lane == 0) {
+          if (p.stage_bufs == 2)
+            bulk_wait_group_read<1>();
+          else
+            bulk_wait_group_read<0>();
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -987,7 +999,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                        tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM + q * 32, tc.b);
           bulk_commit_group();
         }
-        buf ^= 1;
+        buf ^= p.stage_bufs - 1;
       }
     }
     if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
@@ -1291,6 +1303,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
   const int smem = static_cast<int>(gemm_smem_bytes(w, s));
+  kp.stage_bufs = gemm_staging_bufs(w, s);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cg == 2) {
     if (w.pre_op) return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the fused pre-op runs with cta_group 1");
@@ -1502,6 +1515,7 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
   if (grid > kp.num_tiles) grid = kp.num_tiles;
   const int smem = static_cast<int>(gemm_smem_bytes(g, s));
+  kp.stage_bufs = gemm_staging_bufs(g, s);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (d.out_dtype) {
     case ALCOP_F32: return launch_conv_typed<float>(ta, tb, tc, kp, grid, smem, st);

@@ -15,7 +15,7 @@ import torch
 import paper_2210_16691_b200 as alcop
 from paper_2210_16691_b200.timing import Rotating, time_graph
 
-DEFAULT = ["4096x768x768", "4096x3072x768", "4096x768x3072", "4096x4096x4096", "8192x8192x8192",
+DEFAULT = ["4096x768x768", "4096x2304x768", "4096x3072x768", "4096x768x3072", "4096x4096x4096", "8192x8192x8192",
            "512x512x512", "512x512x64x192", "512x64x512x192", "16384x4096x4096"]
 
 

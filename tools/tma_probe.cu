@@ -175,6 +175,82 @@ __global__ void __launch_bounds__(32, 1) probe_burst(const __grid_constant__ CUt
   out[blockIdx.x * 64] = t1 - t0;
 }
 
+
+// primitive costs: one thread times N iterations of a primitive on already
+// completed / fresh mbarriers (clk per iteration)
+__global__ void __launch_bounds__(128, 1) probe_prims(long long* out, int n) {
+  __shared__ __align__(8) uint64_t bars[16];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // (0) try_wait on a phase that is already complete (parity 1 of a fresh barrier)
+    long long t0 = clock64();
+    uint32_t acc = 0;
+    for (int i = 0; i < n; ++i) acc += mbar_try_wait(smem_u32(&bars[i & 15]), 1);
+    long long t1 = clock64();
+    out[0] = (t1 - t0) / n;
+    // (1) mbarrier.arrive (count 1 -> phase flips each time)
+    t0 = clock64();
+    for (int i = 0; i < n; ++i) mbar_arrive(smem_u32(&bars[i & 15]));
+    t1 = clock64();
+    out[1] = (t1 - t0) / n;
+    // (2) arrive.expect_tx 0 bytes
+    t0 = clock64();
+    for (int i = 0; i < n; ++i) mbar_arrive_expect_tx(smem_u32(&bars[i & 15]), 0);
+    t1 = clock64();
+    out[2] = (t1 - t0) / n;
+    // (3) arrive + try_wait of the phase it just completed (round trip through the barrier)
+    uint32_t ph = 0;
+    t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      mbar_arrive(smem_u32(&bars[0]));
+      while (!mbar_try_wait(smem_u32(&bars[0]), ph)) {
+      }
+      ph ^= 1;
+    }
+    t1 = clock64();
+    out[3] = (t1 - t0) / n;
+    out[8] = acc;
+  }
+  __syncthreads();
+  if (warp == 1 && (threadIdx.x & 31) == 0) {
+    // (4) tcgen05.commit with nothing in flight -> arrive on a barrier, then wait for it
+    uint32_t ph = 0;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&bars[1]))
+                   : "memory");
+      while (!mbar_try_wait(smem_u32(&bars[1]), ph)) {
+      }
+      ph ^= 1;
+    }
+    long long t1 = clock64();
+    out[4] = (t1 - t0) / n;
+    // (5) tcgen05.commit issue cost alone (no wait), 16 barriers round robin
+    t0 = clock64();
+    for (int i = 0; i < n; ++i)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&bars[2 + (i & 7)]))
+                   : "memory");
+    t1 = clock64();
+    out[5] = (t1 - t0) / n;
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tslot), "r"(32));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   void* ptr = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -196,14 +272,6 @@ int main(int argc, char** argv) {
   // configs: {grid, box_rows, box_w, nbox, stages, share, csize, spin}
   // configs: {grid, box_rows, box_w, nbox, stages, share, csize, spin, multicast}
   std::vector<std::vector<int>> cfgs = {
-      {148, 128, 64, 2, 4, 1, 1, 0, 0},  // unicast, no cluster (baseline)
-      {148, 128, 64, 2, 4, 2, 2, 0, 0},  // clusters of 2, same chunk, unicast, cross-CTA empties
-      {148, 128, 64, 2, 4, 2, 2, 0, 1},  // clusters of 2, multicast halves
-      {148, 128, 64, 4, 3, 4, 4, 0, 0},  // clusters of 4, unicast (64 KB chunks)
-      {148, 128, 64, 4, 3, 4, 4, 0, 1},  // clusters of 4, multicast quarters
-      {148, 128, 64, 4, 3, 1, 1, 0, 0},  // 64 KB chunks, no cluster
-      {8, 128, 64, 2, 4, 2, 2, 0, 1},    // few CTAs: multicast at low load
-      {8, 128, 64, 2, 4, 1, 1, 0, 0},
   };
   printf("grid box_rows box_w nbox stages share csize | chunkKB  GB/s_total  B/clk_chip  B/clk_SM  rows/clk_chip  clk/chunk\n");
   for (auto& c : cfgs) {
@@ -287,6 +355,15 @@ int main(int argc, char** argv) {
     }
   }
 
+  {
+    probe_prims<<<1, 128>>>(cyc, 1024);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<long long> h(16);
+    cudaMemcpy(h.data(), cyc, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
+    printf("prims (clk/iter): try_wait(done) %lld  arrive %lld  arrive.expect_tx %lld  arrive+wait %lld  "
+           "tcgen05.commit+wait %lld  tcgen05.commit issue %lld  [%s]\n", h[0], h[1], h[2], h[3], h[4], h[5],
+           cudaGetErrorString(e));
+  }
   // ---- burst completion timelines (grid 1 and 148): nb 16 KB boxes (128 rows x 128 B)
   cudaFuncSetAttribute(probe_burst, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int g : {1, 148}) {
