@@ -217,6 +217,15 @@ int64_t alcop_gemm_workspace_bytes(const alcop_gemm_desc* w);
 int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
                     void* hC, void* workspace, void* stream);
 
+/* Stream-ordered variant (returns before the copies finish): A's row blocks go
+ * up on an internal copy stream, each block is multiplied on `stream` as it
+ * lands, C's blocks come back on a second copy stream; `stream` is made to
+ * wait for the last D2H, so C is valid after cudaStreamSynchronize(stream).
+ * Consecutive calls overlap (the H2D of call k+1 with the D2H of call k) when
+ * each call in flight has its own workspace and host buffers. */
+int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
+                          void* hC, void* workspace, void* stream);
+
 /* Implicit-GEMM conv2d (new; the reference excludes it). */
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
                  void* stream);

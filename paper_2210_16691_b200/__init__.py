@@ -37,7 +37,7 @@ MODE_WRAP, MODE_FUSED = 0, 1
 EXPORTED_SYMBOLS = [
     "alcop_version", "alcop_last_error", "alcop_schedule_default", "alcop_parse_schedule_script",
     "alcop_validate", "alcop_smem_bytes", "alcop_enumerate_pipeline", "alcop_gemm", "alcop_gemm_traced",
-    "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_conv2d", "alcop_hw_default_b200",
+    "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_gemm_host_async", "alcop_conv2d", "alcop_hw_default_b200",
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
     "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
 ]
@@ -180,6 +180,7 @@ def load_library(path: str | None = None):
     lib.alcop_gemm_workspace_bytes.restype = ctypes.c_int64
     lib.alcop_gemm_host.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p]
+    lib.alcop_gemm_host_async.argtypes = lib.alcop_gemm_host.argtypes
     lib.alcop_conv2d.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.c_void_p]
     lib.alcop_hw_default_b200.argtypes = [P(HW)]

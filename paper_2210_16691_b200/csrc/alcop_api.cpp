@@ -16,6 +16,35 @@ namespace {
 thread_local std::string g_last_error;
 }
 
+struct HostPipe {
+  static constexpr int kBlocks = 8;
+  bool ready = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kBlocks] = {}, ev_out[kBlocks] = {};
+};
+
+// Copy streams + events of the pipelined host-buffer GEMM, one set per host
+// thread and device (the entry point is synchronous, so a thread never has
+// two calls in flight on the same set).
+HostPipe* host_pipe() {
+  thread_local HostPipe pipes[16];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  HostPipe& hp = pipes[dev];
+  if (!hp.ready) {
+    bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&hp.ev_start, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&hp.ev_done, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < HostPipe::kBlocks && ok; ++i)
+      ok = cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&hp.ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return nullptr;
+    hp.ready = true;
+  }
+  return &hp;
+}
+
 int set_error(int code, const std::string& tag, const std::string& msg) {
   g_last_error = tag + ": " + msg;
   return code;
@@ -188,8 +217,8 @@ int64_t alcop_gemm_workspace_bytes(const alcop_gemm_desc* w) {
   return al(w->batch * w->M * w->K * 2) + al(w->batch * w->K * w->N * 2) + al(w->batch * w->M * w->N * ob);
 }
 
-int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB, void* hC,
-                    void* workspace, void* stream) {
+static int gemm_host_impl(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
+                          void* hC, void* workspace, void* stream, bool sync) {
   if (!w || !s || !hA || !hB || !hC || !workspace)
     return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
   clear_error();
@@ -205,15 +234,71 @@ int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const voi
   char* dB = dA + al(bytesA);
   char* dC = dB + al(bytesB);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemcpyAsync(dA, hA, bytesA, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, bytesB, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
-  rc = launch_gemm(*w, *s, dA, dB, dC, nullptr, 0, stream);
-  if (rc) return rc;
-  e = cudaMemcpyAsync(hC, dC, bytesC, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  // The load-and-use pipeline one level up: A is streamed to the device in
+  // row blocks on a copy stream, block i is multiplied on the caller's stream
+  // as soon as it lands, and its C rows go back on a second copy stream while
+  // block i+1 is multiplied and block i+2 copied in (H2D, compute and D2H
+  // overlap; the two copy directions run on separate engines).  B is needed
+  // whole by every block and goes first.  Batched / small problems: one block.
+  const int64_t tm = s->tileM;
+  int nblk = (w->batch == 1 && w->M >= 4 * tm) ? 8 : 1;
+  int64_t rows = (w->M + nblk - 1) / nblk;
+  rows = (rows + tm - 1) / tm * tm;
+  nblk = static_cast<int>((w->M + rows - 1) / rows);
+  HostPipe* hp = host_pipe();
+  if (!hp) return set_error(ALCOP_ERR_CUDA, "CudaError", "could not create the copy streams");
+  cudaError_t e = cudaSuccess;
+  if (sync) {  // earlier work on `stream` (it may still use the workspace) first
+    e = cudaEventRecord(hp->ev_start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->h2d, hp->ev_start, 0);
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, bytesB, cudaMemcpyHostToDevice, hp->h2d);
+  for (int i = 0; i < nblk && e == cudaSuccess; ++i) {
+    const int64_t r0 = i * rows, nr = std::min(rows, w->M - r0);
+    const int64_t off = nblk == 1 ? 0 : r0 * w->K * 2, len = nblk == 1 ? bytesA : nr * w->K * 2;
+    e = cudaMemcpyAsync(dA + off, static_cast<const char*>(hA) + off, len, cudaMemcpyHostToDevice, hp->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->ev_in[i], hp->h2d);
+  }
+  for (int i = 0; i < nblk && e == cudaSuccess && rc == ALCOP_OK; ++i) {
+    const int64_t r0 = i * rows, nr = std::min(rows, w->M - r0);
+    e = cudaStreamWaitEvent(st, hp->ev_in[i], 0);
+    if (e != cudaSuccess) break;
+    alcop_gemm_desc sub = *w;
+    if (nblk > 1) {
+      sub.M = nr;
+      sub.lda = w->K;
+      sub.ldc = w->N;
+    }
+    rc = launch_gemm(sub, *s, dA + (nblk == 1 ? 0 : r0 * w->K * 2), dB, dC + (nblk == 1 ? 0 : r0 * w->N * ob),
+                     nullptr, 0, stream);
+    if (rc == ALCOP_OK) e = cudaEventRecord(hp->ev_out[i], st);
+  }
+  if (rc != ALCOP_OK) {
+    cudaStreamSynchronize(hp->h2d);
+    return rc;
+  }
+  for (int i = 0; i < nblk && e == cudaSuccess; ++i) {
+    const int64_t r0 = i * rows, nr = std::min(rows, w->M - r0);
+    const int64_t off = nblk == 1 ? 0 : r0 * w->N * ob, len = nblk == 1 ? bytesC : nr * w->N * ob;
+    e = cudaStreamWaitEvent(hp->d2h, hp->ev_out[i], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(static_cast<char*>(hC) + off, dC + off, len, cudaMemcpyDeviceToHost,
+                                              hp->d2h);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(hp->ev_done, hp->d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp->ev_done, 0);  // stream order for the caller
+  if (e == cudaSuccess && sync) e = cudaEventSynchronize(hp->ev_done);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
+}
+
+int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB, void* hC,
+                    void* workspace, void* stream) {
+  return gemm_host_impl(w, s, hA, hB, hC, workspace, stream, true);
+}
+
+int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
+                          void* hC, void* workspace, void* stream) {
+  return gemm_host_impl(w, s, hA, hB, hC, workspace, stream, false);
 }
 
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* wt, void* y,

@@ -218,3 +218,28 @@ def test_atom_views_batched(alcop, cg, tileN, tileK):
     s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, cta_group=cg)
     C, exact = _run(alcop, 512, 768, 384, batch=3, sched=s, seed=11)
     _assert_exact(C, exact, torch.float32)
+
+
+@pytest.mark.parametrize("M,N,K,batch,out", [(4096, 384, 256, 1, "f32"), (1000, 192, 128, 1, "bf16"),
+                                             (256, 128, 64, 3, "f32"), (640, 256, 192, 1, "f32")])
+def test_gemm_host_pipelined_exact(alcop, M, N, K, batch, out):
+    """alcop_gemm_host (HOST buffers): A streamed in row blocks on a copy stream,
+    each block multiplied as it lands, C blocks copied back on a second stream —
+    the result must equal the exact integer product like the device-buffer call."""
+    import ctypes
+    a, b = gemm_inputs(M, N, K, batch, seed=5)
+    exact = _exact(a, b, batch > 1)
+    out_dt = torch.float32 if out == "f32" else torch.bfloat16
+    A = torch.from_numpy(a).to(torch.bfloat16).pin_memory()
+    B = torch.from_numpy(b).to(torch.bfloat16).pin_memory()
+    C = torch.zeros(exact.shape, dtype=out_dt).pin_memory()
+    d = alcop.gemm_desc(M, N, K, batch, alcop.BF16, alcop.F32 if out == "f32" else alcop.BF16, alcop.B_KN)
+    s = alcop.choose_schedule(d)
+    lib = alcop.load_library()
+    ws = torch.empty(lib.alcop_gemm_workspace_bytes(ctypes.byref(d)), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    rc = lib.alcop_gemm_host(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
+                             ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                             ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(st.cuda_stream))
+    assert rc == 0, lib.alcop_last_error()
+    _assert_exact(C, exact, out_dt)
