@@ -5,6 +5,7 @@ n_stage, n_stage_inner, mode) point for a set of GEMM shapes and writes JSON
 python tools/sweep.py out.json [shape ...]   shape = MxNxK[xbatch]
 """
 import itertools
+import random
 import json
 import os
 import sys
@@ -40,7 +41,8 @@ def main():
         rot = Rotating(mk, bytes_set, max_sets=6)
         d = alcop.gemm_desc(M, N, K, b, alcop.BF16, alcop.BF16, alcop.B_KN)
         flops = 2.0 * M * N * K * b
-        iters = 3 if flops > 1e12 else (10 if flops > 1e11 else 30)
+        iters = 4 if flops > 1e12 else (10 if flops > 1e11 else 30)
+        cands = []
         for cg, tN, tK, st, inner, mode in itertools.product([1, 2], [64, 128, 192, 256], [32, 64, 128], range(1, 9),
                                                              [1, 2], [alcop.MODE_FUSED, alcop.MODE_WRAP]):
             s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg)
@@ -50,15 +52,29 @@ def main():
                 continue
             if mode == alcop.MODE_WRAP and inner == 1 and st > 1:
                 continue
-
-            def f(i):
-                A, B, C = rot.next()
-                alcop.matmul(A, B, s, out=C)
-            try:
-                ms = time_graph(f, iters=iters, warmup=2)
-            except Exception as e:  # noqa
-                print("skip", s, e, flush=True)
+            cands.append(((cg, tN, tK, st, inner, mode), s))
+        # two passes in shuffled order, best of the two per point: the GPU's
+        # power/thermal state drifts over a long sweep, so one ordered pass
+        # biases whichever schedules run last
+        best_ms = {}
+        rng = random.Random(M * 7 + N * 13 + K)
+        for _ in range(2):
+            order = list(cands)
+            rng.shuffle(order)
+            for key, s in order:
+                def f(i, s=s):
+                    A, B, C = rot.next()
+                    alcop.matmul(A, B, s, out=C)
+                try:
+                    ms = time_graph(f, iters=iters, warmup=2)
+                except Exception as e:  # noqa
+                    print("skip", s, e, flush=True)
+                    continue
+                best_ms[key] = min(ms, best_ms.get(key, ms))
+        for (cg, tN, tK, st, inner, mode), s in cands:
+            if (cg, tN, tK, st, inner, mode) not in best_ms:
                 continue
+            ms = best_ms[(cg, tN, tK, st, inner, mode)]
             pred = alcop.predict(d, s)["seconds"] * 1e3
             res.append({"M": M, "N": N, "K": K, "batch": b, "tileN": tN, "tileK": tK, "stages": st, "inner": inner,
                         "mode": mode, "cg": cg, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12, "pred_ms": pred})
