@@ -342,6 +342,32 @@ def main_gpu(args, rank, world, local_rank):
             state["i"] = (state["i"] + 1) % nsets
         return step, nsets, set_bytes
 
+    def loaded_sm_clock(gl, iters=40):
+        """Effective SM clock under this workload's load: CTA 0 of the step's
+        last GEMM stamps clock64 and %globaltimer at start and end (debug
+        stamps, alcop_debug_set_stamps) after `iters` back-to-back steps.
+        NVML's SM clock reading does not show the loaded clock."""
+        lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
+        buf = torch.zeros(148 * 8 + 64 + 128 + 2, dtype=torch.int64, device=dev)
+        ins = []
+        for name, M, N, K in gl:
+            ins.append(((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
+                        (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
+                        torch.empty((M, N), device=dev, dtype=torch.bfloat16), (M, N, K)))
+        torch.cuda.synchronize()
+        lib.alcop_debug_set_stamps(ctypes.c_void_p(buf.data_ptr()))
+        try:
+            for _ in range(iters):
+                for A, B, C, shape in ins:
+                    launch(A, B, C, sched[shape], shape)
+            torch.cuda.synchronize()
+        finally:
+            lib.alcop_debug_set_stamps(None)
+        t = buf.cpu().tolist()
+        ns = t[7] - t[0]
+        cyc = t[148 * 8 + 193] - t[148 * 8 + 192]
+        return round(cyc / ns * 1e3) if ns > 0 and cyc > 0 else None
+
     step, nsets, set_bytes = make_step(gemms)
     shapes = sorted(set((M, N, K) for _, M, N, K in gemms))
 
@@ -384,6 +410,7 @@ def main_gpu(args, rank, world, local_rank):
 
     # ---- warmup + timed region (the headline)
     ms_max, clk = timed(step, args.steps, sample_clocks=True)
+    kclk = loaded_sm_clock(gemms)
     flops = step_flops()
     value = world * flops * args.steps / (ms_max * 1e-3) / 1e12
     # the other decomposition of the same layer (same FLOPs), same run
@@ -623,7 +650,10 @@ def main_gpu(args, rank, world, local_rank):
                                         if args.schedule == "tune" else "alcop_choose_schedule (model pick)"),
                            "schedules": {"%dx%dx%d" % k: v.as_dict() for k, v in sched.items()}},
                 "gpu_launches": len(gemms) * args.steps,
-                "clocks": clk.summary(),
+                "clocks": {**clk.summary(), "sm_mhz_in_kernel": kclk,
+                           "note": "sm_mhz: NVML samples during the timed region; sm_mhz_in_kernel: clock64 over "
+                                   "%globaltimer in CTA 0 of the step's last GEMM under back-to-back steps (the "
+                                   "loaded clock; NVML does not show it)"},
                 "roofline": roofline,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
