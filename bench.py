@@ -528,20 +528,83 @@ def main_gpu(args, rank, world, local_rank):
                                                                         "cta_group")}},
                 "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
         extra["n_stage_sweep"] = sweep
-        # ---- large square GEMM (config 5 point): 8192^3 bf16
-        n = 8192
-        dsq = alcop.gemm_desc(n, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
-        ssq = alcop.choose_schedule(dsq)
-        A = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
-        B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
-        C = torch.empty((n, n), device=dev, dtype=torch.bfloat16)
-        dsq_c = alcop.gemm_desc(n, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
-        descs[(n, n, n)] = dsq_c
-        ms = time_graph(lambda i: launch(A, B, C, ssq, (n, n, n)), iters=10, warmup=3)
-        tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
-        extra["large_square_8192"] = {"tflops": round(tf, 1), "frac_of_peak": round(tf / peaks["bf16_tflops"], 3),
-                                      "schedule": ssq.as_dict()}
-        del A, B, C
+    if not args.quick:
+        # ---- large square GEMMs (BASELINE configs[4]): n^3 bf16, n = 4096..16384,
+        # M-sharded across ranks (rows of A and C split in 256-row granules, B
+        # replicated, no collective on the compute path); aggregate =
+        # total FLOPs / max-over-ranks time.  At N > 1 the optional NCCL
+        # all-gather of C is timed separately.
+        from paper_2210_16691_b200.sharded import shard_range, gather_rows
+        squares = {}
+        for n in (4096, 8192, 12288, 16384):
+            sh = shard_range(n, rank, world, granule=256)
+            m = sh.size
+            dsq = alcop.gemm_desc(m, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+            descs[(m, n, n)] = dsq
+            ssq = sched.get((m, n, n)) or alcop.choose_schedule(dsq)
+            sched[(m, n, n)] = ssq
+            A = (torch.rand((m, n), device=dev) - 0.5).to(torch.bfloat16)
+            B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
+            C = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
+            barrier()
+            ms = time_graph(lambda i: launch(A, B, C, ssq, (m, n, n)), iters=8 if n < 12288 else 4, warmup=3)
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tf = 2.0 * n ** 3 / (float(tt.item()) * 1e-3) / 1e12
+            row = {"tflops_aggregate": round(tf, 1), "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
+                   "rows_per_gpu": m, "schedule": ssq.as_dict()}
+            if world > 1 and n == 16384:
+                for _ in range(2):
+                    gather_rows(C, n, rank, world)
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                gather_rows(C, n, rank, world)
+                e1.record()
+                torch.cuda.synchronize()
+                row["allgather_ms"] = round(e0.elapsed_time(e1), 3)
+            squares[str(n)] = row
+            del A, B, C
+            torch.cuda.empty_cache()
+        extra["large_square_m_sharded"] = {"sharding": "M (256-row granules), B replicated", "sizes": squares}
+        # ---- batched GEMMs of attention (BASELINE configs[2]): batch*heads = 192,
+        # seq 512, head_dim 64; QK^T [512x64]@[64x512], PV [512x512]@[512x64];
+        # HBM-bound (AI ~51 FLOP/B), batch-sharded across ranks
+        bmm = {}
+        nb = shard_range(192, rank, world).size
+        for name, (M, N, K) in (("qk_t", (512, 512, 64)), ("pv", (512, 64, 512))):
+            db = alcop.gemm_desc(M, N, K, nb, alcop.BF16, alcop.BF16, alcop.B_KN)
+            descs[("bmm", name)] = db
+            sb = alcop.choose_schedule(db)
+            rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((nb, M, K), device=dev) - 0.5).to(torch.bfloat16),
+                                                     (torch.rand((nb, K, N), device=dev) - 0.5).to(torch.bfloat16),
+                                                     torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
+                           (M * K + K * N + M * N) * 2 * nb, max_sets=16)
+            nr = len(rot.sets)
+
+            def runb(i, s_, rot=rot, nr=nr, db=db):
+                A, B, C = rot.sets[i % nr]
+                rc = lib.alcop_gemm(ctypes.byref(db), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
+                                    ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+                if rc:
+                    raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+            ms = time_graph(lambda i: runb(i, sb), iters=2 * nr, warmup=3, reps_per_graph=nr)
+            s1 = alcop.make_schedule(tileN=sb.tileN, tileK=sb.tileK, n_stage=1, n_stage_inner=1)
+            ms1 = time_graph(lambda i: runb(i, s1), iters=2 * nr, warmup=3, reps_per_graph=nr)
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            byts = (M * K + K * N + M * N) * 2 * 192
+            tsec = float(tt.item()) * 1e-3
+            bmm[name] = {"shape": [M, N, K], "batch": 192, "tflops_aggregate": round(2.0 * M * N * K * 192 / tsec / 1e12, 1),
+                         "gbs_aggregate": round(byts / tsec / 1e9, 1),
+                         "hbm_frac_per_gpu": round(byts / tsec / 1e9 / world / peaks["hbm_gbs"], 3),
+                         "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
+            del rot
+        extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
 
     # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
     if not args.quick:
