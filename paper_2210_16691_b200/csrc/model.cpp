@@ -73,17 +73,18 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   // B200 (sm_100a), 148 SMs, rates per SM-clock cycle at the ~1.9 GHz the
   // short kernels run at.  throughputSM and latLLCRead are fixed from
   // hardware facts (tcgen05 M=128 rate; measured chunk latency in
-  // tools/kbtimeline.py); the rest are least-squares fits to
-  // profiles/sweep_r01.json (tools/fit_model.py).
+  // tools/kbtimeline.py); the rest are fitted by tools/fit_model.py (rms log
+  // time error + model-pick quality) to the measured exhaustive sweep
+  // profiles/sweep_r01.json (10 shapes x ~380 schedules).
   hw->numSM = 148;
   hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
-  hw->bwLLC = 1e9;          // L2 -> SM bytes / clk, chip-wide (not binding in the fit)
-  hw->bwDRAM = 2273;        // HBM read+write bytes / clk (~4.3 TB/s effective)
-  hw->bwDRAMWrite = 11335;  // epilogue TMA-store drain, bytes / clk chip-wide
+  hw->bwLLC = 20381;        // L2 -> SM bytes / clk, chip-wide
+  hw->bwDRAM = 2258;        // HBM read+write bytes / clk (~4.3 TB/s effective)
+  hw->bwDRAMWrite = 29778;  // epilogue TMA-store drain, bytes / clk chip-wide
   hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
   hw->latDRAMRead = 1950;
-  hw->latDRAMWrite = 0;
-  hw->bwSmem = 55.43;       // per-SM L2 -> shared-memory TMA fill, bytes / clk
+  hw->latDRAMWrite = 298.9;  // per-tile epilogue floor
+  hw->bwSmem = 70.3;        // per-SM L2 -> shared-memory TMA fill, bytes / clk
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
   hw->regsPerSM = 262144;
@@ -92,12 +93,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
   hw->clockGHz = 1.9;
-  hw->tIssue = 268.1;
-  hw->tIssuePerBox = 49.24;
-  hw->tLaunch = 160.8;
-  hw->tTile = 0;
-  hw->overlapDRAM = 0.02;
-  hw->tPair = 3878;
+  hw->tIssue = 501.5;       // per-chunk producer/consumer floor (barrier hops + issue)
+  hw->tIssuePerBox = 5.27;
+  hw->tLaunch = 104.7;
+  hw->tTile = 198.0;
+  hw->overlapDRAM = 0.12;
+  hw->tPair = 6738;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -123,7 +124,13 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   out->nSmemLoop = E;
   out->nRegLoop = tK / 16;
   out->flopsOneRegLoop = 2 * (tM / cg) * tN * 16;            // per SM (each CTA owns 128 rows)
-  out->bytesOneSmemLoop = (tM / cg + tN / cg) * tK * eb;      // per CTA: 128 rows of A + tileN/cg of B
+  // per CTA: 128 rows of A + tileN/cg columns of B; a pair with B[K,N] and
+  // 96-column halves stages two 64-column atoms (gemm_sm100.cu b_pad)
+  const int64_t bN = tN / cg;
+  const bool kn = w->b_layout == ALCOP_B_KN;
+  const bool pad = cg == 2 && kn && (bN % 64) != 0;
+  const int64_t bcols = pad ? (bN + 63) / 64 * 64 : bN;
+  out->bytesOneSmemLoop = (tM / cg + bcols) * tK * eb;
   out->bytesWorkset = (w->M * w->K + w->K * w->N) * eb * w->batch;
   out->bytesOutputTile = (tM / cg) * tN * ob;
 
@@ -133,9 +140,12 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // L2 -> SM: the chip-wide share and the per-SM TMA fill rate
   const double tL2 = std::max(static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC,
                               static_cast<double>(out->bytesOneSmemLoop) / hw->bwSmem);
-  const int64_t bN = tN / cg;  // B columns staged per CTA
-  const int64_t bBoxes = w->b_layout == ALCOP_B_KN ? ((bN % 64) ? bN / 32 : bN / 64) : std::max<int64_t>(1, tK / 64);
-  const int64_t boxes = std::max<int64_t>(1, tK / 64) + bBoxes;
+  // TMA instructions per chunk: atom-stacked 4-D views bring all atoms of an
+  // operand in one box when the atom tiles the row (gemm_sm100.cu a_view/b_view)
+  const int64_t aBoxes = (tK > 64 && w->K % 64 == 0 && w->pre_op == 0) ? 1 : std::max<int64_t>(1, tK / 64);
+  const int64_t bBoxes = kn ? (pad ? 2 : ((w->N % 64 == 0 && bN / 64 > 1) ? 1 : std::max<int64_t>(1, bN / 64)))
+                            : std::max<int64_t>(1, tK / 64);
+  const int64_t boxes = aBoxes + bBoxes;
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors
   out->tSmemUse = std::max(tMma, std::max(tL2, tIssue));

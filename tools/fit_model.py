@@ -17,40 +17,52 @@ NSM = 148
 
 
 def pipeline_latency(tLoad, tUse, n, nPipe):
-    # perf_model.hpp:53-57 with nMplx = 1 (one CTA per SM)
-    if tLoad <= (nPipe - 1) * tUse:
-        return tUse * n
-    return (tLoad + tUse) * n / nPipe
+    # perf_model.hpp:53-57 with nMplx = 1 (one CTA per SM); numpy-vectorised
+    return np.where(tLoad <= (nPipe - 1) * tUse, tUse * n, (tLoad + tUse) * n / nPipe)
+
+
+def features(rows):
+    """Per-row arrays of everything the model needs that does not depend on
+    the constants (B[K,N] layout, as the sweep measures)."""
+    f = defaultdict(list)
+    for r in rows:
+        M, N, K, b = r["M"], r["N"], r["K"], r["batch"]
+        BN, BK, s, inner, mode = r["tileN"], r["tileK"], r["stages"], r["inner"], r["mode"]
+        cg = r.get("cg", 1)
+        tiles = math.ceil(M / (128 * cg)) * math.ceil(N / BN) * b
+        units = min(tiles, NSM // cg)   # CTAs (pairs) working at once
+        bN = BN // cg                     # B columns per CTA
+        pad = cg == 2 and bN % 64 != 0    # pair halves of 96 columns: two 64-column atoms
+        bcols = 128 if pad else bN
+        a_boxes = 1 if (BK > 64 and K % 64 == 0) else max(1, BK // 64)   # atom-stacked view
+        b_boxes = 2 if pad else (1 if (N % 64 == 0 and bN // 64 > 1) else max(1, bN // 64))
+        for k, v in (("ctas", units * cg), ("waves", math.ceil(tiles / units)), ("E", math.ceil(K / BK)),
+                     ("bytes_kb", (128 + bcols) * BK * 2), ("mma", 2 * 128 * BN * BK), ("boxes", a_boxes + b_boxes),
+                     ("s", s), ("inner", inner), ("mode", mode), ("cg", cg), ("BN", BN),
+                     ("dram_bytes", (M * K + K * N + M * N) * 2 * b), ("ms", r["ms"])):
+            f[k].append(v)
+    return {k: np.array(v, dtype=np.float64) for k, v in f.items()}
+
+
+def predict_cycles_v(F, P):
+    """model.cpp alcop_predict, vectorised over the sweep rows."""
+    t_mma = F["mma"] / P["tp"]
+    t_l2 = np.maximum(F["bytes_kb"] * F["ctas"] / P["bwL2"], F["bytes_kb"] / P["bwSM"])
+    t_kb = np.maximum(np.maximum(t_mma, t_l2), P["t_issue"] + P["t_issue_b"] * F["boxes"])
+    loads = F["E"] + np.where(F["mode"] == 0, F["s"] - 1, 0)
+    main = pipeline_latency(P["lat"], t_kb, loads, F["s"]) + P["tile0"]
+    main = main + np.where((F["mode"] == 0) | (F["s"] == 1), P["lat"] * 0.5, 0.0)  # per-tile refill bubble
+    epi = 128 * F["BN"] * 2 * F["ctas"] / P["bwW"] + P["epi0"]
+    body = np.where(F["inner"] >= 2, F["waves"] * np.maximum(main, epi) + np.minimum(main, epi),
+                    F["waves"] * (main + epi))
+    t = P["lat"] + body + np.where(F["cg"] == 2, P["pair0"], 0.0)
+    dram = F["dram_bytes"] / P["bwD"]
+    # DRAM and the SM pipeline overlap imperfectly: soft maximum
+    return P["launch"] + np.maximum(t, dram) + P["ovl"] * np.minimum(t, dram)
 
 
 def predict_cycles(r, P):
-    """P = dict of constants (cycles / bytes-per-cycle)."""
-    M, N, K, b = r["M"], r["N"], r["K"], r["batch"]
-    BN, BK, s, inner, mode = r["tileN"], r["tileK"], r["stages"], r["inner"], r["mode"]
-    cg = r.get("cg", 1)
-    tiles = math.ceil(M / (128 * cg)) * math.ceil(N / BN) * b
-    units = min(tiles, NSM // cg)   # CTAs (pairs) working at once
-    ctas = units * cg
-    waves = math.ceil(tiles / units)
-    E = math.ceil(K / BK)
-    bytes_kb = (128 + BN // cg) * BK * 2   # per CTA
-    t_mma = 2 * 128 * BN * BK / P["tp"]
-    t_l2 = max(bytes_kb * ctas / P["bwL2"], bytes_kb / P["bwSM"])
-    boxes = max(1, BK // 64) + max(1, (BN // cg) // 64)
-    t_kb = max(t_mma, t_l2, P["t_issue"] + P["t_issue_b"] * boxes)
-    loads = E + (s - 1 if mode == 0 else 0)
-    main = pipeline_latency(P["lat"], t_kb, loads, s) + P["tile0"]
-    if mode == 0 or s == 1:
-        main += P["lat"] * 0.5  # per-tile refill bubble
-    epi = 128 * BN * 2 * ctas / P["bwW"] + P["epi0"]
-    if inner >= 2:
-        body = waves * max(main, epi) + min(main, epi)
-    else:
-        body = waves * (main + epi)
-    t = P["lat"] + body + (P["pair0"] if cg == 2 else 0.0)
-    dram = (M * K + K * N + M * N) * 2 * b / P["bwD"]
-    # DRAM and the SM pipeline overlap imperfectly: soft maximum
-    return P["launch"] + max(t, dram) + P["ovl"] * min(t, dram)
+    return float(predict_cycles_v(features([r]), P)[0])
 
 
 KEYS = ["tp", "bwL2", "t_issue", "t_issue_b", "lat", "bwW", "epi0", "launch", "bwD", "tile0", "ovl", "bwSM", "pair0"]
@@ -68,22 +80,16 @@ def load(path):
 FIXED = {}
 
 
-def loss(x, rows):
+def loss(x, F, groups):
     """rms log error + a pick-quality term (mean log(pick/best) over shapes)."""
-    P = dict(zip(KEYS, np.exp(x)))
+    P = dict(zip([k for k in KEYS if k not in FIXED], np.exp(x)))
     P.update(FIXED)
-    err = 0.0
-    by = defaultdict(list)
-    for r in rows:
-        pc = predict_cycles(r, P)
-        err += (math.log(pc / CLOCK * 1e3) - math.log(r["ms"])) ** 2
-        by[(r["M"], r["N"], r["K"], r["batch"])].append((pc, r["ms"]))
+    pc = predict_cycles_v(F, P)
+    err = np.log(pc / CLOCK * 1e3) - np.log(F["ms"])
     pick = 0.0
-    for v in by.values():
-        best = min(m for _, m in v)
-        chosen = min(v)[1]
-        pick += math.log(chosen / best)
-    return math.sqrt(err / len(rows)) + PICK_W * pick / len(by)
+    for idx in groups:
+        pick += math.log(F["ms"][idx][np.argmin(pc[idx])] / F["ms"][idx].min())
+    return math.sqrt(float(np.mean(err ** 2))) + PICK_W * pick / len(groups)
 
 
 def report(rows, P):
@@ -113,16 +119,22 @@ def main():
             PICK_W = float(v)
         else:
             FIXED[k] = float(v)
-    x0 = np.log([INIT[k] for k in KEYS])
+    free = [k for k in KEYS if k not in FIXED]
+    x0 = np.log([INIT[k] for k in free])
+    F = features(rows)
+    by = defaultdict(list)
+    for i, r in enumerate(rows):
+        by[(r["M"], r["N"], r["K"], r["batch"])].append(i)
+    groups = [np.array(v) for v in by.values()]
     best = None
-    for trial in range(6):
+    for trial in range(8):
         start = x0 + (np.random.RandomState(trial).randn(len(x0)) * 0.3 if trial else 0)
-        res = minimize(loss, start, args=(rows,), method="Nelder-Mead",
-                       options={"maxiter": 4000, "xatol": 1e-4, "fatol": 1e-7})
+        res = minimize(loss, start, args=(F, groups), method="Nelder-Mead",
+                       options={"maxiter": 8000, "xatol": 1e-4, "fatol": 1e-7})
         if best is None or res.fun < best.fun:
             best = res
     res = best
-    P = dict(zip(KEYS, np.exp(res.x)))
+    P = dict(zip(free, np.exp(res.x)))
     P.update(FIXED)
     print("fit objective:", res.fun)
     print(json.dumps({k: round(v, 2) for k, v in P.items()}))
