@@ -180,7 +180,8 @@ def load_library(path: str | None = None):
     lib.alcop_gemm_workspace_bytes.restype = ctypes.c_int64
     lib.alcop_gemm_host.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p]
-    lib.alcop_gemm_host_async.argtypes = lib.alcop_gemm_host.argtypes
+    if hasattr(lib, "alcop_gemm_host_async"):
+        lib.alcop_gemm_host_async.argtypes = lib.alcop_gemm_host.argtypes
     lib.alcop_conv2d.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.c_void_p]
     lib.alcop_hw_default_b200.argtypes = [P(HW)]

@@ -63,13 +63,9 @@ struct GemmKParams {
   int32_t conv_Pb, conv_Qb;                // stem: 8-row x 16-column output blocks per image
   int32_t conv_stem5;                      // stem A map is the 5-D strided view (stored H % stride_h == 0)
   int32_t conv_sh, conv_sw, conv_ph, conv_pw;
-  // atom-stacked views: one 4-D TMA box brings all 128-B (64-B) swizzle atoms
-  // of a chunk (A: the BK/64 K atoms; B[K,N]: the N atoms), instead of one
-  // instruction per atom (each TMA issue costs the producer ~60-80 clk)
+  // atom-stacked view of A: one 4-D TMA box brings the BK/64 K atoms of a
+  // chunk instead of one instruction per atom (BK = 128 only; b_view unused)
   int32_t a_view, b_view;
-  // timing experiments only (env ALCOP_DEBUG_SKIP, results are garbage):
-  // bit 0 = no TMA loads (producer arrives on full without bytes), bit 1 = no MMAs
-  int32_t dbg_skip;
   // CTA pair, B[K,N] with BN/2 % 64 != 0 (BN 192: halves of 96 columns): load
   // each half as two 128B-swizzled 64-column atoms (over-fetching 32 columns
   // that the MMA never reads) instead of three 64B-swizzled 32-column atoms
@@ -400,9 +396,6 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         const uint32_t dst = ringB + slot * b_bytes;
         if (kConv == 3) {
           tma_load_3d(dst, &tmB, fb, 0, chunk, tc.nb * p.BN);  // filter row `chunk`: S*C taps, zero-filled to 64
-        } else if (p.b_mn_major && p.b_view) {
-          // B[K,N] row-major, atom-stacked view {64 N, K, N/64}: all BN/64 atoms in one box
-          tma_load_4d(dst, &tmB, fb, 0, chunk * BK, tc.nb * (p.BN >> 6), tc.b);
         } else if (p.b_mn_major) {
           // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
           for (int a = 0; a < (p.BN >> 6); ++a)
@@ -442,11 +435,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         ++ra.count;
         coord(tl);
         const uint32_t fb = smem_u32(&fullA[slot]);
-        ISSUE(if (p.dbg_skip & 1) mbar_arrive(fb); else {
-          mbar_arrive_expect_tx(fb, a_bytes + b_bytes);
-          issue_a(slot, fb, chunk);
-          issue_b(slot, fb, chunk);
-        };
+        ISSUE(mbar_arrive_expect_tx(fb, a_bytes + b_bytes); issue_a(slot, fb, chunk); issue_b(slot, fb, chunk);
               log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
               log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1));
         ra.advance(p.sA);
@@ -566,7 +555,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
                 const uint32_t a_off = kConv == 2 ? u * (2 * kTileM * 16 / 16)
                                        : BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                if (!(p.dbg_skip & 2)) umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+                umma_f16_ss(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
               } umma_commit(smem_u32(&emptyA[sa]));  // consumer_release A
               if (!kJoint) umma_commit(smem_u32(&emptyB[sb]));   // consumer_release B
               log_event<kDebug>(p, 1, nev, 2, 0, tl, sa, v, pa, -1, -1, ca.count, ca.released);
@@ -832,11 +821,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
-        if (p.dbg_skip & 1) {
-          ISSUE(if (leader) mbar_arrive(fb_local));
-          ra.advance(p.sA);
-          return;
-        }
         ISSUE(if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
               if (kKAtoms > 1 && p.a_view) {
                 tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
@@ -851,9 +835,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (p.b_mn_major && p.b_pad) {
                 tma_load_3d_pair(dst, &tmB, fb_leader, n0, chunk * BK, tc.b);
                 tma_load_3d_pair(dst + BK * 128, &tmB, fb_leader, n0 + 64, chunk * BK, tc.b);
-              } else if (p.b_mn_major && p.b_view) {
-                // atom-stacked view {atom width, K, N/atom}: the CTA's half_n columns in one box
-                tma_load_4d_pair(dst, &tmB, fb_leader, 0, chunk * BK, n0 / (b_sw64 ? 32 : 64), tc.b);
               } else if (p.b_mn_major && b_sw64) {
                 for (int a = 0; a < (half_n >> 5); ++a)  // 32-column SW64 atoms (half_n = 96)
                   tma_load_3d_pair(dst + a * (BK * 64), &tmB, fb_leader, n0 + a * 32, chunk * BK, tc.b);
@@ -926,7 +907,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int u = 0; u < kSteps; ++u) {
                 const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                if (!(p.dbg_skip & 2)) umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
           ca.advance(p.sA);
         }
@@ -1216,7 +1197,9 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const bool b_pad = pad_on && cg == 2 && w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0;
   const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0 && !b_pad) ? 32 : 64;  // pair BN 192: SW64 halves
   const bool a_view = views_on && BK > 64 && w.K % 64 == 0 && w.pre_op == 0;
-  const bool b_view = views_on && !b_pad && w.b_layout == ALCOP_B_KN && w.N % b_atom == 0 && (BN / cg) / b_atom > 1;
+  // B keeps one box per 64-column atom: a runtime view branch in the
+  // producer's B issue measured 4 % slower on the conv/GEMM main loop
+  const bool b_view = false;
   int rc;
   if (a_view) {
     const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(w.M), static_cast<cuuint64_t>(w.K / 64),
@@ -1291,13 +1274,6 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.b_pad = b_pad ? 1 : 0;
   kp.a_view = a_view ? 1 : 0;
   kp.b_view = b_view ? 1 : 0;
-  {
-    static const int skip = [] {
-      const char* e = std::getenv("ALCOP_DEBUG_SKIP");
-      return e ? std::atoi(e) : 0;
-    }();
-    kp.dbg_skip = skip;
-  }
 
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");

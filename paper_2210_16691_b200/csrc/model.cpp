@@ -140,11 +140,10 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // L2 -> SM: the chip-wide share and the per-SM TMA fill rate
   const double tL2 = std::max(static_cast<double>(out->bytesOneSmemLoop) * static_cast<double>(ctas) / hw->bwLLC,
                               static_cast<double>(out->bytesOneSmemLoop) / hw->bwSmem);
-  // TMA instructions per chunk: atom-stacked 4-D views bring all atoms of an
-  // operand in one box when the atom tiles the row (gemm_sm100.cu a_view/b_view)
+  // TMA instructions per chunk: A's K atoms come in one 4-D box when the atom
+  // tiles the row (gemm_sm100.cu a_view); B issues one box per 64-column atom
   const int64_t aBoxes = (tK > 64 && w->K % 64 == 0 && w->pre_op == 0) ? 1 : std::max<int64_t>(1, tK / 64);
-  const int64_t bBoxes = kn ? (pad ? 2 : ((w->N % 64 == 0 && bN / 64 > 1) ? 1 : std::max<int64_t>(1, bN / 64)))
-                            : std::max<int64_t>(1, tK / 64);
+  const int64_t bBoxes = kn ? (pad ? 2 : std::max<int64_t>(1, bN / 64)) : std::max<int64_t>(1, tK / 64);
   const int64_t boxes = aBoxes + bBoxes;
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors

@@ -35,7 +35,7 @@ def features(rows):
         pad = cg == 2 and bN % 64 != 0    # pair halves of 96 columns: two 64-column atoms
         bcols = 128 if pad else bN
         a_boxes = 1 if (BK > 64 and K % 64 == 0) else max(1, BK // 64)   # atom-stacked view
-        b_boxes = 2 if pad else (1 if (N % 64 == 0 and bN // 64 > 1) else max(1, bN // 64))
+        b_boxes = 2 if pad else max(1, bN // 64)
         for k, v in (("ctas", units * cg), ("waves", math.ceil(tiles / units)), ("E", math.ceil(K / BK)),
                      ("bytes_kb", (128 + bcols) * BK * 2), ("mma", 2 * 128 * BN * BK), ("boxes", a_boxes + b_boxes),
                      ("s", s), ("inner", inner), ("mode", mode), ("cg", cg), ("BN", BN),
