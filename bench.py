@@ -422,6 +422,33 @@ def main_gpu(args, rank, world, local_rank):
            "ms_per_step": alt_ms / alt_steps, "tflops": world * flops * alt_steps / (alt_ms * 1e-3) / 1e12}
     del alt_step
     torch.cuda.empty_cache()
+    # the same GEMMs as ONE persistent launch (alcop_gemm_chain): the smem and
+    # TMEM rings never drain between GEMMs; with row-block dependencies
+    # (A_p row block waits for C_{p-1} row block: the layer order) and as
+    # independent GEMMs (grouped launch, no ordering)
+    chain = {}
+    if not args.unfused_qkv:
+        csets = [[((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
+                   (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
+                   torch.empty((M, N), device=dev, dtype=torch.bfloat16)) for _, M, N, K in gemms]
+                 for _ in range(nsets)]
+        cws = torch.empty(1 << 16, dtype=torch.uint8, device=dev)
+        for label, dep in (("row_block_dependencies", [0] + [1] * (len(gemms) - 1)), ("independent", None)):
+            best = None
+            for tn, tk, st in ((192, 64, 5), (256, 64, 4), (128, 128, 3)):
+                cs_ = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st)
+                ms = time_graph(lambda i: alcop.gemm_chain(csets[i % nsets], cs_, dep=dep, workspace=cws),
+                                iters=max(30, 6 * nsets), reps_per_graph=nsets)
+                if best is None or ms < best[0]:
+                    best = (ms, cs_)
+            tt = torch.tensor([best[0]], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            chain[label] = {"us_per_step": round(float(tt.item()) * 1e3, 2),
+                            "tflops": round(world * flops / (float(tt.item()) * 1e-3) / 1e12, 1),
+                            "schedule": best[1].as_dict()}
+        del csets
+        torch.cuda.empty_cache()
 
     # ---- per-GEMM times (CUDA graphs on the launching stream, each GEMM on its
     # own rotating inputs > 2x L2, i.e. cold operands as inside the step)
@@ -726,6 +753,7 @@ def main_gpu(args, rank, world, local_rank):
                 "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4), "shape": v["shape"],
                                  "launches_per_step": count[k]} for k, v in per.items()},
                 ("step_fused_qkv" if args.unfused_qkv else "step_unfused_qkv"): alt,
+                "step_one_launch": {"entry_point": "alcop_gemm_chain", **chain} if chain else None,
                 **extra}
         print(json.dumps(line), flush=True)
 

@@ -96,6 +96,28 @@ typedef struct {
   int32_t reserved1;
 } alcop_schedule;
 
+/* ---- several GEMMs in one persistent launch (new; no reference form) ------
+ * The GEMMs run as ONE flattened (problem, tile, chunk) stream through the
+ * same smem ring and TMEM accumulator ring, so nothing drains between them
+ * (the holistic pipeline one level up: the last tile's epilogue of GEMM p
+ * overlaps GEMM p+1's main loop).  dep[p] = 1: row block mb (128 rows) of
+ * A_p is read only after every tile of row block mb of C_{p-1} is stored
+ * (requires M_p == M_{p-1}); dep[0] must be 0.  All GEMMs share the schedule
+ * (cta_group 1, FUSED, equal A/B stages), dtypes and B layout; batch 1.
+ * workspace: device memory of alcop_gemm_chain_workspace_bytes() bytes
+ * (row-block counters, zeroed on `stream` by the call). */
+#define ALCOP_CHAIN_MAX 4
+typedef struct {
+  int32_t n; /* 1..ALCOP_CHAIN_MAX */
+  int32_t dep[ALCOP_CHAIN_MAX];
+  alcop_gemm_desc desc[ALCOP_CHAIN_MAX];
+  const void* A[ALCOP_CHAIN_MAX];
+  const void* B[ALCOP_CHAIN_MAX];
+  void* C[ALCOP_CHAIN_MAX];
+} alcop_chain;
+int64_t alcop_gemm_chain_workspace_bytes(const alcop_chain* ch);
+int alcop_gemm_chain(const alcop_chain* ch, const alcop_schedule* s, void* workspace, void* stream);
+
 /* Implicit-GEMM conv2d descriptor (no reference form: SPEC.md:218).
  * x: NHWC, w: KRSC, y: NPQK. */
 typedef struct {

@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = [
     "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_gemm_host_async", "alcop_conv2d", "alcop_hw_default_b200",
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
     "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
+    "alcop_gemm_chain_workspace_bytes", "alcop_gemm_chain",
 ]
 
 
@@ -49,6 +50,15 @@ class GemmDesc(ctypes.Structure):
                 ("pre_op", ctypes.c_int32), ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64),
                 ("ldc", ctypes.c_int64), ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
                 ("stride_c", ctypes.c_int64)]
+
+
+CHAIN_MAX = 4
+
+
+class Chain(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("dep", ctypes.c_int32 * CHAIN_MAX), ("desc", GemmDesc * CHAIN_MAX),
+                ("A", ctypes.c_void_p * CHAIN_MAX), ("B", ctypes.c_void_p * CHAIN_MAX),
+                ("C", ctypes.c_void_p * CHAIN_MAX)]
 
 
 class Schedule(ctypes.Structure):
@@ -180,6 +190,10 @@ def load_library(path: str | None = None):
     lib.alcop_gemm_workspace_bytes.restype = ctypes.c_int64
     lib.alcop_gemm_host.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p]
+    if hasattr(lib, "alcop_gemm_chain"):
+        lib.alcop_gemm_chain_workspace_bytes.argtypes = [P(Chain)]
+        lib.alcop_gemm_chain_workspace_bytes.restype = ctypes.c_int64
+        lib.alcop_gemm_chain.argtypes = [P(Chain), P(Schedule), ctypes.c_void_p, ctypes.c_void_p]
     if hasattr(lib, "alcop_gemm_host_async"):
         lib.alcop_gemm_host_async.argtypes = lib.alcop_gemm_host.argtypes
     lib.alcop_conv2d.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -555,3 +569,30 @@ def tune(A, B, C, budget=8, b_layout=B_KN, hw: HW | None = None, stream=None):
                                      ctypes.byref(n)))
     return best, [{"schedule": arr[i].schedule.as_dict(), "predicted_s": arr[i].predicted_s,
                    "measured_s": arr[i].measured_s} for i in range(n.value)]
+
+
+def make_chain(gemms, dep=None, b_layout=B_KN) -> Chain:
+    """gemms: [(A, B, C), ...] CUDA tensors (A [M,K], B [K,N] or [N,K], C [M,N]);
+    dep[p] = 1: A_p row blocks wait for C_{p-1} row blocks (alcop_gemm_chain)."""
+    ch = Chain()
+    ch.n = len(gemms)
+    for i, (A, B, C) in enumerate(gemms):
+        M, K = A.shape
+        N = B.shape[1] if b_layout == B_KN else B.shape[0]
+        ch.desc[i] = gemm_desc(M, N, K, 1, _dtype_code(A.dtype), _dtype_code(C.dtype), b_layout)
+        ch.A[i], ch.B[i], ch.C[i] = A.data_ptr(), B.data_ptr(), C.data_ptr()
+        ch.dep[i] = int(dep[i]) if dep else 0
+    return ch
+
+
+def gemm_chain(gemms, sched: Schedule, dep=None, b_layout=B_KN, workspace=None, stream=None):
+    """Several GEMMs in one persistent launch (alcop_gemm_chain); returns the Chain."""
+    import torch
+    ch = make_chain(gemms, dep, b_layout)
+    lib = load_library()
+    if workspace is None:
+        workspace = torch.empty(max(4, lib.alcop_gemm_chain_workspace_bytes(ctypes.byref(ch))), dtype=torch.uint8,
+                                device=gemms[0][0].device)
+    _check(lib.alcop_gemm_chain(ctypes.byref(ch), ctypes.byref(sched), ctypes.c_void_p(workspace.data_ptr()),
+                                _stream_ptr(stream)))
+    return ch

@@ -301,6 +301,34 @@ int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, con
   return gemm_host_impl(w, s, hA, hB, hC, workspace, stream, false);
 }
 
+int64_t alcop_gemm_chain_workspace_bytes(const alcop_chain* ch) {
+  if (!ch || ch->n < 1 || ch->n > ALCOP_CHAIN_MAX) return 0;
+  return static_cast<int64_t>(sizeof(int32_t)) * ch->n * chain_max_row_blocks(ch);
+}
+
+int alcop_gemm_chain(const alcop_chain* ch, const alcop_schedule* s, void* workspace, void* stream) {
+  if (!ch || !s || !workspace) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  if (ch->n < 1 || ch->n > ALCOP_CHAIN_MAX)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "chain length must be 1..ALCOP_CHAIN_MAX");
+  if (s->cta_group != 1 || s->mode != ALCOP_MODE_FUSED || s->n_stage_smem_A != s->n_stage_smem_B)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the chain runs cta_group 1, FUSED, equal A/B stages");
+  const alcop_gemm_desc& w0 = ch->desc[0];
+  for (int i = 0; i < ch->n; ++i) {
+    const alcop_gemm_desc& w = ch->desc[i];
+    if (!ch->A[i] || !ch->B[i] || !ch->C[i]) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL operand");
+    if (w.batch != 1 || w.pre_op || w.stride_a || w.stride_b || w.stride_c)
+      return set_error(ALCOP_ERR_CONFIG, "Unsupported", "chain GEMMs are batch 1 without pre-op");
+    if (w.in_dtype != w0.in_dtype || w.out_dtype != w0.out_dtype || w.b_layout != w0.b_layout)
+      return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "chain GEMMs share dtypes and B layout");
+    int rc = validate_gemm(w, *s);
+    if (rc) return rc;
+    if (ch->dep[i] && (i == 0 || w.M != ch->desc[i - 1].M))
+      return set_error(ALCOP_ERR_CONFIG, "BadDependency", "dep[p] needs p > 0 and M_p == M_{p-1}");
+  }
+  return launch_chain(*ch, *s, workspace, stream);
+}
+
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* wt, void* y,
                  void* stream) {
   if (!d || !s || !x || !wt || !y) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");

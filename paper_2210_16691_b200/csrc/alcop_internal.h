@@ -22,6 +22,8 @@ constexpr int kTmemCols = 512;
 int64_t round_up_pow2_cols(int64_t cols);
 int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s);
 int32_t gemm_staging_bufs(const alcop_gemm_desc& w, const alcop_schedule& s);
+int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace, void* stream);
+int64_t chain_max_row_blocks(const alcop_chain* ch);
 int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s);
 // Launch (validated) — implemented in gemm_sm100.cu.
 int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,

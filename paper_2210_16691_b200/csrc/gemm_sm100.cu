@@ -1142,6 +1142,14 @@ int launch_conv_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtens
 
 }  // namespace
 
+// for the chain kernel (chain_sm100.cu)
+int encode_tiled_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int rank, const cuuint64_t* dims,
+                     const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr,
+                     CUtensorMapSwizzle swz, const char* what) {
+  return encode_tiled(m, dt, base, rank, dims, strides_bytes, box, estr, swz, what);
+}
+bool pdl_enabled() { return g_pdl; }
+
 int device_sm_count() {
   static int sms = -1;
   static std::once_flag once;
