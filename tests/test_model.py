@@ -5,6 +5,7 @@ profiles/sweep_r01.json (the B200 stand-in for measure_ground_truth,
 pipe_sim.hpp:195-239)."""
 import json
 import os
+import sys
 
 import pytest
 
@@ -84,3 +85,24 @@ def test_model_assisted_tuning_on_gpu(alcop):
     m40 = min(t["measured_s"] for t in t40)
     assert len(t8) == 8 and len(t40) == 40
     assert m8 <= 1.05 * m40, (m8, m40, best8, best40)
+
+
+def test_fit_script_restates_the_product_model(alcop):
+    """tools/fit_model.py (the calibration's vectorised restatement) must predict
+    exactly what alcop_predict does with the same constants, or the fitted
+    constants would not mean what model.cpp uses them for."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import fit_model
+    hw = alcop.hw_b200()
+    P = {"tp": hw.throughputSM, "bwL2": hw.bwLLC, "t_issue": hw.tIssue, "t_issue_b": hw.tIssuePerBox,
+         "lat": hw.latLLCRead, "bwW": hw.bwDRAMWrite, "epi0": hw.latDRAMWrite, "launch": hw.tLaunch,
+         "bwD": hw.bwDRAM, "tile0": hw.tTile, "ovl": hw.overlapDRAM, "bwSM": hw.bwSmem, "pair0": hw.tPair}
+    with open(SWEEP) as f:
+        rows = json.load(f)
+    for r in rows[::37]:
+        d = alcop.gemm_desc(r["M"], r["N"], r["K"], r["batch"], alcop.BF16, alcop.BF16, alcop.B_KN)
+        s = alcop.make_schedule(tileN=r["tileN"], tileK=r["tileK"], n_stage=r["stages"], n_stage_inner=r["inner"],
+                                mode=r["mode"], cta_group=r.get("cg", 1))
+        want = alcop.predict(d, s)["tKernel"]
+        got = fit_model.predict_cycles(r, P)
+        assert abs(got - want) <= 1e-6 * want, (r, got, want)
