@@ -583,12 +583,12 @@ def main_gpu(args, rank, world, local_rank):
                    "rows_per_gpu": m, "schedule": ssq.as_dict()}
             if world > 1 and n == 16384:
                 for _ in range(2):
-                    gather_rows(C, n, rank, world)
+                    gather_rows(C, n, rank, world, granule=256)
                 torch.cuda.synchronize()
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-                gather_rows(C, n, rank, world)
+                gather_rows(C, n, rank, world, granule=256)
                 e1.record()
                 torch.cuda.synchronize()
                 row["allgather_ms"] = round(e0.elapsed_time(e1), 3)

@@ -72,12 +72,14 @@ def batch_sharded(fn, X, rank, world, gather=False, group=None):
     return gather_rows(local, X.shape[0], rank, world, group=group, dim0=True), sh
 
 
-def gather_rows(local, total, rank, world, group=None, dim0=False):
+def gather_rows(local, total, rank, world, group=None, dim0=False, granule=None):
     """All-gathers uneven row shards (NCCL on GPU, gloo on CPU): pads every
-    shard to the largest, gathers, then trims and concatenates in rank order."""
+    shard to the largest, gathers, then trims and concatenates in rank order.
+    `granule` must be the one the rows were sharded with (default 1 for
+    dim0 / batch, 128 for M rows)."""
     import torch
     import torch.distributed as dist
-    shards = all_shards(total, world, 1 if dim0 else 128)
+    shards = all_shards(total, world, granule or (1 if dim0 else 128))
     axis = 0 if dim0 else local.dim() - 2
     maxn = max(s.size for s in shards)
     pad_shape = list(local.shape)

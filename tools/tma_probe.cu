@@ -236,6 +236,26 @@ __global__ void __launch_bounds__(128, 1) probe_prims(long long* out, int n) {
     }
     long long t1 = clock64();
     out[4] = (t1 - t0) / n;
+    // (6) fence.proxy.async.shared::cta alone
+    t0 = clock64();
+    for (int i = 0; i < n; ++i) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    t1 = clock64();
+    out[6] = (t1 - t0) / n;
+    // (7) 8 x st.shared.v4 (one 4 KB staging chunk per warp) + fence.proxy.async
+    {
+      extern __shared__ uint8_t dyn[];
+      const uint32_t base = smem_u32(dyn);
+      const int lane = threadIdx.x & 31;
+      t0 = clock64();
+      for (int i = 0; i < n; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          st_shared_v4(base + lane * 128 + ((j ^ (lane & 7)) << 4), i, j, i + j, i - j);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      t1 = clock64();
+      out[7] = (t1 - t0) / n;
+    }
     // (5) tcgen05.commit issue cost alone (no wait), 16 barriers round robin
     t0 = clock64();
     for (int i = 0; i < n; ++i)
@@ -356,12 +376,12 @@ int main(int argc, char** argv) {
   }
 
   {
-    probe_prims<<<1, 128>>>(cyc, 1024);
+    probe_prims<<<1, 128, 8192>>>(cyc, 1024);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<long long> h(16);
     cudaMemcpy(h.data(), cyc, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
     printf("prims (clk/iter): try_wait(done) %lld  arrive %lld  arrive.expect_tx %lld  arrive+wait %lld  "
-           "tcgen05.commit+wait %lld  tcgen05.commit issue %lld  [%s]\n", h[0], h[1], h[2], h[3], h[4], h[5],
+           "tcgen05.commit+wait %lld  tcgen05.commit issue %lld  fence.proxy.async %lld  8xst.shared.v4+fence %lld  [%s]\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7],
            cudaGetErrorString(e));
   }
   // ---- burst completion timelines (grid 1 and 148): nb 16 KB boxes (128 rows x 128 B)
