@@ -58,6 +58,12 @@ def _worker(rank, world, port, out):
             coracle.gemm_i64(xs.numpy(), Y[:xs.shape[0]].numpy() * 0 + Y[0].numpy())), X, rank, world, gather=True)
         ref_b = torch.from_numpy(coracle.gemm_i64(xa, np.broadcast_to(xb[0], xb.shape).copy()))
         ok_b = bool(torch.equal(gathered, ref_b))
+        # 256-row granules (the bench's square GEMM shards), uneven: 700 rows over 2 ranks
+        from paper_2210_16691_b200.sharded import gather_rows, shard_range
+        rows = torch.arange(700 * 3, dtype=torch.float32).view(700, 3)
+        s256 = shard_range(700, rank, world, granule=256)
+        g256 = gather_rows(rows[s256.start:s256.stop].clone(), 700, rank, world, granule=256)
+        ok_b = ok_b and bool(torch.equal(g256, rows))
         # max-over-ranks timing reduction
         t = torch.tensor([float(rank + 1)])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
