@@ -22,11 +22,13 @@ def main():
     mode = int(sys.argv[8]) if len(sys.argv) > 8 else 1
     cg = int(sys.argv[9]) if len(sys.argv) > 9 else 1
     nctas = int(sys.argv[10]) if len(sys.argv) > 10 else 0
+    batch = int(sys.argv[11]) if len(sys.argv) > 11 else 1
+    shp = (batch,) if batch > 1 else ()
     lib = alcop.load_library()
     lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
-    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-    B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
-    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    A = torch.randn(shp + (M, K), device="cuda").to(torch.bfloat16)
+    B = torch.randn(shp + (K, N), device="cuda").to(torch.bfloat16)
+    C = torch.empty(shp + (M, N), device="cuda", dtype=torch.bfloat16)
     s = alcop.make_schedule(tileN=tN, tileK=tK, n_stage=st, n_stage_inner=inner, mode=mode, cta_group=cg,
                             num_ctas=nctas)
     stamps = torch.zeros(148 * 8 + 64 + 128 + 2, dtype=torch.int64, device="cuda")
