@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "alcop_internal.h"
 #include "sm100_ptx.cuh"
@@ -85,8 +86,10 @@ static bool g_pdl = [] {
 
 namespace {
 
-constexpr int kThreads = 192;
-constexpr int kThreadsPreOp = 192 + 128;  // + 4 transform warps for the fused pre-op
+constexpr int kThreads = 192;      // producer, MMA, 4 epilogue warps
+constexpr int kThreadsSplit = 224; // + warp 6: the B producer (conv, FUSED joint ring)
+constexpr int kThreadsPair = 224;  // the CTA pair: producer A, MMA, 4 epilogue warps, producer B
+constexpr int kThreadsPreOp = 192 + 128;  // 4 transform warps (6-9) for the fused pre-op, one producer
 constexpr int kStagingBytesPerBuf = 4 * 32 * 128;  // 4 epilogue warps x 32 rows x 128 B
 
 struct TileCoord {
@@ -243,7 +246,7 @@ struct RingCursor {
 // the whole 128 x 64 A chunk in one 128B-swizzled copy; output tiles are
 // 8 x 16 output-pixel blocks
 template <typename OutT, int BK, bool kJoint, bool kDebug, int kConv = 0, bool kPreOp = false>
-__global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
+__global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug && kConv != 0 ? kThreadsSplit : kThreads), 1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
   using namespace ptx;
@@ -320,10 +323,21 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
   const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
   const int E = p.E;
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
+  // Split producer (FUSED, joint ring): a TMA issue costs the issuing thread
+  // ~80 clk and a chunk is 2-5 of them, which bounded the per-chunk time near
+  // or above the MMA time; warp 0 commits the chunk (arrive.expect_tx of all
+  // its bytes) and loads A, warp 6 waits on the same empty barrier and loads B
+  // into the same full barrier (B bytes may land before the expect_tx: the
+  // phase still needs warp 0's arrival).  WRAP / debug / pre-op / split rings
+  // keep one producer (the device trace logs both buffers from one thread).
+  // Measured: +4-11 % on the implicit-GEMM conv layers and the CTA pairs with
+  // 64-wide chunks, -1.5 % on the single-CTA GEMMs of the BERT step, so the
+  // single-CTA GEMM keeps one producer.
+  constexpr bool kSplit = kJoint && !kDebug && !kPreOp && kConv != 0;
 
-  if (warp == 0) {
+  if (warp == 0 || (kSplit && warp == 6)) {
     if (ROLE_GUARD()) {
-      // ======================= producer (TMA) =======================
+      // ======================= producer(s) (TMA) =======================
       RingCursor ra, rb;
       int nev = 0;
       TileCoord tc{0, 0, 0};
@@ -426,7 +440,9 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         r.advance(s);
       };
       // joint ring: both buffers' copies of a chunk under one barrier pair
-      auto load_joint = [&](int tl, int chunk) {
+      // kRole: 0 = commit + A, 1 = B, 2 = both (single producer)
+      auto load_joint = [&](int tl, int chunk, auto role) {
+        constexpr int kRole = decltype(role)::value;
         const uint32_t slot = ra.slot;
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&emptyA[slot]), par);
@@ -435,13 +451,18 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         ++ra.count;
         coord(tl);
         const uint32_t fb = smem_u32(&fullA[slot]);
-        ISSUE(mbar_arrive_expect_tx(fb, a_bytes + b_bytes); issue_a(slot, fb, chunk); issue_b(slot, fb, chunk);
+        ISSUE(if constexpr (kRole != 1) {
+          mbar_arrive_expect_tx(fb, a_bytes + b_bytes);
+          issue_a(slot, fb, chunk);
+        } if constexpr (kRole != 0) issue_b(slot, fb, chunk);
               log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
               log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1));
         ra.advance(p.sA);
       };
 
-      if (wrap) {
+      if (wrap && warp != 0) {
+        // WRAP keeps one producer (warp 0)
+      } else if (wrap) {
         // reference-faithful: per tile, prologue chunks 0..s-2 into slots 0..s-2
         // (pipeline_pass.hpp:647-656), then steady loads of chunk (v+s-1)%E
         // (pipeline_pass.hpp:501-509); the s-1 tail loads wrap to chunks 0..
@@ -451,7 +472,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
           if constexpr (kJoint) {
             int c = 0;
             for (int i = 0; i < E + p.sA - 1; ++i) {
-              load_joint(tl, c);
+              load_joint(tl, c, std::integral_constant<int, 2>{});
               c = (c + 1 == E) ? 0 : c + 1;
             }
           } else {
@@ -469,9 +490,17 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
       } else {
         // fused: one lookahead window over the flattened (tile, chunk) stream;
         // issuing in order is enough, the empty barriers enforce the lookahead
-        if constexpr (kJoint) {
+        if constexpr (kSplit) {
+          if (warp == 0) {
+            for (int tl = 0; tl < my_tiles; ++tl)
+              for (int c = 0; c < E; ++c) load_joint(tl, c, std::integral_constant<int, 0>{});
+          } else {
+            for (int tl = 0; tl < my_tiles; ++tl)
+              for (int c = 0; c < E; ++c) load_joint(tl, c, std::integral_constant<int, 1>{});
+          }
+        } else if constexpr (kJoint) {
           for (int tl = 0; tl < my_tiles; ++tl)
-            for (int c = 0; c < E; ++c) load_joint(tl, c);
+            for (int c = 0; c < E; ++c) load_joint(tl, c, std::integral_constant<int, 2>{});
         } else {
           const int total = my_tiles * E;
           int ta = 0, ca = 0, tb = 0, cb = 0;  // (tile, chunk) of the next A / B load
@@ -634,7 +663,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
         cr.advance(p.sA);
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ======================= epilogue (warps 2-5) =======================
     // TMEM -> registers (tcgen05.ld) -> 128B-swizzled smem staging -> TMA
     // bulk-tensor store; two staging buffers per warp so the store of one
@@ -735,7 +764,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : kThreads, 1)
 // Joint A+B ring only (n_stage_A == n_stage_B).
 // ---------------------------------------------------------------------------
 template <typename OutT, int BK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                      const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
   using namespace ptx;
@@ -801,38 +830,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int E = p.E;
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 6) {
     if (ROLE_GUARD()) {
-      // ======================= producer (both CTAs) =======================
+      // ======================= producers (both CTAs) =======================
       RingCursor ra;
       TileCoord tc{0, 0, 0};
       int tc_tile = -1;
       const uint32_t a_bytes = p.a_stage_bytes, b_bytes = p.b_stage_bytes;
       const uint32_t pair_bytes = 2 * (a_bytes + b_bytes);
-      auto load = [&](int tl, int chunk) {
+      // Producer issue is split over two warps in FUSED mode: a TMA issue
+      // costs the issuing thread ~80 clk and a chunk is 3-4 of them, which
+      // bounded the per-chunk time above the 256x256 MMA time (~540 vs 512
+      // clk, tools/timeline.py).  Warp 0 commits (arrive.expect_tx of all
+      // the chunk's bytes on the leader's full barrier) and loads A; warp 6
+      // waits on the same empty barrier and loads B, completing on the same
+      // full barrier (its bytes may land before the expect_tx: the phase
+      // still needs warp 0's arrival).  kRole: 0 = A + commit, 1 = B, 2 = both.
+      auto load = [&](int tl, int chunk, auto role) {
+        constexpr int kRole = decltype(role)::value;
         const uint32_t slot = ra.slot;
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire (own slot, released by the pair's MMA)
         ra.phase ^= 1u << slot;
-        if (lane == 0) chunkstamp<true>(p, 0, ra.count++);
+        if (lane == 0 && warp == 0) chunkstamp<true>(p, 0, ra.count++);
         if (tl != tc_tile) {
           tc_tile = tl;
           tc = tile_coord(p, cluster_id + tl * nclusters);
         }
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
-        ISSUE(if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
-              if (kKAtoms > 1 && p.a_view) {
-                tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
-                                 tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, chunk * kKAtoms, tc.b);
-              } else {
+        ISSUE(if constexpr (kRole != 1) {
+                if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
+                if (kKAtoms > 1 && p.a_view) {
+                  tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
+                                   tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, chunk * kKAtoms, tc.b);
+                } else {
 #pragma unroll
-                for (int a = 0; a < kKAtoms; ++a) tma_load_3d_pair(
-                    ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
-                    tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
+                  for (int a = 0; a < kKAtoms; ++a) tma_load_3d_pair(
+                      ringA + slot * a_bytes + a * (kTileM * 128), &tmA, fb_leader, chunk * BK + a * kBoxK,
+                      tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
+                }
               }
               const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
-              if (p.b_mn_major && p.b_pad) {
+              if (kRole == 0) {
+              } else if (p.b_mn_major && p.b_pad) {
                 tma_load_3d_pair(dst, &tmB, fb_leader, n0, chunk * BK, tc.b);
                 tma_load_3d_pair(dst + BK * 128, &tmB, fb_leader, n0 + 64, chunk * BK, tc.b);
               } else if (p.b_mn_major && b_sw64) {
@@ -849,17 +890,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ra.advance(p.sA);
       };
       if (wrap) {
-        for (int tl = 0; tl < my_tiles; ++tl) {
-          ra.slot = 0;
-          int c = 0;
-          for (int i = 0; i < E + p.sA - 1; ++i) {
-            load(tl, c);
-            c = (c + 1 == E) ? 0 : c + 1;
+        if (warp == 0) {
+          for (int tl = 0; tl < my_tiles; ++tl) {
+            ra.slot = 0;
+            int c = 0;
+            for (int i = 0; i < E + p.sA - 1; ++i) {
+              load(tl, c, std::integral_constant<int, 2>{});
+              c = (c + 1 == E) ? 0 : c + 1;
+            }
           }
         }
+      } else if (warp == 0) {
+        for (int tl = 0; tl < my_tiles; ++tl)
+          for (int c = 0; c < E; ++c) load(tl, c, std::integral_constant<int, 0>{});
       } else {
         for (int tl = 0; tl < my_tiles; ++tl)
-          for (int c = 0; c < E; ++c) load(tl, c);
+          for (int c = 0; c < E; ++c) load(tl, c, std::integral_constant<int, 1>{});
       }
     }
     __syncwarp();
@@ -926,7 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // ======================= epilogue (both CTAs) =======================
     const int q = warp & 3;
     const uint32_t stage_base = staging + (warp - 2) * p.stage_bufs * 4096;
@@ -1071,7 +1117,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kThreadsPair);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1093,7 +1139,7 @@ int launch_typed_conv(const CUtensorMap& ta, const CUtensorMap& tb, const CUtens
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kDebug ? kThreads : kThreadsSplit);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -1,0 +1,32 @@
+"""A/B of CTA-pair GEMM schedules against a given libalcop build
+(measurement tool): python tools/pair_ab.py [path/to/libalcop.so]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2210_16691_b200 as alcop
+from paper_2210_16691_b200.timing import Rotating, time_graph
+
+if len(sys.argv) > 1:
+    alcop.LIB_PATH = sys.argv[1]
+res = {}
+for name, (M, N, K), (tn, tk, st) in (("ffn1_64s6", (4096, 3072, 768), (256, 64, 6)),
+                                      ("ffn1_128s3", (4096, 3072, 768), (256, 128, 3)),
+                                      ("qkv_64s6", (4096, 2304, 768), (256, 64, 6)),
+                                      ("ffn2_192s6", (4096, 768, 3072), (192, 64, 6)),
+                                      ("sq8192_64s6", (8192, 8192, 8192), (256, 64, 6)),
+                                      ("sq8192_128s3", (8192, 8192, 8192), (256, 128, 3))):
+    rot = Rotating(lambda i: ((torch.rand(M, K, device="cuda") - 0.5).to(torch.bfloat16),
+                              (torch.rand(K, N, device="cuda") - 0.5).to(torch.bfloat16),
+                              torch.empty(M, N, device="cuda", dtype=torch.bfloat16)), (M * K + K * N + M * N) * 2,
+                   max_sets=8)
+    nr = len(rot.sets)
+    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=2)
+    ms = time_graph(lambda i: alcop.matmul(rot.sets[i % nr][0], rot.sets[i % nr][1], s, out=rot.sets[i % nr][2]),
+                    iters=max(4 * nr, 8), reps_per_graph=nr)
+    res[name] = round(2.0 * M * N * K / ms / 1e9, 1)
+    del rot
+print(json.dumps({"lib": alcop.LIB_PATH[-24:], "pair": res}))

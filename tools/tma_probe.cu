@@ -271,6 +271,33 @@ __global__ void __launch_bounds__(128, 1) probe_prims(long long* out, int n) {
   }
 }
 
+
+// issue-rate probe: `nw` warps each issue `per` TMA boxes (16 KB) back to
+// back on their own barrier; clk from start to the last issue, per warp
+__global__ void __launch_bounds__(128, 1) probe_issue(const __grid_constant__ CUtensorMap tm, int nw, int per,
+                                                     long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 12 * 16384);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  if (warp < nw && (threadIdx.x & 31) == 0) {
+    const uint32_t b = smem_u32(&bars[warp]);
+    mbar_arrive_expect_tx(b, 16384 * per);
+    for (int i = 0; i < per; ++i)
+      tma_load_2d(smem_u32(smem) + ((warp * per + i) % 12) * 16384, &tm, b, (i % 32) * 64, (warp * 8 + i / 32) * 128);
+    out[warp] = clock64() - t0;
+    while (!mbar_try_wait(b, 0)) {
+    }
+    out[4 + warp] = clock64() - t0;
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   void* ptr = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -383,6 +410,28 @@ int main(int argc, char** argv) {
     printf("prims (clk/iter): try_wait(done) %lld  arrive %lld  arrive.expect_tx %lld  arrive+wait %lld  "
            "tcgen05.commit+wait %lld  tcgen05.commit issue %lld  fence.proxy.async %lld  8xst.shared.v4+fence %lld  [%s]\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7],
            cudaGetErrorString(e));
+  }
+  {
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {uint64_t(cols), uint64_t(rows)};
+    cuuint64_t strides[1] = {uint64_t(cols) * 2};
+    cuuint32_t box[2] = {64u, 128u};
+    cuuint32_t es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, X, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cudaFuncSetAttribute(probe_issue, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int nw : {1, 2, 4}) {
+      const int per = 12 / nw;
+      for (int w = 0; w < 3; ++w) probe_issue<<<1, 128, 1024 + 12 * 16384 + 64>>>(tm, nw, per, cyc);
+      cudaDeviceSynchronize();
+      std::vector<long long> h(8);
+      cudaMemcpy(h.data(), cyc, 8 * sizeof(long long), cudaMemcpyDeviceToHost);
+      printf("issue: %d warps x %d boxes: last issue at", nw, per);
+      for (int i = 0; i < nw; ++i) printf(" %lld", h[i]);
+      printf(" clk; all landed at");
+      for (int i = 0; i < nw; ++i) printf(" %lld", h[4 + i]);
+      printf("\n");
+    }
   }
   // ---- burst completion timelines (grid 1 and 148): nb 16 KB boxes (128 rows x 128 B)
   cudaFuncSetAttribute(probe_burst, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
