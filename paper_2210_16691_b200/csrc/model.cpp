@@ -78,13 +78,13 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   // profiles/sweep_r01.json (10 shapes x ~380 schedules).
   hw->numSM = 148;
   hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
-  hw->bwLLC = 20381;        // L2 -> SM bytes / clk, chip-wide
-  hw->bwDRAM = 2258;        // HBM read+write bytes / clk (~4.3 TB/s effective)
-  hw->bwDRAMWrite = 29778;  // epilogue TMA-store drain, bytes / clk chip-wide
+  hw->bwLLC = 11096;        // L2 -> SM bytes / clk, chip-wide
+  hw->bwDRAM = 2448;        // HBM read+write bytes / clk (~4.3 TB/s effective)
+  hw->bwDRAMWrite = 10956;  // epilogue TMA-store drain, bytes / clk chip-wide
   hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
   hw->latDRAMRead = 1950;
-  hw->latDRAMWrite = 298.9;  // per-tile epilogue floor
-  hw->bwSmem = 70.3;        // per-SM L2 -> shared-memory TMA fill, bytes / clk
+  hw->latDRAMWrite = 146.0;  // per-tile epilogue floor
+  hw->bwSmem = 79.35;        // per-SM L2 -> shared-memory TMA fill, bytes / clk
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
   hw->regsPerSM = 262144;
@@ -93,12 +93,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
   hw->clockGHz = 1.9;
-  hw->tIssue = 501.5;       // per-chunk producer/consumer floor (barrier hops + issue)
-  hw->tIssuePerBox = 5.27;
-  hw->tLaunch = 104.7;
-  hw->tTile = 198.0;
-  hw->overlapDRAM = 0.12;
-  hw->tPair = 6738;
+  hw->tIssue = 348.8;       // per-chunk producer/consumer floor (barrier hops + issue)
+  hw->tIssuePerBox = 10.17;
+  hw->tLaunch = 1108.9;
+  hw->tTile = 30.95;
+  hw->overlapDRAM = 0.22;
+  hw->tPair = 5169;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
