@@ -69,16 +69,36 @@ static int64_t gemm_smem_base(const alcop_gemm_desc& w, const alcop_schedule& s)
   return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + bars;
 }
 
+// Epilogue warps: 8 (two per TMEM lane quarter) when a tile's main loop is at
+// most two chunks and the tile has at least two output column chunks — the
+// drain then sets the per-tile time (attention QK^T, K = 64); else 4.
+int32_t gemm_epi_warps(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  const int64_t E = (w.K + s.tileK - 1) / s.tileK;
+  const int64_t chunk_cols = w.out_dtype == ALCOP_F32 ? 32 : 64;
+  const bool eligible = s.cta_group == 1 && !w.pre_op && s.n_stage_smem_A == s.n_stage_smem_B &&
+                        s.mode == ALCOP_MODE_FUSED;
+  // only where one staging buffer per warp fits: never needs more shared
+  // memory than 4 warps would (4 x 2 buffers), so validity does not change
+  return (eligible && E <= 2 && s.tileN / chunk_cols >= 2 && gemm_smem_base(w, s) + 8 * 32 * 128 <= kMaxSmemBytes)
+             ? 8
+             : 4;
+}
+
 // Epilogue TMA-store staging: two 4 KB buffers per epilogue warp (the store of
 // one chunk overlaps the TMEM read of the next) when they fit beside the ring,
 // else one — shared memory goes to pipeline stages first (one more stage of
 // lookahead is worth more than the store overlap).
-int32_t gemm_staging_bufs(const alcop_gemm_desc& w, const alcop_schedule& s) {
-  return gemm_smem_base(w, s) + 4 * 2 * 32 * 128 <= kMaxSmemBytes ? 2 : 1;
+int32_t gemm_staging_bufs_epi(const alcop_gemm_desc& w, const alcop_schedule& s, int32_t epi) {
+  return gemm_smem_base(w, s) + epi * 2 * 32 * 128 <= kMaxSmemBytes ? 2 : 1;
 }
-
+int64_t gemm_smem_bytes_epi(const alcop_gemm_desc& w, const alcop_schedule& s, int32_t epi) {
+  return gemm_smem_base(w, s) + epi * gemm_staging_bufs_epi(w, s, epi) * 32 * 128;
+}
+int32_t gemm_staging_bufs(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  return gemm_staging_bufs_epi(w, s, gemm_epi_warps(w, s));
+}
 int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s) {
-  return gemm_smem_base(w, s) + 4 * gemm_staging_bufs(w, s) * 32 * 128;
+  return gemm_smem_bytes_epi(w, s, gemm_epi_warps(w, s));
 }
 
 static int dtype_bytes(int32_t dt) { return dt == ALCOP_F32 ? 4 : 2; }

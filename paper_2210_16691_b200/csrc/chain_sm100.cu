@@ -444,8 +444,8 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
   }
   kp.max_key = tiles;
   alcop_gemm_desc wsm = w0;
-  const int smem = static_cast<int>(gemm_smem_bytes(wsm, s));
-  kp.stage_bufs = gemm_staging_bufs(wsm, s);
+  const int smem = static_cast<int>(gemm_smem_bytes_epi(wsm, s, 4));
+  kp.stage_bufs = gemm_staging_bufs_epi(wsm, s, 4);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(workspace, 0, sizeof(int32_t) * kp.max_mb * ch.n, st);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));

@@ -72,6 +72,7 @@ struct GemmKParams {
   // that the MMA never reads) instead of three 64B-swizzled 32-column atoms
   int32_t b_pad;
   int32_t stage_bufs;  // epilogue staging buffers per warp (1 or 2), gemm_staging_bufs
+  int32_t epi_warps;   // 4 or 8 (gemm_epi_warps)
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
 };
@@ -87,10 +88,11 @@ static bool g_pdl = [] {
 namespace {
 
 constexpr int kThreads = 192;      // producer, MMA, 4 epilogue warps
+constexpr int kThreadsEpi8 = 320;  // producer, MMA, 8 epilogue warps (short-K tiles, see kEpi)
 constexpr int kThreadsSplit = 224; // + warp 6: the B producer (conv, FUSED joint ring)
 constexpr int kThreadsPair = 224;  // the CTA pair: producer A, MMA, 4 epilogue warps, producer B
 constexpr int kThreadsPreOp = 192 + 128;  // 4 transform warps (6-9) for the fused pre-op, one producer
-constexpr int kStagingBytesPerBuf = 4 * 32 * 128;  // 4 epilogue warps x 32 rows x 128 B
+constexpr int kStagingBytesPerWarp = 32 * 128;  // one staging buffer: 32 rows x 128 B
 
 struct TileCoord {
   int b, mb, nb;
@@ -245,8 +247,15 @@ struct RingCursor {
 // row, so a tiled TMA box over an overlapping (pixel-stride) view of x loads
 // the whole 128 x 64 A chunk in one 128B-swizzled copy; output tiles are
 // 8 x 16 output-pixel blocks
-template <typename OutT, int BK, bool kJoint, bool kDebug, int kConv = 0, bool kPreOp = false>
-__global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug && kConv != 0 ? kThreadsSplit : kThreads), 1)
+// kEpi: epilogue warps.  8 for tiles whose main loop is one or two chunks
+// (attention QK^T: K = 64), where draining the accumulator, not loading or
+// multiplying, sets the per-tile time; two warps then share each TMEM lane
+// quarter, taking alternate column chunks.
+template <typename OutT, int BK, bool kJoint, bool kDebug, int kConv = 0, bool kPreOp = false, int kEpi = 4>
+__global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
+                                         : (kEpi == 8 ? kThreadsEpi8
+                                                      : (kJoint && !kDebug && kConv != 0 ? kThreadsSplit : kThreads)),
+                                  1)
     alcop_pipelined_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
   using namespace ptx;
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug &&
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), 128B-swizzled for the TMA store
   const uint32_t staging = ringB + p.sB * p.b_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * p.a_stage_bytes + p.sB * p.b_stage_bytes +
-                                               kStagingBytesPerBuf * p.stage_bufs);
+                                               kEpi * kStagingBytesPerWarp * p.stage_bufs);
   uint64_t* fullA = bars;
   uint64_t* emptyA = fullA + p.sA;
   uint64_t* fullB = kJoint ? fullA : emptyA + p.sA;
@@ -298,7 +307,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug &&
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(smem_u32(&tfull[i]), 1);
-        mbar_init(smem_u32(&tempty[i]), 4);
+        mbar_init(smem_u32(&tempty[i]), kEpi);
       }
       if (kPreOp)
         for (int i = 0; i < p.sA; ++i) mbar_init(smem_u32(&ready[i]), 4);
@@ -663,8 +672,8 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug &&
         cr.advance(p.sA);
       }
     }
-  } else if (warp < 6) {
-    // ======================= epilogue (warps 2-5) =======================
+  } else if (warp < 2 + kEpi) {
+    // ======================= epilogue (warps 2-5, or 2-9 with kEpi 8) =======================
     // TMEM -> registers (tcgen05.ld) -> 128B-swizzled smem staging -> TMA
     // bulk-tensor store; two staging buffers per warp so the store of one
     // chunk overlaps the TMEM read of the next.
@@ -680,7 +689,14 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug &&
       if (tl == 0 && warp == 2 && lane == 0) stamp<kDebug>(p, 5);
       const TileCoord tc = tile_coord(p, static_cast<int>(blockIdx.x) + tl * grid);
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < nchunks; ++c) {
+      constexpr int kStep = kEpi / 4;  // warps per TMEM lane quarter
+      const int c0 = (warp - 2) / 4;   // this warp's first column chunk
+      if (c0 >= nchunks) {             // no chunk for this warp in this tile: release at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+      }
+      for (int c = c0; c < nchunks; c += kStep) {
         uint32_t w[32];
         epistamp<kDebug>(p, warp, lane, c, 0);
         if constexpr (sizeof(OutT) == 4) {
@@ -697,8 +713,8 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp : (kJoint && !kDebug &&
             w[16 + i] = pack2<OutT>(r1[2 * i], r1[2 * i + 1]);
           }
         }
-        if (c == nchunks - 1) {
-          // all TMEM reads of this accumulator done: hand it back to the MMA warp
+        if (c + kStep >= nchunks) {
+          // all this warp's TMEM reads of this accumulator done: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
@@ -780,7 +796,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const uint32_t ringB = ringA + p.sA * p.a_stage_bytes;
   const uint32_t staging = ringB + p.sA * p.b_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sA * (p.a_stage_bytes + p.b_stage_bytes) +
-                                               kStagingBytesPerBuf * p.stage_bufs);
+                                               4 * kStagingBytesPerWarp * p.stage_bufs);
   uint64_t* full = bars;
   uint64_t* empty = full + p.sA;
   uint64_t* tfull = empty + p.sA;
@@ -1087,15 +1103,15 @@ int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint6
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK, bool kJoint, bool kDebug, bool kPreOp = false>
+template <typename OutT, int BK, bool kJoint, bool kDebug, bool kPreOp = false, int kEpi = 4>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                  int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug, false, kPreOp>;
+  auto kern = alcop_pipelined_gemm_kernel<OutT, BK, kJoint, kDebug, false, kPreOp, kEpi>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kPreOp ? kThreadsPreOp : kThreads);
+  cfg.blockDim = dim3(kPreOp ? kThreadsPreOp : (kEpi == 8 ? kThreadsEpi8 : kThreads));
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1166,7 +1182,8 @@ int launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   }
   if (joint) {
     return debug ? launch_typed<OutT, BK, true, true>(ta, tb, tc, kp, grid, smem, st)
-                 : launch_typed<OutT, BK, true, false>(ta, tb, tc, kp, grid, smem, st);
+                 : (kp.epi_warps == 8 ? launch_typed<OutT, BK, true, false, false, 8>(ta, tb, tc, kp, grid, smem, st)
+                                      : launch_typed<OutT, BK, true, false>(ta, tb, tc, kp, grid, smem, st));
   }
   return debug ? launch_typed<OutT, BK, false, true>(ta, tb, tc, kp, grid, smem, st)
                : launch_typed<OutT, BK, false, false>(ta, tb, tc, kp, grid, smem, st);
@@ -1332,8 +1349,9 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
-  const int smem = static_cast<int>(gemm_smem_bytes(w, s));
-  kp.stage_bufs = gemm_staging_bufs(w, s);
+  kp.epi_warps = cg == 1 ? gemm_epi_warps(w, s) : 4;
+  const int smem = static_cast<int>(gemm_smem_bytes_epi(w, s, kp.epi_warps));
+  kp.stage_bufs = gemm_staging_bufs_epi(w, s, kp.epi_warps);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cg == 2) {
     if (w.pre_op) return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the fused pre-op runs with cta_group 1");
@@ -1544,8 +1562,8 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
   if (grid > kp.num_tiles) grid = kp.num_tiles;
-  const int smem = static_cast<int>(gemm_smem_bytes(g, s));
-  kp.stage_bufs = gemm_staging_bufs(g, s);
+  const int smem = static_cast<int>(gemm_smem_bytes_epi(g, s, 4));
+  kp.stage_bufs = gemm_staging_bufs_epi(g, s, 4);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (d.out_dtype) {
     case ALCOP_F32: return launch_conv_typed<float>(ta, tb, tc, kp, grid, smem, st);

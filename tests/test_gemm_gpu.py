@@ -243,3 +243,14 @@ def test_gemm_host_pipelined_exact(alcop, M, N, K, batch, out):
                              ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(st.cuda_stream))
     assert rc == 0, lib.alcop_last_error()
     _assert_exact(C, exact, out_dt)
+
+
+@pytest.mark.parametrize("N,K,tileN,out", [(512, 64, 256, "bf16"), (512, 64, 128, "f32"), (384, 128, 192, "bf16"),
+                                           (320, 64, 64, "f32")])
+def test_short_k_eight_epilogue_warps_exact(alcop, N, K, tileN, out):
+    """Tiles whose main loop is <= 2 chunks drain with 8 epilogue warps (two per
+    TMEM lane quarter, alternate column chunks; gemm_epi_warps): batched, ragged N."""
+    out_dt = torch.float32 if out == "f32" else torch.bfloat16
+    s = alcop.make_schedule(tileN=tileN, tileK=64, n_stage=4)
+    C, exact = _run(alcop, 512, N, K, batch=5, out_dt=out_dt, sched=s, seed=17)
+    _assert_exact(C, exact, out_dt)
