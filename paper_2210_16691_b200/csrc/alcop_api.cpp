@@ -57,16 +57,28 @@ int64_t round_up_pow2_cols(int64_t cols) {
   return c;
 }
 
-static int64_t gemm_smem_base(const alcop_gemm_desc& w, const alcop_schedule& s) {
-  const int64_t cg = s.cta_group == 2 ? 2 : 1;
-  const int64_t a_stage = kTileM * s.tileK * 2;         // per CTA: 128 rows of A
-  // per CTA: tileN/cta_group columns of B (a CTA pair with B[K,N] and 96-column
-  // halves stages two 64-column 128B-swizzled atoms, see gemm_sm100.cu b_pad)
-  const int64_t half = s.tileN / cg;
-  const int64_t b_cols = (cg == 2 && w.b_layout == ALCOP_B_KN && half % 64 != 0) ? (half + 63) / 64 * 64 : half;
+static int64_t smem_base_cols(const alcop_schedule& s, int64_t b_cols) {
+  const int64_t a_stage = kTileM * s.tileK * 2;  // per CTA: 128 rows of A
   const int64_t b_stage = b_cols * s.tileK * 2;
   const int64_t bars = 8 * (3 * s.n_stage_smem_A + 2 * s.n_stage_smem_B + 4) + 16;  // + ready[] (pre-op)
   return 1024 /* alignment slack */ + s.n_stage_smem_A * a_stage + s.n_stage_smem_B * b_stage + bars;
+}
+
+// A CTA pair with B[K,N] and 96-column halves (tileN 192) stages each half as
+// two 128B-swizzled 64-column atoms (over-fetching 32 columns; gemm_sm100.cu
+// b_pad) when that still fits with one epilogue staging buffer per warp, else
+// as three 64B-swizzled 32-column atoms (the 7th stage of 256x192 fits only so).
+bool pair_b_pad(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  const int64_t cg = s.cta_group == 2 ? 2 : 1;
+  const int64_t half = s.tileN / cg;
+  if (!(cg == 2 && w.b_layout == ALCOP_B_KN && half % 64 != 0)) return false;
+  return smem_base_cols(s, (half + 63) / 64 * 64) + 4 * 32 * 128 <= kMaxSmemBytes;
+}
+
+static int64_t gemm_smem_base(const alcop_gemm_desc& w, const alcop_schedule& s) {
+  const int64_t cg = s.cta_group == 2 ? 2 : 1;
+  const int64_t half = s.tileN / cg;  // B columns per CTA
+  return smem_base_cols(s, pair_b_pad(w, s) ? (half + 63) / 64 * 64 : half);
 }
 
 // Epilogue warps: 8 (two per TMEM lane quarter) when a tile's main loop is at

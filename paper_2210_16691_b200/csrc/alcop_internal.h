@@ -23,6 +23,7 @@ int64_t round_up_pow2_cols(int64_t cols);
 int64_t gemm_smem_bytes(const alcop_gemm_desc& w, const alcop_schedule& s);
 int32_t gemm_staging_bufs(const alcop_gemm_desc& w, const alcop_schedule& s);
 int32_t gemm_epi_warps(const alcop_gemm_desc& w, const alcop_schedule& s);
+bool pair_b_pad(const alcop_gemm_desc& w, const alcop_schedule& s);
 // the same for a kernel with a fixed number of epilogue warps (conv, chain: 4)
 int32_t gemm_staging_bufs_epi(const alcop_gemm_desc& w, const alcop_schedule& s, int32_t epi);
 int64_t gemm_smem_bytes_epi(const alcop_gemm_desc& w, const alcop_schedule& s, int32_t epi);

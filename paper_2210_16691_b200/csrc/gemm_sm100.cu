@@ -1261,11 +1261,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
     const char* e = std::getenv("ALCOP_ATOM_VIEWS");
     return !(e && e[0] == '0');
   }();
-  static const bool pad_on = [] {
-    const char* e = std::getenv("ALCOP_PAIR_B_PAD");
-    return !(e && e[0] == '0');
-  }();
-  const bool b_pad = pad_on && cg == 2 && w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0;
+  const bool b_pad = pair_b_pad(w, s);
   const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0 && !b_pad) ? 32 : 64;  // pair BN 192: SW64 halves
   const bool a_view = views_on && BK > 64 && w.K % 64 == 0 && w.pre_op == 0;
   // B keeps one box per 64-column atom: a runtime view branch in the

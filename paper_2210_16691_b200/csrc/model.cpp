@@ -78,13 +78,13 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   // profiles/sweep_r01.json (10 shapes x ~380 schedules).
   hw->numSM = 148;
   hw->throughputSM = 8192;  // dense f16/bf16 FLOP / clk / SM
-  hw->bwLLC = 11096;        // L2 -> SM bytes / clk, chip-wide
-  hw->bwDRAM = 2448;        // HBM read+write bytes / clk (~4.3 TB/s effective)
-  hw->bwDRAMWrite = 10956;  // epilogue TMA-store drain, bytes / clk chip-wide
+  hw->bwLLC = 18944;        // L2 -> SM bytes / clk, chip-wide
+  hw->bwDRAM = 2461;        // HBM read+write bytes / clk (~4.3 TB/s effective)
+  hw->bwDRAMWrite = 4685;  // epilogue TMA-store drain, bytes / clk chip-wide
   hw->latLLCRead = 1950;    // TMA chunk latency under load, cycles
   hw->latDRAMRead = 1950;
-  hw->latDRAMWrite = 146.0;  // per-tile epilogue floor
-  hw->bwSmem = 79.35;        // per-SM L2 -> shared-memory TMA fill, bytes / clk
+  hw->latDRAMWrite = 123.7;  // per-tile epilogue floor
+  hw->bwSmem = 176.5;        // per-SM L2 -> shared-memory TMA fill, bytes / clk
   hw->latSmem = 30;
   hw->smemPerSM = 232448;
   hw->regsPerSM = 262144;
@@ -93,12 +93,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->utilKneeWarps = 1;
   hw->tmemColsPerSM = 512;
   hw->clockGHz = 1.9;
-  hw->tIssue = 348.8;       // per-chunk producer/consumer floor (barrier hops + issue)
-  hw->tIssuePerBox = 10.17;
-  hw->tLaunch = 1108.9;
-  hw->tTile = 30.95;
-  hw->overlapDRAM = 0.22;
-  hw->tPair = 5169;
+  hw->tIssue = 384.5;       // per-chunk producer/consumer floor (barrier hops + issue)
+  hw->tIssuePerBox = 9.71;
+  hw->tLaunch = 1139.9;
+  hw->tTile = 38.38;
+  hw->overlapDRAM = 0.20;
+  hw->tPair = 3716;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -128,7 +128,7 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // 96-column halves stages two 64-column atoms (gemm_sm100.cu b_pad)
   const int64_t bN = tN / cg;
   const bool kn = w->b_layout == ALCOP_B_KN;
-  const bool pad = cg == 2 && kn && (bN % 64) != 0;
+  const bool pad = pair_b_pad(*w, *s);
   const int64_t bcols = pad ? (bN + 63) / 64 * 64 : bN;
   out->bytesOneSmemLoop = (tM / cg + bcols) * tK * eb;
   out->bytesWorkset = (w->M * w->K + w->K * w->N) * eb * w->batch;
@@ -143,7 +143,8 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   // TMA instructions per chunk: A's K atoms come in one 4-D box when the atom
   // tiles the row (gemm_sm100.cu a_view); B issues one box per 64-column atom
   const int64_t aBoxes = (tK > 64 && w->K % 64 == 0 && w->pre_op == 0) ? 1 : std::max<int64_t>(1, tK / 64);
-  const int64_t bBoxes = kn ? (pad ? 2 : std::max<int64_t>(1, bN / 64)) : std::max<int64_t>(1, tK / 64);
+  const int64_t bBoxes = kn ? (pad ? 2 : ((bN % 64) ? bN / 32 : std::max<int64_t>(1, bN / 64)))
+                            : std::max<int64_t>(1, tK / 64);
   const int64_t boxes = aBoxes + bBoxes;
   const double tIssue = hw->tIssue + hw->tIssuePerBox * static_cast<double>(boxes);
   out->tRegLoad = 0;  // tcgen05 reads smem operands through descriptors

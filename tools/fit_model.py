@@ -32,10 +32,12 @@ def features(rows):
         tiles = math.ceil(M / (128 * cg)) * math.ceil(N / BN) * b
         units = min(tiles, NSM // cg)   # CTAs (pairs) working at once
         bN = BN // cg                     # B columns per CTA
-        pad = cg == 2 and bN % 64 != 0    # pair halves of 96 columns: two 64-column atoms
+        # pair halves of 96 columns: two 64-column atoms when that fits (alcop_api.cpp pair_b_pad)
+        pad = cg == 2 and bN % 64 != 0 and (1024 + s * (128 * BK * 2 + 128 * BK * 2)
+                                            + 8 * (5 * s + 4) + 16 + 4 * 32 * 128) <= 232448
         bcols = 128 if pad else bN
         a_boxes = 1 if (BK > 64 and K % 64 == 0) else max(1, BK // 64)   # atom-stacked view
-        b_boxes = 2 if pad else max(1, bN // 64)
+        b_boxes = 2 if pad else (bN // 32 if bN % 64 else max(1, bN // 64))
         for k, v in (("ctas", units * cg), ("waves", math.ceil(tiles / units)), ("E", math.ceil(K / BK)),
                      ("bytes_kb", (128 + bcols) * BK * 2), ("mma", 2 * 128 * BN * BK), ("boxes", a_boxes + b_boxes),
                      ("s", s), ("inner", inner), ("mode", mode), ("cg", cg), ("BN", BN),
