@@ -95,6 +95,20 @@ extern "C" int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t 
   int out = 0;
   int rc = ALCOP_OK;
   const int reps = std::max(1, (48 + nsets - 1) / nsets);  // >= 48 launches per timed replay set
+  std::vector<cudaGraphExec_t> execs;
+  std::vector<cudaGraph_t> graphs;
+  std::vector<double> first;  // first-pass median per candidate
+  auto time_replays = [&](cudaGraphExec_t ge, float* out_ms) -> int {
+    cudaEventRecord(e0, ts);
+    for (int k = 0; k < reps; ++k) cudaGraphLaunch(ge, ts);
+    cudaEventRecord(e1, ts);
+    if (cudaEventSynchronize(e1) != cudaSuccess)
+      return set_error(ALCOP_ERR_CUDA, "CudaError", "kernel failed during tuning");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *out_ms = ms / static_cast<float>(reps * nsets);
+    return ALCOP_OK;
+  };
   for (int i = 0; i < n && rc == ALCOP_OK; ++i) {
     const alcop_schedule& s = space[i].second;
     rc = launch_gemm(*w, s, As[0], Bs[0], Cs[0], nullptr, 0, static_cast<void*>(ts));  // validates the launch outside capture
@@ -112,32 +126,47 @@ extern "C" int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t 
       rc = rc != ALCOP_OK ? rc : set_error(ALCOP_ERR_CUDA, "CudaError", "graph capture of the candidate failed");
       break;
     }
+    graphs.push_back(g);
+    execs.push_back(ge);
     cudaGraphLaunch(ge, ts);  // warm-up
     float per[3];
-    for (int r = 0; r < 3; ++r) {
-      cudaEventRecord(e0, ts);
-      for (int k = 0; k < reps; ++k) cudaGraphLaunch(ge, ts);
-      cudaEventRecord(e1, ts);
-      if (cudaEventSynchronize(e1) != cudaSuccess) {
-        rc = set_error(ALCOP_ERR_CUDA, "CudaError", "kernel failed during tuning");
-        break;
-      }
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      per[r] = ms / static_cast<float>(reps * nsets);
-    }
-    cudaGraphExecDestroy(ge);
-    cudaGraphDestroy(g);
+    for (int r = 0; r < 3 && rc == ALCOP_OK; ++r) rc = time_replays(ge, &per[r]);
     if (rc != ALCOP_OK) break;
     std::sort(per, per + 3);
     const double t = per[1] * 1e-3;
+    first.push_back(t);
     if (trials && out < trials_cap) trials[out] = alcop_tune_trial{s, space[i].first, t};
     ++out;
-    if (t < bestT) {
-      bestT = t;
-      *best = s;
+  }
+  // Final: the three fastest of the first pass re-timed round-robin (5 rounds,
+  // median): the GPU's power state drifts over a tuning run, and single
+  // passes ranked near-equal schedules by it (bench: qkv pair vs single).
+  if (rc == ALCOP_OK && !first.empty()) {
+    std::vector<int> order(first.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return first[a] < first[b]; });
+    const int fin = std::min<int>(3, static_cast<int>(order.size()));
+    std::vector<std::vector<float>> samples(fin);
+    for (int r = 0; r < 5 && rc == ALCOP_OK; ++r)
+      for (int f = 0; f < fin && rc == ALCOP_OK; ++f) {
+        float ms = 0;
+        rc = time_replays(execs[order[f]], &ms);
+        samples[f].push_back(ms);
+      }
+    if (rc == ALCOP_OK) {
+      for (int f = 0; f < fin; ++f) {
+        std::sort(samples[f].begin(), samples[f].end());
+        const double t = samples[f][samples[f].size() / 2] * 1e-3;
+        if (t < bestT) {
+          bestT = t;
+          *best = space[order[f]].second;
+        }
+        if (trials && order[f] < trials_cap) trials[order[f]].measured_s = t;
+      }
     }
   }
+  for (auto ge : execs) cudaGraphExecDestroy(ge);
+  for (auto g : graphs) cudaGraphDestroy(g);
   // the caller's C gets the best schedule's result (the tuning runs wrote the scratch copies)
   if (rc == ALCOP_OK) {
     cudaStreamSynchronize(ts);
