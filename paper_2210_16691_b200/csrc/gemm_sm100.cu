@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
 // and hands the accumulator back on the leader's tmem_empty (8 arrivals).
 // Joint A+B ring only (n_stage_A == n_stage_B).
 // ---------------------------------------------------------------------------
-template <typename OutT, int BK>
+template <typename OutT, int BK, bool kDebug>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                      const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
@@ -809,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
   const bool b_sw64 = (half_n & 63) != 0 && !p.b_pad;  // BN = 192: N-major halves of 96 columns
-  if (threadIdx.x == 0) stamp<true>(p, 0);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 0);
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tmA);
@@ -838,7 +838,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const uint32_t tmem_base = *tmem_slot;
   grid_dependency_wait();
   grid_launch_dependents();
-  if (threadIdx.x == 0) stamp<true>(p, 1);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 1);
 
   const int cluster_id = static_cast<int>(blockIdx.x) >> 1;
   const int nclusters = static_cast<int>(gridDim.x) >> 1;
@@ -868,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire (own slot, released by the pair's MMA)
         ra.phase ^= 1u << slot;
-        if (lane == 0 && warp == 0) chunkstamp<true>(p, 0, ra.count++);
+        if (lane == 0 && warp == 0) chunkstamp<kDebug>(p, 0, ra.count++);
         if (tl != tc_tile) {
           tc_tile = tl;
           tc = tile_coord(p, cluster_id + tl * nclusters);
@@ -959,9 +959,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
           mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
           ca.phase ^= 1u << slot;
-          if (lane == 0) chunkstamp<true>(p, 1, ca.count++);
+          if (lane == 0) chunkstamp<kDebug>(p, 1, ca.count++);
           tc_fence_after();
-          if (tl == 0 && v == 0 && lane == 0) stamp<true>(p, 3);
+          if (tl == 0 && v == 0 && lane == 0) stamp<kDebug>(p, 3);
           const uint64_t ad = adesc0 + slot * a_stage16;
           const uint64_t bd = bdesc0 + slot * b_stage16;
           ISSUE(
@@ -974,7 +974,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           ca.advance(p.sA);
         }
         ISSUE(umma_commit_pair_multicast(smem_u32(&tfull[acc]), 0x3));
-        if (tl == my_tiles - 1 && lane == 0) stamp<true>(p, 4);
+        if (tl == my_tiles - 1 && lane == 0) stamp<kDebug>(p, 4);
         if (wrap) {
           // drain the s-1 wrapped tail groups (no MMA): release both CTAs' slots
           for (int d = 0; d < p.sA - 1; ++d) {
@@ -999,7 +999,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
       tc_fence_after();
-      if (tl == 0 && warp == 2 && lane == 0) stamp<true>(p, 5);
+      if (tl == 0 && warp == 2 && lane == 0) stamp<kDebug>(p, 5);
       const TileCoord tc = tile_coord(p, cluster_id + tl * nclusters);
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c) {
@@ -1047,7 +1047,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     }
     if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
     __syncwarp();
-    if (warp == 2 && lane == 0) stamp<true>(p, 6);
+    if (warp == 2 && lane == 0) stamp<kDebug>(p, 6);
   }
 
   tc_fence_before();
@@ -1056,7 +1056,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, p.tmem_cols);
   }
-  if (threadIdx.x == 0) stamp<true>(p, 7);
+  if (threadIdx.x == 0) stamp<kDebug>(p, 7);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
@@ -1125,10 +1125,10 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK>
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
-                int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK>;
+template <typename OutT, int BK, bool kDebug = false>
+int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
+                  int smem, cudaStream_t st) {
+  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -1145,6 +1145,14 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
+}
+
+// timeline stamps (alcop_debug_set_stamps) select the instrumented variant
+template <typename OutT, int BK>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
+                int smem, cudaStream_t st) {
+  return kp.stamps ? launch_pair_t<OutT, BK, true>(ta, tb, tc, kp, grid, smem, st)
+                   : launch_pair_t<OutT, BK, false>(ta, tb, tc, kp, grid, smem, st);
 }
 
 template <typename OutT, bool kDebug, int kConv>
