@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
         mbar_wait(smem_u32(&full[slot]), par);
         r.phase ^= 1u << slot;
         ++r.count;
-        ISSUE(log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released));
+        if constexpr (kDebug) ISSUE(log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released));
         return par;
       };
       for (int tl = 0; tl < my_tiles; ++tl) {
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
             if (lane == 0) chunkstamp<kDebug>(p, 1, ca.count - 1);
             pb = pa;
             ++cb.count;
-            ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
+            if constexpr (kDebug) ISSUE(log_event<kDebug>(p, 1, nev, 1, 1, tl, sb, v, pb, -1, -1, cb.count, cb.released));
           } else {
             pa = cwait(ca, fullA, 0, tl, v);  // consumer_wait A
             pb = cwait(cb, fullB, 1, tl, v);  // consumer_wait B
