@@ -556,6 +556,43 @@ def main_gpu(args, rank, world, local_rank):
                 "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
         extra["n_stage_sweep"] = sweep
     if not args.quick:
+        # ---- batched GEMMs of attention (BASELINE configs[2]): batch*heads = 192,
+        # seq 512, head_dim 64; QK^T [512x64]@[64x512], PV [512x512]@[512x64];
+        # HBM-bound (AI ~51 FLOP/B), batch-sharded across ranks
+        bmm = {}
+        from paper_2210_16691_b200.sharded import shard_range
+        nb = shard_range(192, rank, world).size
+        for name, (M, N, K) in (("qk_t", (512, 512, 64)), ("pv", (512, 64, 512))):
+            db = alcop.gemm_desc(M, N, K, nb, alcop.BF16, alcop.BF16, alcop.B_KN)
+            descs[("bmm", name)] = db
+            sb = alcop.choose_schedule(db)
+            rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((nb, M, K), device=dev) - 0.5).to(torch.bfloat16),
+                                                     (torch.rand((nb, K, N), device=dev) - 0.5).to(torch.bfloat16),
+                                                     torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
+                           (M * K + K * N + M * N) * 2 * nb, max_sets=16)
+            nr = len(rot.sets)
+
+            def runb(i, s_, rot=rot, nr=nr, db=db):
+                A, B, C = rot.sets[i % nr]
+                rc = lib.alcop_gemm(ctypes.byref(db), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
+                                    ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+                if rc:
+                    raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+            ms = time_graph(lambda i: runb(i, sb), iters=12 * nr, warmup=3, reps_per_graph=nr)
+            s1 = alcop.make_schedule(tileN=sb.tileN, tileK=sb.tileK, n_stage=1, n_stage_inner=1)
+            ms1 = time_graph(lambda i: runb(i, s1), iters=6 * nr, warmup=3, reps_per_graph=nr)
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            byts = (M * K + K * N + M * N) * 2 * 192
+            tsec = float(tt.item()) * 1e-3
+            bmm[name] = {"shape": [M, N, K], "batch": 192, "tflops_aggregate": round(2.0 * M * N * K * 192 / tsec / 1e12, 1),
+                         "gbs_aggregate": round(byts / tsec / 1e9, 1),
+                         "hbm_frac_per_gpu": round(byts / tsec / 1e9 / world / peaks["hbm_gbs"], 3),
+                         "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
+            del rot
+        extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
         # ---- large square GEMMs (BASELINE configs[4]): n^3 bf16, n = 4096..16384,
         # M-sharded across ranks (rows of A and C split in 256-row granules, B
         # replicated, no collective on the compute path); aggregate =
@@ -596,42 +633,6 @@ def main_gpu(args, rank, world, local_rank):
             del A, B, C
             torch.cuda.empty_cache()
         extra["large_square_m_sharded"] = {"sharding": "M (256-row granules), B replicated", "sizes": squares}
-        # ---- batched GEMMs of attention (BASELINE configs[2]): batch*heads = 192,
-        # seq 512, head_dim 64; QK^T [512x64]@[64x512], PV [512x512]@[512x64];
-        # HBM-bound (AI ~51 FLOP/B), batch-sharded across ranks
-        bmm = {}
-        nb = shard_range(192, rank, world).size
-        for name, (M, N, K) in (("qk_t", (512, 512, 64)), ("pv", (512, 64, 512))):
-            db = alcop.gemm_desc(M, N, K, nb, alcop.BF16, alcop.BF16, alcop.B_KN)
-            descs[("bmm", name)] = db
-            sb = alcop.choose_schedule(db)
-            rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((nb, M, K), device=dev) - 0.5).to(torch.bfloat16),
-                                                     (torch.rand((nb, K, N), device=dev) - 0.5).to(torch.bfloat16),
-                                                     torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
-                           (M * K + K * N + M * N) * 2 * nb, max_sets=16)
-            nr = len(rot.sets)
-
-            def runb(i, s_, rot=rot, nr=nr, db=db):
-                A, B, C = rot.sets[i % nr]
-                rc = lib.alcop_gemm(ctypes.byref(db), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
-                                    ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
-                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-                if rc:
-                    raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
-            ms = time_graph(lambda i: runb(i, sb), iters=2 * nr, warmup=3, reps_per_graph=nr)
-            s1 = alcop.make_schedule(tileN=sb.tileN, tileK=sb.tileK, n_stage=1, n_stage_inner=1)
-            ms1 = time_graph(lambda i: runb(i, s1), iters=2 * nr, warmup=3, reps_per_graph=nr)
-            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            byts = (M * K + K * N + M * N) * 2 * 192
-            tsec = float(tt.item()) * 1e-3
-            bmm[name] = {"shape": [M, N, K], "batch": 192, "tflops_aggregate": round(2.0 * M * N * K * 192 / tsec / 1e12, 1),
-                         "gbs_aggregate": round(byts / tsec / 1e9, 1),
-                         "hbm_frac_per_gpu": round(byts / tsec / 1e9 / world / peaks["hbm_gbs"], 3),
-                         "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
-            del rot
-        extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
 
     # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
     if not args.quick:
