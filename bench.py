@@ -593,46 +593,6 @@ def main_gpu(args, rank, world, local_rank):
                          "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
             del rot
         extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
-        # ---- large square GEMMs (BASELINE configs[4]): n^3 bf16, n = 4096..16384,
-        # M-sharded across ranks (rows of A and C split in 256-row granules, B
-        # replicated, no collective on the compute path; SURVEY §8e); aggregate =
-        # total FLOPs / max-over-ranks time.  At N > 1 the optional NCCL
-        # all-gather of C is timed separately.
-        from paper_2210_16691_b200.sharded import shard_range, gather_rows
-        squares = {}
-        for n in (4096, 8192, 12288, 16384):
-            sh = shard_range(n, rank, world, granule=256)
-            m = sh.size
-            dsq = alcop.gemm_desc(m, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
-            descs[(m, n, n)] = dsq
-            ssq = sched.get((m, n, n)) or alcop.choose_schedule(dsq)
-            sched[(m, n, n)] = ssq
-            A = (torch.rand((m, n), device=dev) - 0.5).to(torch.bfloat16)
-            B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
-            C = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
-            barrier()
-            ms = time_graph(lambda i: launch(A, B, C, ssq, (m, n, n)), iters=8 if n < 12288 else 4, warmup=3)
-            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tf = 2.0 * n ** 3 / (float(tt.item()) * 1e-3) / 1e12
-            row = {"tflops_aggregate": round(tf, 1), "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
-                   "rows_per_gpu": m, "schedule": ssq.as_dict()}
-            if world > 1 and n == 16384:
-                for _ in range(2):
-                    gather_rows(C, n, rank, world, granule=256)
-                torch.cuda.synchronize()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                gather_rows(C, n, rank, world, granule=256)
-                e1.record()
-                torch.cuda.synchronize()
-                row["allgather_ms"] = round(e0.elapsed_time(e1), 3)
-            squares[str(n)] = row
-            del A, B, C
-            torch.cuda.empty_cache()
-        extra["large_square_m_sharded"] = {"sharding": "M (256-row granules), B replicated", "sizes": squares}
 
     # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
     if not args.quick:
@@ -677,6 +637,46 @@ def main_gpu(args, rank, world, local_rank):
                     "zero-padded, FLOPs counted at C=3); "
                     "per-layer CUDA-graph timing, model schedules"}
         torch.cuda.empty_cache()
+        # ---- large square GEMMs (BASELINE configs[4]): n^3 bf16, n = 4096..16384,
+        # M-sharded across ranks (rows of A and C split in 256-row granules, B
+        # replicated, no collective on the compute path; SURVEY §8e); aggregate =
+        # total FLOPs / max-over-ranks time.  At N > 1 the optional NCCL
+        # all-gather of C is timed separately.
+        from paper_2210_16691_b200.sharded import shard_range, gather_rows
+        squares = {}
+        for n in (4096, 8192, 12288, 16384):
+            sh = shard_range(n, rank, world, granule=256)
+            m = sh.size
+            dsq = alcop.gemm_desc(m, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+            descs[(m, n, n)] = dsq
+            ssq = sched.get((m, n, n)) or alcop.choose_schedule(dsq)
+            sched[(m, n, n)] = ssq
+            A = (torch.rand((m, n), device=dev) - 0.5).to(torch.bfloat16)
+            B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
+            C = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
+            barrier()
+            ms = time_graph(lambda i: launch(A, B, C, ssq, (m, n, n)), iters=8 if n < 12288 else 4, warmup=3)
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tf = 2.0 * n ** 3 / (float(tt.item()) * 1e-3) / 1e12
+            row = {"tflops_aggregate": round(tf, 1), "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
+                   "rows_per_gpu": m, "schedule": ssq.as_dict()}
+            if world > 1 and n == 16384:
+                for _ in range(2):
+                    gather_rows(C, n, rank, world, granule=256)
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                gather_rows(C, n, rank, world, granule=256)
+                e1.record()
+                torch.cuda.synchronize()
+                row["allgather_ms"] = round(e0.elapsed_time(e1), 3)
+            squares[str(n)] = row
+            del A, B, C
+            torch.cuda.empty_cache()
+        extra["large_square_m_sharded"] = {"sharding": "M (256-row granules), B replicated", "sizes": squares}
 
     # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)
     host = []
