@@ -13,11 +13,15 @@ at M = 4096 tokens, bf16 in / bf16 out, fp32 accumulate:
 launches; that variant's step time is reported beside the headline too.)
 B is the reference layout [K, N] row-major (schedule.hpp:389).  One "step" is
 one pass over those GEMMs, each launched through the C ABI (alcop_gemm)
-with the schedule the analytical model picks (alcop_choose_schedule).  Inputs
+with the schedule alcop_tune picks (the analytical model's top schedules
+timed on this GPU; --schedule model: the model's first pick).  Inputs
 rotate over copies whose footprint exceeds 2x the 126 MB L2, so every step
 reads HBM.  Reported beside it, in the same run: the n_stage 1..6 sweep of
 each distinct shape (speedup vs the non-pipelined n_stage=1 variant), the
-model pick vs the best swept schedule, a large square GEMM, the roofline of
+model pick vs the best swept schedule, BASELINE config 1 (fp16 512^3 with the
+reference's own schedule script, and the reference interpreter on the whole
+problem on the host cores), the attention BMMs, the ResNet-50 convs, the
+large square GEMMs, the roofline of
 the dominant kernel, the end-to-end number through the host-buffer ABI entry
 point, and the reference CPU path timed on the host cores.
 
@@ -497,6 +501,83 @@ def main_gpu(args, rank, world, local_rank):
                 "algorithmic_flops_per_launch": dflops,
                 "timing": "CUDA events around CUDA graphs of this GEMM alone, rotating cold inputs > 2x L2"}
 
+    def attainable(fl, byts):
+        """min(P, AI * BW) in TFLOP/s, AI = FLOPs / compulsory bytes."""
+        return min(peaks["bf16_tflops"], fl / byts * peaks["hbm_gbs"] * 1e-3)
+
+    def config1_block():
+        """BASELINE configs[0]: fp16 512^3 with the reference's
+        own schedule script (tile 128x128x32, 2 shared + 2 register stages)
+        mapped through alcop_parse_schedule_script, in WRAP (the pass's exact
+        index algebra) and FUSED mode, plus the model pick; L2 flushed between
+        launches (rotating inputs > 2x L2).  Beside it, on this host: the
+        reference interpreter on the WHOLE C1 problem (its 16 output tiles as
+        concurrent processes; makespan) and the C oracle (OpenMP)."""
+        M = N = K = 512
+        d1 = alcop.gemm_desc(M, N, K, 1, alcop.F16, alcop.F16, alcop.B_KN)
+        script = _ref_sample_script(128, 128, K).replace("i0=1", "i0=%d" % (M // 128)).replace(
+            "j0=1", "j0=%d" % (N // 128))
+        s_ref, _ = alcop.apply_script(d1, script)
+        s_fused = alcop.Schedule.from_buffer_copy(s_ref)
+        s_fused.mode = alcop.MODE_FUSED
+        s_model = alcop.choose_schedule(d1)
+        rot = Rotating(lambda i: ((torch.rand((M, K), device=dev) - 0.5).to(torch.float16),
+                                  (torch.rand((K, N), device=dev) - 0.5).to(torch.float16),
+                                  torch.empty((M, N), device=dev, dtype=torch.float16)),
+                       (M * K + K * N + M * N) * 2, max_sets=192)
+        nr = len(rot.sets)
+
+        def run1(i, s_):
+            A, B, C = rot.sets[i % nr]
+            rc = lib.alcop_gemm(ctypes.byref(d1), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
+                                ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            if rc:
+                raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+        out = {"shape": [M, N, K], "dtype": "f16", "script": script.strip().split("\n"),
+               "l2": "flushed (%d rotating input sets)" % nr}
+        fl = 2.0 * M * N * K
+        for label, s_ in (("reference_schedule_wrap", s_ref), ("reference_schedule_fused", s_fused),
+                          ("model_pick", s_model)):
+            ms = time_graph(lambda i, s_=s_: run1(i, s_), iters=2 * nr, warmup=3, reps_per_graph=nr)
+            out[label] = {"us": round(ms * 1e3, 2), "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+                          "schedule": s_.as_dict()}
+        del rot
+        if args.no_cpu:
+            return out
+        import tempfile
+        drv = _ref_driver()
+        if drv is not None:
+            sp = os.path.join(tempfile.mkdtemp(), "c1_tile.txt")
+            with open(sp, "w") as f:
+                f.write(_ref_sample_script(128, 128, K))
+            t0 = time.perf_counter()
+            ps = [subprocess.Popen([drv, "time", "--M", "128", "--N", "128", "--K", str(K), "--script", sp,
+                                    "--mode", "stale", "--seed", str(t)], stdout=subprocess.PIPE,
+                                   stderr=subprocess.PIPE, text=True) for t in range((M // 128) * (N // 128))]
+            outs = [p.communicate() for p in ps]
+            dt = time.perf_counter() - t0
+            if all(p.returncode == 0 for p in ps):
+                run_s = [json.loads(o.strip().splitlines()[-1])["best_s"] for o, _ in outs]
+                out["cpu_reference"] = {
+                    "makespan_s": round(dt, 3), "sum_of_run_s": round(sum(run_s), 2),
+                    "processes": len(ps), "host_cores": os.cpu_count(),
+                    "what": "pipec::run on transform(lower(apply_script(...))) of each 128x128 output tile "
+                            "(full K, the config-1 script), 16 concurrent processes = the whole C1 problem"}
+                best_us = min(out[k]["us"] for k in ("reference_schedule_wrap", "reference_schedule_fused",
+                                                     "model_pick"))
+                out["gpu_speedup_vs_cpu_reference"] = round(dt / (best_us * 1e-6), 0)
+        import numpy as np
+        from oracle import coracle
+        A = coracle.to_dtype(np.ones((M, K), np.float32), "f16")
+        B = coracle.to_dtype(np.ones((K, N), np.float32), "f16")
+        coracle.gemm(A, B, "f16", "f16")
+        t0 = time.perf_counter()
+        for _ in range(3):
+            coracle.gemm(A, B, "f16", "f16")
+        out["cpu_oracle_openmp_s"] = round((time.perf_counter() - t0) / 3, 4)
+        return out
+
     extra = {}
     if rank == 0 and not args.quick:
         # ---- n_stage sweep 1..5 per distinct shape (same tile, same run) + model pick vs best
@@ -593,6 +674,8 @@ def main_gpu(args, rank, world, local_rank):
                          "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
             del rot
         extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
+        if rank == 0:
+            extra["config1_512"] = config1_block()
 
     # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
     if not args.quick:
@@ -623,7 +706,9 @@ def main_gpu(args, rank, world, local_rank):
             fl = 2.0 * nloc * P * Q * K * R * R * C
             tot_flops += fl * rep
             tot_ms += ms * rep
+            cbytes = 2 * (nloc * H * H * C + K * R * R * C + nloc * P * Q * K)
             conv_rows.append({"layer": name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+                              "frac_of_attainable": round(fl / (ms * 1e-3) / 1e12 / attainable(fl, cbytes), 3),
                               "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN,
                               "n_stage": cs.n_stage_smem_A})
             del X, Wf, Y
@@ -752,6 +837,10 @@ def main_gpu(args, rank, world, local_rank):
                                        "multiplied as they land, C blocks D2H on a second copy stream), host "
                                        "sync at the end of every step"},
                 "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4), "shape": v["shape"],
+                                 "frac_of_attainable": round(v["tflops"] / attainable(
+                                     2.0 * v["shape"][0] * v["shape"][1] * v["shape"][2],
+                                     2 * (v["shape"][0] * v["shape"][2] + v["shape"][2] * v["shape"][1]
+                                          + v["shape"][0] * v["shape"][1])), 3),
                                  "launches_per_step": count[k]} for k, v in per.items()},
                 ("step_fused_qkv" if args.unfused_qkv else "step_unfused_qkv"): alt,
                 "step_one_launch": {"entry_point": "alcop_gemm_chain", **chain} if chain else None,
