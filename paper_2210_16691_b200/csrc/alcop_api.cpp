@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -22,6 +23,21 @@ struct HostPipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kBlocks] = {}, ev_out[kBlocks] = {};
 };
+
+// Smallest A row block the host-buffer pipeline streams (bytes; 0: always 8
+// blocks).  A lone synchronous call needs the row-block pipeline to overlap
+// its own H2D, MMA and D2H; back-to-back async calls already overlap call
+// k+1's H2D with call k's D2H, and there every extra copy costs PCIe rate to
+// per-copy setup (BERT-layer e2e step: 8 blocks 1.96 ms, >= 8 MB blocks
+// 1.60 ms; tools/e2e_probe.py).  ALCOP_HOST_BLOCK_BYTES overrides both.
+int64_t host_block_bytes(bool sync) {
+  static const int64_t env = [] {
+    const char* e = std::getenv("ALCOP_HOST_BLOCK_BYTES");
+    return e ? std::atoll(e) : int64_t(-1);
+  }();
+  if (env >= 0) return env;
+  return sync ? 0 : int64_t(8) << 20;
+}
 
 // Copy streams + events of the pipelined host-buffer GEMM, one set per host
 // thread and device (the entry point is synchronous, so a thread never has
@@ -274,6 +290,10 @@ static int gemm_host_impl(const alcop_gemm_desc* w, const alcop_schedule* s, con
   // whole by every block and goes first.  Batched / small problems: one block.
   const int64_t tm = s->tileM;
   int nblk = (w->batch == 1 && w->M >= 4 * tm) ? 8 : 1;
+  if (nblk > 1) {
+    const int64_t target = host_block_bytes(sync);
+    if (target > 0) nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, bytesA / target)));
+  }
   int64_t rows = (w->M + nblk - 1) / nblk;
   rows = (rows + tm - 1) / tm * tm;
   nblk = static_cast<int>((w->M + rows - 1) / rows);

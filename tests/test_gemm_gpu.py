@@ -245,6 +245,34 @@ def test_gemm_host_pipelined_exact(alcop, M, N, K, batch, out):
     _assert_exact(C, exact, out_dt)
 
 
+def test_gemm_host_async_back_to_back_exact(alcop):
+    """alcop_gemm_host_async called back to back with one workspace each (the
+    bench's e2e step): call k+1's H2D overlaps call k's D2H; A blocks of >= 8 MB
+    (a 20 MB A streams in 2 row blocks, the small ones in 1); every C exact."""
+    import ctypes
+    lib = alcop.load_library()
+    st = torch.cuda.current_stream()
+    calls = []
+    for i, (M, N, K) in enumerate([(2048, 768, 768), (10240, 256, 1024), (512, 384, 128), (4096, 1536, 768)]):
+        a, b = gemm_inputs(M, N, K, 1, seed=40 + i)
+        A = torch.from_numpy(a).to(torch.bfloat16).pin_memory()
+        B = torch.from_numpy(b).to(torch.bfloat16).pin_memory()
+        C = torch.zeros((M, N), dtype=torch.float32).pin_memory()
+        d = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.F32, alcop.B_KN)
+        ws = torch.empty(lib.alcop_gemm_workspace_bytes(ctypes.byref(d)), dtype=torch.uint8, device="cuda")
+        calls.append((d, alcop.choose_schedule(d), A, B, C, ws, _exact(a, b, False)))
+    for rep in range(2):
+        for d, s, A, B, C, ws, _ in calls:
+            rc = lib.alcop_gemm_host_async(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
+                                           ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                           ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(st.cuda_stream))
+            assert rc == 0, lib.alcop_last_error()
+        torch.cuda.synchronize()
+        for d, s, A, B, C, ws, exact in calls:
+            _assert_exact(C, exact, torch.float32)
+            C.zero_()
+
+
 @pytest.mark.parametrize("N,K,tileN,out", [(512, 64, 256, "bf16"), (512, 64, 128, "f32"), (384, 128, 192, "bf16"),
                                            (320, 64, 64, "f32")])
 def test_short_k_eight_epilogue_warps_exact(alcop, N, K, tileN, out):
