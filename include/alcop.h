@@ -93,7 +93,11 @@ typedef struct {
   int32_t mode;                /* alcop_mode                             */
   int32_t num_ctas;            /* persistent grid; 0 = #SMs              */
   int32_t raster;              /* tile rows per raster group; 0 = auto  */
-  int32_t reserved1;
+  int32_t stream_k;            /* CTA pair, FUSED: 1 = split the output tiles' chunk stream
+                                  evenly over the clusters (a tile cut between two clusters
+                                  is finished from an fp32 partial); the partials live in one
+                                  per-device workspace, so stream_k launches must not run
+                                  concurrently on two streams.  0 = whole tiles per cluster */
 } alcop_schedule;
 
 /* ---- several GEMMs in one persistent launch (new; no reference form) ------
@@ -270,8 +274,9 @@ typedef struct {
  * AnalyticalOnly method of tuner.hpp:407-413 with measure_ground_truth,
  * pipe_sim.hpp:195-239, replaced by the GPU): enumerate the B200 space,
  * rank by alcop_predict, time the top `budget` schedules on the caller's
- * buffers (CUDA events on `stream`, each launch from a cold L2: a 256 MB
- * scratch write precedes it), return the fastest in *best.
+ * buffers (steady-state CUDA-graph timing over rotating copies > 2x L2),
+ * plus a stream_k twin of each CTA-pair candidate whose tiles do not fill
+ * whole waves (up to 2 x budget trials), return the fastest in *best.
  * `trials` (may be NULL) receives up to `trials_cap` measured candidates in
  * rank order; *n_trials their count. */
 int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, const void* A, const void* B, void* C,

@@ -65,7 +65,7 @@ class Schedule(ctypes.Structure):
     _fields_ = [("tileM", ctypes.c_int64), ("tileN", ctypes.c_int64), ("tileK", ctypes.c_int64),
                 ("n_stage_smem_A", ctypes.c_int32), ("n_stage_smem_B", ctypes.c_int32),
                 ("n_stage_inner", ctypes.c_int32), ("cta_group", ctypes.c_int32), ("mode", ctypes.c_int32),
-                ("num_ctas", ctypes.c_int32), ("raster", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
+                ("num_ctas", ctypes.c_int32), ("raster", ctypes.c_int32), ("stream_k", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("reserved")}
@@ -75,7 +75,7 @@ class Schedule(ctypes.Structure):
         return ("Schedule(tile=%dx%dx%d, stages A/B=%d/%d, inner=%d, mode=%s%s)"
                 % (d["tileM"], d["tileN"], d["tileK"], d["n_stage_smem_A"], d["n_stage_smem_B"],
                    d["n_stage_inner"], "FUSED" if d["mode"] == MODE_FUSED else "WRAP",
-                   ", cta_group=2" if d["cta_group"] == 2 else ""))
+                   (", cta_group=2" if d["cta_group"] == 2 else "") + (", stream_k" if d["stream_k"] else "")))
 
 
 class ConvDesc(ctypes.Structure):
@@ -256,11 +256,11 @@ def default_schedule(**kw) -> Schedule:
 
 
 def make_schedule(tileN=256, tileK=64, n_stage=4, n_stage_inner=2, mode=MODE_FUSED, n_stage_B=None,
-                  num_ctas=0, cta_group=1, raster=0) -> Schedule:
+                  num_ctas=0, cta_group=1, raster=0, stream_k=0) -> Schedule:
     return default_schedule(tileM=128 * cta_group, tileN=tileN, tileK=tileK, n_stage_smem_A=n_stage,
                             n_stage_smem_B=n_stage if n_stage_B is None else n_stage_B,
                             n_stage_inner=n_stage_inner, mode=mode, num_ctas=num_ctas, cta_group=cta_group,
-                            raster=raster)
+                            raster=raster, stream_k=stream_k)
 
 
 def apply_script(desc: GemmDesc, script: str):
@@ -560,7 +560,7 @@ def tune(A, B, C, budget=8, b_layout=B_KN, hw: HW | None = None, stream=None):
     N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
     d = gemm_desc(M, N, K, A.shape[0] if batched else 1, _dtype_code(A.dtype), _dtype_code(C.dtype), b_layout)
     best = Schedule()
-    cap = max(1, budget)
+    cap = max(1, 2 * budget)  # the model's top `budget` + stream-K twins of the CTA-pair ones
     arr = (TuneTrial * cap)()
     n = ctypes.c_int32(0)
     _check(load_library().alcop_tune(ctypes.byref(d), ctypes.byref(hw or hw_b200()), budget,

@@ -154,6 +154,8 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256");
   if (s.cta_group == 2 && s.tileN == 64)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "cta_group 2 needs tileN 128, 192 or 256");
+  if (s.stream_k != 0 && (s.stream_k != 1 || s.cta_group != 2 || s.mode != ALCOP_MODE_FUSED))
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "stream_k (0|1) applies to cta_group 2 in FUSED mode");
   if (s.cta_group == 2 && s.n_stage_smem_A != s.n_stage_smem_B)
     return set_error(ALCOP_ERR_CONFIG, "BadStages", "cta_group 2 uses one joint A+B ring: equal stage counts");
   if (s.tileK != 32 && s.tileK != 64 && s.tileK != 128)

@@ -75,6 +75,7 @@ struct GemmKParams {
   int32_t epi_warps;   // 4 or 8 (gemm_epi_warps)
   int32_t in_bf16;  // fused pre-op arithmetic type
   int32_t pre_op;   // 1: A -> 2A+1 before the MMA (the reference's inlined "ew")
+  int32_t* sk_flags;  // stream-K: per writer cluster, partial published (8 arrivals) / consumed
 };
 
 // debug timeline buffer (set through alcop_debug_set_stamps)
@@ -779,10 +780,23 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
 // and hands the accumulator back on the leader's tmem_empty (8 arrivals).
 // Joint A+B ring only (n_stage_A == n_stage_B).
 // ---------------------------------------------------------------------------
-template <typename OutT, int BK, bool kDebug>
+// stream-K partial hand-off (release / acquire across clusters; the partial
+// moves through the async proxy: TMA store by the writer, TMA load by the finisher)
+__device__ __forceinline__ int sk_ld_acquire(const int32_t* f) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sk_red_release_add(int32_t* f, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sk_fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <typename OutT, int BK, bool kDebug, bool kSK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                                     const __grid_constant__ CUtensorMap tmC, const GemmKParams p) {
+                                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmW,
+                                     const GemmKParams p) {
   using namespace ptx;
   constexpr int kSteps = BK / 16;
   constexpr int kBoxK = BK >= 64 ? 64 : BK;
@@ -801,7 +815,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   uint64_t* empty = full + p.sA;
   uint64_t* tfull = empty + p.sA;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fixbar = tempty + 2;  // stream-K: one per epilogue warp (partial landed)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 4);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
@@ -815,6 +830,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     prefetch_tmap(&tmC);
+    if constexpr (kSK) prefetch_tmap(&tmW);
   }
   if (warp == 1) {
     if (elect_one()) {
@@ -826,6 +842,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         mbar_init(smem_u32(&tfull[i]), 1);
         mbar_init(smem_u32(&tempty[i]), 8);  // 4 epilogue warps x 2 CTAs
       }
+      if constexpr (kSK)
+        for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&fixbar[i]), 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -845,6 +863,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const int my_tiles = (p.num_tiles - cluster_id + nclusters - 1) / nclusters;
   const int E = p.E;
   const bool wrap = (p.mode == ALCOP_MODE_WRAP);
+  // This cluster's work as segments (k-th segment: tile, chunks [cb, ce)).
+  // Whole tiles: tiles cluster_id + k * nclusters.  Stream-K (FUSED only):
+  // whole-tile waves as before except the last full wave plus the partial
+  // one (R + n tiles, R = tiles mod n), whose chunk stream is split evenly,
+  // cluster c taking chunks [c T / n, (c+1) T / n) of T = (R + n) x E —
+  // neighbouring clusters stay on neighbouring tiles, so the L2 working set
+  // is that of a whole-tile wave.  With >= E chunks per cluster a tile is cut
+  // between at most two clusters: the later one (it reaches the cut first, at
+  // the start of its range) writes an fp32 partial of the tile's last chunks,
+  // the earlier one (at the end of its range) adds it.
+  auto for_each_seg = [&](auto&& fn) {
+    if constexpr (kSK) {
+      const int dp_waves = p.num_tiles / nclusters - 1;
+      int k = 0;
+      for (; k < dp_waves; ++k) fn(k, cluster_id + k * nclusters, 0, E);
+      const int t0 = dp_waves * nclusters;
+      const int64_t T = static_cast<int64_t>(p.num_tiles - t0) * E;
+      const int64_t e0 = T * (cluster_id + 1) / nclusters;
+      int64_t g = T * cluster_id / nclusters;
+      for (; g < e0; ++k) {
+        const int t = static_cast<int>(g / E);
+        const int cb = static_cast<int>(g - static_cast<int64_t>(t) * E);
+        const int ce = static_cast<int>(min(static_cast<int64_t>(E), cb + (e0 - g)));
+        fn(k, t0 + t, cb, ce);
+        g += ce - cb;
+      }
+    } else {
+      for (int k = 0; k < my_tiles; ++k) fn(k, cluster_id + k * nclusters, 0, E);
+    }
+  };
 
   if (warp == 0 || warp == 6) {
     if (ROLE_GUARD()) {
@@ -862,16 +910,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       // waits on the same empty barrier and loads B, completing on the same
       // full barrier (its bytes may land before the expect_tx: the phase
       // still needs warp 0's arrival).  kRole: 0 = A + commit, 1 = B, 2 = both.
-      auto load = [&](int tl, int chunk, auto role) {
+      auto load = [&](int tile, int chunk, auto role) {
         constexpr int kRole = decltype(role)::value;
         const uint32_t slot = ra.slot;
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&empty[slot]), par);  // producer_acquire (own slot, released by the pair's MMA)
         ra.phase ^= 1u << slot;
         if (lane == 0 && warp == 0) chunkstamp<kDebug>(p, 0, ra.count++);
-        if (tl != tc_tile) {
-          tc_tile = tl;
-          tc = tile_coord(p, cluster_id + tl * nclusters);
+        if (tile != tc_tile) {
+          tc_tile = tile;
+          tc = tile_coord(p, tile);
         }
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
@@ -911,17 +959,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             ra.slot = 0;
             int c = 0;
             for (int i = 0; i < E + p.sA - 1; ++i) {
-              load(tl, c, std::integral_constant<int, 2>{});
+              load(cluster_id + tl * nclusters, c, std::integral_constant<int, 2>{});
               c = (c + 1 == E) ? 0 : c + 1;
             }
           }
         }
       } else if (warp == 0) {
-        for (int tl = 0; tl < my_tiles; ++tl)
-          for (int c = 0; c < E; ++c) load(tl, c, std::integral_constant<int, 0>{});
+        for_each_seg([&](int, int t, int cb, int ce) {
+          for (int c = cb; c < ce; ++c) load(t, c, std::integral_constant<int, 0>{});
+        });
       } else {
-        for (int tl = 0; tl < my_tiles; ++tl)
-          for (int c = 0; c < E; ++c) load(tl, c, std::integral_constant<int, 1>{});
+        for_each_seg([&](int, int t, int cb, int ce) {
+          for (int c = cb; c < ce; ++c) load(t, c, std::integral_constant<int, 1>{});
+        });
       }
     }
     __syncwarp();
@@ -949,19 +999,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       }
       const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
       const uint32_t idesc = p.idesc;
-      for (int tl = 0; tl < my_tiles; ++tl) {
-        const int acc = tl % p.tacc;
-        mbar_wait(smem_u32(&tempty[acc]), ((tl / p.tacc) & 1) ^ 1);  // both CTAs drained it
+      auto mma_seg = [&](int k, int cb, int ce) {
+        const int acc = k % p.tacc;
+        mbar_wait(smem_u32(&tempty[acc]), ((k / p.tacc) & 1) ^ 1);  // both CTAs drained it
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
         if (wrap) ca.slot = 0;
-        for (int v = 0; v < E; ++v) {
+        for (int v = cb; v < ce; ++v) {
           const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
           mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
           ca.phase ^= 1u << slot;
           if (lane == 0) chunkstamp<kDebug>(p, 1, ca.count++);
           tc_fence_after();
-          if (tl == 0 && v == 0 && lane == 0) stamp<kDebug>(p, 3);
+          if (k == 0 && v == cb && lane == 0) stamp<kDebug>(p, 3);
           const uint64_t ad = adesc0 + slot * a_stage16;
           const uint64_t bd = bdesc0 + slot * b_stage16;
           ISSUE(
@@ -969,12 +1019,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
               for (int u = 0; u < kSteps; ++u) {
                 const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > 0 || u > 0) ? 1u : 0u);
+                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > cb || u > 0) ? 1u : 0u);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
           ca.advance(p.sA);
         }
         ISSUE(umma_commit_pair_multicast(smem_u32(&tfull[acc]), 0x3));
-        if (tl == my_tiles - 1 && lane == 0) stamp<kDebug>(p, 4);
+        if (k == my_tiles - 1 && lane == 0) stamp<kDebug>(p, 4);
         if (wrap) {
           // drain the s-1 wrapped tail groups (no MMA): release both CTAs' slots
           for (int d = 0; d < p.sA - 1; ++d) {
@@ -985,7 +1035,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             ca.advance(p.sA);
           }
         }
-      }
+      };
+      for_each_seg([&](int k, int, int cb, int ce) { mma_seg(k, cb, ce); });
     }
     __syncwarp();
   } else if (warp < 6) {
@@ -995,23 +1046,102 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      const int acc = tl % p.tacc;
-      mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
+    const int row0 = static_cast<int>(rank) * kTileM + q * 32;  // this warp's rows of the cluster's 256
+    for_each_seg([&](int k, int t, int cb, int ce) {
+      const int acc = k % p.tacc;
+      mbar_wait(smem_u32(&tfull[acc]), (k / p.tacc) & 1);
       tc_fence_after();
-      if (tl == 0 && warp == 2 && lane == 0) stamp<kDebug>(p, 5);
-      const TileCoord tc = tile_coord(p, cluster_id + tl * nclusters);
+      if (k == 0 && warp == 2 && lane == 0) stamp<kDebug>(p, 5);
+      const TileCoord tc = tile_coord(p, t);
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+      const bool writer = kSK && cb > 0;              // the tile's last chunks: fp32 partial out
+      const bool finisher = kSK && cb == 0 && ce < E;  // the tile's first chunks: add the partial
+      if (writer) {
+        // fp32 partial (32-column chunks) into this cluster's workspace slot
+        for (int c = 0; c < p.BN / 32; ++c) {
+          uint32_t w[32];
+          tmem_ld_32x32b_x32(t_addr + c * 32, w);
+          tmem_wait_ld();
+          if (c == p.BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          }
+          const uint32_t sbuf = stage_base + buf * 4096;
+          if (lane == 0) {
+            if (p.stage_bufs == 2)
+              bulk_wait_group_read<1>();
+            else
+              bulk_wait_group_read<0>();
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                         w[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmW, sbuf, c * 32, row0, cluster_id);
+            bulk_commit_group();
+          }
+          buf ^= p.stage_bufs - 1;
+        }
+        // publish: the partial is in global memory before the release
+        if (lane == 0) {
+          bulk_wait_group<0>();
+          sk_fence_proxy_async_global();
+          sk_red_release_add(p.sk_flags + cluster_id, 1);
+        }
+        __syncwarp();
+        return;
+      }
+      uint32_t part = 0;  // finisher: this warp's 32 rows of the partial, staged in the (idle) ring
+      if (finisher) {
+        part = ringA + static_cast<uint32_t>(q) * static_cast<uint32_t>(p.BN) * 128u;
+        int32_t* flag = p.sk_flags + cluster_id + 1;
+        if (lane == 0) {
+          while (sk_ld_acquire(flag) < 8) __nanosleep(32);  // 4 epilogue warps x 2 CTAs of the writer
+          sk_fence_proxy_async_global();
+          mbar_arrive_expect_tx(smem_u32(&fixbar[q]), static_cast<uint32_t>(p.BN) * 128u);
+          for (int b = 0; b < p.BN / 32; ++b)
+            tma_load_3d(part + b * 4096, &tmW, smem_u32(&fixbar[q]), b * 32, row0, cluster_id + 1);
+        }
+        __syncwarp();
+        mbar_wait(smem_u32(&fixbar[q]), 0);  // one finisher segment per cluster and launch
+        if (lane == 0 && atomicAdd(flag, 1) == 15) atomicExch(flag, 0);  // the last reader re-arms the slot
+        __syncwarp();
+      }
+      auto add_part = [&](uint32_t(&r)[32], int box) {
+        if (!finisher) return;
+        const uint32_t src = part + box * 4096 + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                       : "r"(src + ((j ^ (lane & 7)) << 4)));
+          r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + __uint_as_float(x0));
+          r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + __uint_as_float(x1));
+          r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + __uint_as_float(x2));
+          r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + __uint_as_float(x3));
+        }
+      };
       for (int c = 0; c < nchunks; ++c) {
         uint32_t w[32];
         if constexpr (sizeof(OutT) == 4) {
           tmem_ld_32x32b_x32(t_addr + c * 32, w);
           tmem_wait_ld();
+          if constexpr (kSK) add_part(w, c);
         } else {
           uint32_t r0[32], r1[32];
           tmem_ld_32x32b_x32(t_addr + c * 64, r0);
           tmem_ld_32x32b_x32(t_addr + c * 64 + 32, r1);
           tmem_wait_ld();
+          if constexpr (kSK) {
+            add_part(r0, 2 * c);
+            add_part(r1, 2 * c + 1);
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             w[i] = pack2<OutT>(r0[2 * i], r0[2 * i + 1]);
@@ -1038,13 +1168,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols,
-                       tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM + q * 32, tc.b);
+          tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * (2 * kTileM) + row0, tc.b);
           bulk_commit_group();
         }
         buf ^= p.stage_bufs - 1;
       }
-    }
+    });
     if (lane == 0) bulk_wait_group_read<0>();  // smem reads done; grid completion publishes the writes
     __syncwarp();
     if (warp == 2 && lane == 0) stamp<kDebug>(p, 6);
@@ -1103,6 +1232,49 @@ int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint6
   return ALCOP_OK;
 }
 
+// Stream-K workspace, one per device, grown on demand and kept: the fp32
+// partials (one 256 x BN slot per cluster) and the per-slot flags (zero; each
+// launch's finishers re-arm them).  Not allocated during stream capture: a
+// captured launch without a large-enough workspace runs whole tiles.
+bool sk_workspace(cudaStream_t st, size_t part_bytes, int n, float** part, int32_t** flags) {
+  struct Ws {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  static Ws ws[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  constexpr size_t kFlagBytes = 4096;  // flags first (fixed place whatever the partial size), then partials
+  if (static_cast<size_t>(n + 1) * sizeof(int32_t) > kFlagBytes) return false;
+  const size_t need = kFlagBytes + part_bytes;
+  std::lock_guard<std::mutex> lk(mu);
+  Ws& w = ws[dev];
+  if (w.bytes < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return false;  // earlier launches may use the old one
+    if (w.ptr) cudaFree(w.ptr);
+    w.ptr = nullptr;
+    w.bytes = 0;
+    void* p = nullptr;
+    const size_t alloc = std::max(need, static_cast<size_t>(32) << 20);
+    if (cudaMalloc(&p, alloc) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaMemset(p, 0, alloc) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaFree(p);
+      return false;
+    }
+    w.ptr = p;
+    w.bytes = alloc;
+  }
+  *flags = static_cast<int32_t*>(w.ptr);
+  *part = reinterpret_cast<float*>(static_cast<char*>(w.ptr) + kFlagBytes);
+  return true;
+}
+
 template <typename OutT, int BK, bool kJoint, bool kDebug, bool kPreOp = false, int kEpi = 4>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
                  int grid, int smem, cudaStream_t st) {
@@ -1125,10 +1297,10 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK, bool kDebug = false>
-int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
-                  int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug>;
+template <typename OutT, int BK, bool kDebug = false, bool kSK = false>
+int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tw,
+                  const GemmKParams& kp, int grid, int smem, cudaStream_t st) {
+  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug, kSK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -1141,18 +1313,20 @@ int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp);
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tw, kp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
 }
 
-// timeline stamps (alcop_debug_set_stamps) select the instrumented variant
+// timeline stamps (alcop_debug_set_stamps) select the instrumented variant;
+// kp.sk_flags the stream-K variant (never instrumented)
 template <typename OutT, int BK>
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp, int grid,
-                int smem, cudaStream_t st) {
-  return kp.stamps ? launch_pair_t<OutT, BK, true>(ta, tb, tc, kp, grid, smem, st)
-                   : launch_pair_t<OutT, BK, false>(ta, tb, tc, kp, grid, smem, st);
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tw,
+                const GemmKParams& kp, int grid, int smem, cudaStream_t st) {
+  if (kp.sk_flags) return launch_pair_t<OutT, BK, false, true>(ta, tb, tc, tw, kp, grid, smem, st);
+  return kp.stamps ? launch_pair_t<OutT, BK, true>(ta, tb, tc, tw, kp, grid, smem, st)
+                   : launch_pair_t<OutT, BK, false>(ta, tb, tc, tw, kp, grid, smem, st);
 }
 
 template <typename OutT, bool kDebug, int kConv>
@@ -1363,16 +1537,31 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
       return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the device trace is implemented for cta_group 1");
     grid = (grid / 2) * 2;
     if (grid > 2 * kp.num_tiles) grid = 2 * kp.num_tiles;
+    CUtensorMap tw = tc;  // stream-K partials (unused otherwise)
+    if (s.stream_k && s.mode == ALCOP_MODE_FUSED && !kp.stamps) {
+      // needs >= E chunks per cluster (a tile then spans at most two
+      // clusters) and the ring to hold one 256 x BN fp32 partial per CTA
+      const int n = grid / 2;
+      const bool fits = static_cast<int64_t>(kp.sA) * (kp.a_stage_bytes + kp.b_stage_bytes) >= int64_t(BN) * 512;
+      float* part = nullptr;
+      int32_t* flags = nullptr;
+      if (kp.num_tiles >= n && fits && sk_workspace(st, static_cast<size_t>(n) * 256 * BN * 4, n, &part, &flags)) {
+        rc = encode_3d_dt(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, part, BN, 256, n, BN * 4, int64_t(256) * BN * 4, 32,
+                          32, CU_TENSOR_MAP_SWIZZLE_128B, "stream-K partials");
+        if (rc) return rc;
+        kp.sk_flags = flags;
+      }
+    }
     switch (w.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
-      case ALCOP_F32 * 4 + 0: return launch_pair<float, 32>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_F32 * 4 + 1: return launch_pair<float, 64>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_F32 * 4 + 2: return launch_pair<float, 128>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_BF16 * 4 + 0: return launch_pair<__nv_bfloat16, 32>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_BF16 * 4 + 1: return launch_pair<__nv_bfloat16, 64>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_BF16 * 4 + 2: return launch_pair<__nv_bfloat16, 128>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_F16 * 4 + 0: return launch_pair<__half, 32>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_F16 * 4 + 1: return launch_pair<__half, 64>(ta, tb, tc, kp, grid, smem, st);
-      case ALCOP_F16 * 4 + 2: return launch_pair<__half, 128>(ta, tb, tc, kp, grid, smem, st);
+      case ALCOP_F32 * 4 + 0: return launch_pair<float, 32>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_F32 * 4 + 1: return launch_pair<float, 64>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_F32 * 4 + 2: return launch_pair<float, 128>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 0: return launch_pair<__nv_bfloat16, 32>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 1: return launch_pair<__nv_bfloat16, 64>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_BF16 * 4 + 2: return launch_pair<__nv_bfloat16, 128>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 0: return launch_pair<__half, 32>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 1: return launch_pair<__half, 64>(ta, tb, tc, tw, kp, grid, smem, st);
+      case ALCOP_F16 * 4 + 2: return launch_pair<__half, 128>(ta, tb, tc, tw, kp, grid, smem, st);
     }
     return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
   }
