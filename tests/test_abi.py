@@ -34,6 +34,8 @@ def test_version_and_error_string(alcop):
     ("n_stage_smem_A", 0, "BadStages"), ("n_stage_inner", 3, "BadStages"), ("mode", 7, "BadSchedule"),
     ("raster", -1, "BadRaster"),
     ("cta_group", 4, "BadSchedule"),
+    ("stream_k", 1, "BadSchedule"),  # stream-K needs cta_group 2 (make_schedule default: 1)
+    ("stream_k", 2, "BadSchedule"),
 ])
 def test_validate_rejects(alcop, field, value, rule):
     d = alcop.gemm_desc(1024, 1024, 1024)
