@@ -275,8 +275,8 @@ typedef struct {
  * pipe_sim.hpp:195-239, replaced by the GPU): enumerate the B200 space,
  * rank by alcop_predict, time the top `budget` schedules on the caller's
  * buffers (steady-state CUDA-graph timing over rotating copies > 2x L2),
- * plus a stream_k twin of each CTA-pair candidate whose tiles do not fill
- * whole waves (up to 2 x budget trials), return the fastest in *best.
+ * return the fastest in *best.  Whole-tile schedules only: stream_k is an
+ * explicit opt-in (its workspace is shared per device). 
  * `trials` (may be NULL) receives up to `trials_cap` measured candidates in
  * rank order; *n_trials their count. */
 int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, const void* A, const void* B, void* C,

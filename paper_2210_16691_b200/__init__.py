@@ -560,7 +560,7 @@ def tune(A, B, C, budget=8, b_layout=B_KN, hw: HW | None = None, stream=None):
     N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
     d = gemm_desc(M, N, K, A.shape[0] if batched else 1, _dtype_code(A.dtype), _dtype_code(C.dtype), b_layout)
     best = Schedule()
-    cap = max(1, 2 * budget)  # the model's top `budget` + stream-K twins of the CTA-pair ones
+    cap = max(1, budget)
     arr = (TuneTrial * cap)()
     n = ctypes.c_int32(0)
     _check(load_library().alcop_tune(ctypes.byref(d), ctypes.byref(hw or hw_b200()), budget,

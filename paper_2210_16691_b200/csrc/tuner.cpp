@@ -45,21 +45,6 @@ extern "C" int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t 
   if (space.empty()) return set_error(ALCOP_ERR_CONFIG, "Unschedulable", "no valid schedule for workload");
   std::stable_sort(space.begin(), space.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
   space.resize(std::min<size_t>(static_cast<size_t>(budget), space.size()));
-  // Stream-K twins of the CTA-pair candidates whose whole-tile waves leave
-  // clusters idle (the model times whole tiles; the device decides: stream-K
-  // wins on long-K few-wave shapes and loses on short K, tools/sk_probe.py)
-  {
-    const int nclusters = std::max(1, device_sm_count() / 2);
-    const size_t n0 = space.size();
-    for (size_t i = 0; i < n0; ++i) {
-      alcop_schedule s = space[i].second;
-      if (s.cta_group != 2) continue;
-      const int64_t tiles = ((w->M + 255) / 256) * ((w->N + s.tileN - 1) / s.tileN) * w->batch;
-      if (tiles < nclusters || tiles % nclusters == 0) continue;
-      s.stream_k = 1;
-      space.push_back({space[i].first, s});
-    }
-  }
   const int n = static_cast<int>(space.size());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // Steady-state timing, as inside a layer step: each candidate runs as a
