@@ -1101,7 +1101,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         part = ringA + static_cast<uint32_t>(q) * static_cast<uint32_t>(p.BN) * 128u;
         int32_t* flag = p.sk_flags + cluster_id + 1;
         if (lane == 0) {
-          while (sk_ld_acquire(flag) < 8) __nanosleep(32);  // 4 epilogue warps x 2 CTAs of the writer
+          long long t0 = 0;
+          while (sk_ld_acquire(flag) < 8) {  // 4 epilogue warps x 2 CTAs of the writer
+            if (t0 == 0) t0 = clock64();
+            if (clock64() - t0 > (1ll << 33)) asm volatile("trap;");  // watchdog, as mbar_wait
+            __nanosleep(32);
+          }
           sk_fence_proxy_async_global();
           mbar_arrive_expect_tx(smem_u32(&fixbar[q]), static_cast<uint32_t>(p.BN) * 128u);
           for (int b = 0; b < p.BN / 32; ++b)
