@@ -652,6 +652,8 @@ def main_gpu(args, rank, world, local_rank):
                                                      torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
                            (M * K + K * N + M * N) * 2 * nb, max_sets=16)
             nr = len(rot.sets)
+            if args.schedule == "tune":  # as for the layer GEMMs: the model's top schedules timed here
+                sb, _ = alcop.tune(*rot.sets[0], budget=TUNE_BUDGET)
 
             def runb(i, s_, rot=rot, nr=nr, db=db):
                 A, B, C = rot.sets[i % nr]
