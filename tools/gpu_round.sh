@@ -15,4 +15,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:alcop -s 8 -c 4 \
     -o gpurun_out/prof_step -f python tools/profile_step.py --bench gpurun_out/bench.json --steps 3 > gpurun_out/ncu_full.log 2>&1
 ncu -i gpurun_out/prof_step.ncu-rep --page raw --csv > gpurun_out/prof_step_raw.csv 2>/dev/null
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/pcie.json; head -c 1500 gpurun_out/bench.json
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/pcie.json; head -c 1500 gpurun_out/bench.json
