@@ -248,7 +248,13 @@ int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const voi
  * lands, C's blocks come back on a second copy stream; `stream` is made to
  * wait for the last D2H, so C is valid after cudaStreamSynchronize(stream).
  * Consecutive calls overlap (the H2D of call k+1 with the D2H of call k) when
- * each call in flight has its own workspace and host buffers. */
+ * each call in flight has its own workspace and host buffers.
+ * Ordering: a call's H2D copies start after the previous call's kernels on this
+ * host thread and device (so a shared workspace is safe, as is all work enqueued
+ * on `stream` before them) and, when hA or hB overlaps the previous call's hC,
+ * after that call's D2H (a chain where C_k is A_{k+1}).  Host inputs written by
+ * OTHER work (the caller's own copies, another thread) must be complete on the
+ * host before the call. */
 int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
                           void* hC, void* workspace, void* stream);
 

@@ -12,6 +12,8 @@
  *  3. GEMM / BMM with fp32 accumulation  schedule.hpp:543-572 (mma nest) over
  *     fp16/bf16 inputs; int64 GEMM      interp.hpp:364-366 (integer mma)
  *  4. direct conv2d NHWC x KRSC          (no reference form)
+ *  4b. sampled exact GEMM rows / columns and conv output pixels at benchmark
+ *     scale (check_equivalence, interp.hpp:469-509, on samples)
  *  5. pipeline index algebra             pipeline_pass.hpp:482-552, 622-748
  *  6. interpreter group counters         interp.hpp:375-418 (+ the two-level
  *     drain leak of pipeline_pass.hpp:340-347,732-742 and its fix)
@@ -179,6 +181,120 @@ void oracle_conv2d(int64_t N, int64_t H, int64_t W, int64_t Cin, int64_t Kout, i
           }
           store_elem(y, out_dt, ((n * P + p) * Q + q) * Kout + k, acc);
         }
+}
+
+/* ---------------------------------------------------------------- 4b */
+/* Sampled exact checks at benchmark scale (the reference's check_equivalence,
+ * interp.hpp:469-509, compares every transformed program against the
+ * untransformed one; at 16384^3 the checker evaluates sampled rows, columns
+ * and output pixels instead of the whole product).
+ *
+ * Inputs are the reference's D-int draws (SplitMix64 range(-8,8),
+ * cli.hpp:41-46) stored as int8.  Every partial sum is bounded by 64*K
+ * (< 2^31 for K < 2^25), so int32 accumulation is the interpreter's int64 mma
+ * (interp.hpp:364-366) exactly; results are widened to int64. */
+
+/* the same draws as oracle_random_tensor, element-parallel (SplitMix64 is a
+ * counter generator: draw i is mix(seed + (i+1)*gamma)) */
+void oracle_random_i8(int64_t count, uint64_t seed, int64_t lo, int64_t hi, int8_t* out) {
+  const uint64_t n = (uint64_t)(hi - lo + 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < count; ++i) {
+    uint64_t z = seed + (uint64_t)(i + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    out[i] = (int8_t)(lo + (int64_t)(z % n));
+  }
+}
+
+/* C rows `rows[i]` (global row = b*M + m) of C = A @ B:
+ * A [batch,M,K] int8, B [batch,K,N] (b_layout 0) or [batch,N,K] (1) int8;
+ * out [nrows, N] int64.  Parallel over (row, column block); each thread
+ * streams the rows of B once per row block. */
+void oracle_gemm_rows_i8(int64_t M, int64_t N, int64_t K, int64_t batch, const int8_t* A, const int8_t* B,
+                         int b_layout, int64_t nrows, const int64_t* rows, int64_t* out) {
+  const int64_t JB = 2048;
+  const int64_t nj = (N + JB - 1) / JB;
+  (void)batch;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int64_t i = 0; i < nrows; ++i)
+    for (int64_t jb = 0; jb < nj; ++jb) {
+      const int64_t r = rows[i], b = r / M;
+      const int8_t* a = A + r * K;
+      const int64_t j0 = jb * JB, j1 = j0 + JB < N ? j0 + JB : N;
+      int32_t acc[2048];
+      for (int64_t j = 0; j < j1 - j0; ++j) acc[j] = 0;
+      if (b_layout == 0) {
+        const int8_t* bb = B + b * K * N;
+        for (int64_t k = 0; k < K; ++k) {
+          const int32_t av = a[k];
+          const int8_t* brow = bb + k * N + j0;
+          for (int64_t j = 0; j < j1 - j0; ++j) acc[j] += av * (int32_t)brow[j];
+        }
+      } else {
+        const int8_t* bb = B + b * N * K;
+        for (int64_t j = 0; j < j1 - j0; ++j) {
+          const int8_t* bcol = bb + (j0 + j) * K;
+          int32_t s = 0;
+          for (int64_t k = 0; k < K; ++k) s += (int32_t)a[k] * (int32_t)bcol[k];
+          acc[j] = s;
+        }
+      }
+      for (int64_t j = 0; j < j1 - j0; ++j) out[i * N + j0 + j] = acc[j];
+    }
+}
+
+/* C columns `cols[j]` of every row of every batch: out [batch*M, ncols] int64 */
+void oracle_gemm_cols_i8(int64_t M, int64_t N, int64_t K, int64_t batch, const int8_t* A, const int8_t* B,
+                         int b_layout, int64_t ncols, const int64_t* cols, int64_t* out) {
+  for (int64_t b = 0; b < batch; ++b) {
+    /* gather the sampled columns of B_b as [K, ncols] int32 */
+    int32_t* bp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(K * ncols));
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t j = 0; j < ncols; ++j)
+        bp[k * ncols + j] = b_layout == 0 ? B[(b * K + k) * N + cols[j]] : B[(b * N + cols[j]) * K + k];
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+      int32_t* acc = (int32_t*)calloc((size_t)ncols, sizeof(int32_t));
+      const int8_t* a = A + (b * M + m) * K;
+      for (int64_t k = 0; k < K; ++k) {
+        const int32_t av = a[k];
+        const int32_t* br = bp + k * ncols;
+        for (int64_t j = 0; j < ncols; ++j) acc[j] += av * br[j];
+      }
+      for (int64_t j = 0; j < ncols; ++j) out[(b * M + m) * ncols + j] = acc[j];
+      free(acc);
+    }
+    free(bp);
+  }
+}
+
+/* direct conv2d (as oracle_conv2d) at output pixels pts[i] = (n, p, q), all K
+ * channels: x NHWC int8, w KRSC int8, out [npts, K] int64 */
+void oracle_conv2d_points_i8(int64_t N, int64_t H, int64_t W, int64_t Cin, int64_t Kout, int64_t R, int64_t S,
+                             int sh, int sw, int ph, int pw, const int8_t* x, const int8_t* w, int64_t npts,
+                             const int64_t* pts, int64_t* out) {
+  (void)N;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < npts; ++i) {
+    const int64_t n = pts[3 * i], p = pts[3 * i + 1], q = pts[3 * i + 2];
+    for (int64_t k = 0; k < Kout; ++k) {
+      int32_t acc = 0;
+      for (int64_t r = 0; r < R; ++r) {
+        const int64_t h = p * sh - ph + r;
+        if (h < 0 || h >= H) continue;
+        for (int64_t s = 0; s < S; ++s) {
+          const int64_t ww = q * sw - pw + s;
+          if (ww < 0 || ww >= W) continue;
+          const int8_t* xp = x + ((n * H + h) * W + ww) * Cin;
+          const int8_t* wp = w + ((k * R + r) * S + s) * Cin;
+          for (int64_t c = 0; c < Cin; ++c) acc += (int32_t)xp[c] * (int32_t)wp[c];
+        }
+      }
+      out[i * Kout + k] = acc;
+    }
+  }
 }
 
 /* ---------------------------------------------------------------- 5 */

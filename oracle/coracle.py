@@ -39,6 +39,10 @@ def lib():
         L.oracle_gemm.argtypes = [i64, i64, i64, i64, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_gemm_i64.argtypes = [i64, i64, i64, i64, vp, vp, vp]
         L.oracle_conv2d.argtypes = [i64] * 7 + [ctypes.c_int] * 4 + [vp, vp, vp, ctypes.c_int, ctypes.c_int]
+        L.oracle_random_i8.argtypes = [i64, ctypes.c_uint64, i64, i64, vp]
+        L.oracle_gemm_rows_i8.argtypes = [i64, i64, i64, i64, vp, vp, ctypes.c_int, i64, vp, vp]
+        L.oracle_gemm_cols_i8.argtypes = [i64, i64, i64, i64, vp, vp, ctypes.c_int, i64, vp, vp]
+        L.oracle_conv2d_points_i8.argtypes = [i64] * 7 + [ctypes.c_int] * 4 + [vp, vp, i64, vp, vp]
         L.oracle_root_schedule.argtypes = [i64, i64, vp, vp, vp]
         L.oracle_nested_schedule.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp]
         L.oracle_sync_trace.argtypes = [i64, i64, i64, i64, i64, i64, i64, ctypes.c_int, vp, i64]
@@ -122,6 +126,56 @@ def conv2d(x, w, stride, pad, in_dt, out_dt):
     lib().oracle_conv2d(N, H, W, C, K, R, S, stride[0], stride[1], pad[0], pad[1], _p(x), _p(w), _p(y),
                         DT[in_dt], DT[out_dt])
     return y
+
+
+def random_i8(count, seed, lo=-8, hi=8):
+    """random_tensor's draws (cli.hpp:41-46) as int8, element-parallel."""
+    out = np.empty(count, dtype=np.int8)
+    lib().oracle_random_i8(count, seed, lo, hi, _p(out))
+    return out
+
+
+def _bshape(A, B, b_layout):
+    batched = A.ndim == 3
+    batch = A.shape[0] if batched else 1
+    M, K = A.shape[-2:]
+    N = B.shape[-1] if b_layout == 0 else B.shape[-2]
+    return M, N, K, batch
+
+
+def gemm_rows_i8(A, B, rows, b_layout=0):
+    """Exact rows (global index b*M + m) of A @ B on int8 D-int inputs -> int64 [len(rows), N]."""
+    A = np.ascontiguousarray(A, dtype=np.int8)
+    B = np.ascontiguousarray(B, dtype=np.int8)
+    M, N, K, batch = _bshape(A, B, b_layout)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty((len(rows), N), dtype=np.int64)
+    lib().oracle_gemm_rows_i8(M, N, K, batch, _p(A), _p(B), b_layout, len(rows), _p(rows), _p(out))
+    return out
+
+
+def gemm_cols_i8(A, B, cols, b_layout=0):
+    """Exact columns of A @ B for every (batch, row) -> int64 [batch*M, len(cols)]."""
+    A = np.ascontiguousarray(A, dtype=np.int8)
+    B = np.ascontiguousarray(B, dtype=np.int8)
+    M, N, K, batch = _bshape(A, B, b_layout)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty((batch * M, len(cols)), dtype=np.int64)
+    lib().oracle_gemm_cols_i8(M, N, K, batch, _p(A), _p(B), b_layout, len(cols), _p(cols), _p(out))
+    return out
+
+
+def conv2d_points_i8(x, w, stride, pad, pts):
+    """Exact direct conv at output pixels pts [(n, p, q)] -> int64 [len(pts), K]."""
+    x = np.ascontiguousarray(x, dtype=np.int8)
+    w = np.ascontiguousarray(w, dtype=np.int8)
+    N, H, W, C = x.shape
+    K, R, S, _ = w.shape
+    pts = np.ascontiguousarray(pts, dtype=np.int64).reshape(-1, 3)
+    out = np.empty((len(pts), K), dtype=np.int64)
+    lib().oracle_conv2d_points_i8(N, H, W, C, K, R, S, stride[0], stride[1], pad[0], pad[1], _p(x), _p(w),
+                                  len(pts), _p(pts), _p(out))
+    return out
 
 
 def root_schedule(E, s):

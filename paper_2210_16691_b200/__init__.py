@@ -370,33 +370,62 @@ def _require_cuda(*ts):
             raise RuntimeError("alcop compute entry points take CUDA tensors (no CPU fallback)")
 
 
+def _gemm_operands(A, B, b_layout, out=None, out_dtype=None):
+    """Shape / dtype checks of a (batched) GEMM call before anything reaches
+    the ABI: the descriptor is built from these shapes, so a mismatch would let
+    the kernel read or write outside the buffers.  Returns (M, N, K, batch,
+    batched, out_dtype)."""
+    if A.dim() not in (2, 3) or B.dim() != A.dim():
+        raise ValueError("matmul: A and B must both be 2-D or both 3-D (batched); got %d-D and %d-D"
+                         % (A.dim(), B.dim()))
+    if A.dtype != B.dtype:
+        raise TypeError("matmul: A and B dtypes differ (%s, %s)" % (A.dtype, B.dtype))
+    batched = A.dim() == 3
+    M, K = A.shape[-2], A.shape[-1]
+    if b_layout == B_KN:
+        Kb, N = B.shape[-2], B.shape[-1]
+    elif b_layout == B_NK:
+        N, Kb = B.shape[-2], B.shape[-1]
+    else:
+        raise ValueError("matmul: b_layout must be B_KN or B_NK")
+    if Kb != K:
+        raise ValueError("matmul: reduction sizes differ (A has K=%d, B has K=%d)" % (K, Kb))
+    batch = A.shape[0] if batched else 1
+    if batched and B.shape[0] != batch:
+        raise ValueError("matmul: batch sizes differ (%d, %d)" % (batch, B.shape[0]))
+    out_dtype = out_dtype or (out.dtype if out is not None else A.dtype)
+    if out is not None:
+        want = ((batch,) if batched else ()) + (M, N)
+        if tuple(out.shape) != want:
+            raise ValueError("matmul: out has shape %s, expected %s" % (tuple(out.shape), want))
+        if out.dtype != out_dtype:
+            raise TypeError("matmul: out dtype %s != out_dtype %s" % (out.dtype, out_dtype))
+        if not out.is_contiguous():
+            raise ValueError("matmul: out must be contiguous")
+        if out.device != A.device:
+            raise ValueError("matmul: out is on %s, A on %s" % (out.device, A.device))
+    return M, N, K, batch, batched, out_dtype
+
+
 def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, out=None, stream=None, pre_op=0):
     """Pipelined matmul C = A @ B (or batched) through alcop_gemm; pre_op=1
     computes C = (2A+1) @ B with f fused into the pipeline (the reference's
     inlined elementwise pre-op).
 
     A: [M,K] or [b,M,K]; B: [K,N] / [b,K,N] (b_layout B_KN, the reference
-    layout) or [N,K] / [b,N,K] (B_NK).  fp16/bf16 in, fp32 accumulate."""
+    layout) or [N,K] / [b,N,K] (B_NK).  fp16/bf16 in, fp32 accumulate.
+    Shapes, dtypes and `out` are checked (no broadcasting)."""
     import torch
+    M, N, K, batch, batched, out_dtype = _gemm_operands(A, B, b_layout, out, out_dtype)
     _require_cuda(A, B)
-    batched = A.dim() == 3
-    M, K = A.shape[-2], A.shape[-1]
-    N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
-    batch = A.shape[0] if batched else 1
-    out_dtype = out_dtype or A.dtype
     if out is None:
         out = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, device=A.device)
     A = A.contiguous()
     B = B.contiguous()
     d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout, pre_op=pre_op)
-    if sched is not None:
-        s = sched
-    elif pre_op:
-        s = choose_schedule(gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout))
-        if s.cta_group == 2:
-            s = make_schedule(tileN=s.tileN, tileK=s.tileK, n_stage=s.n_stage_smem_A, n_stage_inner=s.n_stage_inner)
-    else:
-        s = choose_schedule(d)
+    # the model ranks the space valid for this descriptor (with pre_op: the
+    # single-CTA kernel with the transform warps and its shared-memory budget)
+    s = sched if sched is not None else choose_schedule(d)
     _check(load_library().alcop_gemm(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(A.data_ptr()),
                                      ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                      _stream_ptr(stream)))
@@ -406,12 +435,10 @@ def matmul(A, B, sched: Schedule | None = None, out_dtype=None, b_layout=B_KN, o
 def matmul_traced(A, B, sched: Schedule, out_dtype=None, b_layout=B_KN, events_cap=None):
     """matmul with the device debug trace; returns (C, trace[cta][role] -> list of event dicts)."""
     import torch
+    M, N, K, batch, batched, out_dtype = _gemm_operands(A, B, b_layout, None, out_dtype)
     _require_cuda(A, B)
-    batched = A.dim() == 3
-    M, K = A.shape[-2], A.shape[-1]
-    N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
-    batch = A.shape[0] if batched else 1
-    out_dtype = out_dtype or A.dtype
+    A = A.contiguous()
+    B = B.contiguous()
     out = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, device=A.device)
     d = gemm_desc(M, N, K, batch, _dtype_code(A.dtype), _dtype_code(out_dtype), b_layout)
     tiles = -(-M // 128) * -(-N // sched.tileN) * batch
@@ -442,11 +469,16 @@ def matmul_host(A_host, B_host, sched: Schedule, out_dtype, b_layout=B_KN, C_hos
     """End-to-end call with HOST (pinned) tensors through alcop_gemm_host:
     H2D copies, kernel, D2H copy, synchronous.  Returns C_host."""
     import torch
-    batched = A_host.dim() == 3
-    M, K = A_host.shape[-2], A_host.shape[-1]
-    N = B_host.shape[-1] if b_layout == B_KN else B_host.shape[-2]
-    batch = A_host.shape[0] if batched else 1
+    if A_host.is_cuda or B_host.is_cuda:
+        raise ValueError("matmul_host takes host (pinned) tensors")
+    if not (A_host.is_contiguous() and B_host.is_contiguous()):
+        raise ValueError("matmul_host takes packed (contiguous) host tensors")
+    M, N, K, batch, batched, out_dtype = _gemm_operands(A_host, B_host, b_layout, None, out_dtype)
     d = gemm_desc(M, N, K, batch, _dtype_code(A_host.dtype), _dtype_code(out_dtype), b_layout)
+    if C_host is not None:
+        want = ((batch,) if batched else ()) + (M, N)
+        if tuple(C_host.shape) != want or C_host.dtype != out_dtype or not C_host.is_contiguous() or C_host.is_cuda:
+            raise ValueError("matmul_host: C_host must be a contiguous host %s tensor of shape %s" % (out_dtype, want))
     if C_host is None:
         C_host = torch.empty(((batch,) if batched else ()) + (M, N), dtype=out_dtype, pin_memory=True)
     if workspace is None:
@@ -492,18 +524,31 @@ def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_d
         H, W = H - 2 * pad[0], W - 2 * pad[1]
     K, R, S, _ = w.shape
     P, Q = conv_out_hw(H, W, R, S, stride, pad)
-    out_dtype = out_dtype or x.dtype
+    if w.dim() != 4 or w.shape[-1] != C or w.dtype != x.dtype:
+        raise ValueError("conv2d: w must be KRSC with x's channel count and dtype (x %s %s, w %s %s)"
+                         % (tuple(x.shape), x.dtype, tuple(w.shape), w.dtype))
+    out_dtype = out_dtype or (out.dtype if out is not None else x.dtype)
     if out is None:
         out = torch.empty((N, P, Q, K), dtype=out_dtype, device=x.device)
+    elif tuple(out.shape) != (N, P, Q, K) or out.dtype != out_dtype or not out.is_contiguous():
+        raise ValueError("conv2d: out must be a contiguous %s tensor of shape %s" % (out_dtype, (N, P, Q, K)))
     d = conv_desc(N, H, W, C, K, R, S, stride, pad, _dtype_code(x.dtype), _dtype_code(out_dtype))
     d.x_halo = 1 if x_halo else 0
     if sched is None:
         kv = R * 64 if (x_halo and S * C <= 64) else R * S * C
         g = gemm_desc(N * P * Q, K, kv, 1, _dtype_code(x.dtype), _dtype_code(out_dtype), B_NK)
         sched = choose_conv_schedule(g)
-    _check(load_library().alcop_conv2d(ctypes.byref(d), ctypes.byref(sched), ctypes.c_void_p(x.contiguous().data_ptr()),
-                                       ctypes.c_void_p(w.contiguous().data_ptr()), ctypes.c_void_p(out.data_ptr()),
+    # keep the contiguous operands alive across the launch: a temporary freed
+    # before the kernel runs could be reused by the other operand's copy
+    xc = x.contiguous()
+    wc = w.contiguous()
+    if stream is not None:  # the launch stream is not the one the allocator ties the copies to
+        xc.record_stream(stream)
+        wc.record_stream(stream)
+    _check(load_library().alcop_conv2d(ctypes.byref(d), ctypes.byref(sched), ctypes.c_void_p(xc.data_ptr()),
+                                       ctypes.c_void_p(wc.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                        _stream_ptr(stream)))
+    del xc, wc
     return out
 
 

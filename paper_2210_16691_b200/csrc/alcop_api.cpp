@@ -22,6 +22,23 @@ struct HostPipe {
   bool ready = false;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kBlocks] = {}, ev_out[kBlocks] = {};
+  // the previous call on this pipe: its kernels' completion (recorded on the
+  // caller's stream after its last block) and the host range its D2H writes
+  cudaEvent_t ev_kernels = nullptr;
+  bool have_prev = false;
+  const char* prev_c = nullptr;
+  int64_t prev_c_bytes = 0;
+  ~HostPipe() {
+    if (!ready) return;
+    // errors ignored: at process exit the runtime may already be unloading
+    for (cudaEvent_t ev : ev_in) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : ev_out) cudaEventDestroy(ev);
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_done);
+    cudaEventDestroy(ev_kernels);
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(d2h);
+  }
 };
 
 // Smallest A row block the host-buffer pipeline streams (bytes; 0: always 8
@@ -51,7 +68,8 @@ HostPipe* host_pipe() {
     bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
               cudaEventCreateWithFlags(&hp.ev_start, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&hp.ev_done, cudaEventDisableTiming) == cudaSuccess;
+              cudaEventCreateWithFlags(&hp.ev_done, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&hp.ev_kernels, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < HostPipe::kBlocks && ok; ++i)
       ok = cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&hp.ev_out[i], cudaEventDisableTiming) == cudaSuccess;
@@ -302,9 +320,26 @@ static int gemm_host_impl(const alcop_gemm_desc* w, const alcop_schedule* s, con
   HostPipe* hp = host_pipe();
   if (!hp) return set_error(ALCOP_ERR_CUDA, "CudaError", "could not create the copy streams");
   cudaError_t e = cudaSuccess;
-  if (sync) {  // earlier work on `stream` (it may still use the workspace) first
+  // Ordering of this call's H2D copies (they write the workspace and read hA/hB):
+  //  * sync: after all earlier work on `stream`;
+  //  * async: after the previous call's kernels (they may still read a shared
+  //    workspace; everything enqueued on `stream` before them is covered too)
+  //    and, when hA or hB overlaps the host range the previous call's D2H
+  //    writes (its C feeds this call), after that D2H.  Not after an
+  //    unrelated previous D2H: that overlap (H2D of call k+1 with the D2H of
+  //    call k on the other copy engine) is the point of the async variant.
+  const char* a0 = static_cast<const char*>(hA);
+  const char* b0 = static_cast<const char*>(hB);
+  auto overlaps = [&](const char* p, int64_t n) {
+    return hp->have_prev && p < hp->prev_c + hp->prev_c_bytes && hp->prev_c < p + n;
+  };
+  if (sync) {
     e = cudaEventRecord(hp->ev_start, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->h2d, hp->ev_start, 0);
+  } else if (hp->have_prev) {
+    e = cudaStreamWaitEvent(hp->h2d, hp->ev_kernels, 0);
+    if (e == cudaSuccess && (overlaps(a0, bytesA) || overlaps(b0, bytesB)))
+      e = cudaStreamWaitEvent(hp->h2d, hp->ev_done, 0);
   }
   if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, bytesB, cudaMemcpyHostToDevice, hp->h2d);
   for (int i = 0; i < nblk && e == cudaSuccess; ++i) {
@@ -331,6 +366,7 @@ static int gemm_host_impl(const alcop_gemm_desc* w, const alcop_schedule* s, con
     cudaStreamSynchronize(hp->h2d);
     return rc;
   }
+  if (e == cudaSuccess) e = cudaEventRecord(hp->ev_kernels, st);
   for (int i = 0; i < nblk && e == cudaSuccess; ++i) {
     const int64_t r0 = i * rows, nr = std::min(rows, w->M - r0);
     const int64_t off = nblk == 1 ? 0 : r0 * w->N * ob, len = nblk == 1 ? bytesC : nr * w->N * ob;
@@ -341,7 +377,13 @@ static int gemm_host_impl(const alcop_gemm_desc* w, const alcop_schedule* s, con
   if (e == cudaSuccess) e = cudaEventRecord(hp->ev_done, hp->d2h);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp->ev_done, 0);  // stream order for the caller
   if (e == cudaSuccess && sync) e = cudaEventSynchronize(hp->ev_done);
-  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    hp->have_prev = false;
+    return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  }
+  hp->have_prev = true;
+  hp->prev_c = static_cast<const char*>(hC);
+  hp->prev_c_bytes = bytesC;
   return ALCOP_OK;
 }
 

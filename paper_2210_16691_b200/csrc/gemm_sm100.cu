@@ -1627,6 +1627,8 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
     return set_error(ALCOP_ERR_CONFIG, "Unsupported", "stride <= 8 and padding/filter within TMA im2col range");
   if (s.tileK != 64 || s.n_stage_smem_A != s.n_stage_smem_B)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "conv needs tileK 64 and equal A/B stage counts");
+  if (s.cta_group != 1 || s.stream_k != 0)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the implicit-GEMM conv kernel runs with cta_group 1, whole tiles");
   const int64_t P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
   const int64_t Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");

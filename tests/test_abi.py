@@ -75,3 +75,48 @@ def test_host_entry_rejects_strided(alcop):
     dummy = ctypes.c_void_p(16)
     rc = lib.alcop_gemm_host(ctypes.byref(d), ctypes.byref(s), dummy, dummy, dummy, dummy, None)
     assert rc == alcop.ALCOP_ERR_CONFIG
+
+
+@pytest.mark.parametrize("cg,sk", [(2, 0), (2, 1), (1, 1)])
+def test_conv_rejects_pair_and_stream_k(alcop, cg, sk):
+    """the conv kernel is single-CTA with whole tiles; a
+    CTA-pair or stream-K schedule is rejected before any launch."""
+    lib = alcop.load_library()
+    d = alcop.conv_desc(2, 14, 14, 64, 128, 3, 3, (1, 1), (1, 1))
+    s = alcop.make_schedule(tileN=256, tileK=64, n_stage=4, cta_group=cg, stream_k=sk)
+    dummy = ctypes.c_void_p(256)
+    rc = lib.alcop_conv2d(ctypes.byref(d), ctypes.byref(s), dummy, dummy, dummy, None)
+    assert rc == alcop.ALCOP_ERR_CONFIG
+    assert lib.alcop_last_error().decode().startswith("BadSchedule")
+
+
+def test_pre_op_model_pick_is_valid(alcop):
+    """the model's pick for a pre-op GEMM comes from the space valid
+    for the pre-op kernel (cta_group 1, its shared-memory budget)."""
+    for shape in ((4096, 4096, 4096), (4096, 3072, 768), (4096, 768, 3072), (512, 512, 512)):
+        d = alcop.gemm_desc(*shape, pre_op=1)
+        s = alcop.choose_schedule(d)
+        assert s.cta_group == 1
+        alcop.validate(d, s)
+
+
+def test_matmul_checks_operands(alcop):
+    """shapes, dtypes and `out` are checked before the descriptor is
+    built (no silent out-of-bounds reads from a mismatched B)."""
+    torch = pytest.importorskip("torch")
+    A = torch.zeros(3, 64, 32, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="both be 2-D or both 3-D"):
+        alcop.matmul(A, torch.zeros(32, 16, dtype=torch.bfloat16))
+    with pytest.raises(ValueError, match="reduction sizes"):
+        alcop.matmul(A, torch.zeros(3, 48, 16, dtype=torch.bfloat16))
+    with pytest.raises(ValueError, match="batch sizes"):
+        alcop.matmul(A, torch.zeros(2, 32, 16, dtype=torch.bfloat16))
+    with pytest.raises(TypeError, match="dtypes differ"):
+        alcop.matmul(A, torch.zeros(3, 32, 16, dtype=torch.float16))
+    with pytest.raises(ValueError, match="out has shape"):
+        alcop.matmul(A, torch.zeros(3, 32, 16, dtype=torch.bfloat16), out=torch.zeros(3, 64, 8))
+    with pytest.raises(TypeError, match="out dtype"):
+        alcop.matmul(A, torch.zeros(3, 32, 16, dtype=torch.bfloat16), out=torch.zeros(3, 64, 16),
+                     out_dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="reduction sizes"):
+        alcop.matmul(A[0], torch.zeros(16, 48, dtype=torch.bfloat16), b_layout=alcop.B_NK)

@@ -273,6 +273,41 @@ def test_gemm_host_async_back_to_back_exact(alcop):
             C.zero_()
 
 
+def test_gemm_host_async_chain_shared_workspace_exact(alcop):
+    """alcop_gemm_host_async where call k's host C is call k+1's host A, all
+    calls sharing ONE workspace: call k+1's H2D must wait for call
+    k's kernels (workspace) and for its D2H (the host data).  B_k are
+    permutation matrices, so every C is exact in bf16 and the final C is A_0
+    with its columns permuted three times."""
+    import ctypes
+    lib = alcop.load_library()
+    st = torch.cuda.current_stream()
+    M, N = 24576, 768
+    a, _ = gemm_inputs(M, N, N, 1, seed=71)
+    rng = np.random.default_rng(3)
+    perms = [rng.permutation(N) for _ in range(3)]
+    hosts = [torch.from_numpy(a).to(torch.bfloat16).pin_memory()]
+    Bs = []
+    for p in perms:
+        b = np.zeros((N, N), dtype=np.float32)
+        b[p, np.arange(N)] = 1.0  # C[:, j] = A[:, p[j]]
+        Bs.append(torch.from_numpy(b).to(torch.bfloat16).pin_memory())
+        hosts.append(torch.full((M, N), -1.0, dtype=torch.bfloat16).pin_memory())
+    d = alcop.gemm_desc(M, N, N, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+    s = alcop.choose_schedule(d)
+    ws = torch.empty(lib.alcop_gemm_workspace_bytes(ctypes.byref(d)), dtype=torch.uint8, device="cuda")
+    for k in range(3):
+        rc = lib.alcop_gemm_host_async(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(hosts[k].data_ptr()),
+                                       ctypes.c_void_p(Bs[k].data_ptr()), ctypes.c_void_p(hosts[k + 1].data_ptr()),
+                                       ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(st.cuda_stream))
+        assert rc == 0, lib.alcop_last_error()
+    torch.cuda.synchronize()
+    want = a
+    for p in perms:
+        want = want[:, p]
+    assert torch.equal(hosts[3], torch.from_numpy(np.ascontiguousarray(want)).to(torch.bfloat16))
+
+
 @pytest.mark.parametrize("N,K,tileN,out", [(512, 64, 256, "bf16"), (512, 64, 128, "f32"), (384, 128, 192, "bf16"),
                                            (320, 64, 64, "f32")])
 def test_short_k_eight_epilogue_warps_exact(alcop, N, K, tileN, out):
