@@ -7,9 +7,15 @@ import pytest
 from tests import golden_util as G
 
 CASES = G.scripts()
+# The reference's ValidationError cases are its own lower() emitting a program
+# its validator rejects (a batched pre-op program whose A index drops the batch
+# dim; a register cache of a global tensor whose consumer already reads the
+# shared cache): lowering-IR defects, not schedule-surface decisions, and the
+# B200 path has no lowered IR.  They are excluded from the parity set.
+FUZZ = [c for c in G.scripts_fuzz() if c["result"].get("class") != "ValidationError"]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", CASES + FUZZ, ids=lambda c: c["name"])
 def test_script_matches_reference(alcop, case):
     desc = alcop.gemm_desc(case["M"], case["N"], case["K"], case["batch"], pre_op=case.get("preop", 0))
     res = case["result"]
