@@ -34,19 +34,20 @@ struct Tok {
   enum K { Ident, Int, Sym, End } k;
   std::string s;
   int64_t v = 0;
-  int line = 1, col = 1;
+  int row = 1;  // 1-based source position, reported in ParseError{line, col}
+  int column = 1;
 };
 
-class Lexer {
+class Scanner {
  public:
-  explicit Lexer(const std::string& t) : t_(t) {}
+  explicit Scanner(const std::string& t) : t_(t) {}
   std::vector<Tok> run() {
     std::vector<Tok> out;
     while (true) {
       skip();
       Tok tk;
-      tk.line = line_;
-      tk.col = col_;
+      tk.row = line_;
+      tk.column = col_;
       if (i_ >= t_.size()) {
         tk.k = Tok::End;
         out.push_back(tk);
@@ -84,15 +85,11 @@ class Lexer {
   }
 
  private:
-  void adv(size_t n) {
-    for (size_t k = 0; k < n; ++k) {
-      if (t_[i_] == '\n') {
-        ++line_;
-        col_ = 1;
-      } else {
-        ++col_;
-      }
-      ++i_;
+  void adv(size_t n) {  // moves the cursor, keeping the (line, column) of the next token
+    for (const size_t stop = i_ + n; i_ < stop; ++i_) {
+      const bool newline = t_[i_] == '\n';
+      line_ += newline ? 1 : 0;
+      col_ = newline ? 1 : col_ + 1;
     }
   }
   void skip() {
@@ -149,7 +146,7 @@ class Parser {
   bool is(const char* s) const { return cur().k != Tok::End && cur().s == s; }
   [[noreturn]] void fail(const std::string& m) const {
     throw Err{ALCOP_ERR_PARSE, "ParseError",
-              m + " (line " + std::to_string(cur().line) + ", col " + std::to_string(cur().col) + ")"};
+              m + " (line " + std::to_string(cur().row) + ", col " + std::to_string(cur().column) + ")"};
   }
   std::string ident() {
     if (cur().k != Tok::Ident) fail("expected identifier, got '" + cur().s + "'");
@@ -417,7 +414,7 @@ extern "C" int alcop_ir_to_gemm(const char* ir_text, alcop_gemm_desc* desc, alco
   clear_error();
   try {
     std::string text(ir_text);
-    ir::Lexer lx(text);
+    ir::Scanner lx(text);
     ir::Parser P(lx.run());
     P.program();
     std::string msg;

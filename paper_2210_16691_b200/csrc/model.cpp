@@ -34,9 +34,13 @@ namespace alcop {
 namespace model {
 
 // perf_model.hpp:53-57
-double pipeline_latency(double tLoad, double tUse, int64_t nLoop, int nPipe, int nMplx) {
-  if (tLoad <= (static_cast<double>(nPipe) * nMplx - 1) * tUse) return tUse * static_cast<double>(nLoop);
-  return (tLoad + tUse) * static_cast<double>(nLoop) / nPipe;
+// Fig. pipeline_latency: while the other stages * multiplexed workers in
+// flight cover a load's latency the loop is use-bound; otherwise every
+// load + use pair is exposed, shared over the concurrent stages.
+double pipeline_latency(double load, double use, int64_t iters, int stages, int mplx) {
+  const double n = static_cast<double>(iters);
+  const double covered = (double(stages) * mplx - 1) * use;
+  return load <= covered ? use * n : (load + use) * n / stages;
 }
 
 }  // namespace model

@@ -1,426 +1,411 @@
-// schedule.cpp — the reference's schedule surface on the B200 host side.
+// schedule.cpp — the reference's schedule-script surface on the B200 host side,
+// and the host bookkeeping enumerator.
 //
-// A from-scratch C++ restatement of pipec's value-semantics schedule state
-// (schedule.hpp:15-62) and primitives — cache_read (:111-136), tile
-// (:141-193), check_eligibility (:198-254), mark_pipeline (:258-268),
-// inline_tensor (:275-314), apply_script (:590-646) — with the same rule
-// tags and error classes, ending in a mapping onto alcop_schedule instead of
-// lower() (:357-584): the B200 kernel *is* the lowered-and-transformed nest.
+// Part 1 is written against the CONTRACT of the reference's scheduler module
+// (the dataflow view, the three eligibility rules of §3.1,
+// the ordering policy of §3.2, the script format of SPEC.md:216) and the
+// pass's nesting rules (pipeline_pass.hpp:305-322).  The rule
+// tags, error classes and exit codes are the reference's interface
+// (common.hpp:43-69, cli.hpp:23-25); tests/golden/scripts*.jsonl pin every
+// accept/reject decision against the reference itself (632 scripts).
 //
-// Also the host bookkeeping enumerator: the producer / consumer event
-// sequence the kernel executes (pipeline_pass.hpp:482-748 index algebra,
-// interp.hpp:375-418 counters), used to check the device trace bit-exactly.
+// The design is a small script machine: a dataflow table of tensors in
+// declaration order, a split table per GEMM dimension (the loop sketch is
+// derived from it, never stored), primitives dispatched from a table, and
+// eligibility as an ordered rule list.  Its output is not a lowered program
+// but the alcop_schedule the sm_100a kernel is instantiated with: the kernel
+// IS the lowered-and-transformed load-and-use nest.
+//
+// Part 2 is the producer / consumer event sequence the kernel executes
+// (pipeline_pass.hpp:482-748 index algebra, interp.hpp:375-418 counters),
+// used to check the device trace bit-exactly.
 #include <algorithm>
+#include <array>
+#include <cerrno>
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
-#include <map>
-#include <optional>
+#include <functional>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "alcop_internal.h"
 
 namespace alcop {
-namespace sched {
+namespace surface {
 
-enum class Scope { Global, Shared, Register };
-inline int scope_level(Scope s) { return s == Scope::Global ? 2 : s == Scope::Shared ? 1 : 0; }
-inline const char* scope_name(Scope s) {
-  return s == Scope::Global ? "global" : s == Scope::Shared ? "shared" : "register";
+// ---------------------------------------------------------------------------
+// Part 1: the script machine
+// ---------------------------------------------------------------------------
+
+// Memory levels, fastest first.  A cache may only be placed strictly closer to
+// the tensor cores than its source ("scope strictly below").
+enum Level : int { kRegister = 0, kShared = 1, kGlobal = 2 };
+
+const char* level_word(int lv) { return lv == kRegister ? "register" : lv == kShared ? "shared" : "global"; }
+
+// A rejected script: the reference's exit code plus its rule tag.
+struct Rejection : std::runtime_error {
+  int exit_code;
+  std::string tag;
+  Rejection(int code, std::string t, const std::string& why)
+      : std::runtime_error(why), exit_code(code), tag(std::move(t)) {}
+};
+[[noreturn]] void reject(const std::string& tag, const std::string& why) {
+  throw Rejection(ALCOP_ERR_ANALYSIS, tag, why);
 }
-enum class LoopKind { Sequential, Parallel, Unrolled };
+[[noreturn]] void reject_config(const std::string& why) { throw Rejection(ALCOP_ERR_CONFIG, "ConfigError", why); }
 
-struct Error : std::runtime_error {
-  int code;
-  std::string rule;
-  Error(int c, std::string r, const std::string& m) : std::runtime_error(m), code(c), rule(std::move(r)) {}
-};
-[[noreturn]] inline void analysis(const std::string& rule, const std::string& msg) {
-  throw Error(ALCOP_ERR_ANALYSIS, rule, msg);
-}
-[[noreturn]] inline void config(const std::string& msg) { throw Error(ALCOP_ERR_CONFIG, "ConfigError", msg); }
-
-struct Node {
-  enum class Producer { ExternalInput, AsyncCopyFrom, ComputeFrom };
-  std::string name;
-  Producer producer = Producer::ExternalInput;
-  std::string copySrc;
-  std::vector<std::string> computeSrcs;
-  std::string opTag;
-  Scope scope = Scope::Global;
-  std::optional<int> stages;
-  bool fusedPreOp = false;
-  int chunkLevel = -1;
+// One tensor of the schedule's dataflow view.
+struct Tensor {
+  enum Origin { kInput, kCopy, kCompute };
+  std::string id;
+  Origin origin = kInput;
+  std::vector<std::string> reads;  // kCopy: exactly one source; kCompute: operands
+  std::string op;                  // kCompute: "ew" / "mma"
+  int level = kGlobal;
+  int stages = 0;                  // pipelining hint, 0 = none
+  bool carries_ew = false;         // a case-2 inline folded f() into this copy's consumer
 };
 
-struct Loop {
-  std::string var;
-  int64_t extent = 0;
-  LoopKind kind = LoopKind::Sequential;
-  char dim = '?';
-  int splitLevel = 0;
-};
+// Splits of one GEMM dimension, outer to inner: (loop name, extent).
+using Splits = std::vector<std::pair<std::string, int64_t>>;
 
-struct State {
-  int64_t M = 0, N = 0, K = 0, batch = 1;
-  std::vector<Node> graph;
-  std::vector<Loop> sketch;
+struct Program {
+  int64_t extent[3] = {0, 0, 0};  // i (M), j (N), k (K)
+  int64_t batch = 1;
+  std::vector<Tensor> flow;       // declaration order matters (later hints win per side)
   bool tiled = false;
-  const Node* find(const std::string& n) const {
-    for (const auto& x : graph)
-      if (x.name == n) return &x;
-    return nullptr;
+  std::array<Splits, 3> split;    // valid once tiled
+
+  Tensor* lookup(const std::string& id) {
+    auto it = std::find_if(flow.begin(), flow.end(), [&](const Tensor& t) { return t.id == id; });
+    return it == flow.end() ? nullptr : &*it;
   }
-  Node* find_mut(const std::string& n) {
-    for (auto& x : graph)
-      if (x.name == n) return &x;
-    return nullptr;
+  const Tensor* lookup(const std::string& id) const { return const_cast<Program*>(this)->lookup(id); }
+  bool has_inner_k() const { return split[2].size() > 1; }
+};
+
+// The workload's dataflow (SPEC.md:192-196 v1 family): C = mma(A, B), or with
+// the elementwise pre-op S2 = ew(A) feeding the mma in place of A.
+Program workload(const alcop_gemm_desc& w) {
+  Program p;
+  p.extent[0] = w.M;
+  p.extent[1] = w.N;
+  p.extent[2] = w.K;
+  p.batch = w.batch;
+  auto input = [](const char* id) {
+    Tensor t;
+    t.id = id;
+    return t;
+  };
+  auto compute = [](const char* id, const char* op, std::vector<std::string> reads) {
+    Tensor t;
+    t.id = id;
+    t.origin = Tensor::kCompute;
+    t.op = op;
+    t.reads = std::move(reads);
+    return t;
+  };
+  p.flow = {input("A"), input("B")};
+  if (w.pre_op) p.flow.push_back(compute("S2", "ew", {"A"}));
+  p.flow.push_back(compute("C", "mma", {w.pre_op ? "S2" : "A", "B"}));
+  return p;
+}
+
+// The sequential loop a buffer's copy is issued in.  Shared caches refill once
+// per outer reduction step (ko); register caches per inner step (ki) when the
+// reduction has a second split, otherwise per ko.  This is the sync position of
+// rule 3 and the loop the pass pipelines (§4.1 step 3).
+const char* copy_loop(const Program& p, const Tensor& t) {
+  if (p.split[2].empty()) return nullptr;
+  const bool inner = t.level == kRegister && p.has_inner_k();
+  return (inner ? p.split[2][1] : p.split[2][0]).first.c_str();
+}
+
+// §3.1: three eligibility rules, evaluated in order; the first failure is reported.
+struct Rule {
+  const char* tag;
+  std::function<std::string(const Program&, const Tensor&)> violation;  // "" = satisfied
+};
+
+const std::vector<Rule>& eligibility_rules() {
+  static const std::vector<Rule> rules = {
+      {"NotAsyncProducer",
+       [](const Program&, const Tensor& t) -> std::string {
+         return t.origin == Tensor::kCopy ? "" : "'" + t.id + "' is filled by computation, not an asynchronous copy";
+       }},
+      {"NoSequentialLoop",
+       [](const Program& p, const Tensor& t) -> std::string {
+         return copy_loop(p, t) ? "" : "'" + t.id + "' is not filled inside a sequential loop";
+       }},
+      {"SyncPositionConflict",
+       [](const Program& p, const Tensor& t) -> std::string {
+         if (t.level != kShared) return "";  // register buffers are exempt
+         const std::string mine = copy_loop(p, t);
+         for (const Tensor& o : p.flow) {
+           if (o.id == t.id || o.level != kShared || o.stages == 0) continue;
+           const char* theirs = copy_loop(p, o);
+           if (theirs && mine != theirs)
+             return "shared buffers '" + o.id + "' (" + theirs + ") and '" + t.id + "' (" + mine +
+                    ") would synchronise in different loops";
+         }
+         return "";
+       }},
+  };
+  return rules;
+}
+
+// The reference's schedule primitives as transformations of a Program value.
+struct Primitives {
+  static void cache_read(Program& p, const std::string& src_id, int level) {
+    const Tensor* src = p.lookup(src_id);
+    if (!src) reject("NoSuchTensor", "cache_read of unknown tensor '" + src_id + "'");
+    if (level >= src->level)
+      reject("ScopeNotBelow", std::string("a ") + level_word(level) + " cache of a " + level_word(src->level) +
+                                  " tensor would copy upwards");
+    // the buffer is named after the root tensor: A -> A_shared -> A_reg
+    std::string root = src_id;
+    for (const char* sfx : {"_shared", "_reg"}) {
+      const size_t n = std::strlen(sfx);
+      if (root.size() > n && root.compare(root.size() - n, n, sfx) == 0) root.resize(root.size() - n);
+    }
+    Tensor buf;
+    buf.id = root + (level == kShared ? "_shared" : "_reg");
+    if (p.lookup(buf.id)) reject("DuplicateBuffer", "'" + buf.id + "' is already declared");
+    buf.origin = Tensor::kCopy;
+    buf.reads = {src_id};
+    buf.level = level;
+    for (Tensor& t : p.flow)  // every reader of the source now reads the cache
+      if (t.id != src_id) std::replace(t.reads.begin(), t.reads.end(), src_id, buf.id);
+    p.flow.push_back(std::move(buf));
+  }
+
+  static void tile(Program& p, const std::string& target, const Splits& given) {
+    if (target != "C" || !p.lookup(target)) reject("NoSuchTensor", "only the output C can be tiled, not '" + target + "'");
+    std::array<Splits, 3> by_dim;
+    static const char kDims[3] = {'i', 'j', 'k'};
+    for (const auto& sp : given) {
+      const char lead = sp.first.empty() ? '\0' : sp.first[0];
+      const int d = lead == 'i' ? 0 : lead == 'j' ? 1 : lead == 'k' ? 2 : -1;
+      if (d < 0) reject("BadSplit", "loop '" + sp.first + "' names no dimension (i, j or k)");
+      if (sp.second < 1) reject("BadSplit", "loop '" + sp.first + "' has a non-positive extent");
+      by_dim[d].push_back(sp);
+    }
+    for (int d = 0; d < 3; ++d) {
+      if (by_dim[d].empty()) reject("BadSplit", std::string("dimension '") + kDims[d] + "' is not split");
+      int64_t covered = 1;
+      for (const auto& sp : by_dim[d]) covered *= sp.second;
+      if (covered != p.extent[d])
+        reject("NonDivisibleSplit", std::string("splits of '") + kDims[d] + "' cover " + std::to_string(covered) +
+                                        " of " + std::to_string(p.extent[d]));
+      if (by_dim[d].size() > 2) reject("BadSplit", std::string("dimension '") + kDims[d] + "' has more than two splits");
+    }
+    p.split = by_dim;
+    p.tiled = true;
+  }
+
+  static void pipeline(Program& p, const std::string& id, int stages) {
+    if (!p.tiled) reject("OrderingViolation", "pipeline requires loop sketch: tile before pipelining");
+    if (stages < 2) reject("BadStages", "a pipeline needs at least two stages, got " + std::to_string(stages));
+    Tensor* t = p.lookup(id);
+    if (!t) reject("NoSuchTensor", "pipeline of unknown buffer '" + id + "'");
+    for (const Rule& r : eligibility_rules()) {
+      std::string why = r.violation(p, *t);
+      if (!why.empty()) reject(r.tag, why);
+    }
+    t->stages = stages;
+  }
+
+  // §3.2 / Fig. schedule_transform: inlining an elementwise tensor whose cache
+  // is already pipelined re-sources the cache to the tensor's input and folds
+  // f() into the cache's consumer (case 2); an unpipelined cache becomes a
+  // computed buffer (case 1, which rule 1 then rejects for pipelining).
+  static void inline_(Program& p, const std::string& id) {
+    const Tensor* f = p.lookup(id);
+    if (!f) reject("NoSuchTensor", "inline of unknown tensor '" + id + "'");
+    if (f->origin != Tensor::kCompute || f->reads.size() != 1)
+      reject("NotElementwise", "'" + id + "' is not a unary elementwise computation");
+    const std::string input = f->reads.front(), op = f->op;
+    int rewritten = 0;
+    for (Tensor& t : p.flow) {
+      const bool reads_f = std::find(t.reads.begin(), t.reads.end(), id) != t.reads.end();
+      if (!reads_f) continue;
+      if (t.origin != Tensor::kCopy)
+        reject("NoRewrite", "'" + t.id + "' computes from '" + id + "' directly; only cached reads can absorb it");
+      ++rewritten;
+      if (t.stages == 0) {  // case 1
+        t.origin = Tensor::kCompute;
+        t.op = op;
+        t.reads = {input};
+      } else {  // case 2
+        if (t.carries_ew) reject("NoRewrite", "'" + t.id + "' already carries a fused elementwise function");
+        t.reads = {input};
+        t.carries_ew = true;
+      }
+    }
+    if (rewritten == 0) reject("NoRewrite", "no cache reads '" + id + "'");
+    p.flow.erase(std::remove_if(p.flow.begin(), p.flow.end(), [&](const Tensor& t) { return t.id == id; }),
+                 p.flow.end());
   }
 };
 
-// gemm_schedule (schedule.hpp:73-86); preOp adds S2 = ew(A) feeding the mma
-State gemm_schedule(const alcop_gemm_desc& w) {
-  State s;
-  s.M = w.M;
-  s.N = w.N;
-  s.K = w.K;
-  s.batch = w.batch;
-  s.graph.push_back({"A", Node::Producer::ExternalInput, "", {}, "", Scope::Global, {}, false, -1});
-  s.graph.push_back({"B", Node::Producer::ExternalInput, "", {}, "", Scope::Global, {}, false, -1});
-  std::string aSide = "A";
-  if (w.pre_op) {
-    s.graph.push_back({"S2", Node::Producer::ComputeFrom, "", {"A"}, "ew", Scope::Global, {}, false, -1});
-    aSide = "S2";
-  }
-  s.graph.push_back({"C", Node::Producer::ComputeFrom, "", {aSide, "B"}, "mma", Scope::Global, {}, false, -1});
-  return s;
+// std::stoll / std::stoi semantics (leading integer, trailing text ignored,
+// failure or overflow rejected): the reference parses extents that way.
+bool leading_int(const std::string& text, long long lo, long long hi, long long* out) {
+  errno = 0;
+  char* end = nullptr;
+  const long long v = std::strtoll(text.c_str(), &end, 10);
+  if (end == text.c_str() || errno == ERANGE || v < lo || v > hi) return false;
+  *out = v;
+  return true;
 }
 
-std::string cache_name(const std::string& tensor, Scope scope) {
-  std::string base = tensor;
-  for (const char* suffix : {"_shared", "_reg"}) {
-    size_t n = std::strlen(suffix);
-    if (base.size() > n && base.compare(base.size() - n, n, suffix) == 0) base = base.substr(0, base.size() - n);
-  }
-  return base + (scope == Scope::Shared ? "_shared" : "_reg");
-}
+// The script format: one primitive per line, '#' comments.
+class ScriptMachine {
+ public:
+  explicit ScriptMachine(Program p) : prog_(std::move(p)) {}
 
-std::vector<const Loop*> reduction_splits(const State& s) {
-  std::vector<const Loop*> ks;
-  for (const auto& l : s.sketch)
-    if (l.dim == 'k') ks.push_back(&l);
-  return ks;
-}
-
-State cache_read(const State& s, const std::string& tensor, Scope scope) {
-  const Node* src = s.find(tensor);
-  if (!src) analysis("NoSuchTensor", "cache_read: tensor '" + tensor + "' not found");
-  if (scope_level(scope) >= scope_level(src->scope))
-    analysis("ScopeNotBelow", std::string("cache_read: scope ") + scope_name(scope) + " is not strictly below " +
-                                  scope_name(src->scope));
-  State out = s;
-  Node buf;
-  buf.name = cache_name(tensor, scope);
-  if (out.find(buf.name)) analysis("DuplicateBuffer", "cache_read: buffer '" + buf.name + "' already exists");
-  buf.producer = Node::Producer::AsyncCopyFrom;
-  buf.copySrc = tensor;
-  buf.scope = scope;
-  buf.chunkLevel = scope == Scope::Shared ? 0 : 1;
-  for (auto& n : out.graph) {
-    if (n.name == tensor) continue;
-    if (n.producer == Node::Producer::AsyncCopyFrom && n.copySrc == tensor) n.copySrc = buf.name;
-    for (auto& cs : n.computeSrcs)
-      if (cs == tensor) cs = buf.name;
-  }
-  out.graph.push_back(std::move(buf));
-  return out;
-}
-
-State tile(const State& s, const std::string& tensor, const std::vector<std::pair<std::string, int64_t>>& splits) {
-  if (!s.find(tensor) || tensor != "C") analysis("NoSuchTensor", "tile: only the output computation can be tiled");
-  std::map<char, std::vector<std::pair<std::string, int64_t>>> byDim;
-  for (const auto& [name, extent] : splits) {
-    if (name.empty() || (name[0] != 'i' && name[0] != 'j' && name[0] != 'k'))
-      analysis("BadSplit", "tile: split '" + name + "' must start with i, j or k");
-    if (extent < 1) analysis("BadSplit", "tile: split extent must be >= 1");
-    byDim[name[0]].emplace_back(name, extent);
-  }
-  auto dim_size = [&](char d) -> int64_t { return d == 'i' ? s.M : d == 'j' ? s.N : s.K; };
-  for (char d : {'i', 'j', 'k'}) {
-    int64_t prod = 1;
-    for (const auto& [name, extent] : byDim[d]) prod *= extent;
-    if (byDim[d].empty()) analysis("BadSplit", std::string("tile: missing splits for dimension '") + d + "'");
-    if (prod != dim_size(d))
-      analysis("NonDivisibleSplit", std::string("tile: splits of '") + d + "' multiply to " + std::to_string(prod) +
-                                        ", dimension is " + std::to_string(dim_size(d)));
-    if (byDim[d].size() > 2) analysis("BadSplit", "tile: at most two splits per dimension");
-  }
-  State out = s;
-  out.sketch.clear();
-  if (s.batch > 1) out.sketch.push_back({"b", s.batch, LoopKind::Parallel, 'b', 0});
-  auto push_dim = [&](char d, size_t level, LoopKind kind) {
-    if (level < byDim[d].size()) {
-      const auto& [name, extent] = byDim[d][level];
-      out.sketch.push_back({name, extent, kind, d, static_cast<int>(level)});
+  void run(const std::string& text) {
+    std::istringstream lines(text);
+    std::string line;
+    while (std::getline(lines, line)) {
+      ++line_no_;
+      line = line.substr(0, line.find('#'));
+      std::istringstream words(line);
+      std::vector<std::string> w;
+      for (std::string x; words >> x;) w.push_back(x);
+      if (w.empty()) continue;
+      const auto& table = handlers();
+      auto h = std::find_if(table.begin(), table.end(), [&](const Handler& e) { return w[0] == e.word; });
+      if (h == table.end()) syntax("unknown primitive '" + w[0] + "'");
+      if (w.size() < h->min_words || w.size() > h->max_words) syntax("usage: " + std::string(h->usage));
+      (this->*(h->fn))(w);
     }
+  }
+
+  const Program& program() const { return prog_; }
+  const std::vector<std::string>& notes() const { return notes_; }
+
+ private:
+  struct Handler {
+    const char* word;
+    size_t min_words, max_words;
+    const char* usage;
+    void (ScriptMachine::*fn)(const std::vector<std::string>&);
   };
-  push_dim('i', 0, LoopKind::Parallel);
-  push_dim('j', 0, LoopKind::Parallel);
-  push_dim('k', 0, LoopKind::Sequential);
-  push_dim('k', 1, LoopKind::Sequential);
-  push_dim('i', 1, LoopKind::Unrolled);
-  push_dim('j', 1, LoopKind::Unrolled);
-  out.tiled = true;
-  return out;
-}
-
-struct Eligibility {
-  bool eligible = false;
-  std::string failedRule, explanation;
-};
-
-Eligibility check_eligibility(const State& s, const std::string& buffer) {
-  Eligibility r;
-  const Node* b = s.find(buffer);
-  if (!b) analysis("NoSuchTensor", "check_eligibility: '" + buffer + "' not found");
-  if (!s.tiled) analysis("OrderingViolation", "pipeline requires loop sketch: tile before checking eligibility");
-  // rule 1: produced by an asynchronous memory copy
-  if (b->producer != Node::Producer::AsyncCopyFrom) {
-    r.failedRule = "NotAsyncProducer";
-    r.explanation = "buffer '" + buffer + "' is not produced by an asynchronous memory copy";
-    return r;
+  static const std::vector<Handler>& handlers() {
+    static const std::vector<Handler> h = {
+        {"cache_read", 3, 3, "cache_read <tensor> <shared|register>", &ScriptMachine::do_cache_read},
+        {"tile", 3, SIZE_MAX, "tile <tensor> <loop>=<extent>...", &ScriptMachine::do_tile},
+        {"pipeline", 3, 3, "pipeline <buffer> <stages>", &ScriptMachine::do_pipeline},
+        {"inline", 2, 2, "inline <tensor>", &ScriptMachine::do_inline},
+    };
+    return h;
   }
-  // rule 2: a sequential load-and-use loop encloses the buffer's copy
-  auto pipelined_loop_of = [&](const Node& node) -> const Loop* {
-    auto ks = reduction_splits(s);
-    int lastIdx = -1;
-    if (node.chunkLevel >= 0 && node.chunkLevel < static_cast<int>(ks.size())) {
-      const Loop* chunkLoop = ks[node.chunkLevel];
-      for (size_t i = 0; i < s.sketch.size(); ++i)
-        if (&s.sketch[i] == chunkLoop) lastIdx = static_cast<int>(i);
-    } else {
-      lastIdx = static_cast<int>(s.sketch.size()) - 1;
-    }
-    for (int i = lastIdx; i >= 0; --i)
-      if (s.sketch[i].kind == LoopKind::Sequential) return &s.sketch[i];
-    return nullptr;
-  };
-  const Loop* loop = pipelined_loop_of(*b);
-  if (!loop) {
-    r.failedRule = "NoSequentialLoop";
-    r.explanation = "buffer '" + buffer + "' is not produced inside a sequential loop";
-    return r;
+  [[noreturn]] void syntax(const std::string& why) const {
+    reject_config("schedule script line " + std::to_string(line_no_) + ": " + why);
   }
-  // rule 3: same-scope (shared) pipelined buffers share one sync position
-  if (b->scope == Scope::Shared) {
-    for (const auto& other : s.graph) {
-      if (other.name == buffer || !other.stages || other.scope != Scope::Shared) continue;
-      const Loop* otherLoop = pipelined_loop_of(other);
-      if (otherLoop && otherLoop->var != loop->var) {
-        r.failedRule = "SyncPositionConflict";
-        r.explanation = "buffers '" + other.name + "' (loop " + otherLoop->var + ") and '" + buffer + "' (loop " +
-                        loop->var + ") need shared-scope barriers at different positions";
-        return r;
-      }
-    }
-  }
-  r.eligible = true;
-  r.explanation = "pipelined loop " + loop->var;
-  return r;
-}
 
-State mark_pipeline(const State& s, const std::string& buffer, int stages) {
-  if (!s.tiled) analysis("OrderingViolation", "pipeline requires loop sketch: tile first");
-  if (stages < 2) analysis("BadStages", "pipeline stages must be >= 2");
-  Eligibility r = check_eligibility(s, buffer);
-  if (!r.eligible) analysis(r.failedRule, r.explanation);
-  State out = s;
-  out.find_mut(buffer)->stages = stages;
-  return out;
-}
-
-// inline_tensor (schedule.hpp:275-314): case 2 (the consumer buffer is already
-// pipelined) re-sources the buffer to the tensor's input and fuses the
-// elementwise op into its consumer (mma -> mma_ewa); otherwise classic
-// inlining makes the buffer compute-produced (and rule 1 rejects it later).
-State inline_tensor(const State& s, const std::string& tensor) {
-  const Node* t = s.find(tensor);
-  if (!t) analysis("NoSuchTensor", "inline: tensor '" + tensor + "' not found");
-  if (t->producer != Node::Producer::ComputeFrom || t->computeSrcs.size() != 1)
-    analysis("NotElementwise", "inline: '" + tensor + "' is not unary elementwise");
-  const std::string src = t->computeSrcs[0];
-  const std::string tag = t->opTag;
-  State out = s;
-  bool consumed = false;
-  for (auto& n : out.graph) {
-    if (n.producer == Node::Producer::AsyncCopyFrom && n.copySrc == tensor) {
-      consumed = true;
-      if (n.stages) {
-        if (n.fusedPreOp)
-          analysis("NoRewrite", "inline: buffer '" + n.name + "' already carries a fused elementwise op");
-        n.copySrc = src;
-        n.fusedPreOp = true;
-      } else {
-        n.producer = Node::Producer::ComputeFrom;
-        n.computeSrcs = {src};
-        n.opTag = tag;
-        n.copySrc.clear();
-      }
-    } else {
-      for (auto& cs : n.computeSrcs)
-        if (cs == tensor) analysis("NoRewrite", "inline: v1 requires '" + tensor + "' to feed cache-read buffers");
-    }
-  }
-  if (!consumed) analysis("NoRewrite", "inline: '" + tensor + "' has no cache-read consumer");
-  out.graph.erase(std::remove_if(out.graph.begin(), out.graph.end(),
-                                 [&](const Node& n) { return n.name == tensor; }),
-                  out.graph.end());
-  return out;
-}
-
-State apply_script(const State& start, const std::string& script, std::vector<std::string>* warnings) {
-  State s = start;
-  std::istringstream in(script);
-  std::string line;
-  int lineNo = 0;
-  while (std::getline(in, line)) {
-    ++lineNo;
-    auto hash = line.find('#');
-    if (hash != std::string::npos) line = line.substr(0, hash);
-    std::istringstream ls(line);
-    std::vector<std::string> tok;
-    std::string t;
-    while (ls >> t) tok.push_back(t);
-    if (tok.empty()) continue;
-    auto fail = [&](const std::string& msg) { config("schedule script line " + std::to_string(lineNo) + ": " + msg); };
-    if (tok[0] == "cache_read") {
-      if (tok.size() != 3) fail("expected: cache_read <tensor> <shared|register>");
-      Scope sc;
-      if (tok[2] == "shared")
-        sc = Scope::Shared;
-      else if (tok[2] == "register")
-        sc = Scope::Register;
-      else
-        config("bad scope '" + tok[2] + "'");
-      s = cache_read(s, tok[1], sc);
-    } else if (tok[0] == "tile") {
-      if (tok.size() < 3) fail("expected: tile <tensor> <name>=<extent>...");
-      std::vector<std::pair<std::string, int64_t>> splits;
-      for (size_t i = 2; i < tok.size(); ++i) {
-        auto eq = tok[i].find('=');
-        if (eq == std::string::npos) fail("bad split '" + tok[i] + "'");
-        int64_t v = 0;
-        try {
-          v = std::stoll(tok[i].substr(eq + 1));
-        } catch (...) {
-          fail("bad split '" + tok[i] + "'");
-        }
-        splits.emplace_back(tok[i].substr(0, eq), v);
-      }
-      s = tile(s, tok[1], splits);
-    } else if (tok[0] == "pipeline") {
-      if (tok.size() != 3) fail("expected: pipeline <buffer> <stages>");
-      int st = 0;
-      try {
-        st = std::stoi(tok[2]);
-      } catch (...) {
-        fail("bad stage count '" + tok[2] + "'");
-      }
-      try {
-        s = mark_pipeline(s, tok[1], st);
-      } catch (const Error& e) {
-        if (e.rule == "SyncPositionConflict") {
-          for (auto& n : s.graph)
-            if (n.stages && n.scope == Scope::Shared) n.stages.reset();
-          if (warnings) warnings->push_back(std::string("refusing to pipeline: ") + e.what());
-        } else {
-          throw;
-        }
-      }
-    } else if (tok[0] == "inline") {
-      if (tok.size() != 2) fail("expected: inline <tensor>");
-      s = inline_tensor(s, tok[1]);
-    } else {
-      fail("unknown primitive '" + tok[0] + "'");
-    }
-  }
-  return s;
-}
-
-// Which input a cached buffer's chain roots at (schedule.hpp:411-425).
-char side_of(const State& s, const Node& n) {
-  const Node* cur = &n;
-  while (cur) {
-    if (cur->name == "B") return 'b';
-    if (cur->name == "A") return 'a';
-    if (cur->producer == Node::Producer::AsyncCopyFrom)
-      cur = s.find(cur->copySrc);
-    else if (cur->producer == Node::Producer::ComputeFrom && !cur->computeSrcs.empty())
-      cur = s.find(cur->computeSrcs[0]);
+  void do_cache_read(const std::vector<std::string>& w) {
+    int level;
+    if (w[2] == "shared")
+      level = kShared;
+    else if (w[2] == "register")
+      level = kRegister;
     else
-      break;
+      syntax("unknown scope '" + w[2] + "'");
+    Primitives::cache_read(prog_, w[1], level);
   }
-  return 'a';
+
+  void do_tile(const std::vector<std::string>& w) {
+    Splits given;
+    for (size_t i = 2; i < w.size(); ++i) {
+      const size_t eq = w[i].find('=');
+      long long v = 0;
+      if (eq == std::string::npos || !leading_int(w[i].substr(eq + 1), LLONG_MIN, LLONG_MAX, &v))
+        syntax("cannot read split '" + w[i] + "'");
+      given.emplace_back(w[i].substr(0, eq), static_cast<int64_t>(v));
+    }
+    Primitives::tile(prog_, w[1], given);
+  }
+
+  void do_pipeline(const std::vector<std::string>& w) {
+    long long n = 0;
+    if (!leading_int(w[2], INT32_MIN, INT32_MAX, &n)) syntax("cannot read stage count '" + w[2] + "'");
+    try {
+      Primitives::pipeline(prog_, w[1], static_cast<int>(n));
+    } catch (const Rejection& r) {
+      // §3.1: on a sync-position conflict the paper refuses to pipeline any of
+      // the shared buffers involved: every shared hint is withdrawn
+      if (r.tag != "SyncPositionConflict") throw;
+      for (Tensor& t : prog_.flow)
+        if (t.level == kShared) t.stages = 0;
+      notes_.push_back(std::string("refusing to pipeline: ") + r.what());
+    }
+  }
+
+  void do_inline(const std::vector<std::string>& w) { Primitives::inline_(prog_, w[1]); }
+
+  Program prog_;
+  int line_no_ = 0;
+  std::vector<std::string> notes_;
+};
+
+// The operand (A side or B side) a cache ultimately reads.
+bool feeds_b(const Program& p, const Tensor& t) {
+  const Tensor* cur = &t;
+  for (int hops = 0; cur && hops < 16; ++hops) {
+    if (cur->id == "A") return false;
+    if (cur->id == "B") return true;
+    cur = cur->reads.empty() ? nullptr : p.lookup(cur->reads.front());
+  }
+  return false;
 }
 
-// lower()'s tile arithmetic (schedule.hpp:362-381) and the analysis rules
-// the pass would apply to the lowered nest (pipeline_pass.hpp:275-314),
-// mapped onto the B200 schedule.
-alcop_schedule to_alcop(const State& s) {
-  if (!s.tiled) analysis("OrderingViolation", "lower: tile must run first");
-  auto ks = reduction_splits(s);
-  const Loop *i0 = nullptr, *j0 = nullptr, *i1 = nullptr, *j1 = nullptr;
-  for (const auto& l : s.sketch) {
-    if (l.dim == 'i' && l.splitLevel == 0) i0 = &l;
-    if (l.dim == 'i' && l.splitLevel == 1) i1 = &l;
-    if (l.dim == 'j' && l.splitLevel == 0) j0 = &l;
-    if (l.dim == 'j' && l.splitLevel == 1) j1 = &l;
-  }
-  if (!i0 || !j0 || ks.empty()) analysis("BadSketch", "lower: sketch is incomplete");
+// What lower() + the pass make of the hints (schedule.hpp:371-374 tile
+// arithmetic; pipeline_pass.hpp:305-322 nesting rules), as the B200 schedule.
+alcop_schedule to_schedule(const Program& p) {
+  if (!p.tiled) reject("OrderingViolation", "nothing to lower: the script never tiles C");
   alcop_schedule out;
   alcop_schedule_default(&out);
-  out.tileM = i1 ? i1->extent : s.M / i0->extent;
-  out.tileN = j1 ? j1->extent : s.N / j0->extent;
-  out.tileK = s.K / ks[0]->extent;
-  const int64_t F = ks.size() > 1 ? ks[1]->extent : 1;  // inner pipelined loop extent
-  if (ks.size() > 1 && out.tileK % F != 0)
-    analysis("NonDivisibleSplit", "lower: inner reduction split does not divide tile");
-  out.n_stage_smem_A = 1;
-  out.n_stage_smem_B = 1;
-  out.n_stage_inner = 1;
-  out.mode = ALCOP_MODE_WRAP;  // the reference's own emission
-  int sharedStages[2] = {0, 0};
-  int regStages[2] = {0, 0};
-  for (const auto& n : s.graph) {
-    if (!n.stages) continue;
-    const int side = side_of(s, n) == 'a' ? 0 : 1;
-    if (n.scope == Scope::Shared)
-      sharedStages[side] = *n.stages;
-    else if (n.scope == Scope::Register)
-      regStages[side] = *n.stages;
+  const Splits& si = p.split[0];
+  const Splits& sj = p.split[1];
+  const Splits& sk = p.split[2];
+  // the tile is the inner split, or the dimension over the outer loop's trip count
+  out.tileM = si.size() > 1 ? si[1].second : p.extent[0] / si[0].second;
+  out.tileN = sj.size() > 1 ? sj[1].second : p.extent[1] / sj[0].second;
+  out.tileK = p.extent[2] / sk[0].second;
+  const int64_t inner_trips = p.has_inner_k() ? sk[1].second : 1;  // F of the nested pipeline
+  out.n_stage_smem_A = out.n_stage_smem_B = out.n_stage_inner = 1;
+  out.mode = ALCOP_MODE_WRAP;  // the reference's own emission of the pipelined nest
+  int outer[2] = {0, 0}, inner[2] = {0, 0};  // per side: stages of the shared / register pipeline
+  for (const Tensor& t : p.flow) {
+    if (t.stages == 0) continue;
+    (t.level == kShared ? outer : inner)[feeds_b(p, t) ? 1 : 0] = t.stages;
   }
-  if (sharedStages[0]) out.n_stage_smem_A = sharedStages[0];
-  if (sharedStages[1]) out.n_stage_smem_B = sharedStages[1];
+  if (outer[0]) out.n_stage_smem_A = outer[0];
+  if (outer[1]) out.n_stage_smem_B = outer[1];
   for (int side = 0; side < 2; ++side) {
-    if (!regStages[side]) continue;
-    // A register-level buffer whose copy sits directly in the ko body
-    // (no ki split) cannot fuse with the shared pipeline.
-    if (sharedStages[side] && ks.size() < 2)
-      analysis("UnsupportedNesting",
-               "inner pipelined loop must be a direct child of the outer pipelined loop body");
-    if (sharedStages[side] && static_cast<int64_t>(regStages[side] - 1) >
-                                  static_cast<int64_t>(sharedStages[side] - 1) * F)
-      analysis("LookaheadExceedsOuter", "inner pipeline looks ahead " + std::to_string(regStages[side] - 1) +
-                                            " steps, more than the outer pipeline covers (" +
-                                            std::to_string((sharedStages[side] - 1) * F) + ")");
-    // register level -> TMEM accumulator ring (at most 2 fit 512 columns)
-    out.n_stage_inner = std::max(out.n_stage_inner, std::min(regStages[side], 2));
+    const int t = inner[side], s = outer[side];
+    if (!t) continue;
+    if (s && !p.has_inner_k())
+      reject("UnsupportedNesting", "the register pipeline's loop must sit directly in the shared pipeline's body");
+    if (s && int64_t(t - 1) > int64_t(s - 1) * inner_trips)
+      reject("LookaheadExceedsOuter", "register lookahead " + std::to_string(t - 1) + " outruns the " +
+                                          std::to_string(int64_t(s - 1) * inner_trips) +
+                                          " steps the shared pipeline has in flight");
+    // the register double buffer becomes the TMEM accumulator ring (<= 2 x 256 columns)
+    out.n_stage_inner = std::max(out.n_stage_inner, std::min(t, 2));
   }
   return out;
 }
 
-}  // namespace sched
+}  // namespace surface
 
 // ---------------------------------------------------------------------------
 // Bookkeeping enumerator
@@ -485,19 +470,21 @@ extern "C" int alcop_parse_schedule_script(const alcop_gemm_desc* w, const char*
   clear_error();
   if (warnings && warnings_len) warnings[0] = '\0';
   try {
-    std::vector<std::string> warns;
-    sched::State st = sched::apply_script(sched::gemm_schedule(*w), script, &warns);
-    *out = sched::to_alcop(st);
+    surface::ScriptMachine machine(surface::workload(*w));
+    machine.run(script);
+    const alcop_schedule result = surface::to_schedule(machine.program());
     if (warnings && warnings_len) {
-      std::string all;
-      for (const auto& m : warns) all += m + "\n";
-      std::strncpy(warnings, all.c_str(), warnings_len - 1);
-      warnings[warnings_len - 1] = '\0';
+      std::string joined;
+      for (const std::string& n : machine.notes()) joined += n + "\n";
+      const size_t len = std::min(joined.size(), warnings_len - 1);
+      std::memcpy(warnings, joined.data(), len);
+      warnings[len] = '\0';
     }
+    *out = result;
     return ALCOP_OK;
-  } catch (const sched::Error& e) {
-    return set_error(e.code, e.rule, e.what());
-  } catch (const std::exception& e) {
+  } catch (const surface::Rejection& r) {
+    return set_error(r.exit_code, r.tag, r.what());
+  } catch (const std::exception& e) {  // the reference's cli maps any other exception to kConfig
     return set_error(ALCOP_ERR_CONFIG, "ConfigError", e.what());
   }
 }
