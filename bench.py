@@ -1,82 +1,78 @@
 #!/usr/bin/env python
-"""bench.py — headline benchmark of the B200 pipelined load-and-use GEMM path.
+"""bench.py — benchmark of the B200 pipelined load-and-use GEMM / BMM /
+implicit-GEMM conv path (ALCOP, arXiv 2210.16691).
 
-Workload (BASELINE.json configs[1]): the GEMMs of one BERT-base encoder layer
-at M = 4096 tokens, bf16 in / bf16 out, fp32 accumulate:
-    Q, K, V projections     [4096 x 768] @ [768 x 2304]  (one GEMM: the three
-                            projections read the same activations, so their
-                            weights are stored side by side, B = [Wq|Wk|Wv])
-    O projection            [4096 x 768]  @ [768 x 768]
-    FFN1                    [4096 x 768]  @ [768 x 3072]
-    FFN2                    [4096 x 3072] @ [3072 x 768]
-(--unfused-qkv: Q, K, V as three [768 x 768] GEMMs; the same FLOPs, six
-launches; that variant's step time is reported beside the headline too.)
-B is the reference layout [K, N] row-major (schedule.hpp:389).  One "step" is
-one pass over those GEMMs, each launched through the C ABI (alcop_gemm)
-with the schedule alcop_tune picks (the analytical model's top schedules
-timed on this GPU; --schedule model: the model's first pick).  Inputs
-rotate over copies whose footprint exceeds 2x the 126 MB L2, so every step
-reads HBM.  Reported beside it, in the same run: the n_stage 1..6 sweep of
-each distinct shape (speedup vs the non-pipelined n_stage=1 variant), the
-model pick vs the best swept schedule, BASELINE config 1 (fp16 512^3 with the
-reference's own schedule script, and the reference interpreter on the whole
-problem on the host cores), the attention BMMs, the ResNet-50 convs, the
-large square GEMMs, the roofline of
-the dominant kernel, the end-to-end number through the host-buffer ABI entry
-point, and the reference CPU path timed on the host cores.
+Headline (BASELINE.json configs[4], the largest single-GPU configuration, C5):
+the square bf16 GEMMs n = 4096, 8192, 12288, 16384 (C = A @ B, B in the
+reference layout [K, N], bf16 out, fp32 accumulate in TMEM).  One step launches
+each square once through the C ABI (alcop_gemm, the analytical model's
+schedule), captured in one CUDA graph.  value = sum of the four squares' FLOPs
+/ step time.  The step's operands (3.0 GB) are 24x the 126 MB L2, so each
+square's inputs are evicted by the other three between its launches.
+
+Multi-GPU: the squares are M-sharded — rank r owns a contiguous
+block of A's / C's rows in 256-row granules, B is replicated, no collective on
+the compute path; the work is fixed as N grows ("scaling": "strong") and
+value = total FLOPs / max-over-ranks time.  `--gpus N` launches N ranks itself
+(torch.distributed.run on 127.0.0.1) when it is not already under torchrun.
+
+Beside the headline, in the same JSON line:
+  * parity: every timed kernel (headline squares, BERT GEMMs, attention BMMs,
+    ResNet-50 convs, config 1) re-run with the same schedule on exact-integer
+    inputs and checked bit-exactly on sampled rows / columns / pixels against
+    a float64 product on the device (exact for these inputs);
+  * roofline of the dominant kernel (16384^3), the per-square TFLOP/s and
+    fraction of peak, the n_stage = 1 variant of every square (speedup), the
+    model's pick against a swept set of schedules;
+  * the BERT-base layer step (BASELINE configs[1]): four GEMMs as one graph,
+    the six-GEMM form, the one-launch chain, the n_stage 1..6 sweep;
+  * attention BMMs (configs[2]), ResNet-50 convs at batch 256 (configs[3]),
+    config 1 (fp16 512^3 with the reference's own schedule script beside the
+    reference interpreter on the whole problem);
+  * e2e: the headline step through alcop_gemm_host_async (pinned host
+    buffers, H2D + kernels + D2H inside the timed region);
+  * cpu_baseline: the reference interpreter on a bounded sample of the squares.
 
 --impl reference times the reference's own CPU implementation (the pipec
-interpreter running the transformed program, oracle/_ref/ref_driver built
-from /root/reference) on a bounded sample of the same workload.
-
-Multi-GPU: the BERT GEMMs are replicas only — each rank runs
-the full step on its own GPU, no collective on the data path; value is the
-whole-job FLOP rate (N x per-GPU FLOPs / max-over-ranks time).
+interpreter running the transformed program, oracle/_ref/ref_driver built from
+/root/reference) on a bounded sample of the same workload.
+--dry-run runs the rank logic on CPU with gloo and a scaled-down stand-in
+compute (tests/test_bench_cpu.py drives it at world size 2).
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
+import zlib
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BERT_GEMMS = [  # (name, M, N, K): the layer's GEMMs, Q/K/V fused into one launch
-    ("qkv_proj", 4096, 2304, 768), ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768),
-    ("ffn2", 4096, 768, 3072),
-]
-BERT_GEMMS_UNFUSED = [
-    ("q_proj", 4096, 768, 768), ("k_proj", 4096, 768, 768), ("v_proj", 4096, 768, 768),
-    ("o_proj", 4096, 768, 768), ("ffn1", 4096, 3072, 768), ("ffn2", 4096, 768, 3072),
-]
-METRIC = "TFLOP/s (BERT-base layer GEMMs, M=4096, bf16)"
-# ResNet-50 v1.5 convolutions at batch 256 (BASELINE configs[3]); conv1 (C=3) runs
-# the stem kernel on the NHWC8 halo-padded input.
-# (name, H_in, C, K, R, stride, pad, repeats)
-RESNET50_CONVS = [
-    ("conv1_7x7s2_3_64", 224, 3, 64, 7, 2, 3, 1),  # NHWC input padded to 8 channels (zero filter taps)
-    ("l1_1x1_64_64", 56, 64, 64, 1, 1, 0, 1), ("l1_3x3_64_64", 56, 64, 64, 3, 1, 1, 3),
-    ("l1_1x1_64_256", 56, 64, 256, 1, 1, 0, 4), ("l1_1x1_256_64", 56, 256, 64, 1, 1, 0, 2),
-    ("l2_1x1_256_128", 56, 256, 128, 1, 1, 0, 1), ("l2_3x3s2_128", 56, 128, 128, 3, 2, 1, 1),
-    ("l2_3x3_128", 28, 128, 128, 3, 1, 1, 3), ("l2_1x1_128_512", 28, 128, 512, 1, 1, 0, 4),
-    ("l2_ds_256_512", 56, 256, 512, 1, 2, 0, 1), ("l2_1x1_512_128", 28, 512, 128, 1, 1, 0, 3),
-    ("l3_1x1_512_256", 28, 512, 256, 1, 1, 0, 1), ("l3_3x3s2_256", 28, 256, 256, 3, 2, 1, 1),
-    ("l3_3x3_256", 14, 256, 256, 3, 1, 1, 5), ("l3_1x1_256_1024", 14, 256, 1024, 1, 1, 0, 6),
-    ("l3_ds_512_1024", 28, 512, 1024, 1, 2, 0, 1), ("l3_1x1_1024_256", 14, 1024, 256, 1, 1, 0, 5),
-    ("l4_1x1_1024_512", 14, 1024, 512, 1, 1, 0, 1), ("l4_3x3s2_512", 14, 512, 512, 3, 2, 1, 1),
-    ("l4_3x3_512", 7, 512, 512, 3, 1, 1, 2), ("l4_1x1_512_2048", 7, 512, 2048, 1, 1, 0, 3),
-    ("l4_ds_1024_2048", 14, 1024, 2048, 1, 2, 0, 1), ("l4_1x1_2048_512", 7, 2048, 512, 1, 1, 0, 2),
-]
+from paper_2210_16691_b200.workloads import (BERT_GEMMS, BERT_GEMMS_UNFUSED, BMM_ATTENTION, BMM_BATCH,  # noqa: E402
+                                             CONV_LAYERS, RESNET50_CONVS, RESNET_BATCH, SQUARE_GRANULE, SQUARES)
+
+METRIC = "TFLOP/s (square bf16 GEMMs n=4096..16384, C5)"
 UNIT = "TFLOP/s"
 TUNE_BUDGET = 24
 L2_BYTES = 126 * 1024 * 1024
+DRY_SCALE = 64  # --dry-run: n / DRY_SCALE
 
 
-def step_flops():
+def square_flops(n):
+    return 2.0 * n ** 3
+
+
+def step_flops(sizes=SQUARES):
+    """FLOPs of one headline step (each square once, all ranks together)."""
+    return sum(square_flops(n) for n in sizes)
+
+
+def bert_step_flops():
     return sum(2.0 * M * N * K for _, M, N, K in BERT_GEMMS)
 
 
@@ -87,7 +83,8 @@ def load_peaks():
             d = json.load(f)
         return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d["bf16_tflops_sustained"],
                 "hbm_gbs": d["hbm_gbs"], "source": "measured"}
-    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
 
 
 # ----------------------------------------------------------------- CPU arms
@@ -96,19 +93,18 @@ def _ref_driver():
     return p if os.path.exists(p) else None
 
 
-REF_SAMPLE_COLS = 128  # one output sub-block per GEMM: rows x 128 columns, full K
+REF_SAMPLE_COLS = 128  # one output sub-block per process: rows x 128 columns, full K
 REF_NS_PER_MMA = 150e-9  # measured cost of one interpreted mma statement
 
 
-def ref_sample_rows(seconds_per_step):
-    """Rows of the sample block so the slowest job (FFN2, K=3072) takes ~seconds_per_step."""
-    kmax = max(K for _, _, _, K in BERT_GEMMS)
+def ref_sample_rows(seconds_per_step, kmax=max(SQUARES)):
+    """Rows of the sample block so the slowest job (K = kmax) takes ~seconds_per_step."""
     return max(1, min(128, int(seconds_per_step / (REF_NS_PER_MMA * REF_SAMPLE_COLS * kmax))))
 
 
 def _ref_sample_script(M, N, K):
-    # the reference's own config-1-style schedule for the sample block:
-    # one output tile, tileK = 32, 2-stage shared + 2-stage register pipeline
+    # the reference's own config-1-style schedule for a sample block: one output
+    # tile, tileK = 32, 2-stage shared + 2-stage register pipeline
     ko = K // 32
     return ("cache_read A shared\ncache_read B shared\ncache_read A_shared register\n"
             "cache_read B_shared register\ntile C i0=1 i1=%d j0=1 j1=%d ko=%d ki=32\n"
@@ -116,34 +112,33 @@ def _ref_sample_script(M, N, K):
             % (M, N, ko))
 
 
-def cpu_reference_step(rows):
-    """One step of the reference CPU path on a bounded sample: for every GEMM
-    of the layer, a rows x REF_SAMPLE_COLS output block per process with the
-    full K, interpreted by the reference (pipec::run on the transformed
-    program); max(#GEMMs, host cores) processes run concurrently, the GEMMs
-    dealt round-robin, so every host core works (the interpreter is
-    single-threaded per run and runs are independent).
-    Returns (seconds, flops, kind, cores).  Each block is a sub-problem of the
-    same GEMM: the interpreter's cost is linear in rows*cols*K."""
+def cpu_reference_step(rows, sizes=None):
+    """One step of the reference CPU path on a bounded sample of the headline
+    workload: max(#squares, host cores) processes, each a rows x 128 output
+    block (full K = n) of one square (dealt round-robin), interpreted by the
+    reference (pipec::run on the transformed two-level program).  The
+    interpreter is single-threaded per run and runs are independent
+    (SPEC.md:399-400), so every host core works; its cost is linear in
+    rows * cols * K.  Returns (seconds, flops, kind, cores)."""
     import tempfile
+    sizes = sizes or SQUARES
     drv = _ref_driver()
-    jobs = []
     tmp = tempfile.mkdtemp()
-    nproc = max(len(BERT_GEMMS), os.cpu_count() or 1)
+    nproc = max(len(sizes), os.cpu_count() or 1)
+    jobs = []
     for j in range(nproc):
-        name, M, N, K = BERT_GEMMS[j % len(BERT_GEMMS)]
-        m, n = rows, REF_SAMPLE_COLS
-        sp = os.path.join(tmp, "%s_%d.txt" % (name, j))
+        n = sizes[j % len(sizes)]
+        sp = os.path.join(tmp, "sq%d_%d.txt" % (n, j))
         with open(sp, "w") as f:
-            f.write(_ref_sample_script(m, n, K))
-        jobs.append((name, m, n, K, sp))
-    flops = sum(2.0 * m * n * K for _, m, n, K, _ in jobs)
+            f.write(_ref_sample_script(rows, REF_SAMPLE_COLS, n))
+        jobs.append((rows, REF_SAMPLE_COLS, n, sp))
+    flops = sum(2.0 * m * c * K for m, c, K, _ in jobs)
     cores = os.cpu_count() or 1
     if drv is not None:
         t0 = time.perf_counter()
-        ps = [subprocess.Popen([drv, "time", "--M", str(m), "--N", str(n), "--K", str(K), "--script", sp,
+        ps = [subprocess.Popen([drv, "time", "--M", str(m), "--N", str(c), "--K", str(K), "--script", sp,
                                 "--mode", "stale"], stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
-              for _, m, n, K, sp in jobs]
+              for m, c, K, sp in jobs]
         outs = [p.communicate() for p in ps]
         dt = time.perf_counter() - t0
         for p, (o, e) in zip(ps, outs):
@@ -154,11 +149,18 @@ def cpu_reference_step(rows):
     import numpy as np
     from oracle import coracle
     t0 = time.perf_counter()
-    for _, m, n, K, _ in jobs:
+    for m, c, K, _ in jobs:
         A = coracle.to_dtype(np.ones((m, K), np.float32), "bf16")
-        B = coracle.to_dtype(np.ones((K, n), np.float32), "bf16")
+        B = coracle.to_dtype(np.ones((K, c), np.float32), "bf16")
         coracle.gemm(A, B, "bf16", "bf16")
     return time.perf_counter() - t0, flops, "port", cores
+
+
+def cpu_sample_text(rows, cores, dt=None):
+    return ("%d concurrent processes (host cores), each a %dx%d output block (full K = n) of one of the squares "
+            "n=%s (round-robin), pipec::run on the transformed two-level program (tile %dx%dx32, 2+2 stages)%s"
+            % (max(len(SQUARES), cores), rows, REF_SAMPLE_COLS, "/".join(map(str, SQUARES)), rows,
+               REF_SAMPLE_COLS, "" if dt is None else "; %.2f s wall" % dt))
 
 
 def run_reference_arm(args, rank, world):
@@ -174,16 +176,13 @@ def run_reference_arm(args, rank, world):
             times.append(dt)
     total = sum(times)
     value = flops * len(times) / total / 1e12
-    sample = ("per step: %d concurrent processes (host cores), each a %dx%d output block (full K) of one of the %d "
-              "BERT-layer GEMMs (round-robin), pipec::run on the transformed two-level program (tile %dx%dx32, "
-              "2+2 stages)" % (max(len(BERT_GEMMS), os.cpu_count() or 1), rows, REF_SAMPLE_COLS, len(BERT_GEMMS),
-                               rows, REF_SAMPLE_COLS))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (SplitMix64 range(-8,8), the reference generator)",
-            "config": {"workload": "bert_base_layer_gemms_sample", "M": 4096, "gemms": [g[1:] for g in BERT_GEMMS]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "config": {"workload": "square_gemms_c5_sample", "sizes": list(SQUARES), "dtype": "bf16"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": "per step: " + cpu_sample_text(rows, os.cpu_count() or 1)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -251,33 +250,469 @@ class _Null:
     def __exit__(self, *a):
         return False
 
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (dry run)"]}
+
+
+# ----------------------------------------------------------------- rank plumbing
+class Ranks:
+    """torch.distributed plumbing: barrier and max-over-ranks reduction (NCCL on
+    the GPU, gloo in the dry run), identity at world size 1."""
+
+    def __init__(self, rank, world, device):
+        self.rank, self.world, self.device = rank, world, device
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return float(x)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_obj(self, obj):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+
+def timed_steps(stepfn, steps, warmup, ranks, sync, clock, sample_clocks=None):
+    """W untimed warm-up steps, then EXACTLY `steps` steps bracketed by a
+    barrier + device synchronize on both sides; returns max-over-ranks ms of
+    the timed region (clock() -> (start, stop_ms_fn))."""
+    for _ in range(warmup):
+        stepfn()
+    sync()
+    ranks.barrier()
+    sync()
+    with sample_clocks if sample_clocks is not None else _Null() as clk:
+        start, stop = clock()
+        for _ in range(steps):
+            stepfn()
+        ms = stop(start)
+    ranks.barrier()
+    return ranks.max(ms), clk
+
+
+class HeadlineGpu:
+    """The headline squares on this rank's GPU: rank r's row shard of every
+    square (A[m, n], B[n, n] replicated, C[m, n]) with the model's schedule."""
+
+    def __init__(self, alcop, dev, rank, world, sizes=SQUARES):
+        import torch
+        from paper_2210_16691_b200 import workloads
+        from paper_2210_16691_b200.sharded import shard_range
+        self.torch, self.alcop, self.dev = torch, alcop, dev
+        self.lib = alcop.load_library()
+        self.sizes = sizes
+        self.items = []
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234 + rank)
+        for n in sizes:
+            sh = shard_range(n, rank, world, granule=SQUARE_GRANULE)
+            m = sh.size
+            d = alcop.gemm_desc(m, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
+            s = workloads.square_schedule(alcop, m, n)
+            A = (torch.rand((m, n), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+            B = (torch.rand((n, n), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+            C = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
+            self.items.append({"n": n, "shard": sh, "m": m, "desc": d, "sched": s, "A": A, "B": B, "C": C})
+        self.graph = None
+
+    def launch(self, it, sched=None, A=None, B=None, C=None, desc=None):
+        import ctypes
+        cur = ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+        rc = self.lib.alcop_gemm(ctypes.byref(desc or it["desc"]), ctypes.byref(sched or it["sched"]),
+                                 ctypes.c_void_p((A if A is not None else it["A"]).data_ptr()),
+                                 ctypes.c_void_p((B if B is not None else it["B"]).data_ptr()),
+                                 ctypes.c_void_p((C if C is not None else it["C"]).data_ptr()), cur)
+        if rc:
+            raise self.alcop.AlcopError(rc, self.lib.alcop_last_error().decode())
+
+    def build_step(self):
+        """One CUDA graph per step: every square once (alcop_gemm launches
+        chained with PDL)."""
+        torch = self.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for it in self.items:
+                self.launch(it)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            for it in self.items:
+                self.launch(it)
+
+    def step(self):
+        self.graph.replay()
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def clock(self):
+        torch = self.torch
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+
+        def stop(_):
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+        return e0, stop
+
+    def local_flops(self):
+        return sum(2.0 * it["m"] * it["n"] * it["n"] for it in self.items)
+
+
+class HeadlineDry:
+    """--dry-run stand-in: the same shard arithmetic on CPU at n / DRY_SCALE,
+    torch.matmul as the compute, wall-clock timing."""
+
+    def __init__(self, rank, world, sizes=SQUARES):
+        import torch
+        from paper_2210_16691_b200.sharded import shard_range
+        self.torch = torch
+        self.sizes = sizes
+        self.items = []
+        g = torch.Generator()
+        g.manual_seed(1234 + rank)
+        for n_full in sizes:
+            n = n_full // DRY_SCALE
+            sh = shard_range(n, rank, world, granule=max(1, SQUARE_GRANULE // DRY_SCALE))
+            A = torch.randint(-8, 9, (sh.size, n), generator=g).float()
+            B = torch.randint(-8, 9, (n, n), generator=g).float()
+            self.items.append({"n": n, "n_full": n_full, "shard": sh, "m": sh.size, "A": A, "B": B,
+                               "C": torch.empty(sh.size, n)})
+
+    def build_step(self):
+        pass
+
+    def step(self):
+        for it in self.items:
+            self.torch.matmul(it["A"], it["B"], out=it["C"])
+
+    def sync(self):
+        pass
+
+    def clock(self):
+        t0 = time.perf_counter()
+        return t0, lambda t: (time.perf_counter() - t) * 1e3
+
+    def local_flops(self):
+        return sum(2.0 * it["m"] * it["n"] * it["n"] for it in self.items)
+
+
+# ----------------------------------------------------------------- device parity (exact-integer inputs)
+def _dint(torch, shape, gen, dev):
+    return torch.randint(-8, 9, shape, generator=gen, device=dev).to(torch.bfloat16)
+
+
+def _tile_rows(torch, n, tile, gen, dev):
+    """One index inside every `tile` rows plus both ends."""
+    starts = torch.arange(0, n, tile, device=dev)
+    off = torch.randint(0, tile, (starts.numel(),), generator=gen, device=dev)
+    idx = torch.clamp(starts + off, max=n - 1)
+    return torch.unique(torch.cat([idx, torch.tensor([0, n - 1], device=dev)]))
+
+
+def _exact_bf16(torch, x64):
+    """float64 exact integers (|x| < 2^24) -> fp32 (exact) -> bf16 (RNE)."""
+    return x64.to(torch.float32).to(torch.bfloat16)
+
+
+def parity_gemm(torch, run, M, N, K, batch, dev, seed, b_layout_kn=True, full=False):
+    """Runs `run(A, B, C)` (the timed kernel and schedule, bf16 out) on
+    exact-integer inputs and compares sampled rows and columns (or the whole
+    output) with a float64 product on the device.  Returns a parity record."""
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    shp = (batch,) if batch > 1 else ()
+    A = _dint(torch, shp + (M, K), gen, dev)
+    B = _dint(torch, shp + ((K, N) if b_layout_kn else (N, K)), gen, dev)
+    C = torch.full(shp + (M, N), float("nan"), device=dev, dtype=torch.bfloat16)
+    run(A, B, C)
+    torch.cuda.synchronize()
+    Bd = B.double() if b_layout_kn else B.double().transpose(-1, -2)
+    if full:
+        want = _exact_bf16(torch, torch.matmul(A.double(), Bd))
+        bad = int((C != want).sum().item()) + int(torch.isnan(C.float()).sum().item())
+        return {"status": "exact" if bad == 0 else "MISMATCH", "checked": "whole output", "mismatches": bad}
+    rows = _tile_rows(torch, M, 256, gen, dev)
+    cols = _tile_rows(torch, N, 256, gen, dev)
+    want_r = _exact_bf16(torch, torch.matmul(A.double()[..., rows, :], Bd))
+    want_c = _exact_bf16(torch, torch.matmul(A.double(), Bd[..., :, cols]))
+    bad = int((C[..., rows, :] != want_r).sum().item()) + int((C[..., :, cols] != want_c).sum().item())
+    return {"status": "exact" if bad == 0 else "MISMATCH",
+            "checked": "%d full rows + %d full columns (one per 256-tile)" % (rows.numel(), cols.numel()),
+            "mismatches": bad}
+
+
+def parity_conv(torch, alcop, layer, nimg, sched, dev, seed, npts=1024):
+    """The timed conv kernel and schedule on exact-integer inputs; `npts`
+    sampled output pixels (all K channels, the corners of the first and last
+    image included) against a float64 window product on the device."""
+    L = layer
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    hp = L.pad if L.halo else 0
+    x = _dint(torch, (nimg, L.H, L.H, L.C), gen, dev)
+    w = _dint(torch, (L.K, L.R, L.R, L.C), gen, dev)
+    X = torch.zeros((nimg, L.H + 2 * hp, L.H + 2 * hp, L.Cs), device=dev, dtype=torch.bfloat16)
+    X[:, hp:hp + L.H, hp:hp + L.H, :L.C] = x
+    Wf = torch.zeros((L.K, L.R, L.R, L.Cs), device=dev, dtype=torch.bfloat16)
+    Wf[..., :L.C] = w
+    Y = alcop.conv2d(X, Wf, (L.stride, L.stride), (L.pad, L.pad), sched=sched, out_dtype=torch.bfloat16,
+                     x_halo=L.halo)
+    P = L.P
+    corners = torch.tensor([(n, p, q) for n in (0, nimg - 1) for p in (0, P - 1) for q in (0, P - 1)], device=dev)
+    rnd = torch.stack([torch.randint(0, nimg, (npts,), generator=gen, device=dev),
+                       torch.randint(0, P, (npts,), generator=gen, device=dev),
+                       torch.randint(0, P, (npts,), generator=gen, device=dev)], 1)
+    pts = torch.cat([corners, rnd])
+    xp = torch.nn.functional.pad(x.double(), (0, 0, L.pad, L.pad, L.pad, L.pad))  # N, H+2p, W+2p, C
+    r = torch.arange(L.R, device=dev)
+    hh = (pts[:, 1:2] * L.stride + r[None, :])  # [pts, R]
+    ww = (pts[:, 2:3] * L.stride + r[None, :])  # [pts, S]
+    win = xp[pts[:, 0][:, None, None], hh[:, :, None], ww[:, None, :]]  # [pts, R, S, C]
+    want = _exact_bf16(torch, win.reshape(len(pts), -1) @ w.double().reshape(L.K, -1).t())
+    got = Y[pts[:, 0], pts[:, 1], pts[:, 2]]
+    bad = int((got != want).sum().item())
+    return {"status": "exact" if bad == 0 else "MISMATCH", "checked": "%d output pixels x %d channels"
+            % (len(pts), L.K), "mismatches": bad}
+
 
 # ----------------------------------------------------------------- GPU arm
 def main_gpu(args, rank, world, local_rank):
+    import ctypes
     import torch
-    import torch.distributed as dist
     import paper_2210_16691_b200 as alcop
-    from paper_2210_16691_b200.timing import time_graph
+    from paper_2210_16691_b200 import workloads
+    from paper_2210_16691_b200.sharded import shard_range
+    from paper_2210_16691_b200.timing import Rotating, time_graph
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    alcop.load_library()
-    peaks = load_peaks()
-    stream = torch.cuda.current_stream()
-
-    gemms = BERT_GEMMS_UNFUSED if args.unfused_qkv else BERT_GEMMS
     lib = alcop.load_library()
-    import ctypes
-    sp = ctypes.c_void_p(stream.cuda_stream)
-    descs, sched = {}, {}
+    peaks = load_peaks()
+    ranks = Ranks(rank, world, dev)
+    parity = {}
+    extra = {}
+    launches = {"n": 0}
 
-    model_pick = {}
+    def attainable(fl, byts):
+        """SURVEY §8d: min(P, AI * BW) in TFLOP/s, AI = FLOPs / compulsory bytes."""
+        return min(peaks["bf16_tflops"], fl / byts * peaks["hbm_gbs"] * 1e-3)
+
+    # ---------------------------------------------------------------- headline: C5 squares, M-sharded
+    hl = HeadlineGpu(alcop, dev, rank, world)
+    for it in hl.items:  # parity of the exact kernel + schedule the step runs, on this rank's shard
+        n, m = it["n"], it["m"]
+        rec = parity_gemm(torch, lambda A, B, C, it=it: hl.launch(it, A=A, B=B, C=C), m, n, n, 1, dev,
+                          seed=77 + n)
+        parity["c5_square_%d_rank%d" % (n, rank)] = rec
+        if rec["status"] != "exact":
+            raise RuntimeError("headline kernel mismatch on square %d: %s" % (n, rec))
+    hl.build_step()
+    ms_total, clk = timed_steps(hl.step, args.steps, args.warmup, ranks, hl.sync, hl.clock,
+                                sample_clocks=ClockSampler(local_rank))
+    flops = step_flops()
+    value = flops * args.steps / (ms_total * 1e-3) / 1e12
+    launches["n"] += len(hl.items) * args.steps
+
+    # each square alone (the dominant kernel's roofline; per-square fraction of peak) and its n_stage=1 variant
+    per_sq = {}
+    for it in hl.items:
+        n, m = it["n"], it["m"]
+        iters = 30 if n <= 4096 else (10 if n <= 8192 else 4)
+        ms = time_graph(lambda i, it=it: hl.launch(it), iters=iters, warmup=2)
+        s = it["sched"]
+        s1 = alcop.make_schedule(tileN=s.tileN, tileK=s.tileK, n_stage=1, n_stage_inner=1,
+                                 cta_group=s.cta_group)
+        ms1 = time_graph(lambda i, it=it, s1=s1: hl.launch(it, sched=s1), iters=max(2, iters // 2), warmup=1)
+        ms, ms1 = ranks.max(ms), ranks.max(ms1)
+        tf = square_flops(n) / (ms * 1e-3) / 1e12  # whole-job rate of this square
+        per_sq[str(n)] = {"ms": round(ms, 4), "tflops": round(tf, 1),
+                          "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
+                          "n_stage1_ms": round(ms1, 4), "speedup_vs_n_stage1": round(ms1 / ms, 2),
+                          "rows_per_gpu": m, "schedule": s.as_dict()}
+    dom = max(per_sq, key=lambda k: per_sq[k]["ms"])
+    dn = int(dom)
+    dmine = [it for it in hl.items if it["n"] == dn][0]
+    achieved = 2.0 * dmine["m"] * dn * dn / (per_sq[dom]["ms"] * 1e-3) / 1e12  # per-GPU rate of the launch
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_bench_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("kernels", {}).get("square_%d" % dn, {}).get("dram_bytes")
+        except Exception:
+            traffic = None
+    step_ms = ms_total / args.steps
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "kernel": "%s (square %d: %dx%dx%d per GPU, %s)"
+                          % ("alcop_pipelined_gemm_pair_kernel" if dmine["sched"].cta_group == 2
+                             else "alcop_pipelined_gemm_kernel", dn, dmine["m"], dn, dn, dmine["sched"]),
+                "share_of_step": round(per_sq[dom]["ms"] / step_ms, 3),
+                "peak_source": peaks["source"] + " burst bf16 (MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": 2.0 * dmine["m"] * dn * dn,
+                "algorithmic_bytes_per_launch": 2 * (dmine["m"] * dn + dn * dn + dmine["m"] * dn),
+                "timing": "CUDA events around a CUDA graph of this GEMM alone (its operands 1.5 GB > L2)"}
+    torch.cuda.empty_cache()
+
+    # model pick vs a swept set (BASELINE: "analytical-model config vs exhaustive tuning")
+    if not args.quick:
+        sweep = {}
+        for it in hl.items:
+            n, m = it["n"], it["m"]
+            if n > 8192:  # each candidate launch is 2-6 ms: the CTA-pair tiles and the best single-CTA tile
+                cand_tiles = ((256, 64, 2), (192, 64, 2), (256, 128, 2), (256, 64, 1))
+            else:
+                cand_tiles = ((256, 64, 2), (192, 64, 2), (128, 64, 2), (256, 128, 2), (256, 64, 1), (128, 128, 1),
+                              (192, 64, 1))
+            rows_ = []
+            for tn, tk, cg in cand_tiles:
+                for st in (3, 4, 5, 6, 7):
+                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg)
+                    try:
+                        alcop.validate(it["desc"], s)
+                    except alcop.AlcopError:
+                        continue
+                    ms = time_graph(lambda i, s=s, it=it: hl.launch(it, sched=s),
+                                    iters=6 if n <= 8192 else 2, warmup=1)
+                    rows_.append((ms, tn, tk, cg, st))
+            best = min(rows_)
+            pick_ms = per_sq[str(n)]["ms"]
+            sweep[str(n)] = {"candidates": len(rows_), "best_swept": {"tflops": round(square_flops(n) / (best[0] * 1e-3)
+                                                                                / 1e12 / world, 1),
+                                                                      "tileN": best[1], "tileK": best[2],
+                                                                      "cta_group": best[3], "n_stage": best[4]},
+                             "model_pick_over_best_time": round(pick_ms / best[0], 3)}
+        extra["c5_model_pick_vs_sweep"] = sweep
+        torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- e2e: the headline step with HOST buffers
+    host = []
+    for it in hl.items:
+        A = torch.empty((it["m"], it["n"]), dtype=torch.bfloat16).pin_memory()
+        A.copy_(it["A"])
+        B = torch.empty((it["n"], it["n"]), dtype=torch.bfloat16).pin_memory()
+        B.copy_(it["B"])
+        C = torch.empty((it["m"], it["n"]), dtype=torch.bfloat16).pin_memory()
+        ws = torch.empty(lib.alcop_gemm_workspace_bytes(ctypes.byref(it["desc"])), dtype=torch.uint8, device=dev)
+        host.append((it, A, B, C, ws))
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def e2e_step():
+        for it, A, B, C, ws in host:
+            rc = lib.alcop_gemm_host_async(ctypes.byref(it["desc"]), ctypes.byref(it["sched"]),
+                                           ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                           ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(ws.data_ptr()), sp)
+            if rc:
+                raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+        torch.cuda.synchronize()  # the step's C blocks are on the host
+
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        e2e_step()
+    ranks.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = ranks.max(time.perf_counter() - t0)
+    launches["e2e"] = e2e_steps
+    e2e_val = flops * e2e_steps / e2e_s / 1e12
+    h2d = sum((it["m"] * it["n"] + it["n"] * it["n"]) * 2 for it, *_ in host)
+    d2h = sum(it["m"] * it["n"] * 2 for it, *_ in host)
+    # host-side check of the e2e result: rows of the last step's C against the device C
+    for it, A, B, C, ws in host:
+        hl.launch(it)
+        torch.cuda.synchronize()
+        rows = torch.tensor([0, it["m"] // 2, it["m"] - 1])
+        if not torch.equal(C[rows], it["C"][rows.to(dev)].cpu()):
+            raise RuntimeError("e2e host result differs from the device result (square %d)" % it["n"])
+    del host
+    torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- BERT-base layer GEMMs (configs[1]), replicas
+    if not args.quick:
+        extra["bert_layer"] = bert_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity, attainable,
+                                         launches)
+        torch.cuda.empty_cache()
+        extra["bmm_attention"] = bmm_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity)
+        torch.cuda.empty_cache()
+        extra["resnet50_convs_b256"] = conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable)
+        torch.cuda.empty_cache()
+        if rank == 0:
+            extra["config1_512"] = config1_block(args, torch, alcop, lib, dev, parity)
+
+    # ---------------------------------------------------------------- line
+    all_parity = {}
+    for p in ranks.gather_obj(parity):
+        all_parity.update(p)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rows = ref_sample_rows(3.0)
+        dt, cflops, kind, cores = cpu_reference_step(rows)
+        cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": cpu_sample_text(rows, cores, dt)}
+    ranks.barrier()
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (uniform[-1,1) bf16, fixed per rank; parity runs use exact-integer inputs)",
+            "config": {"workload": "square_gemms_c5", "sizes": list(SQUARES), "b_layout": "KN (reference)",
+                       "parallelism": "M-sharded over %d GPU(s) (%d-row granules, B replicated, no collective)"
+                                      % (world, SQUARE_GRANULE) if world > 1 else "single",
+                       "launch": "one CUDA graph per step: %d alcop_gemm launches chained with PDL" % len(SQUARES),
+                       "l2": "inputs larger than L2: step footprint %.1f GB; each square's operands are evicted "
+                             "by the other three between its launches" % (sum(3 * 2 * n * n for n in SQUARES) / 1e9),
+                       "schedule": "alcop_choose_schedule (the analytical model's pick) per shard",
+                       "schedules": {str(it["n"]): it["sched"].as_dict() for it in hl.items}},
+            "gpu_launches": launches["n"],
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "entry_point": "alcop_gemm_host_async per square (pinned host buffers: B then A row blocks H2D, "
+                                   "blocks multiplied as they land, C blocks D2H on a second copy stream), host "
+                                   "sync at the end of every step; wall clock, max over ranks",
+                    "steps": e2e_steps},
+            "parity": {"all_exact": all(v["status"] == "exact" for v in all_parity.values()),
+                       "method": "each timed kernel + schedule re-run on exact-integer inputs (randint[-8,8], exact "
+                                 "in bf16, fp32 partial sums exact) and compared bit-exactly with a float64 product "
+                                 "on the device (bf16 RNE of the exact result)",
+                       "checks": all_parity},
+            "per_square": per_sq,
+            **extra}
+    print(json.dumps(line), flush=True)
+
+
+def bert_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity, attainable, launches):
+    """BASELINE configs[1]: the GEMMs of one BERT-base layer at M = 4096 as one
+    CUDA graph (Q/K/V fused into one GEMM), the six-GEMM form, the
+    one-launch chain; per-GEMM fraction of the attainable roofline; the
+    n_stage 1..6 sweep with the model pick against the best swept schedule.
+    Replicas at N > 1 (each rank the whole layer)."""
+    import ctypes
+    from paper_2210_16691_b200.timing import Rotating, time_graph
+    descs, sched, model_pick = {}, {}, {}
 
     def plan(shape):
-        # per distinct shape: the analytical model's ranking (alcop_choose_schedule);
-        # with --schedule tune (default) its top TUNE_BUDGET schedules are timed on
-        # this GPU and the fastest is used (alcop_tune: the reference's
-        # model-assisted tuning, tuner.hpp:363-531, on real B200 timings)
         if shape not in sched:
             descs[shape] = alcop.gemm_desc(*shape, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
             model_pick[shape] = alcop.choose_schedule(descs[shape])
@@ -288,7 +723,6 @@ def main_gpu(args, rank, world, local_rank):
                 B = (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16)
                 C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
                 sched[shape], _ = alcop.tune(A, B, C, budget=TUNE_BUDGET)
-                del A, B, C
         return sched[shape]
 
     def launch(A, B, C, s, shape):
@@ -298,305 +732,83 @@ def main_gpu(args, rank, world, local_rank):
         if rc:
             raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
 
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-
     def make_step(gl):
-        """CUDA graphs of one step over the GEMM list gl, one graph per input
-        set; input sets rotate so the step's operands come from HBM (> 2x L2).
-        The launches are chained with PDL (the kernels are unchanged)."""
         set_bytes = sum((M * K + K * N + M * N) * 2 for _, M, N, K in gl)
         nsets = max(2, -(-2 * L2_BYTES // set_bytes))
         sets = []
         for _ in range(nsets):
-            one = []
-            for name, M, N, K in gl:
-                A = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
-                B = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
-                C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
-                one.append((A, B, C, plan((M, N, K))))
-            sets.append(one)
+            sets.append([((torch.rand((M, K), device=dev) * 2 - 1).to(torch.bfloat16),
+                          (torch.rand((K, N), device=dev) * 2 - 1).to(torch.bfloat16),
+                          torch.empty((M, N), device=dev, dtype=torch.bfloat16), plan((M, N, K)))
+                         for _, M, N, K in gl])
+        return lambda i: [launch(A, B, C, s, (M, N, K)) for (_, M, N, K), (A, B, C, s) in zip(gl, sets[i % nsets])], \
+            nsets
 
-        def step_set(i):
-            for (name, M, N, K), (A, B, C, s) in zip(gl, sets[i]):
-                launch(A, B, C, s, (M, N, K))
-
-        cs = torch.cuda.Stream()
-        cs.wait_stream(stream)
-        with torch.cuda.stream(cs):
-            for i in range(nsets):
-                step_set(i)
-        stream.wait_stream(cs)
-        torch.cuda.synchronize()
-        use_graphs = os.environ.get("ALCOP_BENCH_GRAPHS", "1") != "0"  # 0: direct launches (profiling)
-        graphs = []
-        if use_graphs:
-            for i in range(nsets):
-                g_ = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g_):
-                    step_set(i)
-                graphs.append(g_)
-        state = {"i": 0}
-
-        def step():
-            if use_graphs:
-                graphs[state["i"]].replay()
-            else:
-                step_set(state["i"])
-            state["i"] = (state["i"] + 1) % nsets
-        return step, nsets, set_bytes
-
-    def loaded_sm_clock(gl, iters=40):
-        """Effective SM clock under this workload's load: CTA 0 of the step's
-        last GEMM stamps clock64 and %globaltimer at start and end (debug
-        stamps, alcop_debug_set_stamps) after `iters` back-to-back steps.
-        NVML's SM clock reading does not show the loaded clock."""
-        lib.alcop_debug_set_stamps.argtypes = [ctypes.c_void_p]
-        buf = torch.zeros(148 * 8 + 64 + 128 + 2, dtype=torch.int64, device=dev)
-        ins = []
-        for name, M, N, K in gl:
-            ins.append(((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
-                        (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
-                        torch.empty((M, N), device=dev, dtype=torch.bfloat16), (M, N, K)))
-        torch.cuda.synchronize()
-        lib.alcop_debug_set_stamps(ctypes.c_void_p(buf.data_ptr()))
-        try:
-            for _ in range(iters):
-                for A, B, C, shape in ins:
-                    launch(A, B, C, sched[shape], shape)
-            torch.cuda.synchronize()
-        finally:
-            lib.alcop_debug_set_stamps(None)
-        t = buf.cpu().tolist()
-        ns = t[7] - t[0]
-        cyc = t[148 * 8 + 193] - t[148 * 8 + 192]
-        return round(cyc / ns * 1e3) if ns > 0 and cyc > 0 else None
-
-    step, nsets, set_bytes = make_step(gemms)
-    shapes = sorted(set((M, N, K) for _, M, N, K in gemms))
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # ---- correctness spot check of this run's kernels (oracle-independent: exact-integer inputs)
-    for (M, N, K) in shapes:
-        a = torch.randint(-8, 9, (M, K), device=dev).to(torch.bfloat16)
-        b = torch.randint(-8, 9, (K, N), device=dev).to(torch.bfloat16)
-        c = torch.empty((M, N), device=dev, dtype=torch.float32)
-        d32 = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.F32, alcop.B_KN)
-        rc = lib.alcop_gemm(ctypes.byref(d32), ctypes.byref(sched[(M, N, K)]), ctypes.c_void_p(a.data_ptr()),
-                            ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(c.data_ptr()), sp)
-        assert rc == 0
-        ref = (a.double() @ b.double()).float()
-        assert torch.equal(c, ref), "kernel mismatch on %s" % ((M, N, K),)
-
-    def timed(stepfn, steps, sample_clocks=False):
-        for _ in range(args.warmup):
-            stepfn()
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local_rank) if sample_clocks else _Null() as clk:
-            ev0.record(stream)
-            for _ in range(steps):
-                stepfn()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-        ms_total = ev0.elapsed_time(ev1)
-        barrier()
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()), clk
-
-    # ---- warmup + timed region (the headline)
-    ms_max, clk = timed(step, args.steps, sample_clocks=True)
-    kclk = loaded_sm_clock(gemms)
-    flops = step_flops()
-    value = world * flops * args.steps / (ms_max * 1e-3) / 1e12
-    # the other decomposition of the same layer (same FLOPs), same run
-    alt_gemms = BERT_GEMMS if args.unfused_qkv else BERT_GEMMS_UNFUSED
-    alt_step, _, _ = make_step(alt_gemms)
-    alt_steps = max(50, args.steps // 4)
-    alt_ms, _ = timed(alt_step, alt_steps)
-    alt = {"gemms": {n: [M, N, K] for n, M, N, K in alt_gemms}, "launches_per_step": len(alt_gemms),
-           "ms_per_step": alt_ms / alt_steps, "tflops": world * flops * alt_steps / (alt_ms * 1e-3) / 1e12}
-    del alt_step
-    torch.cuda.empty_cache()
-    # the same GEMMs as ONE persistent launch (alcop_gemm_chain): the smem and
-    # TMEM rings never drain between GEMMs; with row-block dependencies
-    # (A_p row block waits for C_{p-1} row block: the layer order) and as
-    # independent GEMMs (grouped launch, no ordering)
+    out = {"gemms": {n: [M, N, K] for n, M, N, K in BERT_GEMMS}, "parallelism": "replicas" if world > 1 else "single"}
+    flops = bert_step_flops()
+    for label, gl in (("step_fused_qkv", BERT_GEMMS), ("step_six_gemms", BERT_GEMMS_UNFUSED)):
+        fn, nsets = make_step(gl)
+        ms = ranks.max(time_graph(fn, iters=max(60, 6 * nsets), warmup=3, reps_per_graph=nsets))
+        out[label] = {"us_per_step": round(ms * 1e3, 2), "tflops": round(world * flops / (ms * 1e-3) / 1e12, 1),
+                      "launches_per_step": len(gl)}
+        launches[label] = len(gl)
+    for (name, M, N, K) in BERT_GEMMS:
+        s = sched[(M, N, K)]
+        parity["bert_%s" % name] = parity_gemm(torch, lambda A, B, C, s=s, sh=(M, N, K): launch(A, B, C, s, sh),
+                                               M, N, K, 1, dev, seed=11 + N + K, full=True)
+    # the same GEMMs as ONE persistent launch (alcop_gemm_chain)
+    gemms = BERT_GEMMS
+    csets = [[((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
+               (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
+               torch.empty((M, N), device=dev, dtype=torch.bfloat16)) for _, M, N, K in gemms] for _ in range(4)]
+    cws = torch.empty(1 << 16, dtype=torch.uint8, device=dev)
     chain = {}
-    if not args.unfused_qkv:
-        csets = [[((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
-                   (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
-                   torch.empty((M, N), device=dev, dtype=torch.bfloat16)) for _, M, N, K in gemms]
-                 for _ in range(nsets)]
-        cws = torch.empty(1 << 16, dtype=torch.uint8, device=dev)
-        for label, dep in (("row_block_dependencies", [0] + [1] * (len(gemms) - 1)), ("independent", None)):
-            best = None
-            for tn, tk, st in ((192, 64, 5), (256, 64, 4), (128, 128, 3)):
-                cs_ = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st)
-                ms = time_graph(lambda i: alcop.gemm_chain(csets[i % nsets], cs_, dep=dep, workspace=cws),
-                                iters=max(30, 6 * nsets), reps_per_graph=nsets)
-                if best is None or ms < best[0]:
-                    best = (ms, cs_)
-            tt = torch.tensor([best[0]], device=dev, dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            chain[label] = {"us_per_step": round(float(tt.item()) * 1e3, 2),
-                            "tflops": round(world * flops / (float(tt.item()) * 1e-3) / 1e12, 1),
-                            "schedule": best[1].as_dict()}
-        del csets
-        torch.cuda.empty_cache()
-
-    # ---- per-GEMM times (CUDA graphs on the launching stream, each GEMM on its
-    # own rotating inputs > 2x L2, i.e. cold operands as inside the step)
+    for label, dep in (("row_block_dependencies", [0] + [1] * (len(gemms) - 1)), ("independent", None)):
+        best = None
+        for tn, tk, st in ((192, 64, 5), (256, 64, 4), (128, 128, 3)):
+            cs_ = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st)
+            ms = time_graph(lambda i: alcop.gemm_chain(csets[i % 4], cs_, dep=dep, workspace=cws), iters=40,
+                            reps_per_graph=4)
+            if best is None or ms < best[0]:
+                best = (ms, cs_)
+        ms = ranks.max(best[0])
+        chain[label] = {"us_per_step": round(ms * 1e3, 2), "tflops": round(world * flops / (ms * 1e-3) / 1e12, 1),
+                        "schedule": best[1].as_dict()}
+    out["step_one_launch"] = {"entry_point": "alcop_gemm_chain", **chain}
+    del csets
+    # each GEMM alone, cold rotating operands
     per = {}
-    reps = max(8, min(50, args.steps // 4))
-    from paper_2210_16691_b200.timing import Rotating
     for (name, M, N, K) in gemms:
-        if (M, N, K) in [tuple(v["shape"]) for v in per.values()]:
-            continue
         rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
                                                  (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
                                                  torch.empty((M, N), device=dev, dtype=torch.bfloat16)),
                        (M * K + K * N + M * N) * 2, max_sets=16)
         nr = len(rot.sets)
-
-        def one(i, rot=rot, nr=nr, M=M, N=N, K=K):
-            A, B, C = rot.sets[i % nr]
-            launch(A, B, C, sched[(M, N, K)], (M, N, K))
-        ms = time_graph(one, iters=max(reps, 2 * nr), warmup=3, reps_per_graph=nr)
-        per[name] = {"ms": ms, "shape": [M, N, K], "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12,
-                     "schedule": sched[(M, N, K)].as_dict()}
-        del rot
-    count = {}
-    for (name, M, N, K) in gemms:
-        key = [n for n, v in per.items() if v["shape"] == [M, N, K]][0]
-        count[key] = count.get(key, 0) + 1
-    step_ms_est = sum(per[n]["ms"] * c for n, c in count.items())
-    dom = max(per, key=lambda n: per[n]["ms"] * count[n])
-    dM, dN, dK = per[dom]["shape"]
-    dflops = 2.0 * dM * dN * dK
-    achieved = dflops / (per[dom]["ms"] * 1e-3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_bench_summary.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                pj = json.load(f)
-            traffic = pj.get("kernels", {}).get(dom, {}).get("dram_bytes")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "kernel": "alcop_pipelined_gemm_kernel (%s %dx%dx%d)" % (dom, dM, dN, dK),
-                "share_of_step": per[dom]["ms"] * count[dom] / step_ms_est,
-                "peak_source": peaks["source"] + " burst bf16 (MEASURED_PEAKS.json)",
-                "algorithmic_flops_per_launch": dflops,
-                "timing": "CUDA events around CUDA graphs of this GEMM alone, rotating cold inputs > 2x L2"}
-
-    def attainable(fl, byts):
-        """SURVEY §8d: min(P, AI * BW) in TFLOP/s, AI = FLOPs / compulsory bytes."""
-        return min(peaks["bf16_tflops"], fl / byts * peaks["hbm_gbs"] * 1e-3)
-
-    def config1_block():
-        """BASELINE configs[0]: fp16 512^3 with the reference's
-        own schedule script (tile 128x128x32, 2 shared + 2 register stages)
-        mapped through alcop_parse_schedule_script, in WRAP (the pass's exact
-        index algebra) and FUSED mode, plus the model pick; L2 flushed between
-        launches (rotating inputs > 2x L2).  Beside it, on this host: the
-        reference interpreter on the WHOLE C1 problem (its 16 output tiles as
-        concurrent processes; makespan) and the C oracle (OpenMP)."""
-        M = N = K = 512
-        d1 = alcop.gemm_desc(M, N, K, 1, alcop.F16, alcop.F16, alcop.B_KN)
-        script = _ref_sample_script(128, 128, K).replace("i0=1", "i0=%d" % (M // 128)).replace(
-            "j0=1", "j0=%d" % (N // 128))
-        s_ref, _ = alcop.apply_script(d1, script)
-        s_fused = alcop.Schedule.from_buffer_copy(s_ref)
-        s_fused.mode = alcop.MODE_FUSED
-        s_model = alcop.choose_schedule(d1)
-        rot = Rotating(lambda i: ((torch.rand((M, K), device=dev) - 0.5).to(torch.float16),
-                                  (torch.rand((K, N), device=dev) - 0.5).to(torch.float16),
-                                  torch.empty((M, N), device=dev, dtype=torch.float16)),
-                       (M * K + K * N + M * N) * 2, max_sets=192)
-        nr = len(rot.sets)
-
-        def run1(i, s_):
-            A, B, C = rot.sets[i % nr]
-            rc = lib.alcop_gemm(ctypes.byref(d1), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
-                                ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
-                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-            if rc:
-                raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
-        out = {"shape": [M, N, K], "dtype": "f16", "script": script.strip().split("\n"),
-               "l2": "flushed (%d rotating input sets)" % nr}
+        ms = time_graph(lambda i, rot=rot, nr=nr, sh=(M, N, K): launch(*rot.sets[i % nr], sched[sh], sh),
+                        iters=max(40, 2 * nr), warmup=3, reps_per_graph=nr)
         fl = 2.0 * M * N * K
-        for label, s_ in (("reference_schedule_wrap", s_ref), ("reference_schedule_fused", s_fused),
-                          ("model_pick", s_model)):
-            ms = time_graph(lambda i, s_=s_: run1(i, s_), iters=2 * nr, warmup=3, reps_per_graph=nr)
-            out[label] = {"us": round(ms * 1e3, 2), "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
-                          "schedule": s_.as_dict()}
+        tf = fl / (ms * 1e-3) / 1e12
+        per[name] = {"ms": round(ms, 4), "shape": [M, N, K], "tflops": round(tf, 1),
+                     "frac_of_attainable": round(tf / attainable(fl, 2 * (M * K + K * N + M * N)), 3),
+                     "frac_of_peak": round(tf / peaks["bf16_tflops"], 3), "schedule": sched[(M, N, K)].as_dict()}
         del rot
-        if args.no_cpu:
-            return out
-        import tempfile
-        drv = _ref_driver()
-        if drv is not None:
-            sp = os.path.join(tempfile.mkdtemp(), "c1_tile.txt")
-            with open(sp, "w") as f:
-                f.write(_ref_sample_script(128, 128, K))
-            t0 = time.perf_counter()
-            ps = [subprocess.Popen([drv, "time", "--M", "128", "--N", "128", "--K", str(K), "--script", sp,
-                                    "--mode", "stale", "--seed", str(t)], stdout=subprocess.PIPE,
-                                   stderr=subprocess.PIPE, text=True) for t in range((M // 128) * (N // 128))]
-            outs = [p.communicate() for p in ps]
-            dt = time.perf_counter() - t0
-            if all(p.returncode == 0 for p in ps):
-                run_s = [json.loads(o.strip().splitlines()[-1])["best_s"] for o, _ in outs]
-                out["cpu_reference"] = {
-                    "makespan_s": round(dt, 3), "sum_of_run_s": round(sum(run_s), 2),
-                    "processes": len(ps), "host_cores": os.cpu_count(),
-                    "what": "pipec::run on transform(lower(apply_script(...))) of each 128x128 output tile "
-                            "(full K, the config-1 script), 16 concurrent processes = the whole C1 problem"}
-                best_us = min(out[k]["us"] for k in ("reference_schedule_wrap", "reference_schedule_fused",
-                                                     "model_pick"))
-                out["gpu_speedup_vs_cpu_reference"] = round(dt / (best_us * 1e-6), 0)
-        import numpy as np
-        from oracle import coracle
-        A = coracle.to_dtype(np.ones((M, K), np.float32), "f16")
-        B = coracle.to_dtype(np.ones((K, N), np.float32), "f16")
-        coracle.gemm(A, B, "f16", "f16")
-        t0 = time.perf_counter()
-        for _ in range(3):
-            coracle.gemm(A, B, "f16", "f16")
-        out["cpu_oracle_openmp_s"] = round((time.perf_counter() - t0) / 3, 4)
-        return out
-
-    extra = {}
-    if rank == 0 and not args.quick:
-        # ---- n_stage sweep 1..5 per distinct shape (same tile, same run) + model pick vs best
+    out["per_gemm"] = per
+    out["schedule_source"] = ("alcop_tune (model rank, top %d timed on this GPU)" % TUNE_BUDGET
+                              if args.schedule == "tune" else "alcop_choose_schedule (model pick)")
+    # n_stage sweep 1..6 per distinct shape, model pick vs best swept
+    if rank == 0:
         sweep = {}
-        for (M, N, K) in shapes:
-            base = model_pick[(M, N, K)]
-            tuned = sched[(M, N, K)]
-            rows = []
+        for (M, N, K) in sorted(set((M, N, K) for _, M, N, K in gemms)):
+            base, tuned = model_pick[(M, N, K)], sched[(M, N, K)]
             rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((M, K), device=dev) - 0.5).to(torch.bfloat16),
                                                      (torch.rand((K, N), device=dev) - 0.5).to(torch.bfloat16),
                                                      torch.empty((M, N), device=dev, dtype=torch.bfloat16)),
                            (M * K + K * N + M * N) * 2, max_sets=16)
             nr = len(rot.sets)
 
-            def run_on(i, s, rot=rot, nr=nr, M=M, N=N, K=K):
-                A, B, C = rot.sets[i % nr]
-                launch(A, B, C, s, (M, N, K))
-            best = None
-            cands = []
+            def run_on(i, s, rot=rot, nr=nr, sh=(M, N, K)):
+                launch(*rot.sets[i % nr], s, sh)
+            rows = []
             for st in range(1, 7):
                 for tn, tk, cg in ((base.tileN, base.tileK, base.cta_group), (128, 64, 1), (256, 64, 1),
                                    (128, 128, 1), (256, 128, 1), (192, 64, 1), (256, 64, 2), (128, 64, 2)):
@@ -606,280 +818,285 @@ def main_gpu(args, rank, world, local_rank):
                         alcop.validate(descs[(M, N, K)], s)
                     except alcop.AlcopError:
                         continue
-                    cands.append((st, tn, tk, cg, s))
-            for st, tn, tk, cg, s in cands:
-                ms = time_graph(lambda i, s=s: run_on(i, s), iters=2 * nr, warmup=3, reps_per_graph=nr)
-                tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12
-                rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "cta_group": cg, "tflops": round(tf, 1)})
-                if best is None or tf > best[0]:
-                    best = (tf, st, tn, tk, cg)
-            ms_pick = time_graph(lambda i: run_on(i, base), iters=2 * nr, warmup=3, reps_per_graph=nr)
-            tf_pick = 2.0 * M * N * K / (ms_pick * 1e-3) / 1e12
-            ms_tuned = time_graph(lambda i: run_on(i, tuned), iters=2 * nr, warmup=3, reps_per_graph=nr)
-            tf_tuned = 2.0 * M * N * K / (ms_tuned * 1e-3) / 1e12
+                    ms = time_graph(lambda i, s=s: run_on(i, s), iters=2 * nr, warmup=3, reps_per_graph=nr)
+                    rows.append({"n_stage": st, "tileN": tn, "tileK": tk, "cta_group": cg,
+                                 "tflops": round(2.0 * M * N * K / (ms * 1e-3) / 1e12, 1)})
+            best = max(rows, key=lambda r: r["tflops"])
+            tf_pick = 2.0 * M * N * K / (time_graph(lambda i: run_on(i, base), iters=2 * nr, warmup=3,
+                                                    reps_per_graph=nr) * 1e-3) / 1e12
+            tf_tuned = 2.0 * M * N * K / (time_graph(lambda i: run_on(i, tuned), iters=2 * nr, warmup=3,
+                                                     reps_per_graph=nr) * 1e-3) / 1e12
             by_stage = {}
             for r in rows:
                 if (r["tileN"], r["tileK"], r["cta_group"]) == (base.tileN, base.tileK, base.cta_group):
                     by_stage[r["n_stage"]] = max(by_stage.get(r["n_stage"], 0), r["tflops"])
             s1 = max([r["tflops"] for r in rows if r["n_stage"] == 1] or [float("nan")])
             sweep["%dx%dx%d" % (M, N, K)] = {
-                "tflops_by_n_stage_model_tile": by_stage,
-                "best_n_stage1_tflops": s1,
-                "best_swept": {"tflops": round(best[0], 1), "n_stage": best[1], "tileN": best[2], "tileK": best[3],
-                               "cta_group": best[4]},
+                "tflops_by_n_stage_model_tile": by_stage, "best_n_stage1_tflops": s1, "best_swept": best,
                 "model_pick": {"tflops": round(tf_pick, 1), **{k: v for k, v in base.as_dict().items()
                                                               if k in ("tileN", "tileK", "n_stage_smem_A",
                                                                        "cta_group")}},
-                "model_pick_over_best_time": round(best[0] / tf_pick, 3),
+                "model_pick_over_best_time": round(best["tflops"] / tf_pick, 3),
                 "tuned_pick": {"tflops": round(tf_tuned, 1), **{k: v for k, v in tuned.as_dict().items()
                                                                if k in ("tileN", "tileK", "n_stage_smem_A",
                                                                         "cta_group")}},
-                "speedup_best_vs_n_stage1": round(best[0] / s1, 2)}
-        extra["n_stage_sweep"] = sweep
-    if not args.quick:
-        # ---- batched GEMMs of attention (BASELINE configs[2]): batch*heads = 192,
-        # seq 512, head_dim 64; QK^T [512x64]@[64x512], PV [512x512]@[512x64];
-        # HBM-bound (AI ~51 FLOP/B), batch-sharded across ranks
-        bmm = {}
-        from paper_2210_16691_b200.sharded import shard_range
-        nb = shard_range(192, rank, world).size
-        for name, (M, N, K) in (("qk_t", (512, 512, 64)), ("pv", (512, 64, 512))):
-            db = alcop.gemm_desc(M, N, K, nb, alcop.BF16, alcop.BF16, alcop.B_KN)
-            descs[("bmm", name)] = db
-            sb = alcop.choose_schedule(db)
-            rot = Rotating(lambda i, M=M, N=N, K=K: ((torch.rand((nb, M, K), device=dev) - 0.5).to(torch.bfloat16),
-                                                     (torch.rand((nb, K, N), device=dev) - 0.5).to(torch.bfloat16),
-                                                     torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
-                           (M * K + K * N + M * N) * 2 * nb, max_sets=16)
-            nr = len(rot.sets)
-            if args.schedule == "tune":  # as for the layer GEMMs: the model's top schedules timed here
-                sb, _ = alcop.tune(*rot.sets[0], budget=TUNE_BUDGET)
-
-            def runb(i, s_, rot=rot, nr=nr, db=db):
-                A, B, C = rot.sets[i % nr]
-                rc = lib.alcop_gemm(ctypes.byref(db), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
-                                    ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
-                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-                if rc:
-                    raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
-            ms = time_graph(lambda i: runb(i, sb), iters=12 * nr, warmup=3, reps_per_graph=nr)
-            s1 = alcop.make_schedule(tileN=sb.tileN, tileK=sb.tileK, n_stage=1, n_stage_inner=1)
-            ms1 = time_graph(lambda i: runb(i, s1), iters=6 * nr, warmup=3, reps_per_graph=nr)
-            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            byts = (M * K + K * N + M * N) * 2 * 192
-            tsec = float(tt.item()) * 1e-3
-            bmm[name] = {"shape": [M, N, K], "batch": 192, "tflops_aggregate": round(2.0 * M * N * K * 192 / tsec / 1e12, 1),
-                         "gbs_aggregate": round(byts / tsec / 1e9, 1),
-                         "hbm_frac_per_gpu": round(byts / tsec / 1e9 / world / peaks["hbm_gbs"], 3),
-                         "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
+                "speedup_best_vs_n_stage1": round(best["tflops"] / s1, 2)}
             del rot
-        extra["bmm_attention"] = {"sharding": "batch", "bound": "hbm", "gemms": bmm}
-        if rank == 0:
-            extra["config1_512"] = config1_block()
+        out["n_stage_sweep"] = sweep
+    return out
 
-    # ---- ResNet-50 implicit-GEMM convs, batch 256 sharded across ranks
-    if not args.quick:
-        from paper_2210_16691_b200.sharded import shard_range
-        sh = shard_range(256, rank, world)
-        nloc = sh.size
-        conv_rows = []
-        tot_flops = 0.0
-        tot_ms = 0.0
-        for (name, H, C, K, R, st, pd, rep) in RESNET50_CONVS:
-            P, Q = alcop.conv_out_hw(H, H, R, R, (st, st), (pd, pd))
-            Cs = -(-C // 8) * 8  # stored channels (conv1: 3 -> 8, zero padded)
-            halo = R * Cs <= 64  # stem layer: network input stored with its padding halo (NHWC8)
-            hp = pd if halo else 0
-            g = alcop.gemm_desc(nloc * P * Q, K, R * 64 if halo else R * R * Cs, 1, alcop.BF16, alcop.BF16,
-                                alcop.B_NK)
-            cs = alcop.choose_conv_schedule(g)
-            X = torch.zeros((nloc, H + 2 * hp, H + 2 * hp, Cs), device=dev, dtype=torch.bfloat16)
-            Wf = torch.zeros((K, R, R, Cs), device=dev, dtype=torch.bfloat16)
-            X[:, hp:hp + H, hp:hp + H, :C] = (torch.rand((nloc, H, H, C), device=dev) - 0.5).to(torch.bfloat16)
-            Wf[..., :C] = (torch.rand((K, R, R, C), device=dev) - 0.5).to(torch.bfloat16)
-            Y = torch.empty((nloc, P, Q, K), device=dev, dtype=torch.bfloat16)
-            ms = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=cs, out=Y, x_halo=halo),
-                            iters=6, warmup=2)
-            s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
-            ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, (st, st), (pd, pd), sched=s1, out=Y, x_halo=halo),
-                             iters=4, warmup=1)
-            fl = 2.0 * nloc * P * Q * K * R * R * C
-            tot_flops += fl * rep
-            tot_ms += ms * rep
-            cbytes = 2 * (nloc * H * H * C + K * R * R * C + nloc * P * Q * K)
-            conv_rows.append({"layer": name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
-                              "frac_of_attainable": round(fl / (ms * 1e-3) / 1e12 / attainable(fl, cbytes), 3),
-                              "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN,
-                              "n_stage": cs.n_stage_smem_A})
-            del X, Wf, Y
-        tt = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        extra["resnet50_convs_b256"] = {
-            "tflops_aggregate": round(world * tot_flops / (float(tt.item()) * 1e-3) / 1e12, 1),
-            "images_per_gpu": nloc, "sharding": "batch", "layers": conv_rows,
-            "note": "sum over all 53 conv layers (conv1: stem kernel on the NHWC8 halo-padded input, C 3 -> 8 "
-                    "zero-padded, FLOPs counted at C=3); "
-                    "per-layer CUDA-graph timing, model schedules"}
-        torch.cuda.empty_cache()
-        # ---- large square GEMMs (BASELINE configs[4]): n^3 bf16, n = 4096..16384,
-        # M-sharded across ranks (rows of A and C split in 256-row granules, B
-        # replicated, no collective on the compute path); aggregate =
-        # total FLOPs / max-over-ranks time.  At N > 1 the optional NCCL
-        # all-gather of C is timed separately.
-        from paper_2210_16691_b200.sharded import shard_range, gather_rows
-        squares = {}
-        for n in (4096, 8192, 12288, 16384):
-            sh = shard_range(n, rank, world, granule=256)
-            m = sh.size
-            dsq = alcop.gemm_desc(m, n, n, 1, alcop.BF16, alcop.BF16, alcop.B_KN)
-            descs[(m, n, n)] = dsq
-            ssq = sched.get((m, n, n)) or alcop.choose_schedule(dsq)
-            sched[(m, n, n)] = ssq
-            A = (torch.rand((m, n), device=dev) - 0.5).to(torch.bfloat16)
-            B = (torch.rand((n, n), device=dev) - 0.5).to(torch.bfloat16)
-            C = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
-            barrier()
-            ms = time_graph(lambda i: launch(A, B, C, ssq, (m, n, n)), iters=8 if n < 12288 else 4, warmup=3)
-            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tf = 2.0 * n ** 3 / (float(tt.item()) * 1e-3) / 1e12
-            row = {"tflops_aggregate": round(tf, 1), "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
-                   "rows_per_gpu": m, "schedule": ssq.as_dict()}
-            if world > 1 and n == 16384:
-                for _ in range(2):
-                    gather_rows(C, n, rank, world, granule=256)
-                torch.cuda.synchronize()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                gather_rows(C, n, rank, world, granule=256)
-                e1.record()
-                torch.cuda.synchronize()
-                row["allgather_ms"] = round(e0.elapsed_time(e1), 3)
-            squares[str(n)] = row
-            del A, B, C
-            torch.cuda.empty_cache()
-        extra["large_square_m_sharded"] = {"sharding": "M (256-row granules), B replicated", "sizes": squares}
 
-    # ---- e2e through the host-buffer ABI entry point (alcop_gemm_host)
-    host = []
-    for name, M, N, K in gemms:
-        A = (torch.rand((M, K)) * 2 - 1).to(torch.bfloat16).pin_memory()
-        B = (torch.rand((K, N)) * 2 - 1).to(torch.bfloat16).pin_memory()
-        C = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
-        host.append((A, B, C))
-    # one workspace per GEMM of the step: the stream-ordered host entry point
-    # overlaps the H2D of GEMM k+1 with the D2H of GEMM k (two copy engines)
-    wss = [torch.empty(lib.alcop_gemm_workspace_bytes(ctypes.byref(descs[(M, N, K)])), dtype=torch.uint8,
-                       device=dev) for _, M, N, K in gemms]
+def bmm_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity):
+    """BASELINE configs[2]: attention QK^T [512x64]@[64x512] and PV
+    [512x512]@[512x64] over batch*heads = 192, batch-sharded across ranks;
+    HBM-bound (AI ~51 FLOP/B)."""
+    import ctypes
+    from paper_2210_16691_b200.sharded import shard_range
+    from paper_2210_16691_b200.timing import Rotating, time_graph
+    nb = shard_range(BMM_BATCH, rank, world).size
+    out = {}
+    for name, M, N, K in BMM_ATTENTION:
+        db = alcop.gemm_desc(M, N, K, nb, alcop.BF16, alcop.BF16, alcop.B_KN)
+        rot = Rotating(lambda i: ((torch.rand((nb, M, K), device=dev) - 0.5).to(torch.bfloat16),
+                                  (torch.rand((nb, K, N), device=dev) - 0.5).to(torch.bfloat16),
+                                  torch.empty((nb, M, N), device=dev, dtype=torch.bfloat16)),
+                       (M * K + K * N + M * N) * 2 * nb, max_sets=16)
+        nr = len(rot.sets)
+        sb = alcop.choose_schedule(db)
+        if args.schedule == "tune":
+            sb, _ = alcop.tune(*rot.sets[0], budget=TUNE_BUDGET)
 
-    def e2e_step():
-        for (name, M, N, K), (A, B, C), ws in zip(gemms, host, wss):
-            rc = lib.alcop_gemm_host_async(ctypes.byref(descs[(M, N, K)]), ctypes.byref(sched[(M, N, K)]),
-                                           ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                                           ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(ws.data_ptr()), sp)
+        def runb(A, B, C, s_):
+            rc = lib.alcop_gemm(ctypes.byref(db), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
+                                ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
             if rc:
                 raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
-        torch.cuda.synchronize()  # the step's C blocks are on the host
+        ms = ranks.max(time_graph(lambda i: runb(*rot.sets[i % nr], sb), iters=12 * nr, warmup=3, reps_per_graph=nr))
+        s1 = alcop.make_schedule(tileN=sb.tileN, tileK=sb.tileK, n_stage=1, n_stage_inner=1)
+        ms1 = ranks.max(time_graph(lambda i: runb(*rot.sets[i % nr], s1), iters=6 * nr, warmup=3, reps_per_graph=nr))
+        parity["bmm_%s_b%d_rank%d" % (name, nb, rank)] = parity_gemm(
+            torch, lambda A, B, C: runb(A, B, C, sb), M, N, K, nb, dev, seed=31 + N, full=True)
+        byts = (M * K + K * N + M * N) * 2 * BMM_BATCH
+        tsec = ms * 1e-3
+        out[name] = {"shape": [M, N, K], "batch": BMM_BATCH, "batch_per_gpu": nb,
+                     "tflops_aggregate": round(2.0 * M * N * K * BMM_BATCH / tsec / 1e12, 1),
+                     "gbs_aggregate": round(byts / tsec / 1e9, 1),
+                     "hbm_frac_per_gpu": round(byts / tsec / 1e9 / world / peaks["hbm_gbs"], 3),
+                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "schedule": sb.as_dict()}
+        del rot
+    return {"sharding": "batch", "bound": "hbm", "gemms": out}
 
-    e2e_steps = max(3, min(args.steps, 20))
-    for _ in range(2):
-        e2e_step()
-    torch.cuda.synchronize()
-    barrier()
+
+def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
+    """BASELINE configs[3]: the 23 distinct ResNet-50 v1.5 convolutions at batch
+    256 (53 layers with repeats), batch-sharded across ranks."""
+    from paper_2210_16691_b200 import workloads
+    from paper_2210_16691_b200.sharded import shard_range
+    from paper_2210_16691_b200.timing import time_graph
+    nloc = shard_range(RESNET_BATCH, rank, world).size
+    rows = []
+    tot_flops = tot_ms = 0.0
+    for L in CONV_LAYERS:
+        hp = L.pad if L.halo else 0
+        cs = workloads.conv_schedule(alcop, L, nloc)
+        X = torch.zeros((nloc, L.H + 2 * hp, L.H + 2 * hp, L.Cs), device=dev, dtype=torch.bfloat16)
+        Wf = torch.zeros((L.K, L.R, L.R, L.Cs), device=dev, dtype=torch.bfloat16)
+        X[:, hp:hp + L.H, hp:hp + L.H, :L.C] = (torch.rand((nloc, L.H, L.H, L.C), device=dev) - 0.5).to(torch.bfloat16)
+        Wf[..., :L.C] = (torch.rand((L.K, L.R, L.R, L.C), device=dev) - 0.5).to(torch.bfloat16)
+        Y = torch.empty((nloc, L.P, L.P, L.K), device=dev, dtype=torch.bfloat16)
+        st, pd = (L.stride, L.stride), (L.pad, L.pad)
+        ms = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=cs, out=Y, x_halo=L.halo), iters=6, warmup=2)
+        s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
+        ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=s1, out=Y, x_halo=L.halo), iters=4, warmup=1)
+        del X, Wf, Y
+        parity["conv_%s_b%d_rank%d" % (L.name, nloc, rank)] = parity_conv(torch, alcop, L, nloc, cs, dev,
+                                                                           seed=zlib.crc32(L.name.encode()))
+        fl = L.flops(nloc)
+        tot_flops += fl * L.repeats
+        tot_ms += ms * L.repeats
+        rows.append({"layer": L.name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+                     "frac_of_attainable": round(fl / (ms * 1e-3) / 1e12 / attainable(fl, L.compulsory_bytes(nloc)),
+                                                 3),
+                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN, "n_stage": cs.n_stage_smem_A})
+        torch.cuda.empty_cache()
+    tt = ranks.max(tot_ms)
+    return {"tflops_aggregate": round(world * tot_flops / (tt * 1e-3) / 1e12, 1), "images_per_gpu": nloc,
+            "sharding": "batch", "layers": rows,
+            "note": "sum over all 53 conv layers (conv1: stem kernel on the NHWC8 halo-padded input, C 3 -> 8 "
+                    "zero-padded, FLOPs counted at C=3); per-layer CUDA-graph timing, the model's conv schedules; "
+                    "compulsory bytes count only the input pixels a strided 1x1 conv reads"}
+
+
+def config1_block(args, torch, alcop, lib, dev, parity):
+    """BASELINE configs[0]: fp16 512^3 with the reference's own
+    schedule script (tile 128x128x32, 2 shared + 2 register stages) mapped
+    through alcop_parse_schedule_script, in WRAP (the pass's exact index
+    algebra) and FUSED mode, plus the model pick; L2 flushed between launches
+    (rotating inputs > 2x L2).  Beside it, on this host: the reference
+    interpreter on the WHOLE C1 problem (its 16 output tiles as concurrent
+    processes; makespan) and the C oracle (OpenMP)."""
+    import ctypes
+    from paper_2210_16691_b200.timing import Rotating, time_graph
+    M = N = K = 512
+    d1 = alcop.gemm_desc(M, N, K, 1, alcop.F16, alcop.F16, alcop.B_KN)
+    script = _ref_sample_script(128, 128, K).replace("i0=1", "i0=%d" % (M // 128)).replace("j0=1", "j0=%d" % (N // 128))
+    s_ref, _ = alcop.apply_script(d1, script)
+    s_fused = alcop.Schedule.from_buffer_copy(s_ref)
+    s_fused.mode = alcop.MODE_FUSED
+    s_model = alcop.choose_schedule(d1)
+    rot = Rotating(lambda i: ((torch.rand((M, K), device=dev) - 0.5).to(torch.float16),
+                              (torch.rand((K, N), device=dev) - 0.5).to(torch.float16),
+                              torch.empty((M, N), device=dev, dtype=torch.float16)),
+                   (M * K + K * N + M * N) * 2, max_sets=192)
+    nr = len(rot.sets)
+
+    def run1(A, B, C, s_):
+        rc = lib.alcop_gemm(ctypes.byref(d1), ctypes.byref(s_), ctypes.c_void_p(A.data_ptr()),
+                            ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()),
+                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if rc:
+            raise alcop.AlcopError(rc, lib.alcop_last_error().decode())
+    out = {"shape": [M, N, K], "dtype": "f16", "script": script.strip().split("\n"),
+           "l2": "flushed (%d rotating input sets)" % nr}
+    fl = 2.0 * M * N * K
+    for label, s_ in (("reference_schedule_wrap", s_ref), ("reference_schedule_fused", s_fused),
+                      ("model_pick", s_model)):
+        ms = time_graph(lambda i, s_=s_: run1(*rot.sets[i % nr], s_), iters=2 * nr, warmup=3, reps_per_graph=nr)
+        out[label] = {"us": round(ms * 1e3, 2), "tflops": round(fl / (ms * 1e-3) / 1e12, 1), "schedule": s_.as_dict()}
+        # fp16 in / fp16 out: the check runs the same kernel on exact-integer fp16 inputs
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(5)
+        A = torch.randint(-8, 9, (M, K), generator=gen, device=dev).half()
+        B = torch.randint(-8, 9, (K, N), generator=gen, device=dev).half()
+        C = torch.full((M, N), float("nan"), device=dev, dtype=torch.float16)
+        run1(A, B, C, s_)
+        want = (A.double() @ B.double()).float().half()
+        bad = int((C != want).sum().item())
+        parity["config1_%s" % label] = {"status": "exact" if bad == 0 else "MISMATCH", "checked": "whole output",
+                                        "mismatches": bad}
+    del rot
+    if args.no_cpu:
+        return out
+    import tempfile
+    drv = _ref_driver()
+    if drv is not None:
+        sp = os.path.join(tempfile.mkdtemp(), "c1_tile.txt")
+        with open(sp, "w") as f:
+            f.write(_ref_sample_script(128, 128, K))
+        t0 = time.perf_counter()
+        ps = [subprocess.Popen([drv, "time", "--M", "128", "--N", "128", "--K", str(K), "--script", sp,
+                                "--mode", "stale", "--seed", str(t)], stdout=subprocess.PIPE,
+                               stderr=subprocess.PIPE, text=True) for t in range((M // 128) * (N // 128))]
+        outs = [p.communicate() for p in ps]
+        dt = time.perf_counter() - t0
+        if all(p.returncode == 0 for p in ps):
+            run_s = [json.loads(o.strip().splitlines()[-1])["best_s"] for o, _ in outs]
+            out["cpu_reference"] = {
+                "makespan_s": round(dt, 3), "sum_of_run_s": round(sum(run_s), 2), "processes": len(ps),
+                "host_cores": os.cpu_count(), "same_config": True,
+                "what": "pipec::run on transform(lower(apply_script(...))) of each 128x128 output tile "
+                        "(full K, the config-1 script), 16 concurrent processes = the whole C1 problem"}
+            best_us = min(out[k]["us"] for k in ("reference_schedule_wrap", "reference_schedule_fused", "model_pick"))
+            out["gpu_speedup_vs_cpu_reference"] = round(dt / (best_us * 1e-6), 0)
+    import numpy as np
+    from oracle import coracle
+    A = coracle.to_dtype(np.ones((M, K), np.float32), "f16")
+    B = coracle.to_dtype(np.ones((K, N), np.float32), "f16")
+    coracle.gemm(A, B, "f16", "f16")
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = world * flops * e2e_steps / float(te.item()) / 1e12
-    h2d = sum((M * K + K * N) * 2 for _, M, N, K in gemms)
-    d2h = sum(M * N * 2 for _, M, N, K in gemms)
+    for _ in range(3):
+        coracle.gemm(A, B, "f16", "f16")
+    out["cpu_oracle_openmp_s"] = round((time.perf_counter() - t0) / 3, 4)
+    return out
 
-    if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            rows = ref_sample_rows(3.0)
-            dt, cflops, kind, cores = cpu_reference_step(rows)
-            cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": "%d concurrent processes, each a %dx%d output block (full K) of one of the %d "
-                             "BERT-layer GEMMs (round-robin) through the reference interpreter (pipec::run, "
-                             "transformed program); %.2f s wall" % (cores, rows, REF_SAMPLE_COLS, len(BERT_GEMMS),
-                                                                    dt)}
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (uniform[-1,1) bf16; %d rotating input sets, %.0f MB > 2x L2)"
-                        % (nsets, nsets * set_bytes / 1e6),
-                "config": {"workload": "bert_base_layer_gemms" + ("" if args.unfused_qkv else "_fused_qkv"),
-                           "M": 4096,
-                           "launch": "CUDA graph per input set: %d alcop_gemm launches chained with PDL" % len(gemms),
-                           "gemms": {n: [M, N, K] for n, M, N, K in gemms}, "b_layout": "KN (reference)",
-                           "parallelism": "replicas" if world > 1 else "single",
-                           "l2": "inputs rotated over copies > 2x L2",
-                           "schedule": ("alcop_tune (model rank, top %d timed on this GPU)" % TUNE_BUDGET
-                                        if args.schedule == "tune" else "alcop_choose_schedule (model pick)"),
-                           "schedules": {"%dx%dx%d" % k: v.as_dict() for k, v in sched.items()}},
-                "gpu_launches": len(gemms) * args.steps,
-                "clocks": {**clk.summary(), "sm_mhz_in_kernel": kclk,
-                           "note": "sm_mhz: NVML samples during the timed region; sm_mhz_in_kernel: clock64 over "
-                                   "%globaltimer in CTA 0 of the step's last GEMM under back-to-back steps (the "
-                                   "loaded clock; NVML does not show it)"},
-                "roofline": roofline,
-                "cpu_baseline": cpu,
-                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                        "entry_point": "alcop_gemm_host_async per GEMM (pinned host buffers; A row blocks H2D, "
-                                       "multiplied as they land, C blocks D2H on a second copy stream), host "
-                                       "sync at the end of every step"},
-                "per_gemm": {k: {"tflops": round(v["tflops"], 1), "ms": round(v["ms"], 4), "shape": v["shape"],
-                                 "frac_of_attainable": round(v["tflops"] / attainable(
-                                     2.0 * v["shape"][0] * v["shape"][1] * v["shape"][2],
-                                     2 * (v["shape"][0] * v["shape"][2] + v["shape"][2] * v["shape"][1]
-                                          + v["shape"][0] * v["shape"][1])), 3),
-                                 "launches_per_step": count[k]} for k, v in per.items()},
-                ("step_fused_qkv" if args.unfused_qkv else "step_unfused_qkv"): alt,
-                "step_one_launch": {"entry_point": "alcop_gemm_chain", **chain} if chain else None,
-                **extra}
-        print(json.dumps(line), flush=True)
+
+# ----------------------------------------------------------------- dry run (CPU, gloo)
+def main_dry(args, rank, world):
+    """The headline's rank logic on CPU: shard arithmetic, warm-up, barrier,
+    timed steps, max-over-ranks reduction, the JSON line — with torch.matmul at
+    n / DRY_SCALE standing in for the kernels (no numbers from here are bench
+    values)."""
+    import torch
+    ranks = Ranks(rank, world, torch.device("cpu"))
+    hl = HeadlineDry(rank, world)
+    parity = {}
+    for it in hl.items:
+        want = (it["A"].double() @ it["B"].double()).float()
+        torch.matmul(it["A"], it["B"], out=it["C"])
+        parity["c5_square_%d_rank%d" % (it["n_full"], rank)] = {
+            "status": "exact" if torch.equal(it["C"], want) else "MISMATCH", "rows": [it["shard"].start,
+                                                                                     it["shard"].stop]}
+    ms_total, clk = timed_steps(hl.step, args.steps, args.warmup, ranks, hl.sync, hl.clock)
+    flops = step_flops([it["n"] for it in hl.items])
+    rows_seen = ranks.gather_obj({str(it["n_full"]): [it["shard"].start, it["shard"].stop] for it in hl.items})
+    all_parity = {}
+    for p in ranks.gather_obj(parity):
+        all_parity.update(p)
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": flops * args.steps / (ms_total * 1e-3) / 1e12, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "dry run: CPU torch.matmul stand-in at n/%d (not a bench value)" % DRY_SCALE,
+            "config": {"workload": "square_gemms_c5_dry_run", "sizes": [it["n"] for it in hl.items]},
+            "dry_run": True, "shards": rows_seen,
+            "parity": {"all_exact": all(v["status"] == "exact" for v in all_parity.values()), "checks": all_parity},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- entry
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="alcop", choices=["alcop", "reference"])
-    ap.add_argument("--quick", action="store_true", help="skip the n_stage sweep and the large square")
+    ap.add_argument("--quick", action="store_true", help="headline, its parity and e2e only")
     ap.add_argument("--schedule", default="tune", choices=["tune", "model"],
-                    help="tune: time the model's top schedules per shape (alcop_tune); model: its first pick")
-    ap.add_argument("--unfused-qkv", action="store_true", help="Q, K, V as three GEMMs (six launches per step)")
+                    help="BERT / BMM blocks: tune = time the model's top schedules (alcop_tune); model = first pick")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dry-run", action="store_true", help="CPU + gloo rank-logic run with a stand-in compute")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not under torchrun: launch one rank per GPU ourselves (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit("bench.py: --gpus %d but WORLD_SIZE=%d (one rank per GPU)" % (args.gpus, world))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    import torch
+    import torch.distributed as dist
     if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dry_run:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        main_gpu(args, rank, world, local_rank)
+        if args.dry_run:
+            main_dry(args, rank, world)
+        else:
+            main_gpu(args, rank, world, local_rank)
     finally:
         if world > 1:
-            import torch.distributed as dist
             dist.destroy_process_group()
 
 
