@@ -1,6 +1,13 @@
-"""SASS evidence for the production kernels (measurement tool): per kernel,
-counts of the tcgen05 / TMA / mbarrier mnemonics and the MMA-issue and
-TMA-issue loops.  python tools/sass_listing.py > profiles/sass_r01.txt"""
+"""SASS evidence for the kernels in libalcop.so (measurement tool).
+
+For every kernel: instruction count and counts of the tcgen05 / TMA / mbarrier
+mnemonics; for the production instantiations the bench times, the MMA-issue and
+TMA-issue sequences.  Exits non-zero (and writes nothing useful) if the
+library has no kernels or a production kernel lacks UTCHMMA / UTMALDG / LDTM —
+a listing that is only a header is a failure, not evidence.
+
+    python tools/sass_listing.py > profiles/sass_r02.txt
+"""
 import collections
 import os
 import re
@@ -9,41 +16,85 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2210_16691_b200", "libalcop.so")
-WANT = ["alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 0, false>",
-        "alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 64>",
-        "alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 1, false>"]
-KEYS = ("UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UTMAPF", "SYNCS", "UTCATOMSWS", "ELECT",
-        "FENCE", "ACQBULK")
+# (substring of the demangled name, what the bench runs it for)
+PRODUCTION = [
+    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 64, false, false>",
+     "CTA-pair GEMM (cta_group::2): C5 squares, BERT QKV / FFN1"),
+    ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 0, false, 4>",
+     "single-CTA GEMM: BERT FFN2 / O, attention PV, config-1 class"),
+    ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 0, false, 8>",
+     "single-CTA GEMM, 8 epilogue warps: attention QK^T (K = 64)"),
+    ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 1, false, 4>",
+     "implicit-GEMM conv, TMA im2col (C % 64 == 0)"),
+    ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 2, false, 4>",
+     "implicit-GEMM conv, 8-channel im2col boxes (small C)"),
+    ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 3, false, 4>",
+     "implicit-GEMM conv, stem (ResNet-50 conv1, halo-padded NHWC8)"),
+    ("alcop_chain_gemm_kernel<__nv_bfloat16, 64>", "several GEMMs in one persistent launch (alcop_gemm_chain)"),
+]
+KEYS = ("UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UTMAPF", "UTMACMDFLUSH", "SYNCS", "UTCATOMSWS",
+        "UTCBAR", "ELECT", "FENCE", "ACQBULK", "MEMBAR")
+REQUIRED = ("UTCHMMA", "UTMALDG", "LDTM")
+
+
+def kernels(sass):
+    for f in re.split(r"\n\s*Function : ", sass)[1:]:
+        mangled = f.split("\n", 1)[0].strip()
+        name = subprocess.run(["c++filt", mangled], capture_output=True, text=True).stdout.strip()
+        ins = [re.sub(r"/\* 0x[0-9a-f]+ \*/", "", l).strip() for l in f.split("\n")]
+        ins = [l for l in ins if re.match(r"^/\*[0-9a-f]{4}\*/", l)]
+        yield name, ins
+
+
+def mnemonic(line):
+    op = line.split("*/", 1)[1].strip().split()
+    if not op:
+        return ""
+    return (op[1] if op[0].startswith("@") and len(op) > 1 else op[0]).rstrip(";")
 
 
 def main():
-    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
-    funcs = re.split(r"\n\s*Function : ", sass)[1:]
-    print("# SASS of the production kernels (sm_100a, cuobjdump -sass %s)" % os.path.relpath(LIB, ROOT))
-    print("# UTCHMMA = tcgen05.mma, UTCBAR = tcgen05.commit, LDTM = tcgen05.ld, UTMALDG/UTMASTG = TMA load/store,")
-    print("# SYNCS.* = mbarrier ops (PHASECHK.TRYWAIT = wait, ARRIVE.TRANS64 = arrive.expect_tx), UTCATOMSWS = TMEM alloc")
-    for f in funcs:
-        mangled = f.split("\n", 1)[0].strip()
-        name = subprocess.run(["c++filt", mangled], capture_output=True, text=True).stdout.strip()
-        hit = [w for w in WANT if w in name]
-        if not hit:
-            continue
-        ins = [re.sub(r"/\* 0x[0-9a-f]+ \*/", "", l).strip() for l in f.split("\n")]
-        ins = [l for l in ins if re.match(r"^/\*[0-9a-f]{4}\*/", l)]
-        cnt = collections.Counter()
-        for l in ins:
-            op = l.split("*/", 1)[1].strip().split()
-            if not op:
-                continue
-            m = op[0] if not op[0].startswith("@") else op[1]
-            if m.startswith(KEYS):
-                cnt[m.rstrip(";")] += 1
-        print("\n## %s\n# %d instructions; key mnemonics:" % (name, len(ins)))
+    if not os.path.exists(LIB):
+        sys.exit("sass_listing: %s not built" % LIB)
+    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
+    rows = []
+    prod = {}
+    for name, ins in kernels(sass):
+        cnt = collections.Counter(m for m in map(mnemonic, ins) if m.startswith(KEYS))
+        short = re.sub(r"alcop::\(anonymous namespace\)::", "", name.split("(CUtensorMap")[0].split("(alcop::")[0])
+        rows.append((short, len(ins), cnt))
+        for key, why in PRODUCTION:
+            if key in name:
+                prod[key] = (why, name, ins, cnt)
+    if not rows:
+        sys.exit("sass_listing: no kernels in %s" % LIB)
+    missing = [k for k, _ in PRODUCTION if k not in prod]
+    weak = [k for k, (_, _, _, c) in prod.items() if not all(any(m.startswith(r) for m in c) for r in REQUIRED)]
+    if missing or weak:
+        sys.exit("sass_listing: production kernels missing %s / without %s: %s" % (missing, REQUIRED, weak))
+    print("# SASS of libalcop.so (sm_100a; cuobjdump -sass %s), %d kernels" % (os.path.relpath(LIB, ROOT), len(rows)))
+    print("# UTCHMMA = tcgen05.mma (kind::f16), UTCBAR = tcgen05.commit -> mbarrier, LDTM = tcgen05.ld,")
+    print("# UTMALDG / UTMASTG = TMA bulk-tensor load / store (.IM2COL = im2col mode, .2CTA = cta_group::2),")
+    print("# SYNCS.* = mbarrier ops (PHASECHK.TRANS64.TRYWAIT = try_wait.parity, ARRIVE.TRANS64 = arrive[.expect_tx]),")
+    print("# UTCATOMSWS = tcgen05.alloc / dealloc (TMEM)")
+    cols = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "SYNCS"]
+    print("\n## Per-kernel mnemonic counts (prefix match)\n%-96s %6s " % ("kernel", "instr") +
+          " ".join("%8s" % c for c in cols))
+    tot = collections.Counter()
+    for short, n, cnt in sorted(rows):
+        agg = {c: sum(v for k, v in cnt.items() if k.startswith(c)) for c in cols}
+        tot.update(agg)
+        print("%-96s %6d " % (short[:96], n) + " ".join("%8d" % agg[c] for c in cols))
+    print("%-96s %6s " % ("TOTAL", "") + " ".join("%8d" % tot[c] for c in cols))
+    for key, _ in PRODUCTION:
+        why, name, ins, cnt = prod[key]
+        print("\n## %s\n# %s\n# %d instructions; key mnemonics:" % (key, why, len(ins)))
         for k, v in sorted(cnt.items()):
             print("   %5d %s" % (v, k))
-        for key, title in (("UTCHMMA", "MMA issue (tcgen05.mma k-steps, then tcgen05.commit -> empty[slot])"),
-                           ("UTMALDG", "TMA issue (producer_commit: arrive.expect_tx + bulk-tensor loads)")):
-            idx = [i for i, l in enumerate(ins) if key in l]
+        for mark, title in (("UTCHMMA", "MMA issue: tcgen05.mma k-steps of one chunk, then tcgen05.commit -> empty[slot]"),
+                            ("UTMALDG", "TMA issue: producer_commit = arrive.expect_tx + bulk-tensor loads"),
+                            ("LDTM", "epilogue: tcgen05.ld of the TMEM accumulator")):
+            idx = [i for i, l in enumerate(ins) if mark in l]
             if not idx:
                 continue
             lo, hi = max(0, idx[0] - 6), min(len(ins), idx[0] + 14)
