@@ -85,7 +85,7 @@ typedef struct {
  * reference cannot express it (stages >= 2, schedule.hpp:261), here it is
  * the in-run baseline variant (one slot: load -> wait -> use -> release). */
 typedef struct {
-  int64_t tileM, tileN, tileK; /* tile; tileM = 128 x cta_group           */
+  int64_t tileM, tileN, tileK; /* tile; tileM = 128 x cta_group; tileN 64..256 (512: pair, 1 accumulator) */
   int32_t n_stage_smem_A;      /* A_shared ring depth (outer level)     */
   int32_t n_stage_smem_B;      /* B_shared ring depth (outer level)     */
   int32_t n_stage_inner;       /* A_reg/B_reg level -> TMEM accumulator buffers (1|2) */

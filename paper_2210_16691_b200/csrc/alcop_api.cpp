@@ -168,8 +168,11 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "cta_group must be 1 or 2");
   if (s.tileM != kTileM * s.cta_group)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileM must be 128 x cta_group (UMMA M 128 / 256)");
-  if (s.tileN != 64 && s.tileN != 128 && s.tileN != 192 && s.tileN != 256)
-    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256");
+  if (s.tileN != 64 && s.tileN != 128 && s.tileN != 192 && s.tileN != 256 && s.tileN != 512)
+    return set_error(ALCOP_ERR_CONFIG, "BadTile", "tileN must be one of 64, 128, 192, 256 (512: CTA pair)");
+  if (s.tileN == 512 && (s.cta_group != 2 || s.n_stage_inner != 1 || s.stream_k != 0))
+    return set_error(ALCOP_ERR_CONFIG, "BadTile",
+                     "tileN 512 is the CTA-pair 256 x 512 tile: cta_group 2, one TMEM accumulator, whole tiles");
   if (s.cta_group == 2 && s.tileN == 64)
     return set_error(ALCOP_ERR_CONFIG, "BadTile", "cta_group 2 needs tileN 128, 192 or 256");
   if (s.stream_k != 0 && (s.stream_k != 1 || s.cta_group != 2 || s.mode != ALCOP_MODE_FUSED))

@@ -824,6 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
   const bool b_sw64 = (half_n & 63) != 0 && !p.b_pad;  // BN = 192: N-major halves of 96 columns
+  const bool wide = p.BN == 512;  // one 256 x 512 tile = two N = 256 MMAs per k-step, one TMEM accumulator
   if (threadIdx.x == 0) stamp<kDebug>(p, 0);
 
   if (warp == 0 && elect_one()) {
@@ -937,6 +938,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
               }
               const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
               if (kRole == 0) {
+              } else if (wide) {
+                // tileN 512: two N = 256 MMAs per k-step; MMA g reads cluster
+                // columns [256 g, 256 g + 256), 128 of them from each CTA, so
+                // this CTA stages columns 256 g + 128 rank + [0, 128) for g = 0, 1
+                const int nw = tc.nb * p.BN + static_cast<int>(rank) * 128;
+                if (p.b_mn_major) {
+                  for (int a = 0; a < 4; ++a)
+                    tma_load_3d_pair(dst + a * (BK * 128), &tmB, fb_leader, nw + (a >> 1) * 256 + (a & 1) * 64,
+                                     chunk * BK, tc.b);
+                } else {
+                  for (int a = 0; a < kKAtoms; ++a)
+                    for (int g = 0; g < 2; ++g)
+                      tma_load_3d_pair(dst + a * (256 * 128) + g * (128 * kBoxK * 2), &tmB, fb_leader,
+                                       chunk * BK + a * kBoxK, nw + g * 256, tc.b);
+                }
               } else if (p.b_mn_major && p.b_pad) {
                 tma_load_3d_pair(dst, &tmB, fb_leader, n0, chunk * BK, tc.b);
                 tma_load_3d_pair(dst + BK * 128, &tmB, fb_leader, n0 + 64, chunk * BK, tc.b);
@@ -997,6 +1013,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         b_small = 2;
         b_big = static_cast<uint32_t>(half_n) * 128 / 16;
       }
+      // tileN 512: the second MMA's 128 columns of this CTA's B (two 64-column
+      // atoms further for N-major B, 128 rows of kBoxK elements further in each
+      // K atom for K-major)
+      const uint32_t b_group = !wide ? 0u : p.b_mn_major ? 2u * BK * 128u / 16u : 128u * kBoxK * 2u / 16u;
       const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
       const uint32_t idesc = p.idesc;
       auto mma_seg = [&](int k, int cb, int ce) {
@@ -1019,7 +1039,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
               for (int u = 0; u < kSteps; ++u) {
                 const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, (v > cb || u > 0) ? 1u : 0u);
+                const uint32_t acc_flag = (v > cb || u > 0) ? 1u : 0u;
+                umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, acc_flag);
+                if (wide) umma_f16_ss_pair(d_tmem + 256, ad + a_off, bd + b_group + b_off, idesc, acc_flag);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
           ca.advance(p.sA);
         }
@@ -1481,7 +1503,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   } else if (w.b_layout == ALCOP_B_KN) {
     rc = encode_3d_dt(&tb, dt, B, w.N, w.K, w.batch, ldb * 2, sb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B, "B");
   } else {
-    rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN / cg, kswz, "B");
+    rc = encode_3d_dt(&tb, dt, B, w.K, w.N, w.batch, ldb * 2, sb * 2, kbox, BN == 512 ? 128 : BN / cg, kswz, "B");
   }
   if (rc) return rc;
   CUtensorMap tc;
@@ -1512,7 +1534,8 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   kp.tacc = s.n_stage_inner;
   kp.mode = s.mode;
   kp.b_mn_major = w.b_layout == ALCOP_B_KN ? 1 : 0;
-  kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM * cg, BN);
+  kp.idesc = ptx::make_idesc_f16(w.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM * cg,
+                                 BN > 256 ? 256 : BN);  // tileN 512 = two N = 256 MMAs
   kp.a_stage_bytes = static_cast<uint32_t>(kTileM * BK * 2);
   kp.b_stage_bytes = static_cast<uint32_t>((b_pad ? (BN / cg + 63) / 64 * 64 : BN / cg) * BK * 2);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));

@@ -172,6 +172,31 @@ def test_cta_pair_exact(alcop, tileN, tileK, st, mode, layout):
     _assert_exact(C, exact, torch.float32)
 
 
+@pytest.mark.parametrize("M,N,K,batch,tileK,st,mode,layout,out", [
+    (768, 1024, 640, 1, 64, 4, 1, 0, "f32"), (768, 1024, 640, 1, 64, 4, 1, 1, "f32"),
+    (512, 1536, 1024, 1, 64, 3, 0, 0, "bf16"), (300, 712, 200, 2, 64, 4, 1, 0, "f32"),
+    (300, 712, 200, 2, 64, 4, 1, 1, "bf16"), (1024, 2048, 512, 1, 128, 2, 1, 0, "bf16"),
+    (1024, 2048, 512, 1, 128, 2, 1, 1, "f32"), (256, 512, 64, 1, 32, 6, 1, 0, "f32"),
+    (2048, 512, 4096, 1, 64, 4, 1, 0, "bf16"), (640, 1000, 96, 3, 32, 5, 0, 1, "f32")])
+def test_cta_pair_wide_exact(alcop, M, N, K, batch, tileK, st, mode, layout, out):
+    """CTA pair with tileN 512: a 256 x 512 tile as two N = 256 tcgen05.mma per
+    k-step (each CTA stages columns 256g + 128 rank + [0,128) of B), one TMEM
+    accumulator of 512 columns; ragged M / N / K, batched, both B layouts."""
+    s = alcop.make_schedule(tileN=512, tileK=tileK, n_stage=st, n_stage_inner=1, mode=mode, cta_group=2)
+    out_dt = torch.float32 if out == "f32" else torch.bfloat16
+    C, exact = _run(alcop, M, N, K, batch=batch, b_layout=layout, sched=s, out_dt=out_dt, seed=M + N)
+    _assert_exact(C, exact, out_dt)
+
+
+def test_cta_pair_wide_rejections(alcop):
+    d = alcop.gemm_desc(1024, 1024, 1024)
+    for kw in (dict(cta_group=1, n_stage_inner=1), dict(cta_group=2, n_stage_inner=2),
+               dict(cta_group=2, n_stage_inner=1, stream_k=1)):
+        with pytest.raises(alcop.AlcopError) as ei:
+            alcop.validate(d, alcop.make_schedule(tileN=512, tileK=64, n_stage=4, **kw))
+        assert ei.value.rule in ("BadTile", "TmemCapacity", "SmemCapacity")
+
+
 def test_cta_pair_ragged_batched(alcop):
     s = alcop.make_schedule(tileN=128, tileK=64, n_stage=4, cta_group=2)
     C, exact = _run(alcop, 300, 200, 136, batch=3, sched=s)

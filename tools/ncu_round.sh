@@ -11,4 +11,6 @@ for c in ${CASES:-square16384 square4096 stem l1_3x3 l3_3x3 qkt pv o_proj ffn1 c
       -c 1 -o gpurun_out/ncu_$c -f python tools/profile_kernels.py $c --reps 1 > gpurun_out/ncu_$c.log 2>&1
   ncu -i gpurun_out/ncu_$c.ncu-rep --page raw --csv > gpurun_out/ncu_${c}_raw.csv 2>/dev/null
   echo "$c rc=$? $(wc -c < gpurun_out/ncu_${c}_raw.csv)"
+  # the report itself stays on the box (gpurun_out/ comes back only under 64 MiB)
+  mkdir -p /tmp/ncu_reps && mv gpurun_out/ncu_$c.ncu-rep /tmp/ncu_reps/
 done
