@@ -155,6 +155,15 @@ typedef struct {
   double tTile;          /* per output tile fixed cost, cycles */
   double overlapDRAM;    /* soft-max weight between the SM pipeline and HBM time */
   double tPair;          /* fixed extra cycles of a cta_group::2 (CTA-pair) launch */
+  /* Power-capped regime (new; tools/fit_power.py on profiles/power_r02.json):
+   * under sustained load the B200 holds its ~1 kW cap by lowering the SM
+   * clock, so a long kernel takes at least energy / power =
+   * tCapFlop * FLOPs + tCapL2Byte * (L2 -> SM bytes) + tCapDramByte * (DRAM bytes). */
+  double tCapFlop;          /* seconds per FLOP at the cap */
+  double tCapL2Byte;        /* seconds per L2 -> shared-memory (TMA) byte at the cap */
+  double tCapDramByte;      /* seconds per HBM byte at the cap */
+  double dramReusePair;     /* DRAM bytes / ideal grouped-raster bytes, CTA pairs, K <= 8192 */
+  double dramReusePairPerK; /* + per reduction element above 8192 (pairs drift apart over long K) */
 } alcop_hw;
 
 /* perf::LatencyBreakdown (perf_model.hpp:40-47); field names follow
@@ -167,6 +176,10 @@ typedef struct {
   int64_t bytesOneSmemLoop, bytesWorkset, bytesOutputTile;
   int64_t flopsOneRegLoop;
   double seconds; /* tKernel / clock (new) */
+  /* new: traffic and the power-capped bound */
+  double bytesL2;  /* L2 -> shared-memory TMA bytes of the whole launch (exact) */
+  double bytesDram; /* estimated HBM bytes (grouped raster, L2 reuse) */
+  double tPower;   /* energy / power-cap bound, cycles; tKernel = max(latency model, tPower) */
 } alcop_breakdown;
 
 /* One pipeline bookkeeping event (host enumerator and device trace).

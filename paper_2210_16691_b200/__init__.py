@@ -92,7 +92,9 @@ class HW(ctypes.Structure):
                 ("maxThreadblkPerSM", ctypes.c_int32), ("maxWarpsPerSM", ctypes.c_int32),
                 ("utilKneeWarps", ctypes.c_int32), ("tmemColsPerSM", ctypes.c_int32), ("clockGHz", ctypes.c_double),
                 ("tIssue", ctypes.c_double), ("tIssuePerBox", ctypes.c_double), ("tLaunch", ctypes.c_double),
-                ("tTile", ctypes.c_double), ("overlapDRAM", ctypes.c_double), ("tPair", ctypes.c_double)]
+                ("tTile", ctypes.c_double), ("overlapDRAM", ctypes.c_double), ("tPair", ctypes.c_double),
+                ("tCapFlop", ctypes.c_double), ("tCapL2Byte", ctypes.c_double), ("tCapDramByte", ctypes.c_double),
+                ("dramReusePair", ctypes.c_double), ("dramReusePairPerK", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -103,7 +105,8 @@ class Breakdown(ctypes.Structure):
                                                 "tSmemLoad", "tRegLoad", "tSmemUse", "tCompute")] + \
                [(n, ctypes.c_int64) for n in ("nThreadblkBatch", "nThreadblkPerSM", "nThreadblkPerBatch",
                                                "nSmemLoop", "nRegLoop", "bytesOneSmemLoop", "bytesWorkset",
-                                               "bytesOutputTile", "flopsOneRegLoop")] + [("seconds", ctypes.c_double)]
+                                               "bytesOutputTile", "flopsOneRegLoop")] + \
+               [(n, ctypes.c_double) for n in ("seconds", "bytesL2", "bytesDram", "tPower")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -292,9 +295,14 @@ def enumerate_pipeline(num_tiles, E, sA, sB, mode, role):
     return [{f: getattr(arr[i], f) for f in EVENT_FIELDS} for i in range(n.value)]
 
 
-def hw_b200() -> HW:
+def hw_b200(burst: bool = False) -> HW:
+    """B200 model constants.  Default: the sustained (power-capped) regime a
+    long run of GEMMs is in; burst=True zeroes the power-cap terms (a kernel
+    timed alone, in short bursts, at full clock)."""
     h = HW()
     load_library().alcop_hw_default_b200(ctypes.byref(h))
+    if burst:
+        h.tCapFlop = h.tCapL2Byte = h.tCapDramByte = 0.0
     return h
 
 

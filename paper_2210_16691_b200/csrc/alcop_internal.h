@@ -34,6 +34,21 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s);
 int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,
                 alcop_event* trace, int64_t trace_cap, void* stream);
 int device_sm_count();
+// Tile rows per raster group for `units` concurrent CTAs (cta_group 1) or CTA
+// pairs: schedule.raster if set, else the group minimising the distinct
+// A-row + B-column panels the tiles in flight touch (G*BM + (units/G)*BN ->
+// G = sqrt(units*BN/BM)); one wave: plain m-fastest order.
+inline int32_t raster_group_of(int32_t raster, int64_t units, int64_t num_m, int64_t num_n, int64_t BM, int64_t BN) {
+  if (raster > 0) return raster;
+  if (units < 1) units = 1;
+  if (num_m * num_n <= units) return static_cast<int32_t>(num_m);
+  double x = static_cast<double>(units) * static_cast<double>(BN) / static_cast<double>(BM);
+  int64_t g = 1;
+  while ((g + 1) * (g + 1) <= x) ++g;  // floor(sqrt(x)), then round to nearest
+  if ((g + 0.5) * (g + 0.5) <= x) ++g;
+  if (g < 1) g = 1;
+  return static_cast<int32_t>(g < num_m ? g : num_m);
+}
 int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt, void* y,
                   void* stream);
 

@@ -1438,13 +1438,9 @@ int device_sm_count() {
 // that minimises the distinct A-row + B-column panels touched by the tiles in
 // flight at once (W = CTAs / cg): G*BM + (W/G)*BN  ->  G = sqrt(W*BN/BM).
 static int32_t raster_group(const alcop_schedule& s, int num_m, int num_n, int BM, int BN, int cg) {
-  if (s.raster > 0) return s.raster;
   const int ctas = s.num_ctas > 0 ? s.num_ctas : device_sm_count();
   const int W = ctas / cg > 0 ? ctas / cg : 1;
-  if (num_m * num_n <= W) return num_m;  // a single wave: order does not matter
-  int g = static_cast<int>(std::sqrt(static_cast<double>(W) * BN / BM) + 0.5);
-  if (g < 1) g = 1;
-  return g < num_m ? g : num_m;
+  return raster_group_of(s.raster, W, num_m, num_n, BM, BN);
 }
 
 int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,

@@ -103,6 +103,12 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->tTile = 38.38;
   hw->overlapDRAM = 0.20;
   hw->tPair = 3716;
+  // power-capped regime: tools/fit_power.py on profiles/power_r02.json
+  hw->tCapFlop = 5.1788e-16;     // s / FLOP
+  hw->tCapL2Byte = 2.5811e-14;   // s / L2 -> SM byte
+  hw->tCapDramByte = 3.4288e-14; // s / HBM byte
+  hw->dramReusePair = 1.2;
+  hw->dramReusePairPerK = 0.000226;
 }
 
 extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
@@ -170,6 +176,34 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   const double sm = out->tSmemLoad + body + (cg == 2 ? hw->tPair : 0.0);
   const double dram = static_cast<double>(out->bytesWorkset + w->M * w->N * ob * w->batch) / hw->bwDRAM;
   out->tKernel = hw->tLaunch + std::max(sm, dram) + hw->overlapDRAM * std::min(sm, dram);
+
+  // Power-capped regime (not in the reference's model): L2 -> SM bytes are
+  // exact (every tile loads its A rows and B columns for every chunk); HBM
+  // bytes follow the grouped raster — per wave of `units` tiles, G A-row and
+  // units/G B-column panels of K elements come from HBM — times the measured
+  // re-read factor (~1.05 for single CTAs; CTA pairs drift apart over long K
+  // and re-read more, profiles/power_r02.json), never below compulsory.
+  const int64_t num_m = (w->M + tM - 1) / tM, num_n = (w->N + tN - 1) / tN;
+  // (WRAP mode re-loads s-1 wrapped chunks per tile, pipeline_pass.hpp:501-509)
+  out->bytesL2 = static_cast<double>(tiles) * static_cast<double>(loads) * static_cast<double>(tM + bcols * cg) *
+                 static_cast<double>(tK * eb);
+  const double compulsory = static_cast<double>(out->bytesWorkset + w->M * w->N * ob * w->batch);
+  double dramEst = compulsory;
+  if (static_cast<double>(out->bytesWorkset) / w->batch > 0.5 * 126e6) {
+    const int64_t G = raster_group_of(s->raster, units, num_m, num_n, tM, tN);
+    const double waves_f = static_cast<double>(tiles) / static_cast<double>(units);
+    const double panels = static_cast<double>(G * tM) + static_cast<double>(units) / G * static_cast<double>(tN);
+    double kappa = 1.05;
+    if (cg == 2)
+      kappa = std::min(2.6, hw->dramReusePair + hw->dramReusePairPerK * std::max<double>(0.0, w->K - 8192.0));
+    dramEst = std::max(compulsory, kappa * waves_f * panels * static_cast<double>(w->K * eb) +
+                                       static_cast<double>(w->M * w->N * ob * w->batch));
+  }
+  out->bytesDram = dramEst;
+  const double flops = 2.0 * static_cast<double>(w->M) * w->N * w->K * w->batch;
+  const double tPowerS = hw->tCapFlop * flops + hw->tCapL2Byte * out->bytesL2 + hw->tCapDramByte * dramEst;
+  out->tPower = tPowerS * hw->clockGHz * 1e9;
+  out->tKernel = std::max(out->tKernel, out->tPower);
   out->seconds = out->tKernel / (hw->clockGHz * 1e9);
   return ALCOP_OK;
 }
@@ -177,13 +211,18 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
 extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out) {
   if (!w || !hw || !out) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
   clear_error();
+  // candidates the power bound ties (same FLOPs and bytes, e.g. tileK 32 vs 64
+  // of one tile) are ranked by the latency model alone
+  alcop_hw lat_hw = *hw;
+  lat_hw.tCapFlop = lat_hw.tCapL2Byte = lat_hw.tCapDramByte = 0;
+  double best_lat = 1e300;
   // enumerate_space + analytical_rank (tuner.hpp:48-80) over the B200 design
   // space: cta_group x tileN x tileK x n_stage (equal for A and B) x n_stage_inner, FUSED
   double best = 1e300;
   alcop_schedule bestS{};
   bool found = false;
   for (int cg = 1; cg <= 2; ++cg)
-  for (int tN : {64, 128, 192, 256})
+  for (int tN : {64, 128, 192, 256, 512})  // 512: the CTA-pair 256 x 512 tile (one accumulator)
     for (int tK : {32, 64, 128})
       for (int inner = 2; inner >= 1; --inner)
         for (int st = 8; st >= 1; --st) {
@@ -197,10 +236,14 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
           s.n_stage_inner = inner;
           s.mode = ALCOP_MODE_FUSED;
           if (validate_gemm(*w, s) != ALCOP_OK) continue;
-          alcop_breakdown b;
+          alcop_breakdown b, bl;
           if (alcop_predict(w, &s, hw, &b) != ALCOP_OK) continue;
-          if (b.tKernel < best * (1.0 - 1e-9)) {  // ties keep the deeper pipeline
+          if (alcop_predict(w, &s, &lat_hw, &bl) != ALCOP_OK) continue;
+          const bool better = b.tKernel < best * (1.0 - 1e-9) ||
+                              (b.tKernel <= best * (1.0 + 1e-9) && bl.tKernel < best_lat * (1.0 - 1e-9));
+          if (better) {  // full ties keep the deeper pipeline (enumerated first)
             best = b.tKernel;
+            best_lat = bl.tKernel;
             bestS = s;
             found = true;
           }

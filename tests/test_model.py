@@ -93,7 +93,7 @@ def test_fit_script_restates_the_product_model(alcop):
     constants would not mean what model.cpp uses them for."""
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import fit_model
-    hw = alcop.hw_b200()
+    hw = alcop.hw_b200(burst=True)
     P = {"tp": hw.throughputSM, "bwL2": hw.bwLLC, "t_issue": hw.tIssue, "t_issue_b": hw.tIssuePerBox,
          "lat": hw.latLLCRead, "bwW": hw.bwDRAMWrite, "epi0": hw.latDRAMWrite, "launch": hw.tLaunch,
          "bwD": hw.bwDRAM, "tile0": hw.tTile, "ovl": hw.overlapDRAM, "bwSM": hw.bwSmem, "pair0": hw.tPair}
@@ -103,6 +103,35 @@ def test_fit_script_restates_the_product_model(alcop):
         d = alcop.gemm_desc(r["M"], r["N"], r["K"], r["batch"], alcop.BF16, alcop.BF16, alcop.B_KN)
         s = alcop.make_schedule(tileN=r["tileN"], tileK=r["tileK"], n_stage=r["stages"], n_stage_inner=r["inner"],
                                 mode=r["mode"], cta_group=r.get("cg", 1))
-        want = alcop.predict(d, s)["tKernel"]
+        want = alcop.predict(d, s, hw)["tKernel"]
         got = fit_model.predict_cycles(r, P)
         assert abs(got - want) <= 1e-6 * want, (r, got, want)
+
+
+def test_power_capped_model_fit(alcop):
+    """The power-cap terms (alcop_hw.tCap*) are the non-negative least-squares
+    fit of tools/fit_power.py to the sustained measurements in
+    profiles/power_r02.json (30 schedules x sizes): compiled defaults equal the
+    fit, the fit is within 10% rms, and each problem size left out of the fit
+    is predicted within 15% rms."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import numpy as np
+    import fit_power
+    data = fit_power.rows()
+    X, y = fit_power.design(data)
+    coef = fit_power.fit(X, y)
+    hw = alcop.hw_b200()
+    assert np.allclose([hw.tCapFlop, hw.tCapL2Byte, hw.tCapDramByte], coef, rtol=0.02)
+    err = (X @ coef - y) / y
+    assert np.sqrt(np.mean(err ** 2)) <= 0.10
+    for n, e in fit_power.held_out(data).items():
+        assert np.sqrt(np.mean(np.square(e))) <= 0.15, (n, e)
+
+
+def test_power_regime_picks_the_wide_pair_tile_for_squares(alcop):
+    """Sustained regime: the model's pick for the C5 squares is the 256 x 512
+    CTA-pair tile, the measured fastest class at the power cap
+    (profiles/power_r02.json: 1398-1425 vs 1151-1194 TFLOP/s for 256 x 256)."""
+    for n in (8192, 12288, 16384):
+        s = alcop.choose_schedule(alcop.gemm_desc(n, n, n))
+        assert (s.cta_group, s.tileN, s.n_stage_inner) == (2, 512, 1), (n, s)

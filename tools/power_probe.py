@@ -43,13 +43,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="time", choices=["time", "ncu"])
     ap.add_argument("--seconds", type=float, default=1.5)
+    ap.add_argument("--sizes", default=",".join(map(str, SIZES)))
+    ap.add_argument("--scheds", default="", help="name=tileN:tileK:stages:cta_group:inner:raster,... (default: SCHEDS)")
     a = ap.parse_args()
+    scheds = SCHEDS
+    if a.scheds:
+        scheds = {}
+        for item in a.scheds.split(","):
+            name, spec = item.split("=")
+            tn, tk, st, cg, inner, r = map(int, spec.split(":"))
+            scheds[name] = dict(tileN=tn, tileK=tk, n_stage=st, cta_group=cg, n_stage_inner=inner, raster=r)
     res = []
-    for n in SIZES:
+    for n in map(int, a.sizes.split(",")):
         A = (torch.rand(n, n, device="cuda") - 0.5).to(torch.bfloat16)
         B = (torch.rand(n, n, device="cuda") - 0.5).to(torch.bfloat16)
         C = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
-        for name, kw in SCHEDS.items():
+        for name, kw in scheds.items():
             s = alcop.make_schedule(**kw)
             alcop.matmul(A, B, s, out=C)
             torch.cuda.synchronize()
