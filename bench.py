@@ -598,9 +598,12 @@ def main_gpu(args, rank, world, local_rank):
             cands = []
             pick = it["sched"]
             pick_key = (pick.tileN, pick.tileK, pick.cta_group, pick.n_stage_smem_A)
-            for tn, tk, cg in cand_tiles:
-                for st in (3, 4, 5, 6, 7):
-                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg)
+            for tn, tk, cg in cand_tiles + ((512, 32, 2), (512, 64, 2), (512, 128, 2)):
+                for st in (2, 3, 4, 5, 6, 7, 8):
+                    if tn != 512 and st in (2, 8):
+                        continue
+                    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg,
+                                            n_stage_inner=1 if tn == 512 else 2)
                     try:
                         alcop.validate(it["desc"], s)
                     except alcop.AlcopError:
