@@ -275,6 +275,39 @@ int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, con
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
                  void* stream);
 
+/* ---- multi-GPU driver (new: the reference runs its parallel
+ * b / i0 / j0 loops sequentially, interp.hpp:330-338) --------------------
+ * The units that shard — rows of A and C (M-sharded GEMM, B replicated),
+ * batch entries (batched GEMM) or images (conv, filter replicated) — split
+ * contiguously over `nshards` in multiples of `granule` (earlier shards take
+ * the remainder granules); no collective on the compute path.  One host
+ * thread per shard sets its device and enqueues that shard's launch on its
+ * stream; the call returns when every shard is enqueued (stream-ordered per
+ * device; synchronise each shard's stream for the results).  Several shards
+ * may name the same device (distinct streams run concurrently). */
+typedef struct {
+  int32_t device;  /* CUDA device ordinal */
+  void* stream;    /* that device's stream (NULL: its legacy default stream) */
+  const void* A;   /* GEMM: this shard's rows (or batch entries) of A; conv: its images of x */
+  const void* B;   /* the replica of B (conv: of the filter) on `device` */
+  void* C;         /* this shard's rows / batch entries of C (conv: its images of y) */
+} alcop_shard;
+
+/* [*start, *start + *count): shard `rank` of `total` units over `world`
+ * shards in `granule` multiples (bench.py and paper_2210_16691_b200/sharded.py
+ * use the same split). */
+int alcop_shard_range(int64_t total, int32_t rank, int32_t world, int64_t granule, int64_t* start,
+                      int64_t* count);
+/* Sharded GEMM: batch == 1 shards M (granule >= 1 rows; 256 = one CTA-pair tile
+ * row), batch > 1 shards the batch.  s == NULL: the model's pick per shard
+ * shape (alcop_choose_schedule with the B200 defaults); empty shards launch
+ * nothing.  Packed tensors only (no lda/ldb/ldc, no batch strides). */
+int alcop_gemm_sharded(const alcop_gemm_desc* w, const alcop_schedule* s, int32_t nshards,
+                       const alcop_shard* shards, int64_t granule);
+/* Batch-sharded implicit-GEMM conv2d (images split one by one). */
+int alcop_conv2d_sharded(const alcop_conv_desc* d, const alcop_schedule* s, int32_t nshards,
+                         const alcop_shard* shards);
+
 /* ---- analytical model (perf_model.hpp:157-187, tuner.hpp:68-80) -------- */
 void alcop_hw_default_b200(alcop_hw* hw);
 void alcop_hw_default_a100_reference(alcop_hw* hw); /* perf_model.hpp:14-30 defaults */

@@ -40,7 +40,8 @@ EXPORTED_SYMBOLS = [
     "alcop_gemm_workspace_bytes", "alcop_gemm_host", "alcop_gemm_host_async", "alcop_conv2d", "alcop_hw_default_b200",
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
     "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
-    "alcop_gemm_chain_workspace_bytes", "alcop_gemm_chain",
+    "alcop_gemm_chain_workspace_bytes", "alcop_gemm_chain", "alcop_shard_range", "alcop_gemm_sharded",
+    "alcop_conv2d_sharded",
 ]
 
 
@@ -59,6 +60,12 @@ class Chain(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("dep", ctypes.c_int32 * CHAIN_MAX), ("desc", GemmDesc * CHAIN_MAX),
                 ("A", ctypes.c_void_p * CHAIN_MAX), ("B", ctypes.c_void_p * CHAIN_MAX),
                 ("C", ctypes.c_void_p * CHAIN_MAX)]
+
+
+class Shard(ctypes.Structure):
+    """alcop_shard: one shard of the multi-GPU driver (device, stream, operands)."""
+    _fields_ = [("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("A", ctypes.c_void_p),
+                ("B", ctypes.c_void_p), ("C", ctypes.c_void_p)]
 
 
 class Schedule(ctypes.Structure):
@@ -201,6 +208,10 @@ def load_library(path: str | None = None):
         lib.alcop_gemm_host_async.argtypes = lib.alcop_gemm_host.argtypes
     lib.alcop_conv2d.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.c_void_p]
+    lib.alcop_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                      P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.alcop_gemm_sharded.argtypes = [P(GemmDesc), P(Schedule), ctypes.c_int32, P(Shard), ctypes.c_int64]
+    lib.alcop_conv2d_sharded.argtypes = [P(ConvDesc), P(Schedule), ctypes.c_int32, P(Shard)]
     lib.alcop_hw_default_b200.argtypes = [P(HW)]
     lib.alcop_hw_default_b200.restype = None
     lib.alcop_hw_default_a100_reference.argtypes = [P(HW)]
@@ -649,3 +660,31 @@ def gemm_chain(gemms, sched: Schedule, dep=None, b_layout=B_KN, workspace=None, 
     _check(lib.alcop_gemm_chain(ctypes.byref(ch), ctypes.byref(sched), ctypes.c_void_p(workspace.data_ptr()),
                                 _stream_ptr(stream)))
     return ch
+
+
+# ---------------------------------------------------------------- multi-GPU driver (C ABI)
+def shard_range(total, rank, world, granule=1):
+    """alcop_shard_range: (start, count) of shard `rank`."""
+    a, n = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load_library().alcop_shard_range(total, rank, world, granule, ctypes.byref(a), ctypes.byref(n)))
+    return a.value, n.value
+
+
+def gemm_sharded(desc: GemmDesc, shards, sched: Schedule | None = None, granule=256):
+    """alcop_gemm_sharded: shards = [(device, stream, A_shard, B_replica, C_shard)] with torch CUDA tensors
+    (A/C: this shard's rows, or batch entries when desc.batch > 1); one host thread per shard."""
+    arr = (Shard * len(shards))()
+    for i, (dev, st, A, B, C) in enumerate(shards):
+        arr[i] = Shard(dev, st.cuda_stream if st is not None else None, A.data_ptr() if A is not None else None,
+                       B.data_ptr() if B is not None else None, C.data_ptr() if C is not None else None)
+    _check(load_library().alcop_gemm_sharded(ctypes.byref(desc), ctypes.byref(sched) if sched is not None else None,
+                                             len(shards), arr, granule))
+
+
+def conv2d_sharded(desc: ConvDesc, sched: Schedule, shards):
+    """alcop_conv2d_sharded: shards = [(device, stream, x_images, w_replica, y_images)]."""
+    arr = (Shard * len(shards))()
+    for i, (dev, st, x, w, y) in enumerate(shards):
+        arr[i] = Shard(dev, st.cuda_stream if st is not None else None, x.data_ptr() if x is not None else None,
+                       w.data_ptr() if w is not None else None, y.data_ptr() if y is not None else None)
+    _check(load_library().alcop_conv2d_sharded(ctypes.byref(desc), ctypes.byref(sched), len(shards), arr))

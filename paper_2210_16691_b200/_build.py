@@ -15,7 +15,8 @@ EXTRA = os.environ.get("ALCOP_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_sm100.cu", "chain_sm100.cu"]
-CPP_SOURCES = ["alcop_api.cpp", "schedule.cpp", "model.cpp", "ir_frontend.cpp", "tuner.cpp", "sim.cpp"]
+CPP_SOURCES = ["alcop_api.cpp", "schedule.cpp", "model.cpp", "ir_frontend.cpp", "tuner.cpp", "sim.cpp",
+               "sharded.cpp"]
 
 
 def _sources():

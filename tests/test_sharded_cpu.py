@@ -84,3 +84,27 @@ def test_gloo_two_ranks_gather_equals_oracle():
         assert ok_m and ok_b
         assert tmax == float(world)
     assert out[0][3] == 0 and out[0][4] == out[1][3] and out[1][4] == 300
+
+
+@pytest.mark.parametrize("total,world,granule", [(16384, 8, 256), (4096, 3, 256), (1000, 4, 128), (192, 8, 1),
+                                                 (256, 5, 1), (7, 8, 1), (0, 2, 1), (300, 2, 256)])
+def test_abi_shard_range_matches_python(total, world, granule):
+    """alcop_shard_range (the C ABI multi-GPU driver's split) == sharded.shard_range (bench / gloo tests)."""
+    import paper_2210_16691_b200 as alcop
+    from paper_2210_16691_b200.sharded import shard_range
+    for r in range(world):
+        sh = shard_range(total, r, world, granule)
+        assert alcop.shard_range(total, r, world, granule) == (sh.start, sh.size)
+
+
+def test_abi_sharded_rejects_bad_shards():
+    import ctypes
+    import paper_2210_16691_b200 as alcop
+    lib = alcop.load_library()
+    d = alcop.gemm_desc(1024, 1024, 1024)
+    assert lib.alcop_gemm_sharded(ctypes.byref(d), None, 0, None, 256) == alcop.ALCOP_ERR_CONFIG
+    assert lib.alcop_last_error().decode().startswith("BadShards")
+    arr = (alcop.Shard * 1)(alcop.Shard(99, None, 16, 16, 16))
+    assert lib.alcop_gemm_sharded(ctypes.byref(d), None, 1, arr, 256) == alcop.ALCOP_ERR_CUDA
+    d.ldc = 2048
+    assert lib.alcop_gemm_sharded(ctypes.byref(d), None, 1, arr, 256) == alcop.ALCOP_ERR_CONFIG
