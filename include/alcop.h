@@ -95,9 +95,11 @@ typedef struct {
   int32_t raster;              /* tile rows per raster group; 0 = auto  */
   int32_t stream_k;            /* CTA pair, FUSED: 1 = split the output tiles' chunk stream
                                   evenly over the clusters (a tile cut between two clusters
-                                  is finished from an fp32 partial); the partials live in one
-                                  per-device workspace, so stream_k launches must not run
-                                  concurrently on two streams.  0 = whole tiles per cluster */
+                                  is finished from an fp32 partial); the partials live in the
+                                  device's stream-K workspace (alcop_set_stream_k_workspace), so
+                                  stream_k launches must not run concurrently on two streams;
+                                  without a large enough workspace the launch runs whole
+                                  tiles.  0 = whole tiles per cluster */
 } alcop_schedule;
 
 /* ---- several GEMMs in one persistent launch (new; no reference form) ------
@@ -271,6 +273,14 @@ int alcop_gemm_host(const alcop_gemm_desc* w, const alcop_schedule* s, const voi
 int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, const void* hA, const void* hB,
                           void* hC, void* workspace, void* stream);
 
+/* Stream-K workspace of the current device (caller-owned device memory; the
+ * library never allocates it): fp32 partials + hand-off flags.  bytes =
+ * alcop_stream_k_workspace_bytes(w, s) covers that problem/schedule; the call
+ * zeroes the flags (cudaMemset on the legacy stream, synchronised).  NULL
+ * unregisters.  Register before capturing stream_k launches in a graph. */
+int64_t alcop_stream_k_workspace_bytes(const alcop_gemm_desc* w, const alcop_schedule* s);
+int alcop_set_stream_k_workspace(void* workspace, int64_t bytes);
+
 /* Implicit-GEMM conv2d (new; the reference excludes it). */
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
                  void* stream);
@@ -326,14 +336,17 @@ typedef struct {
  * AnalyticalOnly method of tuner.hpp:407-413 with measure_ground_truth,
  * pipe_sim.hpp:195-239, replaced by the GPU): enumerate the B200 space,
  * rank by alcop_predict, time the top `budget` schedules on the caller's
- * buffers (steady-state CUDA-graph timing over rotating copies > 2x L2),
+ * buffers (steady-state CUDA-graph timing over rotating copies > 2x L2,
+ * placed in the caller's `workspace` of alcop_tune_workspace_bytes(w)),
  * return the fastest in *best.  Whole-tile schedules only: stream_k is an
  * explicit opt-in (its workspace is shared per device). 
  * `trials` (may be NULL) receives up to `trials_cap` measured candidates in
  * rank order; *n_trials their count. */
 int alcop_tune(const alcop_gemm_desc* w, const alcop_hw* hw, int32_t budget, const void* A, const void* B, void* C,
-               void* stream, alcop_schedule* best, alcop_tune_trial* trials, int32_t trials_cap,
-               int32_t* n_trials);
+               void* workspace, int64_t workspace_bytes, void* stream, alcop_schedule* best,
+               alcop_tune_trial* trials, int32_t trials_cap, int32_t* n_trials);
+/* Device bytes alcop_tune needs for its rotating operand copies (> 2 x L2). */
+int64_t alcop_tune_workspace_bytes(const alcop_gemm_desc* w);
 
 /* ---- event-level pipeline simulation (pipe_sim.hpp:16-167) ------------ */
 /* SimConfig (pipe_sim.hpp:16-22): nMplx workers share one compute unit, each

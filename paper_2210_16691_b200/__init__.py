@@ -41,7 +41,8 @@ EXPORTED_SYMBOLS = [
     "alcop_hw_default_a100_reference", "alcop_predict", "alcop_choose_schedule", "alcop_ir_to_gemm",
     "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
     "alcop_gemm_chain_workspace_bytes", "alcop_gemm_chain", "alcop_shard_range", "alcop_gemm_sharded",
-    "alcop_conv2d_sharded",
+    "alcop_conv2d_sharded", "alcop_tune_workspace_bytes", "alcop_stream_k_workspace_bytes",
+    "alcop_set_stream_k_workspace",
 ]
 
 
@@ -220,7 +221,13 @@ def load_library(path: str | None = None):
     lib.alcop_choose_schedule.argtypes = [P(GemmDesc), P(HW), P(Schedule)]
     lib.alcop_ir_to_gemm.argtypes = [ctypes.c_char_p, P(GemmDesc), P(Schedule), ctypes.c_char_p, ctypes.c_size_t]
     lib.alcop_tune.argtypes = [P(GemmDesc), P(HW), ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                               ctypes.c_void_p, P(Schedule), P(TuneTrial), ctypes.c_int32, P(ctypes.c_int32)]
+                               ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, P(Schedule), P(TuneTrial),
+                               ctypes.c_int32, P(ctypes.c_int32)]
+    lib.alcop_tune_workspace_bytes.argtypes = [P(GemmDesc)]
+    lib.alcop_tune_workspace_bytes.restype = ctypes.c_int64
+    lib.alcop_stream_k_workspace_bytes.argtypes = [P(GemmDesc), P(Schedule)]
+    lib.alcop_stream_k_workspace_bytes.restype = ctypes.c_int64
+    lib.alcop_set_stream_k_workspace.argtypes = [ctypes.c_void_p, ctypes.c_int64]
     lib.alcop_simulate_pipeline.argtypes = [P(SimConfig), P(SimResult), P(SimEvent), ctypes.c_int64,
                                             P(ctypes.c_int64)]
     lib.alcop_simulate_two_level.argtypes = [P(SimConfig), P(SimConfig), ctypes.c_int32, P(ctypes.c_double)]
@@ -623,14 +630,18 @@ def tune(A, B, C, budget=8, b_layout=B_KN, hw: HW | None = None, stream=None):
     M, K = A.shape[-2], A.shape[-1]
     N = B.shape[-1] if b_layout == B_KN else B.shape[-2]
     d = gemm_desc(M, N, K, A.shape[0] if batched else 1, _dtype_code(A.dtype), _dtype_code(C.dtype), b_layout)
+    import torch
     best = Schedule()
     cap = max(1, budget)
     arr = (TuneTrial * cap)()
     n = ctypes.c_int32(0)
-    _check(load_library().alcop_tune(ctypes.byref(d), ctypes.byref(hw or hw_b200()), budget,
-                                     ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                                     ctypes.c_void_p(C.data_ptr()), _stream_ptr(stream), ctypes.byref(best), arr, cap,
-                                     ctypes.byref(n)))
+    lib = load_library()
+    wsb = lib.alcop_tune_workspace_bytes(ctypes.byref(d))
+    ws = torch.empty(max(1, wsb), dtype=torch.uint8, device=A.device)  # caller-owned (the library never allocates)
+    _check(lib.alcop_tune(ctypes.byref(d), ctypes.byref(hw or hw_b200()), budget, ctypes.c_void_p(A.data_ptr()),
+                          ctypes.c_void_p(B.data_ptr()), ctypes.c_void_p(C.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                          wsb, _stream_ptr(stream), ctypes.byref(best), arr, cap, ctypes.byref(n)))
+    del ws
     return best, [{"schedule": arr[i].schedule.as_dict(), "predicted_s": arr[i].predicted_s,
                    "measured_s": arr[i].measured_s} for i in range(n.value)]
 
@@ -688,3 +699,18 @@ def conv2d_sharded(desc: ConvDesc, sched: Schedule, shards):
         arr[i] = Shard(dev, st.cuda_stream if st is not None else None, x.data_ptr() if x is not None else None,
                        w.data_ptr() if w is not None else None, y.data_ptr() if y is not None else None)
     _check(load_library().alcop_conv2d_sharded(ctypes.byref(desc), ctypes.byref(sched), len(shards), arr))
+
+
+_SK_WS = {}
+
+
+def set_stream_k_workspace(nbytes=64 << 20, device=None):
+    """Registers a caller-owned stream-K workspace (fp32 partials + flags) for
+    the current device (alcop_set_stream_k_workspace); kept alive here."""
+    import torch
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _check(load_library().alcop_set_stream_k_workspace(ctypes.c_void_p(ws.data_ptr()), nbytes))
+    _SK_WS[dev.index] = ws
+    return ws

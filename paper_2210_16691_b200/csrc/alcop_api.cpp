@@ -428,6 +428,20 @@ int alcop_gemm_chain(const alcop_chain* ch, const alcop_schedule* s, void* works
   return launch_chain(*ch, *s, workspace, stream);
 }
 
+int64_t alcop_stream_k_workspace_bytes(const alcop_gemm_desc* w, const alcop_schedule* s) {
+  if (!w || !s || validate_gemm(*w, *s) != ALCOP_OK || s->cta_group != 2) return 0;
+  const int sms = device_sm_count() > 0 ? device_sm_count() : 148;
+  const int64_t grid = (s->num_ctas > 0 ? s->num_ctas : sms) / 2;
+  const int64_t tiles = ((w->M + 255) / 256) * ((w->N + s->tileN - 1) / s->tileN) * w->batch;
+  const int n = static_cast<int>(std::min<int64_t>(grid, tiles));
+  return static_cast<int64_t>(sk_bytes_needed(n, static_cast<int>(s->tileN)));
+}
+
+int alcop_set_stream_k_workspace(void* workspace, int64_t bytes) {
+  clear_error();
+  return set_sk_workspace(workspace, bytes);
+}
+
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* wt, void* y,
                  void* stream) {
   if (!d || !s || !x || !wt || !y) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");

@@ -34,6 +34,10 @@ int validate_gemm(const alcop_gemm_desc& w, const alcop_schedule& s);
 int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A, const void* B, void* C,
                 alcop_event* trace, int64_t trace_cap, void* stream);
 int device_sm_count();
+// stream-K workspace (gemm_sm100.cu): bytes for n clusters of 256 x BN fp32
+// partials + flags; registration for the current device
+size_t sk_bytes_needed(int n_clusters, int BN);
+int set_sk_workspace(void* ptr, int64_t bytes);
 // Tile rows per raster group for `units` concurrent CTAs (cta_group 1) or CTA
 // pairs: schedule.raster if set, else the group minimising the distinct
 // A-row + B-column panels the tiles in flight touch (G*BM + (units/G)*BN ->

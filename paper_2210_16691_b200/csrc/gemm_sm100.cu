@@ -1259,48 +1259,61 @@ int encode_3d_dt(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint6
   return ALCOP_OK;
 }
 
-// Stream-K workspace, one per device, grown on demand and kept: the fp32
-// partials (one 256 x BN slot per cluster) and the per-slot flags (zero; each
-// launch's finishers re-arm them).  Not allocated during stream capture: a
-// captured launch without a large-enough workspace runs whole tiles.
-bool sk_workspace(cudaStream_t st, size_t part_bytes, int n, float** part, int32_t** flags) {
-  struct Ws {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-  };
-  static Ws ws[64];
-  static std::mutex mu;
+// Stream-K workspace, one per device, registered by the caller
+// (alcop_set_stream_k_workspace): the flags first (fixed place whatever the
+// partial size; zero, each launch's finishers re-arm them), then the fp32
+// partials (one 256 x BN slot per cluster).  A launch whose problem needs more
+// than the registered bytes runs whole tiles.
+namespace {
+constexpr size_t kSkFlagBytes = 4096;
+struct SkWs {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+SkWs g_sk_ws[64];
+std::mutex g_sk_mu;
+}  // namespace
+
+}  // namespace (leave the kernels' anonymous namespace: these two are library-internal API)
+
+size_t sk_bytes_needed(int n_clusters, int BN) {
+  return kSkFlagBytes + static_cast<size_t>(n_clusters) * 256 * BN * 4;
+}
+
+namespace {
+
+bool sk_workspace(size_t part_bytes, int n, float** part, int32_t** flags) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-  constexpr size_t kFlagBytes = 4096;  // flags first (fixed place whatever the partial size), then partials
-  if (static_cast<size_t>(n + 1) * sizeof(int32_t) > kFlagBytes) return false;
-  const size_t need = kFlagBytes + part_bytes;
-  std::lock_guard<std::mutex> lk(mu);
-  Ws& w = ws[dev];
-  if (w.bytes < need) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return false;  // earlier launches may use the old one
-    if (w.ptr) cudaFree(w.ptr);
-    w.ptr = nullptr;
-    w.bytes = 0;
-    void* p = nullptr;
-    const size_t alloc = std::max(need, static_cast<size_t>(32) << 20);
-    if (cudaMalloc(&p, alloc) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    if (cudaMemset(p, 0, alloc) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
-      cudaFree(p);
-      return false;
-    }
-    w.ptr = p;
-    w.bytes = alloc;
-  }
+  if (static_cast<size_t>(n + 1) * sizeof(int32_t) > kSkFlagBytes) return false;
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  const SkWs& w = g_sk_ws[dev];
+  if (!w.ptr || w.bytes < kSkFlagBytes + part_bytes) return false;
   *flags = static_cast<int32_t*>(w.ptr);
-  *part = reinterpret_cast<float*>(static_cast<char*>(w.ptr) + kFlagBytes);
+  *part = reinterpret_cast<float*>(static_cast<char*>(w.ptr) + kSkFlagBytes);
   return true;
 }
+
+}  // namespace
+
+int set_sk_workspace(void* ptr, int64_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+    return set_error(ALCOP_ERR_CUDA, "CudaError", "no current CUDA device");
+  if (ptr && bytes < static_cast<int64_t>(kSkFlagBytes))
+    return set_error(ALCOP_ERR_CONFIG, "Workspace", "stream-K workspace needs at least 4096 bytes");
+  if (ptr) {
+    cudaError_t e = cudaMemset(ptr, 0, kSkFlagBytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  g_sk_ws[dev].ptr = ptr;
+  g_sk_ws[dev].bytes = ptr ? static_cast<size_t>(bytes) : 0;
+  return ALCOP_OK;
+}
+
+namespace {
 
 template <typename OutT, int BK, bool kJoint, bool kDebug, bool kPreOp = false, int kEpi = 4>
 int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmKParams& kp,
@@ -1569,7 +1582,7 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
       const bool fits = static_cast<int64_t>(kp.sA) * (kp.a_stage_bytes + kp.b_stage_bytes) >= int64_t(BN) * 512;
       float* part = nullptr;
       int32_t* flags = nullptr;
-      if (kp.num_tiles >= n && fits && sk_workspace(st, static_cast<size_t>(n) * 256 * BN * 4, n, &part, &flags)) {
+      if (kp.num_tiles >= n && fits && sk_workspace(static_cast<size_t>(n) * 256 * BN * 4, n, &part, &flags)) {
         rc = encode_3d_dt(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, part, BN, 256, n, BN * 4, int64_t(256) * BN * 4, 32,
                           32, CU_TENSOR_MAP_SWIZZLE_128B, "stream-K partials");
         if (rc) return rc;

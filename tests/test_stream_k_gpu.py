@@ -17,6 +17,14 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+@pytest.fixture(autouse=True)
+def _stream_k_workspace(alcop):
+    """The caller-owned stream-K workspace (the library never allocates it)."""
+    ws = alcop.set_stream_k_workspace(256 << 20)
+    yield ws
+    alcop.load_library().alcop_set_stream_k_workspace(None, 0)
+
+
 def _sk(alcop, tileN=256, tileK=64, n_stage=6, stream_k=1):
     return alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=n_stage, cta_group=2, stream_k=stream_k)
 
@@ -86,3 +94,16 @@ def test_stream_k_rejected_outside_pairs(alcop):
         alcop.validate(d, alcop.make_schedule(tileN=256, cta_group=1, stream_k=1))
     with pytest.raises(alcop.AlcopError):
         alcop.validate(d, alcop.make_schedule(tileN=256, cta_group=2, stream_k=1, mode=alcop.MODE_WRAP))
+
+
+def test_stream_k_without_workspace_runs_whole_tiles(alcop):
+    """No registered workspace (or one too small): the stream_k schedule runs
+    whole tiles — still exact, and nothing is allocated on the call path."""
+    lib = alcop.load_library()
+    lib.alcop_set_stream_k_workspace(None, 0)
+    _check(alcop, 4096, 3072, 768, sched=_sk(alcop), seed=9)
+    small = torch.empty(8192, dtype=torch.uint8, device="cuda")
+    assert lib.alcop_set_stream_k_workspace(small.data_ptr(), 8192) == 0
+    d = alcop.gemm_desc(4096, 3072, 768)
+    assert lib.alcop_stream_k_workspace_bytes(d, _sk(alcop)) > 8192
+    _check(alcop, 4096, 3072, 768, sched=_sk(alcop), seed=10)

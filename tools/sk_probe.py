@@ -21,6 +21,7 @@ if len(sys.argv) > 1:
 
 
 def main():
+    alcop.set_stream_k_workspace(256 << 20)  # caller-owned stream-K workspace
     res = {}
     for M, N, K, tn, st in SHAPES:
         rot = Rotating(lambda i: ((torch.rand((M, K), device="cuda") - 0.5).to(torch.bfloat16),
