@@ -920,6 +920,7 @@ def bmm_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity):
 def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
     """BASELINE configs[3]: the 23 distinct ResNet-50 v1.5 convolutions at batch
     256 (53 layers with repeats), batch-sharded across ranks."""
+    import ctypes
     from paper_2210_16691_b200 import workloads
     from paper_2210_16691_b200.sharded import shard_range
     from paper_2210_16691_b200.timing import time_graph
@@ -938,6 +939,31 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         ms = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=cs, out=Y, x_halo=L.halo), iters=6, warmup=2)
         s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
         ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=s1, out=Y, x_halo=L.halo), iters=4, warmup=1)
+        # the model's pick against a sweep of the conv kernel's space (each tile width at its two
+        # deepest valid rings), timed like the pick
+        sweep_best = ms
+        gview = workloads.conv_gemm_desc(alcop, L, nloc)
+        for tn in (64, 128, 192, 256):
+            valid = []
+            for stg in range(8, 0, -1):
+                c = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg)
+                try:
+                    alcop.validate(gview, c)
+                except alcop.AlcopError:
+                    continue
+                if alcop.load_library().alcop_smem_bytes(ctypes.byref(gview), ctypes.byref(c)) <= 232448:
+                    valid.append(c)
+                if len(valid) == 2:
+                    break
+            for c in valid:
+                if (c.tileN, c.n_stage_smem_A, c.n_stage_inner) == (cs.tileN, cs.n_stage_smem_A, cs.n_stage_inner):
+                    continue
+                try:
+                    mc = time_graph(lambda i, c=c: alcop.conv2d(X, Wf, st, pd, sched=c, out=Y, x_halo=L.halo),
+                                    iters=4, warmup=1)
+                except alcop.AlcopError:
+                    continue
+                sweep_best = min(sweep_best, mc)
         del X, Wf, Y
         parity["conv_%s_b%d_rank%d" % (L.name, nloc, rank)] = parity_conv(torch, alcop, L, nloc, cs, dev,
                                                                            seed=zlib.crc32(L.name.encode()))
@@ -947,10 +973,14 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         rows.append({"layer": L.name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
                      "frac_of_attainable": round(fl / (ms * 1e-3) / 1e12 / attainable(fl, L.compulsory_bytes(nloc)),
                                                  3),
-                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN, "n_stage": cs.n_stage_smem_A})
+                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN, "n_stage": cs.n_stage_smem_A,
+                     "model_pick_over_best_swept": round(ms / sweep_best, 3)})
         torch.cuda.empty_cache()
     tt = ranks.max(tot_ms)
+    picks = [r["model_pick_over_best_swept"] for r in rows]
     return {"tflops_aggregate": round(world * tot_flops / (tt * 1e-3) / 1e12, 1), "images_per_gpu": nloc,
+            "model_pick_over_best_swept": {"max": max(picks), "within_10pct": sum(p <= 1.10 for p in picks),
+                                           "layers": len(picks)},
             "sharding": "batch", "layers": rows,
             "note": "sum over all 53 conv layers (conv1: stem kernel on the NHWC8 halo-padded input, C 3 -> 8 "
                     "zero-padded, FLOPs counted at C=3); per-layer CUDA-graph timing, the model's conv schedules; "

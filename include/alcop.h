@@ -324,6 +324,9 @@ void alcop_hw_default_a100_reference(alcop_hw* hw); /* perf_model.hpp:14-30 defa
 int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
                   alcop_breakdown* out);
 int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out);
+/* The same over the implicit-GEMM conv kernel's space (tileK 64, equal
+ * stages, cta_group 1), ranked on the conv's GEMM view. */
+int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_hw* hw, alcop_schedule* out);
 
 /* One measured candidate of the model-assisted tuner. */
 typedef struct {

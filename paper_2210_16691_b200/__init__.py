@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = [
     "alcop_tune", "alcop_simulate_pipeline", "alcop_simulate_two_level", "alcop_simulate_kernel",
     "alcop_gemm_chain_workspace_bytes", "alcop_gemm_chain", "alcop_shard_range", "alcop_gemm_sharded",
     "alcop_conv2d_sharded", "alcop_tune_workspace_bytes", "alcop_stream_k_workspace_bytes",
-    "alcop_set_stream_k_workspace",
+    "alcop_set_stream_k_workspace", "alcop_choose_conv_schedule",
 ]
 
 
@@ -219,6 +219,7 @@ def load_library(path: str | None = None):
     lib.alcop_hw_default_a100_reference.restype = None
     lib.alcop_predict.argtypes = [P(GemmDesc), P(Schedule), P(HW), P(Breakdown)]
     lib.alcop_choose_schedule.argtypes = [P(GemmDesc), P(HW), P(Schedule)]
+    lib.alcop_choose_conv_schedule.argtypes = [P(ConvDesc), P(HW), P(Schedule)]
     lib.alcop_ir_to_gemm.argtypes = [ctypes.c_char_p, P(GemmDesc), P(Schedule), ctypes.c_char_p, ctypes.c_size_t]
     lib.alcop_tune.argtypes = [P(GemmDesc), P(HW), ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, P(Schedule), P(TuneTrial),
@@ -561,9 +562,7 @@ def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_d
     d = conv_desc(N, H, W, C, K, R, S, stride, pad, _dtype_code(x.dtype), _dtype_code(out_dtype))
     d.x_halo = 1 if x_halo else 0
     if sched is None:
-        kv = R * 64 if (x_halo and S * C <= 64) else R * S * C
-        g = gemm_desc(N * P * Q, K, kv, 1, _dtype_code(x.dtype), _dtype_code(out_dtype), B_NK)
-        sched = choose_conv_schedule(g)
+        sched = choose_conv_schedule(d)
     # keep the contiguous operands alive across the launch: a temporary freed
     # before the kernel runs could be reused by the other operand's copy
     xc = x.contiguous()
@@ -578,22 +577,12 @@ def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_d
     return out
 
 
-def choose_conv_schedule(gview: GemmDesc, hw: HW | None = None) -> Schedule:
-    """Model pick restricted to the conv kernel's space (tileK 64, equal stages)."""
-    best, best_s = None, None
-    for tn in (64, 128, 192, 256):
-        for st in range(8, 0, -1):
-            for inner in (2, 1):
-                s = make_schedule(tileN=tn, tileK=64, n_stage=st, n_stage_inner=inner)
-                try:
-                    t = predict(gview, s, hw)["tKernel"]
-                except AlcopError:
-                    continue
-                if best is None or t < best * (1 - 1e-9):
-                    best, best_s = t, s
-    if best_s is None:
-        raise AlcopError(ALCOP_ERR_CONFIG, "Unschedulable: no conv schedule")
-    return best_s
+def choose_conv_schedule(conv: ConvDesc, hw: HW | None = None) -> Schedule:
+    """alcop_choose_conv_schedule: the model's pick over the conv kernel's space."""
+    s = Schedule()
+    _check(load_library().alcop_choose_conv_schedule(ctypes.byref(conv), ctypes.byref(hw or hw_b200()),
+                                                     ctypes.byref(s)))
+    return s
 
 
 def ir_to_gemm(ir_text: str):

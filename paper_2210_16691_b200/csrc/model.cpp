@@ -253,3 +253,51 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
   *out = bestS;
   return ALCOP_OK;
 }
+
+// The conv kernel's design space (implicit GEMM: tileK 64, equal A/B stages,
+// single CTA, whole tiles) ranked by alcop_predict on the GEMM view the
+// launch uses (M = N*P*Q, N = K, K = R*S*C, or R*64 for the stem's
+// one-box-per-filter-row path) — analytical_rank (tuner.hpp:68-80) for conv.
+extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_hw* hw, alcop_schedule* out) {
+  if (!d || !hw || !out) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL argument");
+  clear_error();
+  if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride_h < 1 ||
+      d->stride_w < 1 || d->pad_h < 0 || d->pad_w < 0)
+    return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "conv dimensions must be positive, padding >= 0");
+  const int64_t P = (d->H + 2 * d->pad_h - d->R) / d->stride_h + 1;
+  const int64_t Q = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
+  if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  const bool stem = d->x_halo && d->S * d->C <= 64 && d->stride_w * 16 <= 256 && d->stride_h * 8 <= 256;
+  alcop_gemm_desc g{};
+  g.M = d->N * P * Q;
+  g.N = d->K;
+  g.K = stem ? d->R * 64 : d->R * d->S * d->C;
+  g.batch = 1;
+  g.in_dtype = d->in_dtype;
+  g.out_dtype = d->out_dtype;
+  g.b_layout = ALCOP_B_NK;
+  double best = 1e300;
+  bool found = false;
+  for (int tN : {64, 128, 192, 256})
+    for (int st = 8; st >= 1; --st)
+      for (int inner = 2; inner >= 1; --inner) {
+        alcop_schedule s;
+        alcop_schedule_default(&s);
+        s.tileN = tN;
+        s.tileK = 64;
+        s.n_stage_smem_A = s.n_stage_smem_B = st;
+        s.n_stage_inner = inner;
+        if (validate_gemm(g, s) != ALCOP_OK) continue;
+        if (gemm_smem_bytes_epi(g, s, 4) > kMaxSmemBytes) continue;  // the conv kernel runs 4 epilogue warps
+        alcop_breakdown b;
+        if (alcop_predict(&g, &s, hw, &b) != ALCOP_OK) continue;
+        if (b.tKernel < best * (1.0 - 1e-9)) {  // ties keep the deeper pipeline
+          best = b.tKernel;
+          *out = s;
+          found = true;
+        }
+      }
+  clear_error();
+  if (!found) return set_error(ALCOP_ERR_CONFIG, "Unschedulable", "no conv schedule for workload");
+  return ALCOP_OK;
+}

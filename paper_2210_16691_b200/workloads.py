@@ -99,9 +99,19 @@ def conv_gemm_desc(alcop, layer: ConvLayer, nimg: int, in_dtype=None, out_dtype=
                            alcop.BF16 if out_dtype is None else out_dtype, alcop.B_NK)
 
 
+def conv_desc(alcop, layer: ConvLayer, nimg: int, in_dtype=None, out_dtype=None):
+    """The ABI descriptor of the layer as the bench stores it (NHWC, C padded to
+    Cs; the stem's input carries its zero-padding halo)."""
+    d = alcop.conv_desc(nimg, layer.H, layer.H, layer.Cs, layer.K, layer.R, layer.R, (layer.stride, layer.stride),
+                        (layer.pad, layer.pad), alcop.BF16 if in_dtype is None else in_dtype,
+                        alcop.BF16 if out_dtype is None else out_dtype)
+    d.x_halo = 1 if layer.halo else 0
+    return d
+
+
 def conv_schedule(alcop, layer: ConvLayer, nimg: int):
-    """The schedule the bench runs the layer with (the model's conv pick)."""
-    return alcop.choose_conv_schedule(conv_gemm_desc(alcop, layer, nimg))
+    """The schedule the bench runs the layer with (alcop_choose_conv_schedule)."""
+    return alcop.choose_conv_schedule(conv_desc(alcop, layer, nimg))
 
 
 def square_schedule(alcop, m: int, n: int):

@@ -135,3 +135,18 @@ def test_power_regime_picks_the_wide_pair_tile_for_squares(alcop):
     for n in (8192, 12288, 16384):
         s = alcop.choose_schedule(alcop.gemm_desc(n, n, n))
         assert (s.cta_group, s.tileN, s.n_stage_inner) == (2, 512, 1), (n, s)
+
+
+def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
+    """alcop_choose_conv_schedule (C ABI) returns a launchable conv schedule
+    (tileK 64, equal stages, cta_group 1, within the 4-epilogue-warp shared
+    memory) for all 23 ResNet-50 layers, stem included."""
+    from paper_2210_16691_b200 import workloads as W
+    import ctypes
+    lib = alcop.load_library()
+    for L in W.CONV_LAYERS:
+        s = W.conv_schedule(alcop, L, 256)
+        assert s.tileK == 64 and s.cta_group == 1 and s.n_stage_smem_A == s.n_stage_smem_B, L.name
+        g = W.conv_gemm_desc(alcop, L, 256)
+        alcop.validate(g, s)
+        assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448

@@ -22,7 +22,7 @@ for (name, H, C, K, R, st, pd, rep) in RESNET50_CONVS[:6] + RESNET50_CONVS[13:14
     halo = R * Cs <= 64
     hp = pd if halo else 0
     g = alcop.gemm_desc(n * P * Q, K, R * 64 if halo else R * R * Cs, 1, alcop.BF16, alcop.BF16, alcop.B_NK)
-    cs = alcop.choose_conv_schedule(g)
+    cs = alcop.choose_conv_schedule(alcop.conv_desc(n, H, H, C, K, R, R, (st, st), (pd, pd)))
     X = torch.zeros((n, H + 2 * hp, H + 2 * hp, Cs), device="cuda", dtype=torch.bfloat16)
     Wf = torch.zeros((K, R, R, Cs), device="cuda", dtype=torch.bfloat16)
     X[:, hp:hp + H, hp:hp + H, :C] = (torch.rand((n, H, H, C), device="cuda") - 0.5).to(torch.bfloat16)

@@ -12,7 +12,7 @@ import paper_2210_16691_b200 as alcop
 n, H, C, K, R = 256, 14, 256, 256, 3
 P, Q = alcop.conv_out_hw(H, H, R, R, (1, 1), (1, 1))
 g = alcop.gemm_desc(n * P * Q, K, R * R * C, 1, alcop.BF16, alcop.BF16, alcop.B_NK)
-cs = alcop.choose_conv_schedule(g)
+cs = alcop.choose_conv_schedule(alcop.conv_desc(n, H, H, C, K, R, R, (1, 1), (1, 1)))
 X = (torch.rand((n, H, H, C), device="cuda") - 0.5).to(torch.bfloat16)
 W = (torch.rand((K, R, R, C), device="cuda") - 0.5).to(torch.bfloat16)
 Y = torch.empty((n, P, Q, K), device="cuda", dtype=torch.bfloat16)
