@@ -19,9 +19,8 @@ torch = pytest.importorskip("torch")
 
 
 def _exact(a, b, batched):
-    a = a.astype(np.int64)
-    b = b.astype(np.int64)
-    return np.matmul(a, b)
+    # float64 BLAS product: exact for D-int inputs (|sum| <= 64 K << 2^53), far faster than an int64 matmul
+    return np.rint(np.matmul(a.astype(np.float64), b.astype(np.float64))).astype(np.int64)
 
 
 def _run(alcop, M, N, K, batch=1, in_dt=None, out_dt=None, b_layout=0, sched=None, seed=0):
