@@ -537,10 +537,20 @@ def conv2d(x, w, stride=(1, 1), pad=(0, 0), sched: Schedule | None = None, out_d
     (fp16/bf16 in, fp32 accumulate).  Default schedule: the model's pick for
     the GEMM view (M=N*P*Q, N=K, K=R*S*C) with tileK 64.  x_halo=True: x is
     stored with its zero padding halo, [N, H+2*pad_h, W+2*pad_w, C] (enables
-    the one-box-per-filter-row stem kernel when S*C <= 64)."""
+    the one-box-per-filter-row kernel when S*C <= 64).  C <= 4 with
+    horizontal stride 2 (ResNet-50 conv1) runs on the stem kernel
+    (csrc/stem_sm100.cu) with the channels padded to 4; other C % 8 != 0
+    are padded to 8."""
     import torch
     _require_cuda(x, w)
-    if x.shape[-1] % 8:
+    ob = 4 if (out_dtype or (out.dtype if out is not None else x.dtype)) == torch.float32 else 2
+    if (x.shape[-1] <= 4 and not x_halo and stride[1] == 2 and x.shape[2] % 16 == 0 and w.shape[0] % 16 == 0
+            and w.shape[0] <= 256 and (w.shape[0] * ob) % 128 == 0):
+        # the stem kernel: C = 4 (pixel pairs are 16-byte UMMA rows); zero channels contribute nothing
+        if x.shape[-1] < 4:
+            x = torch.nn.functional.pad(x, (0, 4 - x.shape[-1]))
+            w = torch.nn.functional.pad(w, (0, 4 - w.shape[-1]))
+    elif x.shape[-1] % 8:
         # NHWC channel padding to the 16-byte TMA granule (ResNet-50 conv1: 3 -> 8); zero filter
         # channels make the padded taps contribute nothing
         padc = 8 - x.shape[-1] % 8

@@ -14,7 +14,7 @@ LIB = os.environ.get("ALCOP_BUILD_LIB", os.path.join(HERE, "libalcop.so"))
 EXTRA = os.environ.get("ALCOP_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["gemm_sm100.cu", "chain_sm100.cu"]
+CU_SOURCES = ["gemm_sm100.cu", "chain_sm100.cu", "stem_sm100.cu"]
 CPP_SOURCES = ["alcop_api.cpp", "schedule.cpp", "model.cpp", "ir_frontend.cpp", "tuner.cpp", "sim.cpp",
                "sharded.cpp"]
 
@@ -43,16 +43,27 @@ def build(force=False, verbose=False):
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I" + os.path.join(ROOT, "include")] + EXTRA
+    headers = [d for d in _deps() if d.endswith((".h", ".cuh"))]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
+    def fresh(src, o):  # per-object rebuild: the object is newer than its source and every header
+        return (not force and os.path.exists(o) and os.path.getmtime(o) >= os.path.getmtime(src)
+                and os.path.getmtime(o) >= newest_header)
+
     for f in CU_SOURCES:
         o = os.path.join(objdir, f + ".o")
+        objs.append(o)
+        if fresh(os.path.join(CSRC, f), o):
+            continue
         cmd = [NVCC, *ARCH, *common, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, f), "-o", o]
         subprocess.run(cmd, check=True)
-        objs.append(o)
     for f in CPP_SOURCES:
         o = os.path.join(objdir, f + ".o")
+        objs.append(o)
+        if fresh(os.path.join(CSRC, f), o):
+            continue
         cmd = [NVCC, *ARCH, *common, "-x", "c++", "-c", os.path.join(CSRC, f), "-o", o]
         subprocess.run(cmd, check=True)
-        objs.append(o)
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"],
                    check=True)

@@ -53,6 +53,20 @@ inline int32_t raster_group_of(int32_t raster, int64_t units, int64_t num_m, int
   if (g < 1) g = 1;
   return static_cast<int32_t>(g < num_m ? g : num_m);
 }
+// The stem kernel (stem_sm100.cu): C = 4, stride_w 2 convs whose A operand is
+// read straight from the raw input rows (pixel pairs = 16-byte UMMA rows).
+struct StemGeometry {
+  int64_t P, Q, QB;          // output rows / columns, 128-column blocks per row
+  int32_t o_min, T2, NB;     // pair offset of group 0, pair groups per filter row (even), 8-pair blocks per window row
+  uint32_t row_bytes, slot_bytes, wbytes;
+  int64_t kdim;              // GEMM-view reduction length R * T2 * 8
+};
+bool stem_pairs_applicable(const alcop_conv_desc& d);
+StemGeometry stem_pairs_geometry(const alcop_conv_desc& d);
+int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s);
+int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s);
+int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt,
+                             void* y, void* stream);
 int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt, void* y,
                   void* stream);
 

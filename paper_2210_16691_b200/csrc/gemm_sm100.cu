@@ -1640,9 +1640,11 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   if (d.N < 1 || d.H < 1 || d.W < 1 || d.C < 1 || d.K < 1 || d.R < 1 || d.S < 1 || d.stride_h < 1 ||
       d.stride_w < 1 || d.pad_h < 0 || d.pad_w < 0)
     return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "conv dimensions must be positive, padding >= 0");
+  if (d.C == 4) return launch_conv2d_stem_pairs(d, s, x, wt, y, stream);  // stem_sm100.cu
   if (d.C % 8)
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
-                     "implicit-GEMM conv needs C to be a multiple of 8 (pad NHWC channels, e.g. conv1 3 -> 8)");
+                     "implicit-GEMM conv needs C to be a multiple of 8 (pad NHWC channels, e.g. 3 -> 8), or C = 4 "
+                     "with stride_w 2 (the stem kernel)");
   const bool small_c = (d.C % 64) != 0;  // 8-channel im2col boxes (no-swizzle core matrices)
   const bool halo = d.x_halo != 0;
   // stem kernel: a filter row's S*C taps are contiguous in the halo-padded input

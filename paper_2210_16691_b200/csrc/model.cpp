@@ -254,6 +254,61 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
   return ALCOP_OK;
 }
 
+// The stem kernel (stem_sm100.cu): one tile = 128 output columns of one output
+// row x all K filters, one chunk = the tile's input window (R rows), the
+// filter resident.  Its space is the window ring depth (n_stage) x the TMEM
+// accumulator ring (n_stage_inner).  Per tile, on each SM:
+//   T_use = max(MMA (R*T2/2 k-steps of M=128 x N=K x 16), window fill at the
+//               per-SM TMA rate, the SM's share of the HBM output stream)
+//   with one accumulator the epilogue serialises behind the MMAs;
+//   T_main = pipeline_latency(T_load, T_use, tiles per SM, n_stage, 1)
+// — the paper's stage formula with the window as the pipelined chunk.
+static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, const alcop_schedule& s,
+                              const alcop_hw& hw) {
+  const double tiles = static_cast<double>(d.N * g.P * g.QB);
+  const double per_sm = std::ceil(tiles / hw.numSM);
+  const double ob = d.out_dtype == ALCOP_F32 ? 4.0 : 2.0;
+  const double mma = static_cast<double>(d.R) * (g.T2 / 2) * (128.0 * d.K * 16 * 2) / hw.throughputSM;
+  const double fill = static_cast<double>(d.R) * g.row_bytes / hw.bwSmem;
+  const double out_bytes = static_cast<double>(d.N * g.P * g.Q) * d.K * ob;
+  const double in_bytes = static_cast<double>(d.N) * d.H * d.W * 8.0;
+  const double hbm_tile = (out_bytes + in_bytes) / tiles / (hw.bwDRAMWrite / hw.numSM);
+  const double epi = hw.latDRAMWrite + (d.K * ob / 128.0) * hw.tTile;
+  double use = std::max({mma, fill, hbm_tile, hw.tIssue});
+  if (s.n_stage_inner == 1) use = std::max(use, mma + epi);
+  const double main = model::pipeline_latency(hw.latLLCRead, use, static_cast<int64_t>(per_sm), s.n_stage_smem_A, 1);
+  return (hw.tLaunch + main + epi) / (hw.clockGHz * 1e9);
+}
+
+static int choose_stem_pairs(const alcop_conv_desc& d, const alcop_hw& hw, alcop_schedule* out) {
+  if (!stem_pairs_applicable(d))
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported",
+                     "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256");
+  const StemGeometry g = stem_pairs_geometry(d);
+  if (g.P < 1 || g.Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  double best = 1e300;
+  bool found = false;
+  for (int st = 8; st >= 1; --st)
+    for (int inner = 4; inner >= 1; --inner) {
+      alcop_schedule s;
+      alcop_schedule_default(&s);
+      s.tileN = static_cast<int32_t>(d.K);
+      s.tileK = 64;
+      s.n_stage_smem_A = s.n_stage_smem_B = st;
+      s.n_stage_inner = inner;
+      if (validate_stem_pairs(d, s) != ALCOP_OK) continue;
+      const double t = stem_pairs_time(d, g, s, hw);
+      if (t < best * (1.0 - 1e-9)) {  // ties keep the deeper rings
+        best = t;
+        *out = s;
+        found = true;
+      }
+    }
+  clear_error();
+  if (!found) return set_error(ALCOP_ERR_CONFIG, "Unschedulable", "no stem schedule for workload");
+  return ALCOP_OK;
+}
+
 // The conv kernel's design space (implicit GEMM: tileK 64, equal A/B stages,
 // single CTA, whole tiles) ranked by alcop_predict on the GEMM view the
 // launch uses (M = N*P*Q, N = K, K = R*S*C, or R*64 for the stem's
@@ -267,6 +322,7 @@ extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_
   const int64_t P = (d->H + 2 * d->pad_h - d->R) / d->stride_h + 1;
   const int64_t Q = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  if (d->C == 4) return choose_stem_pairs(*d, *hw, out);
   const bool stem = d->x_halo && d->S * d->C <= 64 && d->stride_w * 16 <= 256 && d->stride_h * 8 <= 256;
   alcop_gemm_desc g{};
   g.M = d->N * P * Q;

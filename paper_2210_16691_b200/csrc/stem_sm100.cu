@@ -1,0 +1,536 @@
+// stem_sm100.cu — the small-channel, stride-2 "stem" convolution (ResNet-50
+// conv1: 7x7, stride 2, 3 -> 64 channels on 224x224 images) as a pipelined
+// load-and-use kernel whose A operand is never expanded.
+//
+// The implicit-GEMM view of conv1 has K = R*S*C = 147 with C = 3: the generic
+// kernel pads every filter tap to 8 channels and gathers an im2col tile per
+// chunk, which re-reads each input pixel ~9x from L2 and runs the tensor
+// cores on 3/8 useful lanes (0.09 of the attainable roofline, round 1).
+//
+// Here x is NHWC with C = 4 (3 real channels + one zero), so one 16-byte
+// shared-memory row holds a PAIR of horizontally adjacent pixels
+// (2u, 2u+1) x 4 channels.  With horizontal stride 2, output column q and
+// filter taps (s, s+1) of equal pair offset read pair q + o: consecutive
+// output columns read consecutive 16-byte rows.  That is exactly the UMMA
+// K-major no-swizzle layout (core matrix = 8 rows x 16 B):
+//   M row m (output column q0+m)   -> +16 B per row   (SBO = 8 rows = 128 B)
+//   K group t (tap pair offset t)  -> +16 B per group (LBO = 16 B)
+// so the MMA descriptors read the im2col matrix straight out of the raw
+// input rows — the core matrices of neighbouring K groups overlap, shifted by
+// one row.  A tile = one output row segment of 128 columns x all K filters;
+// its A chunk = the R input rows the filter covers (one 4-D TMA box of
+// 128-byte pixel-pair blocks, zero-filled outside the image); per filter row
+// T2/2 tcgen05.mma (M=128, N=K, K=16) with the start address moved 32 B per
+// k-step.  The filter (K x R x T2 x 8, zero taps where the pairing overhangs
+// the filter) stays resident in shared memory for the kernel's lifetime.
+//
+// Pipeline: the paper's outer level is the ring of n_stage windows
+// (producer_acquire = wait empty[slot], producer_commit = expect_tx + TMA,
+// consumer_wait = wait full[slot], consumer_release = tcgen05.commit ->
+// empty[slot]); the inner level is the ring of n_stage_inner TMEM
+// accumulators, so the epilogue of tile i (TMEM -> bf16 -> TMA store) overlaps
+// the MMAs of tile i+1.  Warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer, warps 2-5 = epilogue.  Persistent: CTA b walks tiles b + i*grid.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <string>
+
+#include "alcop_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace alcop {
+
+int encode_tiled_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int rank, const cuuint64_t* dims,
+                     const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estr,
+                     CUtensorMapSwizzle swz, const char* what);
+bool pdl_enabled();
+
+namespace {
+
+constexpr int kStemThreads = 192;
+constexpr uint32_t kStemStaging = 32 * 128;  // one epilogue staging buffer: 32 rows x 128 B
+
+struct StemKParams {
+  int32_t P, Q, QB, num_tiles;  // output rows / columns per image, 128-column blocks per row
+  int32_t R, S, T2, o_min;      // filter rows / taps, pair groups per filter row (even), pair offset of group 0
+  int32_t sh, ph, pw;
+  int32_t BN;                   // = K filters (the whole N of the GEMM view)
+  int32_t stages, nacc;
+  uint32_t row_bytes, slot_bytes, wbytes;  // window row (NB blocks x 128 B), ring slot, resident filter
+  uint32_t acc_stride, tmem_cols, idesc;
+  int32_t dn, dp, dq;           // the grid as (images, rows, column blocks): the tile cursor's step
+  int32_t shift, blk_off;       // window: first MMA row `shift` pairs into it; block of column block 0
+  const uint16_t* w;            // KRSC, C = 4
+  int32_t skip;                 // measurement only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
+};
+
+template <typename OutT>
+__device__ __forceinline__ uint32_t pack2s(uint32_t a, uint32_t b);
+template <>
+__device__ __forceinline__ uint32_t pack2s<__nv_bfloat16>(uint32_t a, uint32_t b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(a), __uint_as_float(b));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2s<__half>(uint32_t a, uint32_t b) {
+  __half2 h = __floats2half2_rn(__uint_as_float(a), __uint_as_float(b));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+#ifdef STEM_TRACE
+// measurement build only (-DSTEM_TRACE): CTA 0 prints per-tile timestamps of each role
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  t = clock64();
+  return t;
+}
+#define TRACE_DECL unsigned long long tr_[24]; int trn_ = 0;
+#define TRACE_AT(tl) if (blockIdx.x == 0 && (tl) >= 40 && trn_ < 24) tr_[trn_++] = gtimer();
+#define TRACE_DUMP(tag) if (blockIdx.x == 0 && lane == 0) { for (int i = 0; i < trn_; ++i) printf("%s %d %llu\n", tag, i, tr_[i]); }
+#else
+#define TRACE_DECL
+#define TRACE_AT(tl) ;
+#define TRACE_DUMP(tag) ;
+#endif
+
+
+// Tile cursor: tile t = (image n, output row p, column block qb), qb
+// fastest.  A CTA walks t = blockIdx.x + i * grid; the cursor advances by
+// the grid's (dn, dp, dq) decomposition with carries — no integer division
+// in the tile loops (the divisions' dependent chains on the uniform datapath
+// cost ~900 clk per tile in the MMA warp).
+struct StemCursor {
+  int n, p, qb;
+  __device__ __forceinline__ void start(const StemKParams& k) {
+    const int t = static_cast<int>(blockIdx.x);
+    const int per_img = k.P * k.QB;
+    n = t / per_img;
+    const int rem = t - n * per_img;
+    p = rem / k.QB;
+    qb = rem - p * k.QB;
+  }
+  __device__ __forceinline__ void advance(const StemKParams& k) {
+    qb += k.dq;
+    int carry = qb >= k.QB;
+    qb -= carry ? k.QB : 0;
+    p += k.dp + carry;
+    carry = p >= k.P;
+    p -= carry ? k.P : 0;
+    n += k.dn + carry;
+  }
+};
+
+// kR, kKS: filter rows and k-steps per filter row fixed at compile time (the
+// ResNet-50 stem: 7 x 2) so the 14 MMAs of a tile issue back to back with
+// immediate descriptor offsets; 0, 0 = run-time loop (any filter)
+template <typename OutT, int kR, int kKS>
+__global__ void __launch_bounds__(kStemThreads, 1)
+    alcop_stem_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+                           const StemKParams p) {
+  using namespace ptx;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t ring = smem_u32(smem);
+  const uint32_t wsm = ring + p.stages * p.slot_bytes;
+  const uint32_t staging = wsm + p.wbytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes + 4 * 2 * kStemStaging);
+  uint64_t* full = bars;
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint64_t* tempty = tfull + p.nacc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + p.nacc);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmY);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < p.stages; ++i) {
+        mbar_init(smem_u32(&full[i]), 1);
+        mbar_init(smem_u32(&empty[i]), 1);
+      }
+      for (int i = 0; i < p.nacc; ++i) {
+        mbar_init(smem_u32(&tfull[i]), 1);
+        mbar_init(smem_u32(&tempty[i]), 4);
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
+    tmem_relinquish();
+  }
+  // PDL: setup overlapped the previous kernel's tail; global data from here on
+  grid_dependency_wait();
+  grid_launch_dependents();
+
+  // The filter, resident for the kernel's lifetime, in the B operand's
+  // K-major no-swizzle layout [k group kg][filter n][8 elements]
+  // (LBO = BN*16 bytes between k groups, SBO = 128 bytes between 8-filter
+  // groups).  k group kg = (filter row r, pair group t); element e = (tap
+  // parity e/4, channel e%4); tap s = 2*(o_min+t) + e/4 + pad_w, zero outside
+  // [0, S) (the pairing overhangs the filter by at most one tap per side).
+  {
+    const int groups = p.R * p.T2;
+    for (int idx = threadIdx.x; idx < groups * p.BN; idx += blockDim.x) {
+      const int kg = idx / p.BN, n = idx - kg * p.BN;
+      const int r = kg / p.T2, t = kg - r * p.T2;
+      uint32_t v[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = 2 * (p.o_min + t) + h + p.pw;
+        uint2 taps = make_uint2(0u, 0u);
+        if (s >= 0 && s < p.S)  // 4 channels of tap s: 8 bytes, 8-byte aligned (C = 4)
+          taps = __ldg(reinterpret_cast<const uint2*>(p.w + ((static_cast<int64_t>(n) * p.R + r) * p.S + s) * 4));
+        v[2 * h] = taps.x;
+        v[2 * h + 1] = taps.y;
+      }
+      st_shared_v4(wsm + static_cast<uint32_t>(idx) * 16u, v[0], v[1], v[2], v[3]);
+    }
+    fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor cores
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int grid = gridDim.x;
+  const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
+
+  if (warp == 0) {
+    // ======================= producer (TMA) =======================
+    // the whole warp walks the loop (coordinates stay on the uniform
+    // datapath), one elected lane issues
+    const uint32_t bytes = static_cast<uint32_t>(p.R) * p.row_bytes;  // the box, zero fill included
+    int slot = 0;
+    uint32_t phase = 0;
+    StemCursor cur;
+    cur.start(p);
+    TRACE_DECL
+    for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
+      mbar_wait(smem_u32(&empty[slot]), ((phase >> slot) & 1u) ^ 1u);  // producer_acquire
+      TRACE_AT(tl)
+      phase ^= 1u << slot;
+      if (elect_one()) {
+        if (p.skip & 2) {
+          mbar_arrive(smem_u32(&full[slot]));
+        } else {
+          mbar_arrive_expect_tx(smem_u32(&full[slot]), bytes);            // producer_commit
+          tma_load_4d(ring + slot * p.slot_bytes, &tmX, smem_u32(&full[slot]), 0, cur.qb * 16 + p.blk_off,
+                      cur.p * p.sh - p.ph, cur.n);
+        }
+      }
+      __syncwarp();
+      slot = slot + 1 == p.stages ? 0 : slot + 1;
+    }
+    TRACE_DUMP("P")
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    // warp-uniform loop, one elected lane issues: the descriptors stay in
+    // uniform registers (a single-thread loop made the compiler move every
+    // descriptor into uniform registers per MMA — ~250 clk per tcgen05.mma)
+    int slot = 0;
+    uint32_t phase = 0;
+    const uint32_t lbo_b = static_cast<uint32_t>(p.BN) * 16u;
+    const int ksteps = (p.skip & 1) ? 0 : p.T2 / 2;
+    const uint64_t b_step = (2 * lbo_b) >> 4;
+    const uint64_t a_row_step = (p.row_bytes >> 4) - 2 * ksteps;
+    const uint64_t a_row16 = p.row_bytes >> 4;
+    TRACE_DECL
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);  // accumulator drained
+      TRACE_AT(tl)
+      tc_fence_after();
+      mbar_wait(smem_u32(&full[slot]), (phase >> slot) & 1u);      // consumer_wait
+      TRACE_AT(tl)
+      phase ^= 1u << slot;
+      tc_fence_after();
+      TRACE_AT(tl)
+      const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
+      const uint32_t a0 = ring + slot * p.slot_bytes + static_cast<uint32_t>(p.shift) * 16u;
+      if (elect_one()) {
+        // descriptors advance by constants: +32 B of A (two pair groups) and
+        // two k groups of B per k-step, A to the next window row per filter row
+        uint64_t ad = make_smem_desc(a0, 16u, 128u, kLayoutNone);
+        uint64_t bd = make_smem_desc(wsm, lbo_b, 128u, kLayoutNone);
+        if constexpr (kR > 0) {
+          if (!(p.skip & 1)) {
+#pragma unroll
+            for (int r = 0; r < kR; ++r)
+#pragma unroll
+              for (int j = 0; j < kKS; ++j)
+                umma_f16_ss(d_tmem, ad + r * a_row16 + 2 * j, bd + (r * kKS + j) * b_step, p.idesc,
+                            (r > 0 || j > 0) ? 1u : 0u);
+          }
+        } else {
+          uint32_t accumulate = 0;
+          for (int r = 0; r < p.R; ++r) {
+#pragma unroll 4
+            for (int j = 0; j < ksteps; ++j) {
+              // A: rows m -> pair (m + 2j [+1]) of window row r; B: k groups (r, 2j), (r, 2j+1)
+              umma_f16_ss(d_tmem, ad, bd, p.idesc, accumulate);
+              accumulate = 1;
+              ad += 2;
+              bd += b_step;
+            }
+            ad += a_row_step;
+          }
+        }
+        TRACE_AT(tl)
+        umma_commit(smem_u32(&empty[slot]));  // consumer_release: the window slot is free once these retire
+        umma_commit(smem_u32(&tfull[acc]));   // accumulator ready
+      }
+      __syncwarp();
+      TRACE_AT(tl)
+      slot = slot + 1 == p.stages ? 0 : slot + 1;
+      if (++acc == p.nacc) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+    TRACE_DUMP("M")
+  } else {
+    // ======================= epilogue (warps 2-5) =======================
+    const int q = warp & 3;  // TMEM lane quarter = output columns q0 + 32q .. +31
+    const uint32_t stage_base = staging + (warp - 2) * 2 * kStemStaging;
+    constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
+    const int nchunks = p.BN / kChunkCols;
+    int buf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    StemCursor cur;
+    cur.start(p);
+    TRACE_DECL
+    for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
+      mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      if (warp == 2) TRACE_AT(tl)
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+      const int q0 = cur.qb * 128;
+      const bool rows_live = q0 + q * 32 < p.Q;
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t w[32];
+        if constexpr (sizeof(OutT) == 4) {
+          tmem_ld_32x32b_x32(t_addr + c * 32, w);
+          tmem_wait_ld();
+        } else {
+          uint32_t r0[32], r1[32];
+          tmem_ld_32x32b_x32(t_addr + c * 64, r0);
+          tmem_ld_32x32b_x32(t_addr + c * 64 + 32, r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack2s<OutT>(r0[2 * i], r0[2 * i + 1]);
+            w[16 + i] = pack2s<OutT>(r1[2 * i], r1[2 * i + 1]);
+          }
+        }
+        if (c == nchunks - 1) {  // this warp's TMEM reads of the accumulator are done
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+        }
+        if (!rows_live || (p.skip & 4)) continue;  // columns past Q (the M=128 tile overhangs a 112-column row)
+        const uint32_t sbuf = stage_base + buf * kStemStaging;
+        if (lane == 0) bulk_wait_group_read<1>();  // the store that last read sbuf is done
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                       w[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmY, sbuf, c * kChunkCols, q0 + q * 32, cur.n * p.P + cur.p);
+          bulk_commit_group();
+        }
+        buf ^= 1;
+      }
+      if (++acc == p.nacc) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+    if (lane == 0) bulk_wait_group_read<0>();
+    __syncwarp();
+    if (warp == 2) TRACE_DUMP("E")
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+template <typename OutT>
+int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKParams& kp, int grid, int smem,
+                      cudaStream_t st) {
+  auto kern = (kp.R == 7 && kp.T2 == 4) ? alcop_stem_conv_kernel<OutT, 7, 2> : alcop_stem_conv_kernel<OutT, 0, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStemThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tx, ty, kp);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
+  return ALCOP_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+bool stem_pairs_applicable(const alcop_conv_desc& d) {
+  const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
+  return d.C == 4 && d.stride_w == 2 && !d.x_halo && d.W % 16 == 0 && d.K % 16 == 0 && d.K >= 16 && d.K <= 256 &&
+         (d.K * ob) % 128 == 0 && d.R <= 32 && d.S <= 32 && d.stride_h <= 8 && d.pad_h <= 64 && d.pad_w <= 64;
+}
+
+StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
+  StemGeometry g{};
+  g.P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
+  g.Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
+  g.QB = (g.Q + 127) / 128;
+  // tap s reads pixel 2q - pad_w + s = pair q + floor((s - pad_w) / 2)
+  auto fdiv2 = [](int64_t v) { return v >= 0 ? v / 2 : -((1 - v) / 2); };
+  g.o_min = static_cast<int32_t>(fdiv2(-d.pad_w));
+  const int32_t o_max = static_cast<int32_t>(fdiv2(d.S - 1 - d.pad_w));
+  const int32_t T = o_max - g.o_min + 1;
+  g.T2 = (T + 1) & ~1;
+  // window: shift (0..7) + 128 rows + T2-1 further pairs, in 8-pair (128 B) blocks
+  g.NB = (7 + 128 + g.T2 - 1 + 7) / 8;
+  g.row_bytes = static_cast<uint32_t>(g.NB * 128);
+  g.slot_bytes = static_cast<uint32_t>((d.R * g.row_bytes + 1023) / 1024 * 1024);
+  g.wbytes = static_cast<uint32_t>((d.R * g.T2 * d.K * 16 + 1023) / 1024 * 1024);
+  g.kdim = d.R * g.T2 * 8;
+  return g;
+}
+
+int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
+  const StemGeometry g = stem_pairs_geometry(d);
+  const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner) + 16;
+  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 4 * 2 * kStemStaging + bars;
+}
+
+int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
+  if (s.tileM != kTileM || s.tileK != 64 || s.tileN != d.K)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
+                     "the stem kernel's tile is 128 output columns x all K filters (tileM 128, tileN = K, tileK 64)");
+  if (s.cta_group != 1 || s.stream_k != 0 || s.mode != ALCOP_MODE_FUSED)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
+                     "the stem kernel runs one CTA per tile with one window chunk per tile (FUSED, cta_group 1)");
+  if (s.n_stage_smem_A != s.n_stage_smem_B || s.n_stage_smem_A < 1 || s.n_stage_smem_A > kMaxStages)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the stem kernel's window ring: equal A/B stages in 1..16");
+  if (s.n_stage_inner < 1 || s.n_stage_inner > 4 || s.n_stage_inner * d.K > kTmemCols)
+    return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner accumulators of K columns exceed TMEM");
+  if (stem_pairs_smem_bytes(d, s) > kMaxSmemBytes)
+    return set_error(ALCOP_ERR_CONFIG, "SmemCapacity", "window ring + resident filter exceed shared memory");
+  return ALCOP_OK;
+}
+
+int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt,
+                             void* y, void* stream) {
+  if (!stem_pairs_applicable(d))
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported",
+                     "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256, "
+                     "K * out bytes % 128 == 0, no halo layout");
+  int rc = validate_stem_pairs(d, s);
+  if (rc) return rc;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wt) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return set_error(ALCOP_ERR_CONFIG, "Alignment", "x, w and y must be 16-byte aligned");
+  const StemGeometry g = stem_pairs_geometry(d);
+  if (g.P < 1 || g.Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  const CUtensorMapDataType dt =
+      d.in_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType odt = d.out_dtype == ALCOP_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : d.out_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
+  CUtensorMap tx, ty;
+  // x viewed as {64 elements = 8 pixel pairs (128 B), W/16 blocks, H, N}; box
+  // = NB blocks of R consecutive rows: the tile's whole input window, zero
+  // filled above/below the image and left/right of it (pairs never straddle
+  // the border: W is even, pad columns come in whole out-of-range pairs)
+  const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W / 16), static_cast<cuuint64_t>(d.H),
+                               static_cast<cuuint64_t>(d.N)};
+  const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 8), static_cast<cuuint64_t>(d.H * d.W * 8)};
+  const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), static_cast<cuuint32_t>(d.R), 1};
+  const cuuint32_t one[4] = {1, 1, 1, 1};
+  rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_NONE, "x (stem pairs)");
+  if (rc) return rc;
+  // y viewed as {K, Q, N*P}: each epilogue warp stores 32 columns x 128 B
+  const cuuint64_t ydims[3] = {static_cast<cuuint64_t>(d.K), static_cast<cuuint64_t>(g.Q),
+                               static_cast<cuuint64_t>(d.N * g.P)};
+  const cuuint64_t ystr[2] = {static_cast<cuuint64_t>(d.K * ob), static_cast<cuuint64_t>(g.Q * d.K * ob)};
+  const cuuint32_t ybox[3] = {static_cast<cuuint32_t>(128 / ob), 32, 1};
+  rc = encode_tiled_map(&ty, odt, y, 3, ydims, ystr, ybox, one, CU_TENSOR_MAP_SWIZZLE_128B, "y (stem pairs)");
+  if (rc) return rc;
+
+  StemKParams kp{};
+  kp.P = static_cast<int32_t>(g.P);
+  kp.Q = static_cast<int32_t>(g.Q);
+  kp.QB = static_cast<int32_t>(g.QB);
+  const int64_t tiles = d.N * g.P * g.QB;
+  if (tiles > (int64_t(1) << 31) - 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "too many output tiles");
+  kp.num_tiles = static_cast<int32_t>(tiles);
+  kp.R = static_cast<int32_t>(d.R);
+  kp.S = static_cast<int32_t>(d.S);
+  kp.T2 = g.T2;
+  kp.o_min = g.o_min;
+  kp.sh = d.stride_h;
+  kp.ph = d.pad_h;
+  kp.pw = d.pad_w;
+  kp.BN = static_cast<int32_t>(d.K);
+  kp.stages = s.n_stage_smem_A;
+  kp.nacc = s.n_stage_inner;
+  kp.row_bytes = g.row_bytes;
+  kp.slot_bytes = g.slot_bytes;
+  kp.wbytes = g.wbytes;
+  kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(d.K));
+  kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.nacc));
+  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, static_cast<uint32_t>(d.K));
+  kp.w = static_cast<const uint16_t*>(wt);
+  static const int skip_env = [] {
+    const char* e = std::getenv("ALCOP_STEM_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  kp.skip = skip_env;
+  const int sms = device_sm_count();
+  if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
+  int grid = s.num_ctas > 0 ? s.num_ctas : sms;
+  if (grid > kp.num_tiles) grid = kp.num_tiles;
+  kp.dn = grid / (kp.P * kp.QB);
+  kp.dp = (grid - kp.dn * kp.P * kp.QB) / kp.QB;
+  kp.dq = grid - kp.dn * kp.P * kp.QB - kp.dp * kp.QB;
+  // column block qb reads pairs from 128*qb + o_min: block 16*qb + floor(o_min/8), `shift` pairs in
+  kp.blk_off = g.o_min >= 0 ? g.o_min / 8 : -((7 - g.o_min) / 8);
+  kp.shift = g.o_min - 8 * kp.blk_off;
+  const int smem = static_cast<int>(stem_pairs_smem_bytes(d, s));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (d.out_dtype) {
+    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, kp, grid, smem, st);
+    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, kp, grid, smem, st);
+    default: return launch_stem_typed<__half>(tx, ty, kp, grid, smem, st);
+  }
+}
+
+}  // namespace alcop

@@ -30,7 +30,7 @@ SQUARE_GRANULE = 256  # M-shard granule: one CTA-pair tile row
 RESNET_BATCH = 256
 # (name, H_in, C, K, R, stride, pad, repeats in ResNet-50 v1.5)
 RESNET50_CONVS = [
-    ("conv1_7x7s2_3_64", 224, 3, 64, 7, 2, 3, 1),  # stem: NHWC8 halo-padded input (zero channels 3..7)
+    ("conv1_7x7s2_3_64", 224, 3, 64, 7, 2, 3, 1),  # the stem kernel: NHWC4 input (zero channel 3)
     ("l1_1x1_64_64", 56, 64, 64, 1, 1, 0, 1), ("l1_3x3_64_64", 56, 64, 64, 3, 1, 1, 3),
     ("l1_1x1_64_256", 56, 64, 256, 1, 1, 0, 4), ("l1_1x1_256_64", 56, 256, 64, 1, 1, 0, 2),
     ("l2_1x1_256_128", 56, 256, 128, 1, 1, 0, 1), ("l2_3x3s2_128", 56, 128, 128, 3, 2, 1, 1),
@@ -61,17 +61,29 @@ class ConvLayer:
         return (self.H + 2 * self.pad - self.R) // self.stride + 1
 
     @property
+    def stem(self) -> bool:
+        """The stem kernel (csrc/stem_sm100.cu): C <= 4 stored as 4 channels,
+        horizontal stride 2 (ResNet-50 conv1)."""
+        return self.C <= 4 and self.stride == 2 and self.H % 16 == 0 and self.K % 64 == 0 and self.K <= 256
+
+    @property
     def Cs(self) -> int:
-        """Stored channels: NHWC rows padded to the 16-byte TMA granule (conv1: 3 -> 8)."""
-        return -(-self.C // 8) * 8
+        """Stored channels: 4 on the stem kernel, else NHWC rows padded to the
+        16-byte TMA granule."""
+        return 4 if self.stem else -(-self.C // 8) * 8
 
     @property
     def halo(self) -> bool:
-        """Stem layer: the network input is stored with its zero-padding halo
-        (one TMA box per filter row, R*64 reduction elements)."""
-        return self.R * self.Cs <= 64
+        """The input is stored with its zero-padding halo (one TMA box per
+        filter row, R*64 reduction elements) when a filter row's S*C taps fit
+        one 128-byte row (the 1x1 / C = 64 layer; pad 0, so no halo bytes)."""
+        return not self.stem and self.R * self.Cs <= 64
 
     def gemm_k(self) -> int:
+        """Reduction length of the GEMM view the kernel runs."""
+        if self.stem:  # R filter rows x pair groups (pad % 2 + S taps, rounded to an even count of pairs) x 8
+            t = (self.pad % 2 + self.R + 1) // 2
+            return self.R * ((t + 1) // 2 * 2) * 8
         return self.R * 64 if self.halo else self.R * self.R * self.Cs
 
     def flops(self, n: int) -> float:

@@ -1,0 +1,121 @@
+"""GPU parity of the stem kernel (csrc/stem_sm100.cu: C = 4, horizontal stride
+2, the A operand read straight from the raw input rows through overlapping
+no-swizzle descriptors) against the oracle's direct convolution, bit-exact on
+the reference's integer inputs.  ResNet-50 conv1 (7x7/2, 3 -> 64) is the
+shape class; the cases also cover odd/even padding and filter widths, more
+than one 128-column block per output row, stride_h 1, K = 128/256, and every
+ring depth / accumulator count the space holds."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import coracle
+from oracle.splitmix import random_tensor
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+CASES = [  # N, H, W, C, K, R, S, (stride_h, stride_w), (pad_h, pad_w)
+    (2, 32, 32, 3, 64, 7, 7, (2, 2), (3, 3)),     # conv1 class (C 3 -> 4)
+    (1, 224, 224, 3, 64, 7, 7, (2, 2), (3, 3)),   # conv1, one whole image
+    (1, 22, 288, 4, 128, 5, 5, (2, 2), (2, 2)),   # Q = 144: two column blocks; even pad
+    (2, 17, 48, 4, 64, 4, 4, (1, 2), (0, 0)),     # stride_h 1, even S, no padding
+    (1, 9, 64, 4, 256, 3, 3, (2, 2), (1, 1)),     # K = 256
+    (2, 12, 16, 2, 64, 1, 1, (2, 2), (0, 0)),     # 1x1 / 2 (one tap, zero partner)
+    (1, 20, 32, 3, 64, 6, 3, (3, 2), (2, 1)),     # stride_h 3, R != S
+]
+
+
+def _inputs(case, seed):
+    N, H, W, C, K, R, S, st, pd = case
+    x = random_tensor(N * H * W * C, seed).reshape(N, H, W, C)
+    w = random_tensor(K * R * S * C, seed + 1).reshape(K, R, S, C)
+    ref = coracle.conv2d(coracle.to_dtype(x.astype(np.float32), "bf16"),
+                         coracle.to_dtype(w.astype(np.float32), "bf16"), st, pd, "bf16", "f32")
+    return (torch.from_numpy(x).to(torch.bfloat16).cuda(), torch.from_numpy(w).to(torch.bfloat16).cuda(), ref)
+
+
+def _assert_equal(got, want, what):
+    if not torch.equal(got, want):
+        bad = torch.nonzero(got != want)
+        raise AssertionError("%s: mismatch (n=%d) at %s: got %s want %s" % (
+            what, len(bad), bad[:4].tolist(), got[tuple(bad[0])].item(), want[tuple(bad[0])].item()))
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[:7])) + "_s%d%d_p%d%d" % (*c[7], *c[8]))
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_stem_exact(alcop, case, out_dt):
+    X, Wt, ref = _inputs(case, 61)
+    _, _, _, _, K, _, _, st, pd = case
+    odt = torch.float32 if out_dt == "f32" else torch.bfloat16
+    d = alcop.conv_desc(*case[:7], st, pd, alcop.BF16, alcop.F32 if out_dt == "f32" else alcop.BF16)
+    d.C = 4
+    s = alcop.choose_conv_schedule(d)
+    assert s.tileN == K and s.cta_group == 1
+    Y = alcop.conv2d(X, Wt, st, pd, out_dtype=odt)
+    torch.cuda.synchronize()
+    _assert_equal(Y.cpu(), torch.from_numpy(ref).to(odt), "model schedule %s" % s)
+
+
+def test_stem_schedules(alcop):
+    """Every ring depth 1..8 x accumulators 1..4 that fits: same bits."""
+    case = (2, 30, 64, 3, 64, 7, 7, (2, 2), (3, 3))
+    X, Wt, ref = _inputs(case, 71)
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    for st in (1, 2, 3, 5, 8):
+        for inner in (1, 2, 4):
+            s = alcop.make_schedule(tileN=64, tileK=64, n_stage=st, n_stage_inner=inner, mode=1)
+            Y = alcop.conv2d(X, Wt, (2, 2), (3, 3), sched=s, out_dtype=torch.bfloat16)
+            _assert_equal(Y.cpu(), want, "stages %d inner %d" % (st, inner))
+
+
+def test_stem_fourth_channel_and_grid(alcop):
+    """A genuine 4-channel input (no zero channel) and a small persistent grid
+    (each CTA walks many tiles through the rings)."""
+    case = (3, 40, 96, 4, 64, 7, 7, (2, 2), (3, 3))
+    X, Wt, ref = _inputs(case, 81)
+    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=3, n_stage_inner=2, mode=1)
+    s.num_ctas = 5
+    Y = alcop.conv2d(X, Wt, (2, 2), (3, 3), sched=s, out_dtype=torch.float32)
+    _assert_equal(Y.cpu(), torch.from_numpy(ref), "grid 5")
+
+
+def test_stem_float_inputs(alcop):
+    """Float inputs: fp32 accumulation against a float64 direct conv (torch)."""
+    g = torch.Generator().manual_seed(5)
+    x = torch.rand(2, 64, 64, 3, generator=g) * 2 - 1
+    w = torch.rand(64, 7, 7, 3, generator=g) * 2 - 1
+    xb, wb = x.to(torch.bfloat16), w.to(torch.bfloat16)
+    ref = torch.nn.functional.conv2d(xb.double().permute(0, 3, 1, 2), wb.double().permute(0, 3, 1, 2),
+                                     stride=2, padding=3).permute(0, 2, 3, 1)
+    Y = alcop.conv2d(xb.cuda(), wb.cuda(), (2, 2), (3, 3), out_dtype=torch.float32).cpu().double()
+    err = (Y - ref).norm() / ref.norm()
+    assert err < 1e-5, err
+
+
+def test_stem_rejects(alcop):
+    """The ABI's C = 4 path names what it cannot run (and never falls back)."""
+    lib = alcop.load_library()
+    X = torch.zeros(1, 16, 40, 4, dtype=torch.bfloat16, device="cuda")
+    Wt = torch.zeros(64, 7, 7, 4, dtype=torch.bfloat16, device="cuda")
+    Y = torch.zeros(1, 8, 20, 64, dtype=torch.bfloat16, device="cuda")
+
+    def call(d, s):
+        return lib.alcop_conv2d(ctypes.byref(d), ctypes.byref(s), ctypes.c_void_p(X.data_ptr()),
+                                ctypes.c_void_p(Wt.data_ptr()), ctypes.c_void_p(Y.data_ptr()), None)
+
+    good = alcop.make_schedule(tileN=64, tileK=64, n_stage=2, n_stage_inner=2, mode=1)
+    d = alcop.conv_desc(1, 16, 40, 4, 64, 7, 7, (2, 2), (3, 3), alcop.BF16, alcop.BF16)  # W % 16 != 0
+    assert call(d, good) == alcop.ALCOP_ERR_CONFIG
+    assert lib.alcop_last_error().decode().startswith("Unsupported")
+    d = alcop.conv_desc(1, 16, 32, 4, 64, 7, 7, (2, 2), (3, 3), alcop.BF16, alcop.BF16)
+    for bad, tag in ((dict(tileN=128), "BadSchedule"), (dict(mode=0), "BadSchedule"),
+                     (dict(n_stage_inner=4, tileN=64), None)):
+        s = alcop.make_schedule(**{**dict(tileN=64, tileK=64, n_stage=2, n_stage_inner=2, mode=1), **bad})
+        rc = call(d, s)
+        if tag is None:
+            assert rc == 0, lib.alcop_last_error()
+        else:
+            assert rc == alcop.ALCOP_ERR_CONFIG and lib.alcop_last_error().decode().startswith(tag), bad
+    torch.cuda.synchronize()

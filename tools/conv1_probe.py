@@ -1,5 +1,7 @@
-"""ResNet-50 conv1 (7x7/2, 3 -> 64, batch 256) paths: stem kernel on the
-halo-padded NHWC8 input vs the 8-channel im2col path, per schedule."""
+"""ResNet-50 conv1 (7x7/2, 3 -> 64, batch 256) paths, per schedule: the stem
+kernel on NHWC4 (csrc/stem_sm100.cu, pixel-pair descriptors), the
+one-box-per-filter-row kernel on the halo-padded NHWC8 input, and the
+8-channel im2col path; all three outputs compared bit for bit."""
 import json
 import os
 import sys
@@ -31,9 +33,24 @@ def main():
                             iters=6, warmup=2)
             out["%s_s%d" % ("stem" if halo else "im2col8", stg)] = {"ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
                                                                     "GBps": round(out["bytes_min"] / ms / 1e6, 1)}
+    X4 = X[..., :4].contiguous()
+    W4 = Wf[..., :4].contiguous()
+    out["bytes_min_nhwc4"] = X4.numel() * 2 + Y.numel() * 2
+    d = alcop.conv_desc(n, H, H, 4, K, R, R, (st, st), (pd, pd), alcop.BF16, alcop.BF16)
+    pick = alcop.choose_conv_schedule(d)
+    out["pairs_model_pick"] = pick.as_dict()
+    for stg, inn in ((8, 4), (8, 2), (8, 1), (6, 2), (4, 2), (2, 2), (1, 1), (4, 4)):
+        s = alcop.make_schedule(tileN=K, tileK=64, n_stage=stg, n_stage_inner=inn)
+        ms = time_graph(lambda i: alcop.conv2d(X4, W4, (st, st), (pd, pd), sched=s, out=Y, x_halo=False),
+                        iters=10, warmup=3)
+        out["pairs_s%d_a%d" % (stg, inn)] = {"ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1),
+                                             "GBps": round(out["bytes_min_nhwc4"] / ms / 1e6, 1)}
+    Y3 = torch.empty_like(Y)
     alcop.conv2d(Xh, Wf, (st, st), (pd, pd), out=Y, x_halo=True)
     alcop.conv2d(X, Wf, (st, st), (pd, pd), out=Y2)
+    alcop.conv2d(X4, W4, (st, st), (pd, pd), out=Y3)
     out["stem_equals_im2col"] = bool(torch.equal(Y, Y2))
+    out["pairs_equals_im2col"] = bool(torch.equal(Y3, Y2))
     print(json.dumps(out))
 
 
