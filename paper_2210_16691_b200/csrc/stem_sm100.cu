@@ -52,7 +52,7 @@ bool pdl_enabled();
 
 namespace {
 
-constexpr int kStemThreads = 192;
+constexpr int kStemThreads = 352;  // producer; MMA + 4 epilogue warps per tile parity (1, 2-5 even; 6, 7-10 odd)
 constexpr uint32_t kStemStaging = 32 * 128;  // one epilogue staging buffer: 32 rows x 128 B
 
 struct StemKParams {
@@ -66,6 +66,7 @@ struct StemKParams {
   int32_t dn, dp, dq;           // the grid as (images, rows, column blocks): the tile cursor's step
   int32_t shift, blk_off;       // window: first MMA row `shift` pairs into it; block of column block 0
   const uint16_t* w;            // KRSC, C = 4
+  int32_t dual;                 // two MMA-issuing warps (1: even tiles, 6: odd tiles); even rings only
   int32_t skip;                 // measurement only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
 };
 
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   const uint32_t ring = smem_u32(smem);
   const uint32_t wsm = ring + p.stages * p.slot_bytes;
   const uint32_t staging = wsm + p.wbytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes + 4 * 2 * kStemStaging);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes + 8 * 2 * kStemStaging);
   uint64_t* full = bars;
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
@@ -231,23 +232,32 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       slot = slot + 1 == p.stages ? 0 : slot + 1;
     }
     TRACE_DUMP("P")
-  } else if (warp == 1) {
-    // ======================= MMA issuer =======================
+  } else if (warp == 1 || warp == 6) {
+    // ======================= MMA issuers =======================
     // warp-uniform loop, one elected lane issues: the descriptors stay in
     // uniform registers (a single-thread loop made the compiler move every
-    // descriptor into uniform registers per MMA — ~250 clk per tcgen05.mma)
-    int slot = 0;
-    uint32_t phase = 0;
+    // descriptor into uniform registers per MMA — ~250 clk per tcgen05.mma).
+    // Two issuing warps take alternate tiles (their own slots and
+    // accumulators: both rings are even), so one warp's barrier waits and
+    // commits (~500 clk per tile) overlap the other's MMAs; each warp's
+    // tcgen05.commit tracks only the MMAs it issued.
+    const int first = warp == 6 ? 1 : 0;
+    const int step = p.dual ? 2 : 1;
+    if (warp == 6 && !p.dual) {
+      __syncwarp();
+    } else {
+    int slot = first % p.stages;
+    uint32_t phase = 0, acc_phase = 0;  // bit k: current parity of ring slot / accumulator k
     const uint32_t lbo_b = static_cast<uint32_t>(p.BN) * 16u;
     const int ksteps = (p.skip & 1) ? 0 : p.T2 / 2;
     const uint64_t b_step = (2 * lbo_b) >> 4;
     const uint64_t a_row_step = (p.row_bytes >> 4) - 2 * ksteps;
     const uint64_t a_row16 = p.row_bytes >> 4;
     TRACE_DECL
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);  // accumulator drained
+    int acc = first % p.nacc;
+    for (int tl = first; tl < my_tiles; tl += step) {
+      mbar_wait(smem_u32(&tempty[acc]), ((acc_phase >> acc) & 1u) ^ 1u);  // accumulator drained
+      acc_phase ^= 1u << acc;
       TRACE_AT(tl)
       tc_fence_after();
       mbar_wait(smem_u32(&full[slot]), (phase >> slot) & 1u);      // consumer_wait
@@ -291,27 +301,34 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
       __syncwarp();
       TRACE_AT(tl)
-      slot = slot + 1 == p.stages ? 0 : slot + 1;
-      if (++acc == p.nacc) {
-        acc = 0;
-        acc_phase ^= 1u;
-      }
+      slot += step;
+      if (slot >= p.stages) slot -= p.stages;
+      acc += step;
+      if (acc >= p.nacc) acc -= p.nacc;
     }
-    TRACE_DUMP("M")
-  } else {
-    // ======================= epilogue (warps 2-5) =======================
+    if (warp == 1) TRACE_DUMP("M")
+    }
+  } else if ((warp >= 2 && warp <= 5) || (warp >= 7 && p.dual)) {
+    // ======================= epilogue (warps 2-5: even tiles, 7-10: odd tiles) =======================
+    // with two issuing warps the tiles split into two independent
+    // MMA -> epilogue pipelines (their own accumulators); one group's TMEM
+    // drain, staging and TMA store overlap the other's
     const int q = warp & 3;  // TMEM lane quarter = output columns q0 + 32q .. +31
-    const uint32_t stage_base = staging + (warp - 2) * 2 * kStemStaging;
+    const int first = warp >= 7 ? 1 : 0;
+    const int step = p.dual ? 2 : 1;
+    const uint32_t stage_base = staging + (warp >= 7 ? warp - 3 : warp - 2) * 2 * kStemStaging;
     constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
-    int acc = 0;
+    int acc = first % p.nacc;
     uint32_t acc_phase = 0;
     StemCursor cur;
     cur.start(p);
+    if (first) cur.advance(p);
     TRACE_DECL
-    for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
-      mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+    for (int tl = first; tl < my_tiles; tl += step, cur.advance(p), (step == 2 ? cur.advance(p) : void())) {
+      mbar_wait(smem_u32(&tfull[acc]), (acc_phase >> acc) & 1u);
+      acc_phase ^= 1u << acc;
       if (warp == 2) TRACE_AT(tl)
       tc_fence_after();
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
@@ -354,10 +371,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         }
         buf ^= 1;
       }
-      if (++acc == p.nacc) {
-        acc = 0;
-        acc_phase ^= 1u;
-      }
+      acc += step;
+      if (acc >= p.nacc) acc -= p.nacc;
     }
     if (lane == 0) bulk_wait_group_read<0>();
     __syncwarp();
@@ -428,7 +443,7 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
 int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
   const StemGeometry g = stem_pairs_geometry(d);
   const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner) + 16;
-  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 4 * 2 * kStemStaging + bars;
+  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 8 * 2 * kStemStaging + bars;
 }
 
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
@@ -440,7 +455,7 @@ int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
                      "the stem kernel runs one CTA per tile with one window chunk per tile (FUSED, cta_group 1)");
   if (s.n_stage_smem_A != s.n_stage_smem_B || s.n_stage_smem_A < 1 || s.n_stage_smem_A > kMaxStages)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the stem kernel's window ring: equal A/B stages in 1..16");
-  if (s.n_stage_inner < 1 || s.n_stage_inner > 4 || s.n_stage_inner * d.K > kTmemCols)
+  if (s.n_stage_inner < 1 || s.n_stage_inner > 8 || s.n_stage_inner * d.K > kTmemCols)
     return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner accumulators of K columns exceed TMEM");
   if (stem_pairs_smem_bytes(d, s) > kMaxSmemBytes)
     return set_error(ALCOP_ERR_CONFIG, "SmemCapacity", "window ring + resident filter exceed shared memory");
@@ -514,6 +529,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
     return e ? std::atoi(e) : 0;
   }();
   kp.skip = skip_env;
+  kp.dual = (kp.stages % 2 == 0 && kp.nacc % 2 == 0) ? 1 : 0;
   const int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;

@@ -17,9 +17,9 @@ X = (torch.rand((n, 224, 224, 4), device="cuda") - 0.5).to(torch.bfloat16)
 W = (torch.rand((64, 7, 7, 4), device="cuda") - 0.5).to(torch.bfloat16)
 Y = torch.empty((n, 112, 112, 64), device="cuda", dtype=torch.bfloat16)
 out = {"skip": os.environ.get("ALCOP_STEM_SKIP", "0")}
-for stg, inn in ((8, 4), (4, 2)):
+for stg, inn in ((8, 4), (8, 8), (10, 4), (10, 8), (6, 2), (12, 4)):
     s = alcop.make_schedule(tileN=64, tileK=64, n_stage=stg, n_stage_inner=inn)
-    for ctas in (0, 74):
+    for ctas in (0,):
         s.num_ctas = ctas
         try:
             ms = time_graph(lambda i: alcop.conv2d(X, W, (2, 2), (3, 3), sched=s, out=Y), iters=10, warmup=3)
