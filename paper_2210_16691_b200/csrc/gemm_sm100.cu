@@ -792,7 +792,10 @@ __device__ __forceinline__ void sk_red_release_add(int32_t* f, int v) {
 }
 __device__ __forceinline__ void sk_fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-template <typename OutT, int BK, bool kDebug, bool kSK>
+// kWide: tileN 512 (two N = 256 MMAs per k-step into one 512-column
+// accumulator).  A template parameter, not a run-time flag: the per-MMA
+// branch of a run-time flag cost the other pair tiles 12-18 % (tools/pair_ab.py).
+template <typename OutT, int BK, bool kDebug, bool kSK, bool kWide = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmW,
@@ -824,7 +827,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
   const bool leader = rank == 0;
   const int half_n = p.BN / 2;
   const bool b_sw64 = (half_n & 63) != 0 && !p.b_pad;  // BN = 192: N-major halves of 96 columns
-  const bool wide = p.BN == 512;  // one 256 x 512 tile = two N = 256 MMAs per k-step, one TMEM accumulator
+  constexpr bool wide = kWide;  // one 256 x 512 tile = two N = 256 MMAs per k-step, one TMEM accumulator
   if (threadIdx.x == 0) stamp<kDebug>(p, 0);
 
   if (warp == 0 && elect_one()) {
@@ -936,9 +939,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                       tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, tc.b);
                 }
               }
-              const uint32_t dst = ringB + slot * b_bytes; const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
+              const uint32_t dst = ringB + slot * b_bytes; [[maybe_unused]] const int n0 = tc.nb * p.BN + static_cast<int>(rank) * half_n;
               if (kRole == 0) {
-              } else if (wide) {
+              } else if constexpr (wide) {
                 // tileN 512: two N = 256 MMAs per k-step; MMA g reads cluster
                 // columns [256 g, 256 g + 256), 128 of them from each CTA, so
                 // this CTA stages columns 256 g + 128 rank + [0, 128) for g = 0, 1
@@ -1041,7 +1044,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
                 const uint32_t acc_flag = (v > cb || u > 0) ? 1u : 0u;
                 umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, acc_flag);
-                if (wide) umma_f16_ss_pair(d_tmem + 256, ad + a_off, bd + b_group + b_off, idesc, acc_flag);
+                if constexpr (wide) umma_f16_ss_pair(d_tmem + 256, ad + a_off, bd + b_group + b_off, idesc, acc_flag);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
           ca.advance(p.sA);
         }
@@ -1337,10 +1340,10 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK, bool kDebug = false, bool kSK = false>
+template <typename OutT, int BK, bool kDebug = false, bool kSK = false, bool kWide = false>
 int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tw,
                   const GemmKParams& kp, int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug, kSK>;
+  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug, kSK, kWide>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -1364,6 +1367,11 @@ int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
 template <typename OutT, int BK>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tw,
                 const GemmKParams& kp, int grid, int smem, cudaStream_t st) {
+  if (kp.BN == 512) {
+    if (kp.sk_flags) return launch_pair_t<OutT, BK, false, true, true>(ta, tb, tc, tw, kp, grid, smem, st);
+    return kp.stamps ? launch_pair_t<OutT, BK, true, false, true>(ta, tb, tc, tw, kp, grid, smem, st)
+                     : launch_pair_t<OutT, BK, false, false, true>(ta, tb, tc, tw, kp, grid, smem, st);
+  }
   if (kp.sk_flags) return launch_pair_t<OutT, BK, false, true>(ta, tb, tc, tw, kp, grid, smem, st);
   return kp.stamps ? launch_pair_t<OutT, BK, true>(ta, tb, tc, tw, kp, grid, smem, st)
                    : launch_pair_t<OutT, BK, false>(ta, tb, tc, tw, kp, grid, smem, st);

@@ -13,18 +13,21 @@ from paper_2210_16691_b200.timing import Rotating, time_graph
 if len(sys.argv) > 1:
     alcop.LIB_PATH = sys.argv[1]
 res = {}
-for name, (M, N, K), (tn, tk, st) in (("ffn1_64s6", (4096, 3072, 768), (256, 64, 6)),
-                                      ("ffn1_128s3", (4096, 3072, 768), (256, 128, 3)),
-                                      ("qkv_64s6", (4096, 2304, 768), (256, 64, 6)),
-                                      ("ffn2_192s6", (4096, 768, 3072), (192, 64, 6)),
-                                      ("sq8192_64s6", (8192, 8192, 8192), (256, 64, 6)),
-                                      ("sq8192_128s3", (8192, 8192, 8192), (256, 128, 3))):
+for name, (M, N, K), (tn, tk, st, cg) in (("ffn1_64s6", (4096, 3072, 768), (256, 64, 6, 2)),
+                                          ("ffn1_128s3", (4096, 3072, 768), (256, 128, 3, 2)),
+                                          ("qkv_64s6", (4096, 2304, 768), (256, 64, 6, 2)),
+                                          ("ffn2_192s6", (4096, 768, 3072), (192, 64, 6, 2)),
+                                          ("sq8192_64s6", (8192, 8192, 8192), (256, 64, 6, 2)),
+                                          ("sq8192_128s3", (8192, 8192, 8192), (256, 128, 3, 2)),
+                                          ("single_ffn1_256s4", (4096, 3072, 768), (256, 64, 4, 1)),
+                                          ("single_ffn2_192s5", (4096, 768, 3072), (192, 64, 5, 1)),
+                                          ("single_o_192s5", (4096, 768, 768), (192, 64, 5, 1))):
     rot = Rotating(lambda i: ((torch.rand(M, K, device="cuda") - 0.5).to(torch.bfloat16),
                               (torch.rand(K, N, device="cuda") - 0.5).to(torch.bfloat16),
                               torch.empty(M, N, device="cuda", dtype=torch.bfloat16)), (M * K + K * N + M * N) * 2,
                    max_sets=8)
     nr = len(rot.sets)
-    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=2)
+    s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg)
     ms = time_graph(lambda i: alcop.matmul(rot.sets[i % nr][0], rot.sets[i % nr][1], s, out=rot.sets[i % nr][2]),
                     iters=max(4 * nr, 8), reps_per_graph=nr)
     res[name] = round(2.0 * M * N * K / ms / 1e9, 1)
