@@ -55,13 +55,18 @@ inline int32_t raster_group_of(int32_t raster, int64_t units, int64_t num_m, int
 }
 // The stem kernel (stem_sm100.cu): C = 4, stride_w 2 convs whose A operand is
 // read straight from the raw input rows (pixel pairs = 16-byte UMMA rows).
+// Window mode of the same kernel: C = 64, stride 1 convs (3x3) whose tile of
+// TR output rows reads its (TR+R-1)-row input window once; every tap is the
+// window shifted by whole 128-byte pixel rows.
 struct StemGeometry {
   int64_t P, Q, QB;          // output rows / columns, 128-column blocks per row
   int32_t o_min, T2, NB;     // pair offset of group 0, pair groups per filter row (even), 8-pair blocks per window row
-  uint32_t row_bytes, slot_bytes, wbytes;
-  int64_t kdim;              // GEMM-view reduction length R * T2 * 8
+  int32_t TR, WP;            // window mode: output rows per tile, window row pitch in pixels (TR * WP = 128)
+  uint32_t row_bytes, slot_bytes, box_bytes, wbytes;
+  int64_t kdim;              // GEMM-view reduction length
 };
 bool stem_pairs_applicable(const alcop_conv_desc& d);
+bool window_conv_applicable(const alcop_conv_desc& d);
 StemGeometry stem_pairs_geometry(const alcop_conv_desc& d);
 int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s);
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s);

@@ -1649,6 +1649,12 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
       d.stride_w < 1 || d.pad_h < 0 || d.pad_w < 0)
     return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "conv dimensions must be positive, padding >= 0");
   if (d.C == 4) return launch_conv2d_stem_pairs(d, s, x, wt, y, stream);  // stem_sm100.cu
+  // C = 64 stride-1 spatial filters with a resident-filter schedule (tileN = K,
+  // FUSED): the window mode of the same kernel (the input window loaded once
+  // per tile); other schedules run the im2col kernel below
+  if (window_conv_applicable(d) && validate_stem_pairs(d, s) == ALCOP_OK)
+    return launch_conv2d_stem_pairs(d, s, x, wt, y, stream);
+  clear_error();
   if (d.C % 8)
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "implicit-GEMM conv needs C to be a multiple of 8 (pad NHWC channels, e.g. 3 -> 8), or C = 4 "

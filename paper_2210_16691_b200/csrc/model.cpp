@@ -265,13 +265,15 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
 // — the paper's stage formula with the window as the pipelined chunk.
 static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, const alcop_schedule& s,
                               const alcop_hw& hw) {
-  const double tiles = static_cast<double>(d.N * g.P * g.QB);
+  const bool window = d.C == 64;
+  const double tiles = static_cast<double>(d.N * (window ? (g.P + g.TR - 1) / g.TR : g.P) * g.QB);
   const double per_sm = std::ceil(tiles / hw.numSM);
   const double ob = d.out_dtype == ALCOP_F32 ? 4.0 : 2.0;
-  const double mma = static_cast<double>(d.R) * (g.T2 / 2) * (128.0 * d.K * 16 * 2) / hw.throughputSM;
-  const double fill = static_cast<double>(d.R) * g.row_bytes / hw.bwSmem;
+  const double ksteps = window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(d.R * (g.T2 / 2));
+  const double mma = ksteps * (128.0 * d.K * 16 * 2) / hw.throughputSM;
+  const double fill = static_cast<double>(g.box_bytes) / hw.bwSmem;
   const double out_bytes = static_cast<double>(d.N * g.P * g.Q) * d.K * ob;
-  const double in_bytes = static_cast<double>(d.N) * d.H * d.W * 8.0;
+  const double in_bytes = static_cast<double>(d.N) * d.H * d.W * d.C * 2.0;
   const double hbm_tile = (out_bytes + in_bytes) / tiles / (hw.bwDRAMWrite / hw.numSM);
   const double epi = hw.latDRAMWrite + (d.K * ob / 128.0) * hw.tTile;
   double use = std::max({mma, fill, hbm_tile, hw.tIssue});
@@ -281,7 +283,7 @@ static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, c
 }
 
 static int choose_stem_pairs(const alcop_conv_desc& d, const alcop_hw& hw, alcop_schedule* out) {
-  if (!stem_pairs_applicable(d))
+  if (d.C != 64 && !stem_pairs_applicable(d))
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256");
   const StemGeometry g = stem_pairs_geometry(d);
@@ -322,7 +324,7 @@ extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_
   const int64_t P = (d->H + 2 * d->pad_h - d->R) / d->stride_h + 1;
   const int64_t Q = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
-  if (d->C == 4) return choose_stem_pairs(*d, *hw, out);
+  if (d->C == 4 || window_conv_applicable(*d)) return choose_stem_pairs(*d, *hw, out);
   const bool stem = d->x_halo && d->S * d->C <= 64 && d->stride_w * 16 <= 256 && d->stride_h * 8 <= 256;
   alcop_gemm_desc g{};
   g.M = d->N * P * Q;

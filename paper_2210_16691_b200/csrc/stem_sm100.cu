@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -55,17 +56,23 @@ namespace {
 constexpr int kStemThreads = 352;  // producer; MMA + 4 epilogue warps per tile parity (1, 2-5 even; 6, 7-10 odd)
 constexpr uint32_t kStemStaging = 32 * 128;  // one epilogue staging buffer: 32 rows x 128 B
 
+// kMode: 0 = pixel pairs (C = 4, stride_w 2: the ResNet-50 stem); 1 = window
+// (C = 64, stride 1: a TR-output-row tile reads its (TR+R-1)-row input window
+// once; tap (r, s) is the window shifted by r rows and s pixels)
 struct StemKParams {
-  int32_t P, Q, QB, num_tiles;  // output rows / columns per image, 128-column blocks per row
+  int32_t P, Q, QB, num_tiles;  // tile rows (output rows / row blocks) per image, output columns, column blocks
+  int32_t Pout;                 // output rows per image
   int32_t R, S, T2, o_min;      // filter rows / taps, pair groups per filter row (even), pair offset of group 0
-  int32_t sh, ph, pw;
+  int32_t row_step, ph, pw;     // input rows per tile row (stride_h / TR), padding
   int32_t BN;                   // = K filters (the whole N of the GEMM view)
   int32_t stages, nacc;
-  uint32_t row_bytes, slot_bytes, wbytes;  // window row (NB blocks x 128 B), ring slot, resident filter
+  uint32_t row_bytes, slot_bytes, box_bytes, wbytes;  // window row, ring slot, TMA box, resident filter
   uint32_t acc_stride, tmem_cols, idesc;
-  int32_t dn, dp, dq;           // the grid as (images, rows, column blocks): the tile cursor's step
-  int32_t shift, blk_off;       // window: first MMA row `shift` pairs into it; block of column block 0
-  const uint16_t* w;            // KRSC, C = 4
+  int32_t dn, dp, dq;           // the grid as (images, tile rows, column blocks): the tile cursor's step
+  int32_t shift, blk_off;       // window: first MMA row `shift` pairs in; x coordinate of column block 0
+  int32_t lwp;                  // window mode: log2 of the window row pitch WP (pixels); TR = 128 / WP
+  int32_t stage_bufs;           // epilogue staging buffers per warp (1 or 2)
+  const uint16_t* w;            // KRSC
   int32_t dual;                 // two MMA-issuing warps (1: even tiles, 6: odd tiles); even rings only
   int32_t skip;                 // measurement only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
 };
@@ -83,28 +90,11 @@ __device__ __forceinline__ uint32_t pack2s<__half>(uint32_t a, uint32_t b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-#ifdef STEM_TRACE
-// measurement build only (-DSTEM_TRACE): CTA 0 prints per-tile timestamps of each role
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  t = clock64();
-  return t;
-}
-#define TRACE_DECL unsigned long long tr_[24]; int trn_ = 0;
-#define TRACE_AT(tl) if (blockIdx.x == 0 && (tl) >= 40 && trn_ < 24) tr_[trn_++] = gtimer();
-#define TRACE_DUMP(tag) if (blockIdx.x == 0 && lane == 0) { for (int i = 0; i < trn_; ++i) printf("%s %d %llu\n", tag, i, tr_[i]); }
-#else
-#define TRACE_DECL
-#define TRACE_AT(tl) ;
-#define TRACE_DUMP(tag) ;
-#endif
-
-
-// Tile cursor: tile t = (image n, output row p, column block qb), qb
-// fastest.  A CTA walks t = blockIdx.x + i * grid; the cursor advances by
-// the grid's (dn, dp, dq) decomposition with carries — no integer division
-// in the tile loops (the divisions' dependent chains on the uniform datapath
-// cost ~900 clk per tile in the MMA warp).
+// Tile cursor: tile t = (image n, tile row p, column block qb), qb fastest.
+// A CTA walks t = blockIdx.x + i * grid; the cursor advances by the grid's
+// (dn, dp, dq) decomposition with carries — no integer division in the tile
+// loops (the divisions' dependent chains on the uniform datapath cost ~900
+// clk per tile in the MMA warp).
 struct StemCursor {
   int n, p, qb;
   __device__ __forceinline__ void start(const StemKParams& k) {
@@ -126,10 +116,65 @@ struct StemCursor {
   }
 };
 
-// kR, kKS: filter rows and k-steps per filter row fixed at compile time (the
-// ResNet-50 stem: 7 x 2) so the 14 MMAs of a tile issue back to back with
-// immediate descriptor offsets; 0, 0 = run-time loop (any filter)
-template <typename OutT, int kR, int kKS>
+// Issue one tile's MMAs (one elected thread).  kR/kKS (pairs) or kR/kS
+// (window) fixed at compile time unroll the whole tile (immediate descriptor
+// offsets); 0 = run-time loops.
+template <int kMode, int kR, int kKS>
+__device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_tmem, uint32_t a0, uint32_t wsm) {
+  using namespace ptx;
+  if constexpr (kMode == 0) {
+    // pairs: per filter row r, T2/2 k-steps; A rows m -> pair (m + 2j [+1]) of
+    // window row r (LBO 16: overlapping core matrices), B k groups (r, 2j), (r, 2j+1)
+    const uint32_t lbo_b = static_cast<uint32_t>(p.BN) * 16u;
+    const uint64_t b_step = (2 * lbo_b) >> 4;
+    const uint64_t a_row16 = p.row_bytes >> 4;
+    const uint64_t ad = make_smem_desc(a0, 16u, 128u, kLayoutNone);
+    const uint64_t bd = make_smem_desc(wsm, lbo_b, 128u, kLayoutNone);
+    if constexpr (kR > 0) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+#pragma unroll
+        for (int j = 0; j < kKS; ++j)
+          umma_f16_ss(d_tmem, ad + r * a_row16 + 2 * j, bd + (r * kKS + j) * b_step, p.idesc,
+                      (r > 0 || j > 0) ? 1u : 0u);
+    } else {
+      const int ksteps = p.T2 / 2;
+      for (int r = 0; r < p.R; ++r)
+        for (int j = 0; j < ksteps; ++j)
+          umma_f16_ss(d_tmem, ad + r * a_row16 + 2 * j, bd + (r * ksteps + j) * b_step, p.idesc,
+                      (r > 0 || j > 0) ? 1u : 0u);
+    }
+  } else {
+    // window: tap (r, s) = A rows m -> window pixel m + r*WP + s (128 B each,
+    // 128B-swizzled: the swizzle follows the absolute smem address, so a
+    // start moved by whole 128-byte rows reads the shifted rows, base offset
+    // 0 — tools/desc_probe.cu); 4 k-steps of 16 channels per tap; B tap t =
+    // BN rows x 64 channels, 128B-swizzled
+    const uint64_t ad = make_smem_desc(a0, 16u, 1024u, kLayoutSW128);
+    const uint64_t bd = make_smem_desc(wsm, 16u, 1024u, kLayoutSW128);
+    const uint64_t a_row16 = (128u << p.lwp) >> 4;  // one window row
+    const uint64_t b_tap16 = (static_cast<uint32_t>(p.BN) * 128u) >> 4;
+    if constexpr (kR > 0) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+#pragma unroll
+        for (int s = 0; s < kKS; ++s)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            umma_f16_ss(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * kKS + s) * b_tap16 + 2 * u, p.idesc,
+                        (r > 0 || s > 0 || u > 0) ? 1u : 0u);
+    } else {
+      for (int r = 0; r < p.R; ++r)
+        for (int s = 0; s < p.S; ++s)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            umma_f16_ss(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * p.S + s) * b_tap16 + 2 * u, p.idesc,
+                        (r > 0 || s > 0 || u > 0) ? 1u : 0u);
+    }
+  }
+}
+
+template <typename OutT, int kMode, int kR, int kKS>
 __global__ void __launch_bounds__(kStemThreads, 1)
     alcop_stem_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                            const StemKParams p) {
@@ -139,7 +184,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   const uint32_t ring = smem_u32(smem);
   const uint32_t wsm = ring + p.stages * p.slot_bytes;
   const uint32_t staging = wsm + p.wbytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes + 8 * 2 * kStemStaging);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes +
+                                               8 * p.stage_bufs * kStemStaging);
   uint64_t* full = bars;
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
@@ -172,13 +218,13 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   grid_dependency_wait();
   grid_launch_dependents();
 
-  // The filter, resident for the kernel's lifetime, in the B operand's
-  // K-major no-swizzle layout [k group kg][filter n][8 elements]
-  // (LBO = BN*16 bytes between k groups, SBO = 128 bytes between 8-filter
-  // groups).  k group kg = (filter row r, pair group t); element e = (tap
-  // parity e/4, channel e%4); tap s = 2*(o_min+t) + e/4 + pad_w, zero outside
-  // [0, S) (the pairing overhangs the filter by at most one tap per side).
-  {
+  // The filter, resident in shared memory for the kernel's lifetime.
+  if constexpr (kMode == 0) {
+    // B operand in the K-major no-swizzle layout [k group kg][filter n][8
+    // elements] (LBO = BN*16 bytes between k groups, SBO = 128 bytes between
+    // 8-filter groups).  k group kg = (filter row r, pair group t); element e
+    // = (tap parity e/4, channel e%4); tap s = 2*(o_min+t) + e/4 + pad_w, zero
+    // outside [0, S) (the pairing overhangs the filter by at most one tap).
     const int groups = p.R * p.T2;
     for (int idx = threadIdx.x; idx < groups * p.BN; idx += blockDim.x) {
       const int kg = idx / p.BN, n = idx - kg * p.BN;
@@ -195,8 +241,18 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
       st_shared_v4(wsm + static_cast<uint32_t>(idx) * 16u, v[0], v[1], v[2], v[3]);
     }
-    fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor cores
+  } else {
+    // B operand per tap t = (r, s): BN filter rows x 64 channels (128 B),
+    // 128B-swizzled K-major ([t][n][128 B], 16-byte chunk c of row n at c ^ (n & 7))
+    const int rows = p.R * p.S * p.BN;
+    for (int idx = threadIdx.x; idx < rows * 8; idx += blockDim.x) {
+      const int row = idx >> 3, c = idx & 7;
+      const int t = row / p.BN, n = row - t * p.BN;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.w + (static_cast<int64_t>(n) * p.R * p.S + t) * 64) + c);
+      st_shared_v4(wsm + static_cast<uint32_t>(row) * 128u + ((c ^ (n & 7)) << 4), v.x, v.y, v.z, v.w);
+    }
   }
+  fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor cores
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -209,29 +265,25 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     // ======================= producer (TMA) =======================
     // the whole warp walks the loop (coordinates stay on the uniform
     // datapath), one elected lane issues
-    const uint32_t bytes = static_cast<uint32_t>(p.R) * p.row_bytes;  // the box, zero fill included
     int slot = 0;
     uint32_t phase = 0;
     StemCursor cur;
     cur.start(p);
-    TRACE_DECL
     for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
       mbar_wait(smem_u32(&empty[slot]), ((phase >> slot) & 1u) ^ 1u);  // producer_acquire
-      TRACE_AT(tl)
       phase ^= 1u << slot;
       if (elect_one()) {
         if (p.skip & 2) {
           mbar_arrive(smem_u32(&full[slot]));
         } else {
-          mbar_arrive_expect_tx(smem_u32(&full[slot]), bytes);            // producer_commit
+          mbar_arrive_expect_tx(smem_u32(&full[slot]), p.box_bytes);      // producer_commit
           tma_load_4d(ring + slot * p.slot_bytes, &tmX, smem_u32(&full[slot]), 0, cur.qb * 16 + p.blk_off,
-                      cur.p * p.sh - p.ph, cur.n);
+                      cur.p * p.row_step - p.ph, cur.n);
         }
       }
       __syncwarp();
       slot = slot + 1 == p.stages ? 0 : slot + 1;
     }
-    TRACE_DUMP("P")
   } else if (warp == 1 || warp == 6) {
     // ======================= MMA issuers =======================
     // warp-uniform loop, one elected lane issues: the descriptors stay in
@@ -243,80 +295,44 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     // tcgen05.commit tracks only the MMAs it issued.
     const int first = warp == 6 ? 1 : 0;
     const int step = p.dual ? 2 : 1;
-    if (warp == 6 && !p.dual) {
-      __syncwarp();
-    } else {
-    int slot = first % p.stages;
-    uint32_t phase = 0, acc_phase = 0;  // bit k: current parity of ring slot / accumulator k
-    const uint32_t lbo_b = static_cast<uint32_t>(p.BN) * 16u;
-    const int ksteps = (p.skip & 1) ? 0 : p.T2 / 2;
-    const uint64_t b_step = (2 * lbo_b) >> 4;
-    const uint64_t a_row_step = (p.row_bytes >> 4) - 2 * ksteps;
-    const uint64_t a_row16 = p.row_bytes >> 4;
-    TRACE_DECL
-    int acc = first % p.nacc;
-    for (int tl = first; tl < my_tiles; tl += step) {
-      mbar_wait(smem_u32(&tempty[acc]), ((acc_phase >> acc) & 1u) ^ 1u);  // accumulator drained
-      acc_phase ^= 1u << acc;
-      TRACE_AT(tl)
-      tc_fence_after();
-      mbar_wait(smem_u32(&full[slot]), (phase >> slot) & 1u);      // consumer_wait
-      TRACE_AT(tl)
-      phase ^= 1u << slot;
-      tc_fence_after();
-      TRACE_AT(tl)
-      const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
-      const uint32_t a0 = ring + slot * p.slot_bytes + static_cast<uint32_t>(p.shift) * 16u;
-      if (elect_one()) {
-        // descriptors advance by constants: +32 B of A (two pair groups) and
-        // two k groups of B per k-step, A to the next window row per filter row
-        uint64_t ad = make_smem_desc(a0, 16u, 128u, kLayoutNone);
-        uint64_t bd = make_smem_desc(wsm, lbo_b, 128u, kLayoutNone);
-        if constexpr (kR > 0) {
-          if (!(p.skip & 1)) {
-#pragma unroll
-            for (int r = 0; r < kR; ++r)
-#pragma unroll
-              for (int j = 0; j < kKS; ++j)
-                umma_f16_ss(d_tmem, ad + r * a_row16 + 2 * j, bd + (r * kKS + j) * b_step, p.idesc,
-                            (r > 0 || j > 0) ? 1u : 0u);
-          }
-        } else {
-          uint32_t accumulate = 0;
-          for (int r = 0; r < p.R; ++r) {
-#pragma unroll 4
-            for (int j = 0; j < ksteps; ++j) {
-              // A: rows m -> pair (m + 2j [+1]) of window row r; B: k groups (r, 2j), (r, 2j+1)
-              umma_f16_ss(d_tmem, ad, bd, p.idesc, accumulate);
-              accumulate = 1;
-              ad += 2;
-              bd += b_step;
-            }
-            ad += a_row_step;
-          }
+    if (!(warp == 6 && !p.dual)) {
+      int slot = first % p.stages;
+      int acc = first % p.nacc;
+      uint32_t phase = 0, acc_phase = 0;  // bit k: current parity of ring slot / accumulator k
+      for (int tl = first; tl < my_tiles; tl += step) {
+        mbar_wait(smem_u32(&tempty[acc]), ((acc_phase >> acc) & 1u) ^ 1u);  // accumulator drained
+        acc_phase ^= 1u << acc;
+        tc_fence_after();
+        mbar_wait(smem_u32(&full[slot]), (phase >> slot) & 1u);             // consumer_wait
+        phase ^= 1u << slot;
+        tc_fence_after();
+        if (elect_one()) {
+          if (!(p.skip & 1))
+            stem_tile_mmas<kMode, kR, kKS>(p, tmem_base + acc * p.acc_stride,
+                                           ring + slot * p.slot_bytes + static_cast<uint32_t>(p.shift) * 16u, wsm);
+          umma_commit(smem_u32(&empty[slot]));  // consumer_release: the window slot is free once these retire
+          umma_commit(smem_u32(&tfull[acc]));   // accumulator ready
         }
-        TRACE_AT(tl)
-        umma_commit(smem_u32(&empty[slot]));  // consumer_release: the window slot is free once these retire
-        umma_commit(smem_u32(&tfull[acc]));   // accumulator ready
+        __syncwarp();
+        slot += step;
+        if (slot >= p.stages) slot -= p.stages;
+        acc += step;
+        if (acc >= p.nacc) acc -= p.nacc;
       }
-      __syncwarp();
-      TRACE_AT(tl)
-      slot += step;
-      if (slot >= p.stages) slot -= p.stages;
-      acc += step;
-      if (acc >= p.nacc) acc -= p.nacc;
     }
-    if (warp == 1) TRACE_DUMP("M")
-    }
+    __syncwarp();
   } else if ((warp >= 2 && warp <= 5) || (warp >= 7 && p.dual)) {
     // ======================= epilogue (warps 2-5: even tiles, 7-10: odd tiles) =======================
     // with two issuing warps the tiles split into two independent
     // MMA -> epilogue pipelines (their own accumulators); one group's TMEM
-    // drain, staging and TMA store overlap the other's
-    const int q = warp & 3;  // TMEM lane quarter = output columns q0 + 32q .. +31
+    // drain, staging and TMA store overlap the other's.  TMEM lane quarter q
+    // holds tile rows m = 32q..32q+31: pairs mode, output columns q0 + m of
+    // one output row; window mode, output (row m / WP, column m % WP) of the
+    // tile's TR rows.
+    const int q = warp & 3;
     const int first = warp >= 7 ? 1 : 0;
     const int step = p.dual ? 2 : 1;
-    const uint32_t stage_base = staging + (warp >= 7 ? warp - 3 : warp - 2) * 2 * kStemStaging;
+    const uint32_t stage_base = staging + (warp >= 7 ? warp - 3 : warp - 2) * p.stage_bufs * kStemStaging;
     constexpr int kChunkCols = 128 / static_cast<int>(sizeof(OutT));
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
@@ -325,15 +341,18 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     StemCursor cur;
     cur.start(p);
     if (first) cur.advance(p);
-    TRACE_DECL
+    // this warp's first output (column, row-in-tile) of the tile
+    const int m0 = q * 32;
+    const int col0 = kMode == 0 ? m0 : (m0 & ((1 << p.lwp) - 1));
+    const int row0 = kMode == 0 ? 0 : (m0 >> p.lwp);
     for (int tl = first; tl < my_tiles; tl += step, cur.advance(p), (step == 2 ? cur.advance(p) : void())) {
       mbar_wait(smem_u32(&tfull[acc]), (acc_phase >> acc) & 1u);
       acc_phase ^= 1u << acc;
-      if (warp == 2) TRACE_AT(tl)
       tc_fence_after();
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      const int q0 = cur.qb * 128;
-      const bool rows_live = q0 + q * 32 < p.Q;
+      const int oq = cur.qb * 128 + col0;                              // output column of row m0
+      const int op = kMode == 0 ? cur.p : cur.p * p.row_step + row0;   // output row of row m0
+      const bool rows_live = oq < p.Q && op < p.Pout;
       for (int c = 0; c < nchunks; ++c) {
         uint32_t w[32];
         if constexpr (sizeof(OutT) == 4) {
@@ -355,9 +374,14 @@ __global__ void __launch_bounds__(kStemThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
         }
-        if (!rows_live || (p.skip & 4)) continue;  // columns past Q (the M=128 tile overhangs a 112-column row)
+        if (!rows_live || (p.skip & 4)) continue;  // tile rows past the image (the M=128 tile overhangs it)
         const uint32_t sbuf = stage_base + buf * kStemStaging;
-        if (lane == 0) bulk_wait_group_read<1>();  // the store that last read sbuf is done
+        if (lane == 0) {  // the store that last read sbuf is done
+          if (p.stage_bufs == 2)
+            bulk_wait_group_read<1>();
+          else
+            bulk_wait_group_read<0>();
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -366,17 +390,16 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&tmY, sbuf, c * kChunkCols, q0 + q * 32, cur.n * p.P + cur.p);
+          tma_store_4d(&tmY, sbuf, c * kChunkCols, oq, op, cur.n);
           bulk_commit_group();
         }
-        buf ^= 1;
+        buf ^= p.stage_bufs - 1;
       }
       acc += step;
       if (acc >= p.nacc) acc -= p.nacc;
     }
     if (lane == 0) bulk_wait_group_read<0>();
     __syncwarp();
-    if (warp == 2) TRACE_DUMP("E")
   }
 
   tc_fence_before();
@@ -388,9 +411,12 @@ __global__ void __launch_bounds__(kStemThreads, 1)
 }
 
 template <typename OutT>
-int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKParams& kp, int grid, int smem,
-                      cudaStream_t st) {
-  auto kern = (kp.R == 7 && kp.T2 == 4) ? alcop_stem_conv_kernel<OutT, 7, 2> : alcop_stem_conv_kernel<OutT, 0, 0>;
+int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKParams& kp, int mode, int grid,
+                      int smem, cudaStream_t st) {
+  auto kern = mode == 1 ? (kp.R == 3 && kp.S == 3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3>
+                                                  : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
+                        : (kp.R == 7 && kp.T2 == 4 ? alcop_stem_conv_kernel<OutT, 0, 7, 2>
+                                                   : alcop_stem_conv_kernel<OutT, 0, 0, 0>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -414,17 +440,57 @@ int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKP
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
+static int out_bytes(const alcop_conv_desc& d) { return d.out_dtype == ALCOP_F32 ? 4 : 2; }
+
 bool stem_pairs_applicable(const alcop_conv_desc& d) {
-  const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
   return d.C == 4 && d.stride_w == 2 && !d.x_halo && d.W % 16 == 0 && d.K % 16 == 0 && d.K >= 16 && d.K <= 256 &&
-         (d.K * ob) % 128 == 0 && d.R <= 32 && d.S <= 32 && d.stride_h <= 8 && d.pad_h <= 64 && d.pad_w <= 64;
+         (d.K * out_bytes(d)) % 128 == 0 && d.R <= 32 && d.S <= 32 && d.stride_h <= 8 && d.pad_h <= 64 &&
+         d.pad_w <= 64;
+}
+
+// window row pitch: the smallest power of two >= Q + S - 1 (a valid output
+// column's taps stay inside its window row), at least 16, at most 128
+static int64_t window_pitch(const alcop_conv_desc& d) {
+  const int64_t Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
+  int64_t wp = 16;
+  while (wp < Q + d.S - 1) wp *= 2;
+  return wp;
+}
+
+bool window_conv_applicable(const alcop_conv_desc& d) {
+  if (!(d.C == 64 && d.stride_h == 1 && d.stride_w == 1 && !d.x_halo && d.K % 16 == 0 && d.K >= 16 &&
+        d.K <= 256 && (d.K * out_bytes(d)) % 128 == 0 && d.R <= 8 && d.S <= 8 && d.pad_h <= 8 && d.pad_w <= 8))
+    return false;
+  const int64_t wp = window_pitch(d);
+  if (wp > 128) return false;
+  const int64_t tr = 128 / wp;
+  const int64_t P = (d.H + 2 * d.pad_h - d.R) + 1;
+  // worth it only when the tile rows are mostly real output (not for a 7x7 map
+  // in 8-row tiles); the resident filter leaves room for a 2-slot ring
+  return (d.R > 1 || d.S > 1) && P >= tr && (tr + d.R - 1) * wp <= 256 && d.R * d.S * d.K * 128 <= 80 * 1024;
 }
 
 StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   StemGeometry g{};
   g.P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
   g.Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
+  if (d.C == 64) {  // window mode
+    const int64_t wp = window_pitch(d);
+    const int64_t tr = 128 / wp;
+    g.QB = 1;
+    g.TR = static_cast<int32_t>(tr);
+    g.WP = static_cast<int32_t>(wp);
+    g.row_bytes = static_cast<uint32_t>(wp * 128);
+    g.box_bytes = static_cast<uint32_t>((tr + d.R - 1) * wp * 128);
+    // + S-1 pixels of slack: the taps of the tile's last (overhanging, never
+    // stored) rows read past the box
+    g.slot_bytes = static_cast<uint32_t>((g.box_bytes + (d.S - 1) * 128 + 1023) / 1024 * 1024);
+    g.wbytes = static_cast<uint32_t>((d.R * d.S * d.K * 128 + 1023) / 1024 * 1024);
+    g.kdim = d.R * d.S * 64;
+    return g;
+  }
   g.QB = (g.Q + 127) / 128;
+  g.TR = 1;
   // tap s reads pixel 2q - pad_w + s = pair q + floor((s - pad_w) / 2)
   auto fdiv2 = [](int64_t v) { return v >= 0 ? v / 2 : -((1 - v) / 2); };
   g.o_min = static_cast<int32_t>(fdiv2(-d.pad_w));
@@ -434,27 +500,39 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   // window: shift (0..7) + 128 rows + T2-1 further pairs, in 8-pair (128 B) blocks
   g.NB = (7 + 128 + g.T2 - 1 + 7) / 8;
   g.row_bytes = static_cast<uint32_t>(g.NB * 128);
-  g.slot_bytes = static_cast<uint32_t>((d.R * g.row_bytes + 1023) / 1024 * 1024);
+  g.box_bytes = static_cast<uint32_t>(d.R * g.row_bytes);
+  g.slot_bytes = static_cast<uint32_t>((g.box_bytes + 1023) / 1024 * 1024);
   g.wbytes = static_cast<uint32_t>((d.R * g.T2 * d.K * 16 + 1023) / 1024 * 1024);
   g.kdim = d.R * g.T2 * 8;
   return g;
 }
 
-int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
+static int64_t stem_smem_bytes_bufs(const alcop_conv_desc& d, const alcop_schedule& s, int bufs) {
   const StemGeometry g = stem_pairs_geometry(d);
   const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner) + 16;
-  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 8 * 2 * kStemStaging + bars;
+  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 8 * bufs * kStemStaging + bars;
+}
+
+// two staging buffers per epilogue warp when they fit, else one
+static int stem_staging_bufs(const alcop_conv_desc& d, const alcop_schedule& s) {
+  return stem_smem_bytes_bufs(d, s, 2) <= kMaxSmemBytes ? 2 : 1;
+}
+
+int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
+  return stem_smem_bytes_bufs(d, s, stem_staging_bufs(d, s));
 }
 
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
   if (s.tileM != kTileM || s.tileK != 64 || s.tileN != d.K)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the stem kernel's tile is 128 output columns x all K filters (tileM 128, tileN = K, tileK 64)");
+                     "the resident-filter conv kernel's tile is 128 output pixels x all K filters (tileM 128, "
+                     "tileN = K, tileK 64)");
   if (s.cta_group != 1 || s.stream_k != 0 || s.mode != ALCOP_MODE_FUSED)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the stem kernel runs one CTA per tile with one window chunk per tile (FUSED, cta_group 1)");
+                     "the resident-filter conv kernel runs one CTA per tile, one window chunk per tile (FUSED, "
+                     "cta_group 1)");
   if (s.n_stage_smem_A != s.n_stage_smem_B || s.n_stage_smem_A < 1 || s.n_stage_smem_A > kMaxStages)
-    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the stem kernel's window ring: equal A/B stages in 1..16");
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the window ring: equal A/B stages in 1..16");
   if (s.n_stage_inner < 1 || s.n_stage_inner > 8 || s.n_stage_inner * d.K > kTmemCols)
     return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner accumulators of K columns exceed TMEM");
   if (stem_pairs_smem_bytes(d, s) > kMaxSmemBytes)
@@ -464,10 +542,13 @@ int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
 
 int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt,
                              void* y, void* stream) {
-  if (!stem_pairs_applicable(d))
+  const int mode = d.C == 64 ? 1 : 0;
+  if (mode == 0 && !stem_pairs_applicable(d))
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256, "
                      "K * out bytes % 128 == 0, no halo layout");
+  if (mode == 1 && !window_conv_applicable(d))
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "not a window-conv shape (C 64, stride 1, small filter)");
   int rc = validate_stem_pairs(d, s);
   if (rc) return rc;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wt) | reinterpret_cast<uintptr_t>(y)) & 15)
@@ -479,39 +560,54 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   const CUtensorMapDataType odt = d.out_dtype == ALCOP_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                   : d.out_dtype == ALCOP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  const int ob = d.out_dtype == ALCOP_F32 ? 4 : 2;
+  const int ob = out_bytes(d);
   CUtensorMap tx, ty;
-  // x viewed as {64 elements = 8 pixel pairs (128 B), W/16 blocks, H, N}; box
-  // = NB blocks of R consecutive rows: the tile's whole input window, zero
-  // filled above/below the image and left/right of it (pairs never straddle
-  // the border: W is even, pad columns come in whole out-of-range pairs)
-  const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W / 16), static_cast<cuuint64_t>(d.H),
-                               static_cast<cuuint64_t>(d.N)};
-  const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 8), static_cast<cuuint64_t>(d.H * d.W * 8)};
-  const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), static_cast<cuuint32_t>(d.R), 1};
   const cuuint32_t one[4] = {1, 1, 1, 1};
-  rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_NONE, "x (stem pairs)");
+  if (mode == 0) {
+    // x viewed as {64 elements = 8 pixel pairs (128 B), W/16 blocks, H, N}; box
+    // = NB blocks of R consecutive rows: the tile's whole input window, zero
+    // filled above/below the image and left/right of it (pairs never straddle
+    // the border: W is even, pad columns come in whole out-of-range pairs)
+    const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W / 16), static_cast<cuuint64_t>(d.H),
+                                 static_cast<cuuint64_t>(d.N)};
+    const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 8), static_cast<cuuint64_t>(d.H * d.W * 8)};
+    const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), static_cast<cuuint32_t>(d.R), 1};
+    rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_NONE, "x (stem pairs)");
+  } else {
+    // x as {64 channels, W, H, N}; box = WP pixels (from -pad_w) x TR+R-1
+    // rows: the tile's input window, zero filled outside the image
+    const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W), static_cast<cuuint64_t>(d.H),
+                                 static_cast<cuuint64_t>(d.N)};
+    const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 128), static_cast<cuuint64_t>(d.H * d.W * 128)};
+    const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.WP), static_cast<cuuint32_t>(g.TR + d.R - 1), 1};
+    rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "x (window)");
+  }
   if (rc) return rc;
-  // y viewed as {K, Q, N*P}: each epilogue warp stores 32 columns x 128 B
-  const cuuint64_t ydims[3] = {static_cast<cuuint64_t>(d.K), static_cast<cuuint64_t>(g.Q),
-                               static_cast<cuuint64_t>(d.N * g.P)};
-  const cuuint64_t ystr[2] = {static_cast<cuuint64_t>(d.K * ob), static_cast<cuuint64_t>(g.Q * d.K * ob)};
-  const cuuint32_t ybox[3] = {static_cast<cuuint32_t>(128 / ob), 32, 1};
-  rc = encode_tiled_map(&ty, odt, y, 3, ydims, ystr, ybox, one, CU_TENSOR_MAP_SWIZZLE_128B, "y (stem pairs)");
+  // y as {K, Q, P, N}: each epilogue warp stores its 32 tile rows x 128 B
+  // (window mode, WP = 16: two output rows of 16 columns)
+  const int64_t wcols = mode == 0 ? 32 : std::min<int64_t>(32, g.WP);
+  const cuuint64_t ydims[4] = {static_cast<cuuint64_t>(d.K), static_cast<cuuint64_t>(g.Q),
+                               static_cast<cuuint64_t>(g.P), static_cast<cuuint64_t>(d.N)};
+  const cuuint64_t ystr[3] = {static_cast<cuuint64_t>(d.K * ob), static_cast<cuuint64_t>(g.Q * d.K * ob),
+                              static_cast<cuuint64_t>(g.P * g.Q * d.K * ob)};
+  const cuuint32_t ybox[4] = {static_cast<cuuint32_t>(128 / ob), static_cast<cuuint32_t>(wcols),
+                              static_cast<cuuint32_t>(32 / wcols), 1};
+  rc = encode_tiled_map(&ty, odt, y, 4, ydims, ystr, ybox, one, CU_TENSOR_MAP_SWIZZLE_128B, "y (stem)");
   if (rc) return rc;
 
   StemKParams kp{};
-  kp.P = static_cast<int32_t>(g.P);
+  kp.Pout = static_cast<int32_t>(g.P);
+  kp.P = static_cast<int32_t>(mode == 0 ? g.P : (g.P + g.TR - 1) / g.TR);
   kp.Q = static_cast<int32_t>(g.Q);
   kp.QB = static_cast<int32_t>(g.QB);
-  const int64_t tiles = d.N * g.P * g.QB;
+  const int64_t tiles = d.N * static_cast<int64_t>(kp.P) * g.QB;
   if (tiles > (int64_t(1) << 31) - 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "too many output tiles");
   kp.num_tiles = static_cast<int32_t>(tiles);
   kp.R = static_cast<int32_t>(d.R);
   kp.S = static_cast<int32_t>(d.S);
   kp.T2 = g.T2;
   kp.o_min = g.o_min;
-  kp.sh = d.stride_h;
+  kp.row_step = mode == 0 ? d.stride_h : g.TR;
   kp.ph = d.pad_h;
   kp.pw = d.pad_w;
   kp.BN = static_cast<int32_t>(d.K);
@@ -519,11 +615,16 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.nacc = s.n_stage_inner;
   kp.row_bytes = g.row_bytes;
   kp.slot_bytes = g.slot_bytes;
+  kp.box_bytes = g.box_bytes;
   kp.wbytes = g.wbytes;
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(d.K));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.nacc));
   kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, static_cast<uint32_t>(d.K));
   kp.w = static_cast<const uint16_t*>(wt);
+  kp.stage_bufs = stem_staging_bufs(d, s);
+  int lwp = 0;
+  while ((1 << lwp) < g.WP) ++lwp;
+  kp.lwp = lwp;
   static const int skip_env = [] {
     const char* e = std::getenv("ALCOP_STEM_SKIP");
     return e ? std::atoi(e) : 0;
@@ -537,15 +638,20 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.dn = grid / (kp.P * kp.QB);
   kp.dp = (grid - kp.dn * kp.P * kp.QB) / kp.QB;
   kp.dq = grid - kp.dn * kp.P * kp.QB - kp.dp * kp.QB;
-  // column block qb reads pairs from 128*qb + o_min: block 16*qb + floor(o_min/8), `shift` pairs in
-  kp.blk_off = g.o_min >= 0 ? g.o_min / 8 : -((7 - g.o_min) / 8);
-  kp.shift = g.o_min - 8 * kp.blk_off;
+  if (mode == 0) {
+    // column block qb reads pairs from 128*qb + o_min: block 16*qb + floor(o_min/8), `shift` pairs in
+    kp.blk_off = g.o_min >= 0 ? g.o_min / 8 : -((7 - g.o_min) / 8);
+    kp.shift = g.o_min - 8 * kp.blk_off;
+  } else {
+    kp.blk_off = -d.pad_w;  // the window's first pixel
+    kp.shift = 0;
+  }
   const int smem = static_cast<int>(stem_pairs_smem_bytes(d, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (d.out_dtype) {
-    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, kp, grid, smem, st);
-    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, kp, grid, smem, st);
-    default: return launch_stem_typed<__half>(tx, ty, kp, grid, smem, st);
+    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, kp, mode, grid, smem, st);
+    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, kp, mode, grid, smem, st);
+    default: return launch_stem_typed<__half>(tx, ty, kp, mode, grid, smem, st);
   }
 }
 

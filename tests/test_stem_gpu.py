@@ -119,3 +119,48 @@ def test_stem_rejects(alcop):
         else:
             assert rc == alcop.ALCOP_ERR_CONFIG and lib.alcop_last_error().decode().startswith(tag), bad
     torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------
+# Window mode (C = 64, stride 1): a tile of TR output rows loads its input
+# window once; tap (r, s) = the window shifted by r rows and s pixels, read
+# through a 128B-swizzled descriptor whose start moved by whole 128-byte rows.
+WINDOW_CASES = [  # N, H, W, C, K, R, S, (stride), (pad)
+    (2, 56, 56, 64, 64, 3, 3, (1, 1), (1, 1)),    # ResNet-50 l1 3x3 class: pitch 64, 2 rows per tile
+    (2, 28, 28, 64, 64, 3, 3, (1, 1), (1, 1)),    # pitch 32, 4 rows
+    (2, 14, 14, 64, 64, 3, 3, (1, 1), (1, 1)),    # pitch 16, 8 rows (two output rows per epilogue warp)
+    (1, 30, 30, 64, 64, 3, 3, (1, 1), (1, 1)),    # ragged last row block
+    (2, 18, 18, 64, 64, 3, 3, (1, 1), (0, 0)),    # no padding
+    (1, 9, 60, 64, 128, 1, 3, (1, 1), (0, 1)),    # R != S, K = 128
+    (1, 12, 20, 64, 64, 2, 4, (1, 1), (1, 2)),    # even filter, uneven padding
+]
+
+
+@pytest.mark.parametrize("case", WINDOW_CASES, ids=lambda c: "x".join(map(str, c[:7])) + "_p%d%d" % c[8])
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_window_exact(alcop, case, out_dt):
+    X, Wt, ref = _inputs(case, 91)
+    _, _, _, _, K, _, _, st, pd = case
+    odt = torch.float32 if out_dt == "f32" else torch.bfloat16
+    d = alcop.conv_desc(*case[:7], st, pd, alcop.BF16, alcop.F32 if out_dt == "f32" else alcop.BF16)
+    s = alcop.choose_conv_schedule(d)
+    assert s.tileN == K, s  # the resident-filter (window) space
+    Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=odt)
+    torch.cuda.synchronize()
+    _assert_equal(Y.cpu(), torch.from_numpy(ref).to(odt), "window %s" % s)
+
+
+def test_window_schedules_and_im2col_agree(alcop):
+    """Every ring depth x accumulator count of the window mode, and the im2col
+    kernel on the same conv (a WRAP schedule routes there): same bits."""
+    case = (2, 56, 56, 64, 64, 3, 3, (1, 1), (1, 1))
+    X, Wt, ref = _inputs(case, 93)
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    for st in (1, 2, 3):
+        for inner in (1, 2, 4):
+            s = alcop.make_schedule(tileN=64, tileK=64, n_stage=st, n_stage_inner=inner, mode=1)
+            Y = alcop.conv2d(X, Wt, (1, 1), (1, 1), sched=s, out_dtype=torch.bfloat16)
+            _assert_equal(Y.cpu(), want, "window stages %d inner %d" % (st, inner))
+    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=4, n_stage_inner=2, mode=0)  # WRAP: im2col kernel
+    Y = alcop.conv2d(X, Wt, (1, 1), (1, 1), sched=s, out_dtype=torch.bfloat16)
+    _assert_equal(Y.cpu(), want, "im2col")
