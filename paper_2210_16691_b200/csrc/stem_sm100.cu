@@ -467,6 +467,8 @@ bool window_conv_applicable(const alcop_conv_desc& d) {
   const int64_t P = (d.H + 2 * d.pad_h - d.R) + 1;
   // worth it only when the tile rows are mostly real output (not for a 7x7 map
   // in 8-row tiles); the resident filter leaves room for a 2-slot ring
+  // 1x1 convs stay on the implicit-GEMM kernel: both run them at the HBM
+  // bound (tools/window1x1_probe.py: within +-8 % either way)
   return (d.R > 1 || d.S > 1) && P >= tr && (tr + d.R - 1) * wp <= 256 && d.R * d.S * d.K * 128 <= 80 * 1024;
 }
 
