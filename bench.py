@@ -97,6 +97,13 @@ REF_SAMPLE_COLS = 128  # one output sub-block per process: rows x 128 columns, f
 REF_NS_PER_MMA = 150e-9  # measured cost of one interpreted mma statement
 
 
+def model_pred_ms(alcop, M, N, K, sched, b_layout):
+    """alcop_predict's time for the schedule (sustained regime: the bench
+    times every kernel in back-to-back graphs), in ms."""
+    d = alcop.gemm_desc(M, N, K, 1, alcop.BF16, alcop.BF16, b_layout)
+    return alcop.predict(d, sched)["seconds"] * 1e3
+
+
 def ref_sample_rows(seconds_per_step, kmax=max(SQUARES)):
     """Rows of the sample block so the slowest job (K = kmax) takes ~seconds_per_step."""
     return max(1, min(128, int(seconds_per_step / (REF_NS_PER_MMA * REF_SAMPLE_COLS * kmax))))
@@ -553,8 +560,10 @@ def main_gpu(args, rank, world, local_rank):
         n, m, s = it["n"], it["m"], it["sched"]
         ms, ms1 = ranks.max(statistics.median(alone[n])), ranks.max(statistics.median(alone1[n]))
         tf = square_flops(n) / (ms * 1e-3) / 1e12  # whole-job rate of this square
+        pred = model_pred_ms(alcop, m, n, n, s, alcop.B_KN)
         per_sq[str(n)] = {"ms": round(ms, 4), "tflops": round(tf, 1),
                           "frac_of_peak_per_gpu": round(tf / world / peaks["bf16_tflops"], 3),
+                          "model_pred_ms": round(pred, 4), "model_err": round((pred - ms) / ms, 3),
                           "n_stage1_ms": round(ms1, 4), "speedup_vs_n_stage1": round(ms1 / ms, 2),
                           "rows_per_gpu": m, "schedule": s.as_dict(),
                           "timing": "median of 3 round-robin rounds, CUDA graph of this GEMM alone"}
@@ -817,7 +826,9 @@ def bert_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity, 
                         iters=max(40, 2 * nr), warmup=3, reps_per_graph=nr)
         fl = 2.0 * M * N * K
         tf = fl / (ms * 1e-3) / 1e12
+        pred = model_pred_ms(alcop, M, N, K, sched[(M, N, K)], alcop.B_KN)
         per[name] = {"ms": round(ms, 4), "shape": [M, N, K], "tflops": round(tf, 1),
+                     "model_pred_ms": round(pred, 4), "model_err": round((pred - ms) / ms, 3),
                      "frac_of_attainable": round(tf / attainable(fl, 2 * (M * K + K * N + M * N)), 3),
                      "frac_of_peak": round(tf / peaks["bf16_tflops"], 3), "schedule": sched[(M, N, K)].as_dict()}
         del rot

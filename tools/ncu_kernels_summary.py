@@ -106,6 +106,12 @@ def main():
                      "(l2_write_B is what the kernel wrote into L2).",
            "kernels": kernels}
     dst = os.path.join(ROOT, "profiles", "ncu_kernels_%s.json" % a.round)
+    if os.path.exists(dst):  # keep the cases not recaptured this time (marked as from an earlier capture)
+        old = json.load(open(dst)).get("kernels", {})
+        for case, d in old.items():
+            if case not in kernels:
+                d.setdefault("captured", "earlier capture of this round (previous build)")
+                kernels[case] = d
     with open(dst, "w") as f:
         json.dump(out, f, indent=1)
     print(dst, len(kernels), "kernels")

@@ -15,7 +15,11 @@ SHAPES = [(4096, 3072, 768, 256, 6), (4096, 2304, 768, 256, 6), (4096, 4096, 409
           # 148 tiles = 2 full waves: stream-K splits nothing (pure scheduling overhead)
           (9472, 1024, 768, 256, 6), (9472, 1024, 3072, 256, 6),
           # long K, few waves: 80 tiles
-          (2560, 2048, 16384, 256, 6)]
+          (2560, 2048, 16384, 256, 6),
+          # the BERT N = 768 shapes: 64 pair tiles on 74 pairs (ffn2: 48 chunks per tile)
+          (4096, 768, 3072, 192, 6), (4096, 768, 768, 192, 6)]
+if os.environ.get("SK_SHAPES") == "bert":
+    SHAPES = SHAPES[-2:]
 if len(sys.argv) > 1:
     SHAPES = SHAPES[int(sys.argv[1]):]
 
