@@ -67,6 +67,12 @@ class ConvLayer:
         return self.C <= 4 and self.stride == 2 and self.H % 16 == 0 and self.K % 64 == 0 and self.K <= 256
 
     @property
+    def window(self) -> bool:
+        """The window mode of the resident-filter kernel: C = 64, stride 1, a
+        spatial filter whose K x R x S x 64 filter fits (ResNet-50 l1 3x3)."""
+        return self.C == 64 and self.stride == 1 and self.R > 1 and self.R * self.R * self.K * 128 <= 80 * 1024
+
+    @property
     def Cs(self) -> int:
         """Stored channels: 4 on the stem kernel, else NHWC rows padded to the
         16-byte TMA granule."""
