@@ -948,7 +948,7 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         Y = torch.empty((nloc, L.P, L.P, L.K), device=dev, dtype=torch.bfloat16)
         st, pd = (L.stride, L.stride), (L.pad, L.pad)
         ms = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=cs, out=Y, x_halo=L.halo), iters=6, warmup=2)
-        s1 = alcop.make_schedule(tileN=cs.tileN, tileK=64, n_stage=1, n_stage_inner=1)
+        s1 = alcop.make_schedule(tileN=cs.tileN, tileK=cs.tileK, n_stage=1, n_stage_inner=1, cta_group=cs.cta_group)
         ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=s1, out=Y, x_halo=L.halo), iters=4, warmup=1)
         # the model's pick against a sweep of the conv kernel's space (each tile width at its two
         # deepest valid rings), timed like the pick
@@ -967,18 +967,25 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
                     sweep_best = min(sweep_best, mc)
                 continue
             valid = []
-            for stg in range(8, 0, -1):
-                c = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg)
-                try:
-                    alcop.validate(gview, c)
-                except alcop.AlcopError:
+            # 1x1 stride-1 layers run on the GEMM kernels: their CTA-pair tiles are in the space too
+            for cg in ((1, 2) if L.gemm else (1,)):
+                if cg == 2 and tn == 64:
                     continue
-                if alcop.load_library().alcop_smem_bytes(ctypes.byref(gview), ctypes.byref(c)) <= 232448:
-                    valid.append(c)
-                if len(valid) == 2:
-                    break
+                found = 0
+                for stg in range(8, 0, -1):
+                    c = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg, cta_group=cg)
+                    try:
+                        alcop.validate(gview, c)
+                    except alcop.AlcopError:
+                        continue
+                    if alcop.load_library().alcop_smem_bytes(ctypes.byref(gview), ctypes.byref(c)) <= 232448:
+                        valid.append(c)
+                        found += 1
+                    if found == 2:
+                        break
             for c in valid:
-                if (c.tileN, c.n_stage_smem_A, c.n_stage_inner) == (cs.tileN, cs.n_stage_smem_A, cs.n_stage_inner):
+                if (c.tileN, c.tileK, c.n_stage_smem_A, c.n_stage_inner, c.cta_group) == (
+                        cs.tileN, cs.tileK, cs.n_stage_smem_A, cs.n_stage_inner, cs.cta_group):
                     continue
                 try:
                     mc = time_graph(lambda i, c=c: alcop.conv2d(X, Wf, st, pd, sched=c, out=Y, x_halo=L.halo),

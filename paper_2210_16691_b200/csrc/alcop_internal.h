@@ -72,6 +72,20 @@ int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s)
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s);
 int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt,
                              void* y, void* stream);
+// 1x1 / stride 1 / no padding: the conv is the GEMM [N*H*W, C] x [K, C]^T
+inline bool conv_is_gemm(const alcop_conv_desc& d) {
+  return d.R == 1 && d.S == 1 && d.stride_h == 1 && d.stride_w == 1 && d.pad_h == 0 && d.pad_w == 0 && d.C % 8 == 0;
+}
+inline void conv_gemm_view(const alcop_conv_desc& d, alcop_gemm_desc* g) {
+  *g = alcop_gemm_desc{};
+  g->M = d.N * d.H * d.W;
+  g->N = d.K;
+  g->K = d.C;
+  g->batch = 1;
+  g->in_dtype = d.in_dtype;
+  g->out_dtype = d.out_dtype;
+  g->b_layout = ALCOP_B_NK;
+}
 int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt, void* y,
                   void* stream);
 

@@ -1655,6 +1655,17 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   if (window_conv_applicable(d) && validate_stem_pairs(d, s) == ALCOP_OK)
     return launch_conv2d_stem_pairs(d, s, x, wt, y, stream);
   clear_error();
+  // A 1x1, stride-1, unpadded conv is a plain GEMM: x viewed as [N*H*W, C],
+  // the filter as B[K, C] (K-major), y as [N*H*W, K] — it runs on the GEMM
+  // kernels, whose space includes the CTA-pair tiles (the im2col kernel is
+  // single-CTA only)
+  if (conv_is_gemm(d)) {
+    alcop_gemm_desc g{};
+    conv_gemm_view(d, &g);
+    int rc = validate_gemm(g, s);
+    if (rc) return rc;
+    return launch_gemm(g, s, x, wt, y, nullptr, 0, stream);
+  }
   if (d.C % 8)
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "implicit-GEMM conv needs C to be a multiple of 8 (pad NHWC channels, e.g. 3 -> 8), or C = 4 "

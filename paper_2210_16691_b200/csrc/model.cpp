@@ -325,6 +325,11 @@ extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_
   const int64_t Q = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
   if (d->C == 4 || window_conv_applicable(*d)) return choose_stem_pairs(*d, *hw, out);
+  if (conv_is_gemm(*d)) {  // runs on the GEMM kernels: their whole space, CTA pairs included
+    alcop_gemm_desc g;
+    conv_gemm_view(*d, &g);
+    return alcop_choose_schedule(&g, hw, out);
+  }
   const bool stem = d->x_halo && d->S * d->C <= 64 && d->stride_w * 16 <= 256 && d->stride_h * 8 <= 256;
   alcop_gemm_desc g{};
   g.M = d->N * P * Q;

@@ -67,6 +67,12 @@ class ConvLayer:
         return self.C <= 4 and self.stride == 2 and self.H % 16 == 0 and self.K % 64 == 0 and self.K <= 256
 
     @property
+    def gemm(self) -> bool:
+        """1x1, stride 1, no padding: the conv is a plain GEMM and runs on the GEMM
+        kernels (CTA-pair tiles included)."""
+        return self.R == 1 and self.stride == 1 and self.pad == 0
+
+    @property
     def window(self) -> bool:
         """The window mode of the resident-filter kernel: C = 64, stride 1, a
         spatial filter whose K x R x S x 64 filter fits (ResNet-50 l1 3x3)."""

@@ -127,3 +127,28 @@ def test_conv_stem_halo_exact(alcop, case, out_dt):
         if not torch.equal(got, want):
             bad = torch.nonzero(got != want)
             raise AssertionError("mismatch (n=%d) at %s" % (len(bad), bad[:4].tolist()))
+
+
+GEMM_CASES = [  # 1x1 / stride 1 / no padding: the conv runs on the GEMM kernels (CTA pairs included)
+    (2, 14, 14, 256, 1024),
+    (1, 7, 7, 512, 2048),
+    (3, 9, 11, 64, 256),
+]
+
+
+@pytest.mark.parametrize("case", GEMM_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_conv_1x1_on_gemm_kernels(alcop, case):
+    N, H, W, C, K = case
+    x = random_tensor(N * H * W * C, 61).reshape(N, H, W, C)
+    w = random_tensor(K * C, 62).reshape(K, 1, 1, C)
+    ref = coracle.conv2d(coracle.to_dtype(x.astype(np.float32), "bf16"),
+                         coracle.to_dtype(w.astype(np.float32), "bf16"), (1, 1), (0, 0), "bf16", "f32")
+    X = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    Wt = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    d = alcop.conv_desc(N, H, W, C, K, 1, 1, (1, 1), (0, 0), alcop.BF16, alcop.BF16)
+    scheds = [alcop.choose_conv_schedule(d), alcop.make_schedule(tileN=256, tileK=64, n_stage=6, cta_group=2),
+              alcop.make_schedule(tileN=128, tileK=64, n_stage=4)]
+    for s in scheds:
+        Y = alcop.conv2d(X, Wt, (1, 1), (0, 0), sched=s, out_dtype=torch.bfloat16)
+        assert torch.equal(Y.cpu(), want), s

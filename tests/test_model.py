@@ -146,6 +146,11 @@ def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
     lib = alcop.load_library()
     for L in W.CONV_LAYERS:
         s = W.conv_schedule(alcop, L, 256)
+        if L.gemm:  # 1x1 stride 1: the GEMM kernels' space (CTA pairs included)
+            g = W.conv_gemm_desc(alcop, L, 256)
+            alcop.validate(g, s)
+            assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448
+            continue
         assert s.tileK == 64 and s.cta_group == 1 and s.n_stage_smem_A == s.n_stage_smem_B, L.name
         if L.stem or L.window:  # the resident-filter kernel: tile = 128 output pixels x all K filters
             assert s.tileN == L.K and 1 <= s.n_stage_inner <= 8, s
