@@ -947,53 +947,69 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         Wf[..., :L.C] = (torch.rand((L.K, L.R, L.R, L.C), device=dev) - 0.5).to(torch.bfloat16)
         Y = torch.empty((nloc, L.P, L.P, L.K), device=dev, dtype=torch.bfloat16)
         st, pd = (L.stride, L.stride), (L.pad, L.pad)
-        ms = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=cs, out=Y, x_halo=L.halo), iters=6, warmup=2)
+        source = "model"
+        if L.gemm:
+            # 1x1 stride-1 layers are GEMMs ([N*H*W, C] x [K, C]^T) on the GEMM kernels: model-assisted
+            # tuning as for the BERT GEMMs (the model ranks, its top candidates are timed) — on these HBM-bound
+            # shapes it cannot tell a CTA pair from a single CTA (both at the HBM time)
+            cs, _ = alcop.tune(X.view(-1, L.Cs), Wf.view(L.K, L.Cs), Y.view(-1, L.K), budget=TUNE_BUDGET,
+                               b_layout=alcop.B_NK)
+            source = "alcop_tune (model rank, top %d timed)" % TUNE_BUDGET
         s1 = alcop.make_schedule(tileN=cs.tileN, tileK=cs.tileK, n_stage=1, n_stage_inner=1, cta_group=cs.cta_group)
-        ms1 = time_graph(lambda i: alcop.conv2d(X, Wf, st, pd, sched=s1, out=Y, x_halo=L.halo), iters=4, warmup=1)
-        # the model's pick against a sweep of the conv kernel's space (each tile width at its two
-        # deepest valid rings), timed like the pick
-        sweep_best = ms
+        # the pick against a sweep of the layer's space (each tile width at its two deepest valid rings;
+        # the resident-filter kernels: ring depth x accumulators; 1x1 stride-1 layers: CTA-pair tiles too)
         gview = workloads.conv_gemm_desc(alcop, L, nloc)
-        for tn in ((L.K,) if L.stem else (64, 128, 192, 256)):
-            if L.stem:  # the stem kernel's space: window ring depth x TMEM accumulators
-                for c in [alcop.make_schedule(tileN=L.K, tileK=64, n_stage=stg, n_stage_inner=inn)
-                          for stg in (8, 6, 4, 2) for inn in (1, 2, 4)]:
-                    if (c.n_stage_smem_A, c.n_stage_inner) == (cs.n_stage_smem_A, cs.n_stage_inner):
+        cands = []
+        if L.stem or L.window:
+            cands = [alcop.make_schedule(tileN=L.K, tileK=64, n_stage=stg, n_stage_inner=inn)
+                     for stg in (8, 6, 4, 3, 2) for inn in (1, 2, 4)]
+        else:
+            for tn in (64, 128, 192, 256):
+                for cg in ((1, 2) if L.gemm else (1,)):
+                    if cg == 2 and tn == 64:
                         continue
-                    try:
-                        mc = time_graph(lambda i, c=c: alcop.conv2d(X, Wf, st, pd, sched=c, out=Y), iters=4, warmup=1)
-                    except alcop.AlcopError:
-                        continue
-                    sweep_best = min(sweep_best, mc)
-                continue
-            valid = []
-            # 1x1 stride-1 layers run on the GEMM kernels: their CTA-pair tiles are in the space too
-            for cg in ((1, 2) if L.gemm else (1,)):
-                if cg == 2 and tn == 64:
-                    continue
-                found = 0
-                for stg in range(8, 0, -1):
-                    c = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg, cta_group=cg)
-                    try:
-                        alcop.validate(gview, c)
-                    except alcop.AlcopError:
-                        continue
-                    if alcop.load_library().alcop_smem_bytes(ctypes.byref(gview), ctypes.byref(c)) <= 232448:
-                        valid.append(c)
-                        found += 1
-                    if found == 2:
-                        break
-            for c in valid:
-                if (c.tileN, c.tileK, c.n_stage_smem_A, c.n_stage_inner, c.cta_group) == (
-                        cs.tileN, cs.tileK, cs.n_stage_smem_A, cs.n_stage_inner, cs.cta_group):
-                    continue
-                try:
-                    mc = time_graph(lambda i, c=c: alcop.conv2d(X, Wf, st, pd, sched=c, out=Y, x_halo=L.halo),
-                                    iters=4, warmup=1)
-                except alcop.AlcopError:
-                    continue
-                sweep_best = min(sweep_best, mc)
-        del X, Wf, Y
+                    found = 0
+                    for stg in range(8, 0, -1):
+                        c = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg, cta_group=cg)
+                        try:
+                            alcop.validate(gview, c)
+                        except alcop.AlcopError:
+                            continue
+                        if alcop.load_library().alcop_smem_bytes(ctypes.byref(gview), ctypes.byref(c)) <= 232448:
+                            cands.append(c)
+                            found += 1
+                        if found == 2:
+                            break
+        key = lambda c: (c.tileN, c.tileK, c.n_stage_smem_A, c.n_stage_inner, c.cta_group)  # noqa: E731
+        runs = [cs, s1] + [c for c in cands if key(c) != key(cs)]
+
+        # rotating copies of x and y so consecutive launches miss in L2 (footprint > 2x L2; the filter,
+        # which a network keeps hot, is shared)
+        nsets = int(min(16, max(1, -(-2 * 126 * 2 ** 20 // ((X.numel() + Y.numel()) * 2)))))
+        Xs = [X] + [X.clone() for _ in range(nsets - 1)]
+        Ys = [Y] + [torch.empty_like(Y) for _ in range(nsets - 1)]
+
+        def conv_fn(c):
+            return lambda i: alcop.conv2d(Xs[i % nsets], Wf, st, pd, sched=c, out=Ys[i % nsets], x_halo=L.halo)
+        # each schedule >= ~2 ms of launches per measurement; three round-robin rounds over the pick, its
+        # n_stage = 1 variant and the sweep, median per schedule (the GPU's clock drifts by 5-10 % over a
+        # few seconds, so schedules timed one after the other were mis-ranked)
+        iters, times = {}, {}
+        for j, c in enumerate(runs):
+            try:
+                pilot = time_graph(conv_fn(c), iters=2, warmup=1)
+            except alcop.AlcopError:
+                continue  # not launchable in this kernel's space (shared memory)
+            iters[j] = int(min(200, max(4, 2.0 / max(pilot, 1e-3)))) // nsets * nsets + nsets
+            times[j] = []
+        for _ in range(3):
+            for j in iters:
+                times[j].append(time_graph(conv_fn(runs[j]), iters=iters[j], warmup=1))
+        med = {j: statistics.median(v) for j, v in times.items()}
+        ms, ms1 = med[0], med[1]
+        sweep_j = min((j for j in med if j != 1), key=lambda j: med[j])
+        sweep_best, best_c = med[sweep_j], runs[sweep_j]
+        del X, Wf, Y, Xs, Ys
         parity["conv_%s_b%d_rank%d" % (L.name, nloc, rank)] = parity_conv(torch, alcop, L, nloc, cs, dev,
                                                                            seed=zlib.crc32(L.name.encode()))
         fl = L.flops(nloc)
@@ -1002,8 +1018,9 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         rows.append({"layer": L.name, "tflops": round(fl / (ms * 1e-3) / 1e12, 1),
                      "frac_of_attainable": round(fl / (ms * 1e-3) / 1e12 / attainable(fl, L.compulsory_bytes(nloc)),
                                                  3),
-                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN, "n_stage": cs.n_stage_smem_A,
-                     "model_pick_over_best_swept": round(ms / sweep_best, 3)})
+                     "speedup_vs_n_stage1": round(ms1 / ms, 2), "tileN": cs.tileN, "n_stage": cs.n_stage_smem_A, "cta_group": cs.cta_group,
+                     "model_pick_over_best_swept": round(ms / sweep_best, 3), "schedule_source": source,
+                     "schedule": str(cs), "best_swept": str(best_c)})
         torch.cuda.empty_cache()
     tt = ranks.max(tot_ms)
     picks = [r["model_pick_over_best_swept"] for r in rows]
@@ -1012,7 +1029,8 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
                                            "layers": len(picks)},
             "sharding": "batch", "layers": rows,
             "note": "sum over all 53 conv layers (conv1: the stem kernel on the NHWC4 input, C 3 -> 4 "
-                    "zero-padded, FLOPs counted at C=3); per-layer CUDA-graph timing, the model's conv schedules; "
+                    "zero-padded, FLOPs counted at C=3); per-layer CUDA-graph timing over rotating x/y copies "
+                    "(> 2x L2), median of 3 round-robin rounds over the pick, its n_stage=1 variant and the sweep; "
                     "compulsory bytes count only the input pixels a strided 1x1 conv reads"}
 
 
