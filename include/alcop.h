@@ -281,7 +281,20 @@ int alcop_gemm_host_async(const alcop_gemm_desc* w, const alcop_schedule* s, con
 int64_t alcop_stream_k_workspace_bytes(const alcop_gemm_desc* w, const alcop_schedule* s);
 int alcop_set_stream_k_workspace(void* workspace, int64_t bytes);
 
-/* Implicit-GEMM conv2d (new; the reference excludes it). */
+/* Implicit-GEMM conv2d (new; the reference excludes it).
+ * Kernel by shape and schedule (all pipelined, all on sm_100a; no fallback):
+ *  - C == 4, stride_w == 2 (e.g. ResNet-50 conv1 with the 3 channels padded to
+ *    4): the resident-filter kernel in pixel-pair mode; W % 16 == 0,
+ *    K % 16 == 0, K <= 256, K * out bytes % 128 == 0; schedule tileM 128,
+ *    tileN == K, tileK 64, FUSED, cta_group 1, n_stage = window ring depth,
+ *    n_stage_inner = TMEM accumulators (1..8, n_stage_inner * K <= 512);
+ *  - C == 64, stride 1, spatial filter whose K x R x S x 64 filter fits
+ *    (<= 80 KB), with such a resident-filter schedule: window mode of the same
+ *    kernel (the tile's input window loaded once, taps = shifted descriptors);
+ *  - 1x1, stride 1, no padding: the GEMM kernels ([N*H*W, C] x [K, C]^T),
+ *    any GEMM schedule incl. CTA pairs;
+ *  - otherwise C % 8 == 0: the implicit-GEMM kernel with TMA im2col loads
+ *    (tileK 64, equal A/B stages, cta_group 1). */
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
                  void* stream);
 
@@ -324,8 +337,12 @@ void alcop_hw_default_a100_reference(alcop_hw* hw); /* perf_model.hpp:14-30 defa
 int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, const alcop_hw* hw,
                   alcop_breakdown* out);
 int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_schedule* out);
-/* The same over the implicit-GEMM conv kernel's space (tileK 64, equal
- * stages, cta_group 1), ranked on the conv's GEMM view. */
+/* The same for a conv, over the space of the kernel alcop_conv2d runs it on
+ * (see there): the resident-filter kernel's ring depth x accumulators (its
+ * own per-tile model: MMA, window fill, the SM's share of the HBM stream,
+ * pipeline_latency over the windows), the GEMM space for 1x1 stride-1 convs,
+ * else the implicit-GEMM kernel's space (tileK 64, equal stages, cta_group 1)
+ * ranked on the conv's GEMM view. */
 int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_hw* hw, alcop_schedule* out);
 
 /* One measured candidate of the model-assisted tuner. */
