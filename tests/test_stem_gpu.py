@@ -24,6 +24,7 @@ CASES = [  # N, H, W, C, K, R, S, (stride_h, stride_w), (pad_h, pad_w)
     (1, 9, 64, 4, 256, 3, 3, (2, 2), (1, 1)),     # K = 256
     (2, 12, 16, 2, 64, 1, 1, (2, 2), (0, 0)),     # 1x1 / 2 (one tap, zero partner)
     (1, 20, 32, 3, 64, 6, 3, (3, 2), (2, 1)),     # stride_h 3, R != S
+    (1, 5, 32, 3, 64, 7, 7, (2, 2), (3, 3)),      # image shorter than the filter (window box > H)
 ]
 
 
@@ -133,6 +134,7 @@ WINDOW_CASES = [  # N, H, W, C, K, R, S, (stride), (pad)
     (2, 18, 18, 64, 64, 3, 3, (1, 1), (0, 0)),    # no padding
     (1, 9, 60, 64, 128, 1, 3, (1, 1), (0, 1)),    # R != S, K = 128
     (1, 12, 20, 64, 64, 2, 4, (1, 1), (1, 2)),    # even filter, uneven padding
+    (1, 8, 8, 64, 64, 3, 3, (1, 1), (1, 1)),      # window box (10 rows) taller than the image
 ]
 
 
