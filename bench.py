@@ -963,7 +963,10 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         if L.stem or L.window:
             cands = [alcop.make_schedule(tileN=L.K, tileK=64, n_stage=stg, n_stage_inner=inn)
                      for stg in (8, 6, 4, 3, 2) for inn in (1, 2, 4)]
-        else:
+        if L.stream:  # window + streamed filter: taps per filter chunk x window ring x filter ring
+            cands = [alcop.make_schedule(tileN=L.K, tileK=tk, n_stage=sa, n_stage_B=sb, n_stage_inner=2)
+                     for tk in (64, 64 * L.R) for sa in (1, 2, 3) for sb in (2, 3, 4, 6)]
+        if not (L.stem or L.window):  # + the implicit-GEMM (im2col) kernel's space
             for tn in (64, 128, 192, 256):
                 for cg in ((1, 2) if L.gemm else (1,)):
                     if cg == 2 and tn == 64:
@@ -980,7 +983,8 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
                             found += 1
                         if found == 2:
                             break
-        key = lambda c: (c.tileN, c.tileK, c.n_stage_smem_A, c.n_stage_inner, c.cta_group)  # noqa: E731
+        key = lambda c: (c.tileN, c.tileK, c.n_stage_smem_A, c.n_stage_smem_B, c.n_stage_inner,  # noqa: E731
+                         c.cta_group)
         runs = [cs, s1] + [c for c in cands if key(c) != key(cs)]
 
         # rotating copies of x and y so consecutive launches miss in L2 (footprint > 2x L2; the filter,

@@ -67,6 +67,7 @@ struct StemGeometry {
 };
 bool stem_pairs_applicable(const alcop_conv_desc& d);
 bool window_conv_applicable(const alcop_conv_desc& d);
+bool window_stream_applicable(const alcop_conv_desc& d);
 StemGeometry stem_pairs_geometry(const alcop_conv_desc& d);
 int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s);
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s);

@@ -1652,7 +1652,7 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   // C = 64 stride-1 spatial filters with a resident-filter schedule (tileN = K,
   // FUSED): the window mode of the same kernel (the input window loaded once
   // per tile); other schedules run the im2col kernel below
-  if (window_conv_applicable(d) && validate_stem_pairs(d, s) == ALCOP_OK)
+  if ((window_conv_applicable(d) || window_stream_applicable(d)) && validate_stem_pairs(d, s) == ALCOP_OK)
     return launch_conv2d_stem_pairs(d, s, x, wt, y, stream);
   clear_error();
   // A 1x1, stride-1, unpadded conv is a plain GEMM: x viewed as [N*H*W, C],

@@ -265,17 +265,33 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
 // — the paper's stage formula with the window as the pipelined chunk.
 static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, const alcop_schedule& s,
                               const alcop_hw& hw) {
-  const bool window = d.C == 64;
+  const bool window = g.TR > 1 || g.WP > 0;
+  const bool streamed = window && g.wbytes == 0;  // window with the filter streamed per channel block
   const double tiles = static_cast<double>(d.N * (window ? (g.P + g.TR - 1) / g.TR : g.P) * g.QB);
   const double per_sm = std::ceil(tiles / hw.numSM);
   const double ob = d.out_dtype == ALCOP_F32 ? 4.0 : 2.0;
-  const double ksteps = window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(d.R * (g.T2 / 2));
-  const double mma = ksteps * (128.0 * d.K * 16 * 2) / hw.throughputSM;
-  const double fill = static_cast<double>(g.box_bytes) / hw.bwSmem;
+  const double mma_k = (128.0 * d.K * 16 * 2) / hw.throughputSM;  // one k-step of 16
   const double out_bytes = static_cast<double>(d.N * g.P * g.Q) * d.K * ob;
   const double in_bytes = static_cast<double>(d.N) * d.H * d.W * d.C * 2.0;
   const double hbm_tile = (out_bytes + in_bytes) / tiles / (hw.bwDRAMWrite / hw.numSM);
   const double epi = hw.latDRAMWrite + (d.K * ob / 128.0) * hw.tTile;
+  if (streamed) {
+    // per filter chunk: TB taps x 4 k-steps; the chunk's fill = TB x K x 128 B
+    // plus its share of the channel block's window; the B ring pipelines the
+    // chunks (the A ring one window per channel block)
+    const double tb = static_cast<double>(s.tileK / 64);
+    const double chunks = static_cast<double>(d.C / 64) * (d.R * d.S) / tb;
+    const double use = std::max({tb * 4 * mma_k, (tb * d.K * 128 + g.box_bytes * tb / (d.R * d.S)) / hw.bwSmem,
+                                 hbm_tile / chunks, hw.tIssue});
+    double main = model::pipeline_latency(hw.latLLCRead, use, static_cast<int64_t>(per_sm * chunks),
+                                          s.n_stage_smem_B, 1);
+    if (s.n_stage_smem_A == 1) main += per_sm * (d.C / 64) * 0.5 * hw.latLLCRead;  // window refill bubble
+    if (s.n_stage_inner == 1) main += per_sm * epi;
+    return (hw.tLaunch + main + epi) / (hw.clockGHz * 1e9);
+  }
+  const double ksteps = window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(d.R * (g.T2 / 2));
+  const double mma = ksteps * mma_k;
+  const double fill = static_cast<double>(g.box_bytes) / hw.bwSmem;
   double use = std::max({mma, fill, hbm_tile, hw.tIssue});
   if (s.n_stage_inner == 1) use = std::max(use, mma + epi);
   const double main = model::pipeline_latency(hw.latLLCRead, use, static_cast<int64_t>(per_sm), s.n_stage_smem_A, 1);
@@ -283,29 +299,35 @@ static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, c
 }
 
 static int choose_stem_pairs(const alcop_conv_desc& d, const alcop_hw& hw, alcop_schedule* out) {
-  if (d.C != 64 && !stem_pairs_applicable(d))
+  if (d.C == 4 && !stem_pairs_applicable(d))
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256");
   const StemGeometry g = stem_pairs_geometry(d);
   if (g.P < 1 || g.Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
+  const bool streamed = d.C != 4 && window_stream_applicable(d);
   double best = 1e300;
   bool found = false;
-  for (int st = 8; st >= 1; --st)
-    for (int inner = 4; inner >= 1; --inner) {
-      alcop_schedule s;
-      alcop_schedule_default(&s);
-      s.tileN = static_cast<int32_t>(d.K);
-      s.tileK = 64;
-      s.n_stage_smem_A = s.n_stage_smem_B = st;
-      s.n_stage_inner = inner;
-      if (validate_stem_pairs(d, s) != ALCOP_OK) continue;
-      const double t = stem_pairs_time(d, g, s, hw);
-      if (t < best * (1.0 - 1e-9)) {  // ties keep the deeper rings
-        best = t;
-        *out = s;
-        found = true;
-      }
-    }
+  for (int tk : {64, static_cast<int>(64 * d.S)}) {
+    if (tk != 64 && !streamed) continue;
+    for (int sa = streamed ? 4 : 8; sa >= 1; --sa)
+      for (int sb = streamed ? 8 : sa; sb >= (streamed ? 1 : sa); --sb)
+        for (int inner = 4; inner >= 1; --inner) {
+          alcop_schedule s;
+          alcop_schedule_default(&s);
+          s.tileN = static_cast<int32_t>(d.K);
+          s.tileK = tk;
+          s.n_stage_smem_A = sa;
+          s.n_stage_smem_B = sb;
+          s.n_stage_inner = inner;
+          if (validate_stem_pairs(d, s) != ALCOP_OK) continue;
+          const double t = stem_pairs_time(d, g, s, hw);
+          if (t < best * (1.0 - 1e-9)) {  // ties keep the deeper rings
+            best = t;
+            *out = s;
+            found = true;
+          }
+        }
+  }
   clear_error();
   if (!found) return set_error(ALCOP_ERR_CONFIG, "Unschedulable", "no stem schedule for workload");
   return ALCOP_OK;
@@ -324,7 +346,7 @@ extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_
   const int64_t P = (d->H + 2 * d->pad_h - d->R) / d->stride_h + 1;
   const int64_t Q = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
-  if (d->C == 4 || window_conv_applicable(*d)) return choose_stem_pairs(*d, *hw, out);
+  if (d->C == 4 || window_conv_applicable(*d) || window_stream_applicable(*d)) return choose_stem_pairs(*d, *hw, out);
   if (conv_is_gemm(*d)) {  // runs on the GEMM kernels: their whole space, CTA pairs included
     alcop_gemm_desc g;
     conv_gemm_view(*d, &g);

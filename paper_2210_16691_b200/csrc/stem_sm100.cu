@@ -58,7 +58,10 @@ constexpr uint32_t kStemStaging = 32 * 128;  // one epilogue staging buffer: 32 
 
 // kMode: 0 = pixel pairs (C = 4, stride_w 2: the ResNet-50 stem); 1 = window
 // (C = 64, stride 1: a TR-output-row tile reads its (TR+R-1)-row input window
-// once; tap (r, s) is the window shifted by r rows and s pixels)
+// once; tap (r, s) is the window shifted by r rows and s pixels); 2 = window
+// with a streamed filter (C = 64 * CB, stride 1: per 64-channel block the
+// window is one chunk of the A ring and the filter comes in chunks of TB taps
+// through the B ring — the two pipelined buffers with their own stage counts)
 struct StemKParams {
   int32_t P, Q, QB, num_tiles;  // tile rows (output rows / row blocks) per image, output columns, column blocks
   int32_t Pout;                 // output rows per image
@@ -72,8 +75,13 @@ struct StemKParams {
   int32_t shift, blk_off;       // window: first MMA row `shift` pairs in; x coordinate of column block 0
   int32_t lwp;                  // window mode: log2 of the window row pitch WP (pixels); TR = 128 / WP
   int32_t stage_bufs;           // epilogue staging buffers per warp (1 or 2)
+  int32_t stage_warps;          // epilogue warps with staging (8 with two epilogue groups, else 4)
   const uint16_t* w;            // KRSC
   int32_t dual;                 // two MMA-issuing warps (1: even tiles, 6: odd tiles); even rings only
+  // kMode 2 (window + streamed filter): channel blocks of 64, filter chunks of TB taps per block, the
+  // filter ring (n_stage_smem_B slots of TB x BN x 128 B)
+  int32_t CB, TB, nbc, sB;
+  uint32_t b_slot_bytes;
   int32_t skip;                 // measurement only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
 };
 
@@ -177,26 +185,30 @@ __device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_
 template <typename OutT, int kMode, int kR, int kKS>
 __global__ void __launch_bounds__(kStemThreads, 1)
     alcop_stem_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
-                           const StemKParams p) {
+                           const __grid_constant__ CUtensorMap tmW, const StemKParams p) {
   using namespace ptx;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t ring = smem_u32(smem);
-  const uint32_t wsm = ring + p.stages * p.slot_bytes;
+  const uint32_t ringB = ring + p.stages * p.slot_bytes;  // kMode 2: the filter ring
+  const uint32_t wsm = ringB + p.sB * p.b_slot_bytes;
   const uint32_t staging = wsm + p.wbytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.wbytes +
-                                               8 * p.stage_bufs * kStemStaging);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.slot_bytes + p.sB * p.b_slot_bytes + p.wbytes +
+                                               p.stage_warps * p.stage_bufs * kStemStaging);
   uint64_t* full = bars;
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + p.nacc;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + p.nacc);
+  uint64_t* bfull = tempty + p.nacc;
+  uint64_t* bempty = bfull + p.sB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + p.sB);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmY);
+    if (kMode == 2) prefetch_tmap(&tmW);
   }
   if (warp == 1) {
     if (lane == 0) {
@@ -207,6 +219,10 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       for (int i = 0; i < p.nacc; ++i) {
         mbar_init(smem_u32(&tfull[i]), 1);
         mbar_init(smem_u32(&tempty[i]), 4);
+      }
+      for (int i = 0; i < p.sB; ++i) {
+        mbar_init(smem_u32(&bfull[i]), 1);
+        mbar_init(smem_u32(&bempty[i]), 1);
       }
       fence_barrier_init();
     }
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
       st_shared_v4(wsm + static_cast<uint32_t>(idx) * 16u, v[0], v[1], v[2], v[3]);
     }
-  } else {
+  } else if constexpr (kMode == 1) {
     // B operand per tap t = (r, s): BN filter rows x 64 channels (128 B),
     // 128B-swizzled K-major ([t][n][128 B], 16-byte chunk c of row n at c ^ (n & 7))
     const int rows = p.R * p.S * p.BN;
@@ -265,24 +281,41 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     // ======================= producer (TMA) =======================
     // the whole warp walks the loop (coordinates stay on the uniform
     // datapath), one elected lane issues
-    int slot = 0;
-    uint32_t phase = 0;
+    int slot = 0, bslot = 0;
+    uint32_t phase = 0, bphase = 0;
     StemCursor cur;
     cur.start(p);
     for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
-      mbar_wait(smem_u32(&empty[slot]), ((phase >> slot) & 1u) ^ 1u);  // producer_acquire
-      phase ^= 1u << slot;
-      if (elect_one()) {
-        if (p.skip & 2) {
-          mbar_arrive(smem_u32(&full[slot]));
-        } else {
-          mbar_arrive_expect_tx(smem_u32(&full[slot]), p.box_bytes);      // producer_commit
-          tma_load_4d(ring + slot * p.slot_bytes, &tmX, smem_u32(&full[slot]), 0, cur.qb * 16 + p.blk_off,
-                      cur.p * p.row_step - p.ph, cur.n);
+      for (int cb = 0; cb < (kMode == 2 ? p.CB : 1); ++cb) {
+        mbar_wait(smem_u32(&empty[slot]), ((phase >> slot) & 1u) ^ 1u);  // producer_acquire (window)
+        phase ^= 1u << slot;
+        if (elect_one()) {
+          if (p.skip & 2) {
+            mbar_arrive(smem_u32(&full[slot]));
+          } else {
+            mbar_arrive_expect_tx(smem_u32(&full[slot]), p.box_bytes);      // producer_commit
+            tma_load_4d(ring + slot * p.slot_bytes, &tmX, smem_u32(&full[slot]), cb * 64, cur.qb * 16 + p.blk_off,
+                        cur.p * p.row_step - p.ph, cur.n);
+          }
+        }
+        __syncwarp();
+        slot = slot + 1 == p.stages ? 0 : slot + 1;
+        if constexpr (kMode == 2) {
+          // this channel block's filter, TB taps per chunk: tap t = filter columns t*C + cb*64 .. +63
+          for (int j = 0; j < p.nbc; ++j) {
+            mbar_wait(smem_u32(&bempty[bslot]), ((bphase >> bslot) & 1u) ^ 1u);
+            bphase ^= 1u << bslot;
+            if (elect_one()) {
+              mbar_arrive_expect_tx(smem_u32(&bfull[bslot]), p.TB * p.BN * 128u);
+              for (int t = 0; t < p.TB; ++t)
+                tma_load_3d(ringB + bslot * p.b_slot_bytes + t * p.BN * 128u, &tmW, smem_u32(&bfull[bslot]),
+                            (j * p.TB + t) * p.CB * 64 + cb * 64, 0, 0);
+            }
+            __syncwarp();
+            bslot = bslot + 1 == p.sB ? 0 : bslot + 1;
+          }
         }
       }
-      __syncwarp();
-      slot = slot + 1 == p.stages ? 0 : slot + 1;
     }
   } else if (warp == 1 || warp == 6) {
     // ======================= MMA issuers =======================
@@ -295,7 +328,58 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     // tcgen05.commit tracks only the MMAs it issued.
     const int first = warp == 6 ? 1 : 0;
     const int step = p.dual ? 2 : 1;
-    if (!(warp == 6 && !p.dual)) {
+    if constexpr (kMode == 2) {
+      // one issuing warp (the rings carry several chunks per tile in order)
+      if (warp == 1) {
+        int slot = 0, bslot = 0, acc = 0;
+        uint32_t phase = 0, bphase = 0, acc_phase = 0;
+        const uint64_t a_row16 = (128u << p.lwp) >> 4;
+        const uint64_t b_tap16 = (static_cast<uint32_t>(p.BN) * 128u) >> 4;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+          mbar_wait(smem_u32(&tempty[acc]), ((acc_phase >> acc) & 1u) ^ 1u);
+          acc_phase ^= 1u << acc;
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
+          for (int cb = 0; cb < p.CB; ++cb) {
+            mbar_wait(smem_u32(&full[slot]), (phase >> slot) & 1u);     // consumer_wait (window)
+            phase ^= 1u << slot;
+            const uint64_t ad = make_smem_desc(ring + slot * p.slot_bytes, 16u, 1024u, kLayoutSW128);
+            int r = 0, sx = 0;  // tap of the chunk's first filter column
+            for (int j = 0; j < p.nbc; ++j) {
+              mbar_wait(smem_u32(&bfull[bslot]), (bphase >> bslot) & 1u);  // consumer_wait (filter chunk)
+              bphase ^= 1u << bslot;
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t bd = make_smem_desc(ringB + bslot * p.b_slot_bytes, 16u, 1024u, kLayoutSW128);
+                int rr = r, ss = sx;
+                for (int t = 0; t < p.TB; ++t) {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    umma_f16_ss(d_tmem, ad + rr * a_row16 + ss * 8 + 2 * u, bd + t * b_tap16 + 2 * u, p.idesc,
+                                (cb > 0 || j > 0 || t > 0 || u > 0) ? 1u : 0u);
+                  if (++ss == p.S) {
+                    ss = 0;
+                    ++rr;
+                  }
+                }
+                umma_commit(smem_u32(&bempty[bslot]));                     // consumer_release (filter chunk)
+                if (j == p.nbc - 1) umma_commit(smem_u32(&empty[slot]));   // consumer_release (window)
+                if (j == p.nbc - 1 && cb == p.CB - 1) umma_commit(smem_u32(&tfull[acc]));
+              }
+              __syncwarp();
+              sx += p.TB;
+              while (sx >= p.S) {
+                sx -= p.S;
+                ++r;
+              }
+              bslot = bslot + 1 == p.sB ? 0 : bslot + 1;
+            }
+            slot = slot + 1 == p.stages ? 0 : slot + 1;
+          }
+          if (++acc == p.nacc) acc = 0;
+        }
+      }
+    } else if (!(warp == 6 && !p.dual)) {
       int slot = first % p.stages;
       int acc = first % p.nacc;
       uint32_t phase = 0, acc_phase = 0;  // bit k: current parity of ring slot / accumulator k
@@ -411,12 +495,13 @@ __global__ void __launch_bounds__(kStemThreads, 1)
 }
 
 template <typename OutT>
-int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKParams& kp, int mode, int grid,
-                      int smem, cudaStream_t st) {
-  auto kern = mode == 1 ? (kp.R == 3 && kp.S == 3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3>
-                                                  : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
-                        : (kp.R == 7 && kp.T2 == 4 ? alcop_stem_conv_kernel<OutT, 0, 7, 2>
-                                                   : alcop_stem_conv_kernel<OutT, 0, 0, 0>);
+int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const CUtensorMap& tw, const StemKParams& kp,
+                      int mode, int grid, int smem, cudaStream_t st) {
+  auto kern = mode == 2   ? alcop_stem_conv_kernel<OutT, 2, 0, 0>
+              : mode == 1 ? (kp.R == 3 && kp.S == 3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3>
+                                                    : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
+                          : (kp.R == 7 && kp.T2 == 4 ? alcop_stem_conv_kernel<OutT, 0, 7, 2>
+                                                     : alcop_stem_conv_kernel<OutT, 0, 0, 0>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -429,7 +514,7 @@ int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const StemKP
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, tx, ty, kp);
+  e = cudaLaunchKernelEx(&cfg, kern, tx, ty, tw, kp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   return ALCOP_OK;
@@ -457,26 +542,47 @@ static int64_t window_pitch(const alcop_conv_desc& d) {
   return wp;
 }
 
-bool window_conv_applicable(const alcop_conv_desc& d) {
-  if (!(d.C == 64 && d.stride_h == 1 && d.stride_w == 1 && !d.x_halo && d.K % 16 == 0 && d.K >= 16 &&
-        d.K <= 256 && (d.K * out_bytes(d)) % 128 == 0 && d.R <= 8 && d.S <= 8 && d.pad_h <= 8 && d.pad_w <= 8))
+static bool window_common(const alcop_conv_desc& d) {
+  if (!(d.stride_h == 1 && d.stride_w == 1 && !d.x_halo && d.K % 16 == 0 && d.K >= 16 && d.K <= 256 &&
+        (d.K * out_bytes(d)) % 128 == 0 && d.R <= 8 && d.S <= 8 && d.pad_h <= 8 && d.pad_w <= 8 &&
+        (d.R > 1 || d.S > 1)))
     return false;
+  // 1x1 convs stay on the GEMM kernels (both HBM-bound, tools/window1x1_probe.py)
   const int64_t wp = window_pitch(d);
   if (wp > 128) return false;
   const int64_t tr = 128 / wp;
   const int64_t P = (d.H + 2 * d.pad_h - d.R) + 1;
-  // worth it only when the tile rows are mostly real output (not for a 7x7 map
-  // in 8-row tiles); the resident filter leaves room for a 2-slot ring
-  // 1x1 convs stay on the implicit-GEMM kernel: both run them at the HBM
-  // bound (tools/window1x1_probe.py: within +-8 % either way)
-  return (d.R > 1 || d.S > 1) && P >= tr && (tr + d.R - 1) * wp <= 256 && d.R * d.S * d.K * 128 <= 80 * 1024;
+  // worth it only when the tile rows are mostly real output (not a 7x7 map in 8-row tiles)
+  return P >= tr && (tr + d.R - 1) * wp <= 256;
+}
+
+bool window_conv_applicable(const alcop_conv_desc& d) {
+  // the resident filter leaves room for a 2-slot window ring
+  return d.C == 64 && window_common(d) && d.R * d.S * d.K * 128 <= 80 * 1024;
+}
+
+bool window_stream_applicable(const alcop_conv_desc& d) {
+  // the window saves the im2col kernel's A re-reads: half of its L2 -> SM
+  // bytes at K = 128, a third at K = 256, where the im2col kernel's deeper
+  // 48 KB stages win (ResNet-50 l3 3x3: 1297 vs 1130 TFLOP/s; l2 3x3, K = 128:
+  // 888 -> 1098 TFLOP/s on the window kernel)
+  return d.C % 64 == 0 && d.K <= 128 && !window_conv_applicable(d) && window_common(d);
+}
+
+// 0 = pixel pairs, 1 = window (resident filter), 2 = window (streamed filter), -1 = none
+static int stem_mode(const alcop_conv_desc& d) {
+  if (d.C == 4) return 0;
+  if (window_conv_applicable(d)) return 1;
+  if (window_stream_applicable(d)) return 2;
+  return -1;
 }
 
 StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   StemGeometry g{};
   g.P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
   g.Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
-  if (d.C == 64) {  // window mode
+  const int mode = stem_mode(d);
+  if (mode >= 1) {  // window modes
     const int64_t wp = window_pitch(d);
     const int64_t tr = 128 / wp;
     g.QB = 1;
@@ -487,8 +593,8 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
     // + S-1 pixels of slack: the taps of the tile's last (overhanging, never
     // stored) rows read past the box
     g.slot_bytes = static_cast<uint32_t>((g.box_bytes + (d.S - 1) * 128 + 1023) / 1024 * 1024);
-    g.wbytes = static_cast<uint32_t>((d.R * d.S * d.K * 128 + 1023) / 1024 * 1024);
-    g.kdim = d.R * d.S * 64;
+    g.wbytes = mode == 1 ? static_cast<uint32_t>((d.R * d.S * d.K * 128 + 1023) / 1024 * 1024) : 0u;
+    g.kdim = d.R * d.S * d.C;
     return g;
   }
   g.QB = (g.Q + 127) / 128;
@@ -509,10 +615,22 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   return g;
 }
 
+// streamed filter: taps per filter chunk (tileK = 64 x taps), ring of n_stage_smem_B chunks
+static int64_t stream_b_slot_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
+  return stem_mode(d) == 2 ? (s.tileK / 64) * d.K * 128 : 0;
+}
+static bool stem_dual(const alcop_conv_desc& d, const alcop_schedule& s) {
+  return stem_mode(d) != 2 && s.n_stage_smem_A % 2 == 0 && s.n_stage_inner % 2 == 0;
+}
+
 static int64_t stem_smem_bytes_bufs(const alcop_conv_desc& d, const alcop_schedule& s, int bufs) {
   const StemGeometry g = stem_pairs_geometry(d);
-  const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner) + 16;
-  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + g.wbytes + 8 * bufs * kStemStaging + bars;
+  const bool streamed = stem_mode(d) == 2;
+  const int64_t sB = streamed ? s.n_stage_smem_B : 0;
+  const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner + 2 * sB) + 16;
+  const int warps = stem_dual(d, s) ? 8 : 4;
+  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + sB * stream_b_slot_bytes(d, s) + g.wbytes +
+         warps * bufs * kStemStaging + bars;
 }
 
 // two staging buffers per epilogue warp when they fit, else one
@@ -525,32 +643,40 @@ int64_t stem_pairs_smem_bytes(const alcop_conv_desc& d, const alcop_schedule& s)
 }
 
 int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
-  if (s.tileM != kTileM || s.tileK != 64 || s.tileN != d.K)
+  const int mode = stem_mode(d);
+  if (mode < 0)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "not a shape of the resident-filter / window conv kernel");
+  const bool tk_ok = s.tileK == 64 || (mode == 2 && s.tileK == 64 * d.S);
+  if (s.tileM != kTileM || !tk_ok || s.tileN != d.K)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the resident-filter conv kernel's tile is 128 output pixels x all K filters (tileM 128, "
-                     "tileN = K, tileK 64)");
+                     "the window conv kernel's tile is 128 output pixels x all K filters (tileM 128, tileN = K, "
+                     "tileK 64; streamed filter: tileK 64 or 64 x S = taps per filter chunk)");
   if (s.cta_group != 1 || s.stream_k != 0 || s.mode != ALCOP_MODE_FUSED)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the resident-filter conv kernel runs one CTA per tile, one window chunk per tile (FUSED, "
-                     "cta_group 1)");
-  if (s.n_stage_smem_A != s.n_stage_smem_B || s.n_stage_smem_A < 1 || s.n_stage_smem_A > kMaxStages)
+                     "the window conv kernel runs one CTA per tile (FUSED, cta_group 1)");
+  if (mode == 2) {
+    if (s.n_stage_smem_A < 1 || s.n_stage_smem_A > 4 || s.n_stage_smem_B < 1 || s.n_stage_smem_B > kMaxStages)
+      return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "streamed filter: window stages 1..4, filter stages 1..16");
+  } else if (s.n_stage_smem_A != s.n_stage_smem_B || s.n_stage_smem_A < 1 || s.n_stage_smem_A > kMaxStages) {
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the window ring: equal A/B stages in 1..16");
-  if (s.n_stage_inner < 1 || s.n_stage_inner > 8 || s.n_stage_inner * d.K > kTmemCols)
+  }
+  const int max_inner = mode == 2 ? 2 : 8;
+  if (s.n_stage_inner < 1 || s.n_stage_inner > max_inner || s.n_stage_inner * d.K > kTmemCols)
     return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner accumulators of K columns exceed TMEM");
   if (stem_pairs_smem_bytes(d, s) > kMaxSmemBytes)
-    return set_error(ALCOP_ERR_CONFIG, "SmemCapacity", "window ring + resident filter exceed shared memory");
+    return set_error(ALCOP_ERR_CONFIG, "SmemCapacity", "window / filter rings exceed shared memory");
   return ALCOP_OK;
 }
 
 int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, const void* x, const void* wt,
                              void* y, void* stream) {
-  const int mode = d.C == 64 ? 1 : 0;
+  const int mode = stem_mode(d);
   if (mode == 0 && !stem_pairs_applicable(d))
     return set_error(ALCOP_ERR_CONFIG, "Unsupported",
                      "C = 4 convs run on the stem kernel: stride_w 2, W % 16 == 0, K % 16 == 0, K <= 256, "
                      "K * out bytes % 128 == 0, no halo layout");
-  if (mode == 1 && !window_conv_applicable(d))
-    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "not a window-conv shape (C 64, stride 1, small filter)");
+  if (mode < 0)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "not a window-conv shape (C % 64, stride 1, small filter)");
   int rc = validate_stem_pairs(d, s);
   if (rc) return rc;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wt) | reinterpret_cast<uintptr_t>(y)) & 15)
@@ -576,15 +702,28 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
     const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), static_cast<cuuint32_t>(d.R), 1};
     rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_NONE, "x (stem pairs)");
   } else {
-    // x as {64 channels, W, H, N}; box = WP pixels (from -pad_w) x TR+R-1
-    // rows: the tile's input window, zero filled outside the image
-    const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W), static_cast<cuuint64_t>(d.H),
-                                 static_cast<cuuint64_t>(d.N)};
-    const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 128), static_cast<cuuint64_t>(d.H * d.W * 128)};
+    // x as {C channels, W, H, N}; box = 64 channels x WP pixels (from
+    // -pad_w) x TR+R-1 rows: the tile's input window of one channel block,
+    // zero filled outside the image
+    const cuuint64_t xdims[4] = {static_cast<cuuint64_t>(d.C), static_cast<cuuint64_t>(d.W),
+                                 static_cast<cuuint64_t>(d.H), static_cast<cuuint64_t>(d.N)};
+    const cuuint64_t xstr[3] = {static_cast<cuuint64_t>(d.C * 2), static_cast<cuuint64_t>(d.W * d.C * 2),
+                                static_cast<cuuint64_t>(d.H * d.W * d.C * 2)};
     const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.WP), static_cast<cuuint32_t>(g.TR + d.R - 1), 1};
     rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "x (window)");
   }
   if (rc) return rc;
+  // streamed filter: w viewed as [K rows, R*S*C columns]; box = 64 channels of
+  // one tap x all K filters (128B-swizzled, K-major B)
+  CUtensorMap tw = tx;
+  if (mode == 2) {
+    const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(d.R * d.S * d.C), static_cast<cuuint64_t>(d.K), 1};
+    const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(d.R * d.S * d.C * 2),
+                                static_cast<cuuint64_t>(d.K * d.R * d.S * d.C * 2)};
+    const cuuint32_t wbox[3] = {64, static_cast<cuuint32_t>(d.K), 1};
+    rc = encode_tiled_map(&tw, dt, wt, 3, wdims, wstr, wbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "w (window)");
+    if (rc) return rc;
+  }
   // y as {K, Q, P, N}: each epilogue warp stores its 32 tile rows x 128 B
   // (window mode, WP = 16: two output rows of 16 columns)
   const int64_t wcols = mode == 0 ? 32 : std::min<int64_t>(32, g.WP);
@@ -632,7 +771,15 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
     return e ? std::atoi(e) : 0;
   }();
   kp.skip = skip_env;
-  kp.dual = (kp.stages % 2 == 0 && kp.nacc % 2 == 0) ? 1 : 0;
+  kp.dual = stem_dual(d, s) ? 1 : 0;
+  kp.stage_warps = kp.dual ? 8 : 4;
+  if (mode == 2) {
+    kp.CB = static_cast<int32_t>(d.C / 64);
+    kp.TB = static_cast<int32_t>(s.tileK / 64);
+    kp.nbc = static_cast<int32_t>(d.R * d.S / kp.TB);
+    kp.sB = s.n_stage_smem_B;
+    kp.b_slot_bytes = static_cast<uint32_t>(stream_b_slot_bytes(d, s));
+  }
   const int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   int grid = s.num_ctas > 0 ? s.num_ctas : sms;
@@ -651,9 +798,9 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   const int smem = static_cast<int>(stem_pairs_smem_bytes(d, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (d.out_dtype) {
-    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, kp, mode, grid, smem, st);
-    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, kp, mode, grid, smem, st);
-    default: return launch_stem_typed<__half>(tx, ty, kp, mode, grid, smem, st);
+    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, tw, kp, mode, grid, smem, st);
+    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, tw, kp, mode, grid, smem, st);
+    default: return launch_stem_typed<__half>(tx, ty, tw, kp, mode, grid, smem, st);
   }
 }
 

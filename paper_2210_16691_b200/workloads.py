@@ -79,6 +79,17 @@ class ConvLayer:
         return self.C == 64 and self.stride == 1 and self.R > 1 and self.R * self.R * self.K * 128 <= 80 * 1024
 
     @property
+    def stream(self) -> bool:
+        """The window mode with a streamed filter: C = 64 x CB > 64, K <= 128, stride 1, a spatial
+        filter, a map tall enough for the window tiles (ResNet-50 l2 3x3)."""
+        q = self.P
+        wp = 16
+        while wp < q + self.R - 1:
+            wp *= 2
+        return (self.C % 64 == 0 and self.C > 64 and self.K <= 128 and self.stride == 1 and self.R > 1
+                and wp <= 128 and self.P >= 128 // wp)
+
+    @property
     def Cs(self) -> int:
         """Stored channels: 4 on the stem kernel, else NHWC rows padded to the
         16-byte TMA granule."""

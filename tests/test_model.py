@@ -151,6 +151,9 @@ def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
             alcop.validate(g, s)
             assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448
             continue
+        if L.stream:  # window + streamed filter: tileK = 64 x taps per filter chunk, own A / B rings
+            assert s.tileN == L.K and s.tileK in (64, 64 * L.R) and s.cta_group == 1, s
+            continue
         assert s.tileK == 64 and s.cta_group == 1 and s.n_stage_smem_A == s.n_stage_smem_B, L.name
         if L.stem or L.window:  # the resident-filter kernel: tile = 128 output pixels x all K filters
             assert s.tileN == L.K and 1 <= s.n_stage_inner <= 8, s

@@ -166,3 +166,45 @@ def test_window_schedules_and_im2col_agree(alcop):
     s = alcop.make_schedule(tileN=64, tileK=64, n_stage=4, n_stage_inner=2, mode=0)  # WRAP: im2col kernel
     Y = alcop.conv2d(X, Wt, (1, 1), (1, 1), sched=s, out_dtype=torch.bfloat16)
     _assert_equal(Y.cpu(), want, "im2col")
+
+
+# ----------------------------------------------------------------------------
+# Window mode with a streamed filter (C = 64 x CB, stride 1): per channel block
+# the window is one chunk of the A ring, the filter comes in chunks of TB taps
+# (tileK = 64 x TB) through the B ring — separate A / B stage counts.
+STREAM_CASES = [  # N, H, W, C, K, R, S, (stride), (pad)
+    (2, 28, 28, 128, 128, 3, 3, (1, 1), (1, 1)),   # ResNet-50 l2 3x3 class
+    (1, 14, 14, 256, 128, 3, 3, (1, 1), (1, 1)),   # four channel blocks, pitch 16
+    (2, 20, 24, 192, 64, 3, 3, (1, 1), (1, 1)),    # three channel blocks
+    (1, 16, 32, 128, 128, 2, 3, (1, 1), (1, 1)),   # R != S
+]
+
+
+@pytest.mark.parametrize("case", STREAM_CASES, ids=lambda c: "x".join(map(str, c[:7])))
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_window_stream_exact(alcop, case, out_dt):
+    X, Wt, ref = _inputs(case, 101)
+    _, _, _, C, K, R, S, st, pd = case
+    odt = torch.float32 if out_dt == "f32" else torch.bfloat16
+    want = torch.from_numpy(ref).to(odt)
+    d = alcop.conv_desc(*case[:7], st, pd, alcop.BF16, alcop.F32 if out_dt == "f32" else alcop.BF16)
+    pick = alcop.choose_conv_schedule(d)
+    assert pick.tileN == K, pick
+    scheds = [pick]
+    for tk in (64, 64 * S):
+        for sa, sb in ((1, 2), (2, 3), (2, 1)):
+            scheds.append(alcop.make_schedule(tileN=K, tileK=tk, n_stage=sa, n_stage_B=sb, n_stage_inner=2))
+    # schedules only the streamed-filter kernel accepts (a chunk of S taps, or unequal A / B rings: the
+    # im2col kernel needs tileK 64 and equal stages), so a pass proves that kernel ran
+    only_streamed = [alcop.make_schedule(tileN=K, tileK=64 * S, n_stage=2, n_stage_B=1, n_stage_inner=2),
+                     alcop.make_schedule(tileN=K, tileK=64, n_stage=1, n_stage_B=2, n_stage_inner=1)]
+    for s in only_streamed:
+        Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=odt)
+        _assert_equal(Y.cpu(), want, "streamed %s" % s)
+    for s in scheds:
+        try:
+            Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=odt)
+        except alcop.AlcopError as e:
+            assert "SmemCapacity" in str(e) or "BadSchedule" in str(e), (s, e)  # a ring too deep for this K
+            continue
+        _assert_equal(Y.cpu(), want, "streamed %s" % s)
