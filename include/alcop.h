@@ -291,6 +291,11 @@ int alcop_set_stream_k_workspace(void* workspace, int64_t bytes);
  *  - C == 64, stride 1, spatial filter whose K x R x S x 64 filter fits
  *    (<= 80 KB), with such a resident-filter schedule: window mode of the same
  *    kernel (the tile's input window loaded once, taps = shifted descriptors);
+ *  - C % 64 == 0, C > 64, K <= 128, stride 1, spatial filter, with a schedule
+ *    that validates there (tileN == K, tileK 64 or 64 x S = taps per filter
+ *    chunk, n_stage_smem_A = window ring 1..4, n_stage_smem_B = filter ring,
+ *    n_stage_inner 1..2): window mode with the filter streamed through its
+ *    own ring;
  *  - 1x1, stride 1, no padding: the GEMM kernels ([N*H*W, C] x [K, C]^T),
  *    any GEMM schedule incl. CTA pairs;
  *  - otherwise C % 8 == 0: the implicit-GEMM kernel with TMA im2col loads
