@@ -44,7 +44,10 @@ def case_work(case):
         M, N, K = (512, 512, 64) if case == "qkt" else (512, 64, 512)
         b = W.BMM_BATCH
         return 2.0 * M * N * K * b, 2 * b * (M * K + K * N + M * N), "attention %s batch %d" % (case, b)
-    convs = {"stem": "conv1_7x7s2_3_64", "l1_3x3": "l1_3x3_64_64", "l3_3x3": "l3_3x3_256"}
+    if case.startswith("conv_"):
+        L = [c for c in W.CONV_LAYERS if c.name == case[len("conv_"):]][0]
+        return L.flops(W.RESNET_BATCH), L.compulsory_bytes(W.RESNET_BATCH), "ResNet-50 %s batch 256" % L.name
+    convs = {"stem": "conv1_7x7s2_3_64", "l1_3x3": "l1_3x3_64_64", "l2_3x3": "l2_3x3_128", "l3_3x3": "l3_3x3_256"}
     if case in convs:
         L = [c for c in W.CONV_LAYERS if c.name == convs[case]][0]
         return L.flops(W.RESNET_BATCH), L.compulsory_bytes(W.RESNET_BATCH), "ResNet-50 %s batch 256" % L.name

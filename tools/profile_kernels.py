@@ -107,6 +107,10 @@ def main():
         run = conv_case("conv1_7x7s2_3_64")
     elif c == "l1_3x3":
         run = conv_case("l1_3x3_64_64")
+    elif c.startswith("conv_"):  # any ResNet-50 layer by name, e.g. conv_l3_1x1_256_1024
+        run = conv_case(c[len("conv_"):])
+    elif c == "l2_3x3":
+        run = conv_case("l2_3x3_128")
     elif c == "l3_3x3":
         run = conv_case("l3_3x3_256")
     elif c in ("qkt", "pv"):

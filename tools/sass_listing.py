@@ -37,6 +37,8 @@ PRODUCTION = [
      "resident-filter conv, pixel-pair mode: the ResNet-50 stem (C = 4, 7x7/2)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 1, 3, 3>",
      "resident-filter conv, window mode: 3x3 stride-1 C = 64 (ResNet-50 l1 3x3)"),
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 2, 0, 0>",
+     "window conv with a streamed filter (separate A / B rings): C > 64, K <= 128 (ResNet-50 l2 3x3)"),
 ]
 KEYS = ("UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UTMAPF", "UTMACMDFLUSH", "SYNCS", "UTCATOMSWS",
         "UTCBAR", "ELECT", "FENCE", "ACQBULK", "MEMBAR")
