@@ -795,7 +795,11 @@ __device__ __forceinline__ void sk_fence_proxy_async_global() { asm volatile("fe
 // kWide: tileN 512 (two N = 256 MMAs per k-step into one 512-column
 // accumulator).  A template parameter, not a run-time flag: the per-MMA
 // branch of a run-time flag cost the other pair tiles 12-18 % (tools/pair_ab.py).
-template <typename OutT, int BK, bool kDebug, bool kSK, bool kWide = false>
+// kConv: A is an implicit-GEMM conv operand (C % 64 == 0): each CTA's 128
+// output pixels per chunk come as one TMA im2col box (one filter tap x 64
+// channels), the pair's CTAs taking consecutive 128-pixel halves of the
+// 256-pixel tile; B is the filter [K, R*S*C] (K-major).
+template <typename OutT, int BK, bool kDebug, bool kSK, bool kWide = false, bool kConv = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     alcop_pipelined_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmW,
@@ -904,6 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       RingCursor ra;
       TileCoord tc{0, 0, 0};
       int tc_tile = -1;
+      [[maybe_unused]] int cv_tile = -1, cv_n = 0, cv_h = 0, cv_w = 0;  // kConv: this CTA's window origin
       const uint32_t a_bytes = p.a_stage_bytes, b_bytes = p.b_stage_bytes;
       const uint32_t pair_bytes = 2 * (a_bytes + b_bytes);
       // Producer issue is split over two warps in FUSED mode: a TMA issue
@@ -927,9 +932,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         }
         const uint32_t fb_local = smem_u32(&full[slot]);
         const uint32_t fb_leader = mapa_shared(fb_local, 0);
+        if constexpr (kConv) {
+          if (kRole != 1 && tile != cv_tile) {  // window origin of this CTA's first output pixel
+            cv_tile = tile;
+            const int m0 = tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM;
+            const int pq = p.conv_P * p.conv_Q;
+            cv_n = m0 / pq;
+            const int rem = m0 - cv_n * pq;
+            const int pp = rem / p.conv_Q;
+            cv_h = pp * p.conv_sh - p.conv_ph;
+            cv_w = (rem - pp * p.conv_Q) * p.conv_sw - p.conv_pw;
+          }
+        }
         ISSUE(if constexpr (kRole != 1) {
                 if (leader) mbar_arrive_expect_tx(fb_local, pair_bytes);  // producer_commit (both CTAs' bytes)
-                if (kKAtoms > 1 && p.a_view) {
+                if constexpr (kConv) {
+                  const int cb = chunk % p.conv_Cb;
+                  const int rs = chunk / p.conv_Cb;
+                  const int fs = rs % p.conv_S;
+                  tma_load_im2col_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, cb * 64, cv_w, cv_h, cv_n,
+                                          static_cast<uint16_t>(fs), static_cast<uint16_t>(rs / p.conv_S));
+                } else if (kKAtoms > 1 && p.a_view) {
                   tma_load_4d_pair(ringA + slot * a_bytes, &tmA, fb_leader, 0,
                                    tc.mb * (2 * kTileM) + static_cast<int>(rank) * kTileM, chunk * kKAtoms, tc.b);
                 } else {
@@ -1340,10 +1363,10 @@ int launch_typed(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap
   return ALCOP_OK;
 }
 
-template <typename OutT, int BK, bool kDebug = false, bool kSK = false, bool kWide = false>
+template <typename OutT, int BK, bool kDebug = false, bool kSK = false, bool kWide = false, bool kConv = false>
 int launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tw,
                   const GemmKParams& kp, int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug, kSK, kWide>;
+  auto kern = alcop_pipelined_gemm_pair_kernel<OutT, BK, kDebug, kSK, kWide, kConv>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -1686,8 +1709,11 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
     return set_error(ALCOP_ERR_CONFIG, "Unsupported", "stride <= 8 and padding/filter within TMA im2col range");
   if (s.tileK != 64 || s.n_stage_smem_A != s.n_stage_smem_B)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "conv needs tileK 64 and equal A/B stage counts");
-  if (s.cta_group != 1 || s.stream_k != 0)
-    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the implicit-GEMM conv kernel runs with cta_group 1, whole tiles");
+  // CTA pairs: the 64-channel im2col path (C % 64 == 0, no halo layout), whole tiles
+  const bool pair = s.cta_group == 2;
+  if (s.stream_k != 0 || (pair && (small_c || halo)) || (s.cta_group != 1 && !pair))
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
+                     "the implicit-GEMM conv kernel runs whole tiles, with cta_group 1 or (C % 64 == 0, no halo) 2");
   const int64_t P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
   const int64_t Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
   if (P < 1 || Q < 1) return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "empty output");
@@ -1769,7 +1795,8 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return set_error(ALCOP_ERR_CUDA, "CudaError", "cuTensorMapEncodeIm2col failed (CUresult " + std::to_string(r) + ")");
-    rc = encode_3d_dt(&tb, dt, wt, g.K, g.N, 1, g.K * 2, g.N * g.K * 2, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B, "w");
+    rc = encode_3d_dt(&tb, dt, wt, g.K, g.N, 1, g.K * 2, g.N * g.K * 2, 64, pair ? BN / 2 : BN,
+                      CU_TENSOR_MAP_SWIZZLE_128B, "w");
     if (rc) return rc;
     rc = encode_3d_dt(&tc, odt, y, g.N, g.M, 1, g.N * ob, g.M * g.N * ob, 128 / ob, 32, CU_TENSOR_MAP_SWIZZLE_128B,
                       "y");
@@ -1786,10 +1813,10 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   kp.conv_Pb = static_cast<int32_t>((P + 7) / 8);
   kp.conv_Qb = static_cast<int32_t>((Q + 15) / 16);
   kp.num_m = stem ? static_cast<int32_t>(d.N * kp.conv_Pb * kp.conv_Qb)
-                  : static_cast<int32_t>((g.M + kTileM - 1) / kTileM);
+                  : static_cast<int32_t>((g.M + kTileM * s.cta_group - 1) / (kTileM * s.cta_group));
   kp.num_n = static_cast<int32_t>((g.N + BN - 1) / BN);
   kp.num_tiles = kp.num_m * kp.num_n;
-  kp.group_m = raster_group(s, kp.num_m, kp.num_n, kTileM, BN, 1);
+  kp.group_m = raster_group(s, kp.num_m, kp.num_n, kTileM * s.cta_group, BN, s.cta_group);
   kp.E = static_cast<int32_t>((g.K + 63) / 64);  // small C: the last chunk's taps past R*S meet zero filter rows
                                                  // stem: one chunk per filter row (g.K = R * 64)
   kp.sA = s.n_stage_smem_A;
@@ -1797,9 +1824,9 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   kp.tacc = s.n_stage_inner;
   kp.mode = s.mode;
   kp.b_mn_major = 0;
-  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, BN);
+  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM * s.cta_group, BN);
   kp.a_stage_bytes = static_cast<uint32_t>(kTileM * 64 * 2);
-  kp.b_stage_bytes = static_cast<uint32_t>(BN * 64 * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>((pair ? BN / 2 : BN) * 64 * 2);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
   kp.C = y;
@@ -1824,6 +1851,19 @@ int launch_conv2d(const alcop_conv_desc& d, const alcop_schedule& s, const void*
   const int smem = static_cast<int>(gemm_smem_bytes_epi(g, s, 4));
   kp.stage_bufs = gemm_staging_bufs_epi(g, s, 4);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (pair) {
+    if (kp.stamps) return set_error(ALCOP_ERR_CONFIG, "Unsupported", "conv CTA pairs run without timeline stamps");
+    grid = ((s.num_ctas > 0 ? s.num_ctas : sms) / 2) * 2;
+    if (grid > 2 * kp.num_tiles) grid = 2 * kp.num_tiles;
+    kp.epi_warps = 4;
+    switch (d.out_dtype) {
+      case ALCOP_F32: return launch_pair_t<float, 64, false, false, false, true>(ta, tb, tc, tc, kp, grid, smem, st);
+      case ALCOP_BF16:
+        return launch_pair_t<__nv_bfloat16, 64, false, false, false, true>(ta, tb, tc, tc, kp, grid, smem, st);
+      case ALCOP_F16: return launch_pair_t<__half, 64, false, false, false, true>(ta, tb, tc, tc, kp, grid, smem, st);
+    }
+    return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
+  }
   switch (d.out_dtype) {
     case ALCOP_F32: return launch_conv_typed<float>(ta, tb, tc, kp, grid, smem, st);
     case ALCOP_BF16: return launch_conv_typed<__nv_bfloat16>(ta, tb, tc, kp, grid, smem, st);

@@ -77,12 +77,13 @@ def test_host_entry_rejects_strided(alcop):
     assert rc == alcop.ALCOP_ERR_CONFIG
 
 
-@pytest.mark.parametrize("cg,sk", [(2, 0), (2, 1), (1, 1)])
-def test_conv_rejects_pair_and_stream_k(alcop, cg, sk):
-    """the conv kernel is single-CTA with whole tiles; a
-    CTA-pair or stream-K schedule is rejected before any launch."""
+@pytest.mark.parametrize("cg,sk,c", [(2, 0, 24), (2, 1, 64), (1, 1, 64)])
+def test_conv_rejects_pair_and_stream_k(alcop, cg, sk, c):
+    """the conv kernels run whole tiles (no stream-K), and
+    CTA pairs only on the 64-channel im2col path; other schedules are
+    rejected before any launch."""
     lib = alcop.load_library()
-    d = alcop.conv_desc(2, 14, 14, 64, 128, 3, 3, (1, 1), (1, 1))
+    d = alcop.conv_desc(2, 14, 14, c, 128, 3, 3, (2, 2), (1, 1))
     s = alcop.make_schedule(tileN=256, tileK=64, n_stage=4, cta_group=cg, stream_k=sk)
     dummy = ctypes.c_void_p(256)
     rc = lib.alcop_conv2d(ctypes.byref(d), ctypes.byref(s), dummy, dummy, dummy, None)

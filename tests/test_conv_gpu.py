@@ -152,3 +152,33 @@ def test_conv_1x1_on_gemm_kernels(alcop, case):
     for s in scheds:
         Y = alcop.conv2d(X, Wt, (1, 1), (0, 0), sched=s, out_dtype=torch.bfloat16)
         assert torch.equal(Y.cpu(), want), s
+
+
+PAIR_CASES = [  # N, H, W, C, K, R, S, stride, pad: implicit-GEMM conv on CTA pairs (C % 64 == 0)
+    (2, 14, 14, 64, 256, 3, 3, 1, 1),
+    (2, 16, 16, 128, 256, 3, 3, 2, 1),
+    (2, 14, 14, 256, 512, 1, 1, 2, 0),   # strided 1x1 (downsample)
+    (1, 9, 11, 64, 128, 3, 3, 1, 1),     # ragged: the last pair tile's second CTA past M
+    (3, 7, 7, 128, 192, 3, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", PAIR_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_conv_cta_pair_exact(alcop, case):
+    N, H, W, C, K, R, S, st, pd = case
+    x = random_tensor(N * H * W * C, 71).reshape(N, H, W, C)
+    w = random_tensor(K * R * S * C, 72).reshape(K, R, S, C)
+    ref = coracle.conv2d(coracle.to_dtype(x.astype(np.float32), "bf16"),
+                         coracle.to_dtype(w.astype(np.float32), "bf16"), (st, st), (pd, pd), "bf16", "f32")
+    X = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    Wt = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    ran = 0
+    for tn, stg in ((256, 6), (128, 4), (192, 5)):
+        if tn > K and tn != 128:
+            continue
+        s = alcop.make_schedule(tileN=tn, tileK=64, n_stage=stg, cta_group=2)
+        for odt in (torch.float32, torch.bfloat16):
+            Y = alcop.conv2d(X, Wt, (st, st), (pd, pd), sched=s, out_dtype=odt)
+            assert torch.equal(Y.cpu(), torch.from_numpy(ref).to(odt)), (s, odt)
+            ran += 1
+    assert ran >= 2
