@@ -299,7 +299,9 @@ int alcop_set_stream_k_workspace(void* workspace, int64_t bytes);
  *  - 1x1, stride 1, no padding: the GEMM kernels ([N*H*W, C] x [K, C]^T),
  *    any GEMM schedule incl. CTA pairs;
  *  - otherwise C % 8 == 0: the implicit-GEMM kernel with TMA im2col loads
- *    (tileK 64, equal A/B stages, cta_group 1). */
+ *    (tileK 64, equal A/B stages, whole tiles; cta_group 2 = CTA pairs when
+ *    C % 64 == 0 and x is not in the halo layout, each CTA a 128-pixel half
+ *    of the 256-pixel tile). */
 int alcop_conv2d(const alcop_conv_desc* d, const alcop_schedule* s, const void* x, const void* w, void* y,
                  void* stream);
 
@@ -346,8 +348,8 @@ int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_sc
  * (see there): the resident-filter kernel's ring depth x accumulators (its
  * own per-tile model: MMA, window fill, the SM's share of the HBM stream,
  * pipeline_latency over the windows), the GEMM space for 1x1 stride-1 convs,
- * else the implicit-GEMM kernel's space (tileK 64, equal stages, cta_group 1)
- * ranked on the conv's GEMM view. */
+ * else the implicit-GEMM kernel's space (tileK 64, equal stages; CTA pairs
+ * when C % 64 == 0 and R*S*C >= 512) ranked on the conv's GEMM view. */
 int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_hw* hw, alcop_schedule* out);
 
 /* One measured candidate of the model-assisted tuner. */
