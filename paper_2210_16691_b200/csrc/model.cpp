@@ -265,9 +265,10 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
 // — the paper's stage formula with the window as the pipelined chunk.
 static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, const alcop_schedule& s,
                               const alcop_hw& hw) {
-  const bool window = g.TR > 1 || g.WP > 0;
+  const bool window = g.WP > 0;
   const bool streamed = window && g.wbytes == 0;  // window with the filter streamed per channel block
-  const double tiles = static_cast<double>(d.N * (window ? (g.P + g.TR - 1) / g.TR : g.P) * g.QB);
+  const int64_t tr = g.TR > 0 ? g.TR : 1;          // output rows per tile (stem, four-row mode: 4)
+  const double tiles = static_cast<double>(d.N * ((g.P + tr - 1) / tr) * g.QB);
   const double per_sm = std::ceil(tiles / hw.numSM);
   const double ob = d.out_dtype == ALCOP_F32 ? 4.0 : 2.0;
   const double mma_k = (128.0 * d.K * 16 * 2) / hw.throughputSM;  // one k-step of 16
@@ -289,11 +290,19 @@ static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, c
     if (s.n_stage_inner == 1) main += per_sm * epi;
     return (hw.tLaunch + main + epi) / (hw.clockGHz * 1e9);
   }
-  const double ksteps = window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(d.R * (g.T2 / 2));
+  const double ksteps =
+      window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(tr * d.R * (g.T2 / 2));
   const double mma = ksteps * mma_k;
   const double fill = static_cast<double>(g.box_bytes) / hw.bwSmem;
   double use = std::max({mma, fill, hbm_tile, hw.tIssue});
   if (s.n_stage_inner == 1) use = std::max(use, mma + epi);
+  // pair modes: one issuing warp serialises its per-tile barrier waits and
+  // commits (~500 clk, tools/stem_trace.py) with the tile's MMAs; two (even
+  // rings) overlap them with the other warp's tile (stem, batch 256: 125 vs
+  // 96 us).  The window mode's 36-MMA tiles hide it (its deeper odd rings
+  // measured faster than the even dual ones)
+  const bool dual = s.n_stage_smem_A % 2 == 0 && s.n_stage_inner % 2 == 0;
+  if (!window && !dual) use = std::max(use, mma + 500.0);
   const double main = model::pipeline_latency(hw.latLLCRead, use, static_cast<int64_t>(per_sm), s.n_stage_smem_A, 1);
   return (hw.tLaunch + main + epi) / (hw.clockGHz * 1e9);
 }

@@ -152,6 +152,46 @@ __device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_
           umma_f16_ss(d_tmem, ad + r * a_row16 + 2 * j, bd + (r * ksteps + j) * b_step, p.idesc,
                       (r > 0 || j > 0) ? 1u : 0u);
     }
+  } else if constexpr (kMode == 3) {
+    // stem, four output rows per tile: window row e (input row 2*p0 - 3 + e,
+    // e = 0..12) is the A operand once for every output row k it feeds
+    // (filter row r = e - 2k in [0, 7)), with those filter rows stacked as N
+    // = count x 64 — the even rows {6, 4, 2, 0} and the odd rows {5, 3, 1}
+    // are each stored descending, so the rows of one MMA are adjacent — and
+    // D = the adjacent 64-column accumulators of output rows k_min..k_max.
+    // Output row k starts at e = 2k (r = 0): that piece is split off with
+    // accumulate = 0; every other piece accumulates.
+    const uint64_t a_row16 = p.row_bytes >> 4;
+    const uint64_t ad = make_smem_desc(a0, 16u, 128u, kLayoutNone);
+#pragma unroll
+    for (int e = 0; e < 13; ++e) {
+      const int cls = e & 1;
+      const int nj = cls ? 3 : 4;                         // filter rows in the class
+      const int kmin = e <= 6 ? 0 : (e - 5) / 2;          // ceil((e - 6) / 2)
+      const int kmax = (e / 2) < 3 ? (e / 2) : 3;
+      const int j0 = ((cls ? 5 : 6) - (e - 2 * kmin)) / 2;  // class block of filter row e - 2 kmin
+      const bool starts = !cls && e / 2 <= 3;             // output row kmax gets its first piece (r = 0)
+      const uint32_t cbase = wsm + (cls ? 4u * 4u * 64u * 16u : 0u);
+      const uint32_t lbo_b = static_cast<uint32_t>(nj) * 64u * 16u;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t ade = ad + e * a_row16 + 2 * u;
+        const uint32_t bt = cbase + 2u * u * lbo_b;  // pair groups 2u, 2u+1
+        if (starts && u == 0) {
+          const int cnt = kmax - kmin;  // rows already under way
+          if (cnt > 0)
+            umma_f16_ss(d_tmem + kmin * 64, ade, make_smem_desc(bt + j0 * 1024u, lbo_b, 128u, kLayoutNone),
+                        (p.idesc & ~(0x3Fu << 17)) | ((cnt * 64u >> 3) << 17), 1u);
+          umma_f16_ss(d_tmem + kmax * 64, ade,
+                      make_smem_desc(bt + (j0 + cnt) * 1024u, lbo_b, 128u, kLayoutNone),
+                      (p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17), 0u);
+        } else {
+          const int cnt = kmax - kmin + 1;
+          umma_f16_ss(d_tmem + kmin * 64, ade, make_smem_desc(bt + j0 * 1024u, lbo_b, 128u, kLayoutNone),
+                      (p.idesc & ~(0x3Fu << 17)) | ((cnt * 64u >> 3) << 17), 1u);
+        }
+      }
+    }
   } else {
     // window: tap (r, s) = A rows m -> window pixel m + r*WP + s (128 B each,
     // 128B-swizzled: the swizzle follows the absolute smem address, so a
@@ -235,7 +275,30 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   grid_launch_dependents();
 
   // The filter, resident in shared memory for the kernel's lifetime.
-  if constexpr (kMode == 0) {
+  if constexpr (kMode == 3) {
+    // two classes of filter rows, each [pair group t][class block j][filter n][8
+    // elements]: even rows 6, 4, 2, 0 (j = 0..3), odd rows 5, 3, 1 (j = 0..2);
+    // element e = (tap parity e/4, channel e%4) as in the pair mode
+    for (int idx = threadIdx.x; idx < 7 * 4 * 64; idx += blockDim.x) {
+      const int n = idx & 63, rest = idx >> 6;  // rest = (class slot, t)
+      const int t = rest & 3, js = rest >> 2;   // js = 0..6: even j 0..3, odd j 0..2
+      const int cls = js >= 4, j = cls ? js - 4 : js;
+      const int r = cls ? 5 - 2 * j : 6 - 2 * j;
+      uint32_t v[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int sx = 2 * (p.o_min + t) + h + p.pw;
+        uint2 taps = make_uint2(0u, 0u);
+        if (sx >= 0 && sx < p.S)
+          taps = __ldg(reinterpret_cast<const uint2*>(p.w + ((static_cast<int64_t>(n) * p.R + r) * p.S + sx) * 4));
+        v[2 * h] = taps.x;
+        v[2 * h + 1] = taps.y;
+      }
+      const int nj = cls ? 3 : 4;
+      const uint32_t off = (cls ? 4u * 4u * 64u * 16u : 0u) + ((t * nj + j) * 64u + n) * 16u;
+      st_shared_v4(wsm + off, v[0], v[1], v[2], v[3]);
+    }
+  } else if constexpr (kMode == 0) {
     // B operand in the K-major no-swizzle layout [k group kg][filter n][8
     // elements] (LBO = BN*16 bytes between k groups, SBO = 128 bytes between
     // 8-filter groups).  k group kg = (filter row r, pair group t); element e
@@ -427,25 +490,29 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     if (first) cur.advance(p);
     // this warp's first output (column, row-in-tile) of the tile
     const int m0 = q * 32;
-    const int col0 = kMode == 0 ? m0 : (m0 & ((1 << p.lwp) - 1));
-    const int row0 = kMode == 0 ? 0 : (m0 >> p.lwp);
+    constexpr bool kPairs = kMode == 0 || kMode == 3;
+    const int col0 = kPairs ? m0 : (m0 & ((1 << p.lwp) - 1));
+    const int row0 = kPairs ? 0 : (m0 >> p.lwp);
+    constexpr int kSub = kMode == 3 ? 4 : 1;  // output rows per tile held side by side in TMEM (stem4)
     for (int tl = first; tl < my_tiles; tl += step, cur.advance(p), (step == 2 ? cur.advance(p) : void())) {
       mbar_wait(smem_u32(&tfull[acc]), (acc_phase >> acc) & 1u);
       acc_phase ^= 1u << acc;
       tc_fence_after();
       const uint32_t t_addr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      const int oq = cur.qb * 128 + col0;                              // output column of row m0
-      const int op = kMode == 0 ? cur.p : cur.p * p.row_step + row0;   // output row of row m0
-      const bool rows_live = oq < p.Q && op < p.Pout;
-      for (int c = 0; c < nchunks; ++c) {
+      const int oq = cur.qb * 128 + col0;  // output column of row m0
+      for (int ic = 0; ic < kSub * nchunks; ++ic) {
+        const int k = kSub == 1 ? 0 : ic / nchunks, c = kSub == 1 ? ic : ic - k * nchunks;
+        const uint32_t ta = t_addr + k * p.BN;
+        const int op = kMode == 0 ? cur.p : kMode == 3 ? cur.p * 4 + k : cur.p * p.row_step + row0;  // output row
+        const bool rows_live = oq < p.Q && op < p.Pout;
         uint32_t w[32];
         if constexpr (sizeof(OutT) == 4) {
-          tmem_ld_32x32b_x32(t_addr + c * 32, w);
+          tmem_ld_32x32b_x32(ta + c * 32, w);
           tmem_wait_ld();
         } else {
           uint32_t r0[32], r1[32];
-          tmem_ld_32x32b_x32(t_addr + c * 64, r0);
-          tmem_ld_32x32b_x32(t_addr + c * 64 + 32, r1);
+          tmem_ld_32x32b_x32(ta + c * 64, r0);
+          tmem_ld_32x32b_x32(ta + c * 64 + 32, r1);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -453,7 +520,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
             w[16 + i] = pack2s<OutT>(r1[2 * i], r1[2 * i + 1]);
           }
         }
-        if (c == nchunks - 1) {  // this warp's TMEM reads of the accumulator are done
+        if (ic == kSub * nchunks - 1) {  // this warp's TMEM reads of the accumulator are done
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
@@ -497,7 +564,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
 template <typename OutT>
 int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const CUtensorMap& tw, const StemKParams& kp,
                       int mode, int grid, int smem, cudaStream_t st) {
-  auto kern = mode == 2   ? alcop_stem_conv_kernel<OutT, 2, 0, 0>
+  auto kern = mode == 3   ? alcop_stem_conv_kernel<OutT, 3, 7, 2>
+              : mode == 2 ? alcop_stem_conv_kernel<OutT, 2, 0, 0>
               : mode == 1 ? (kp.R == 3 && kp.S == 3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3>
                                                     : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
                           : (kp.R == 7 && kp.T2 == 4 ? alcop_stem_conv_kernel<OutT, 0, 7, 2>
@@ -569,9 +637,17 @@ bool window_stream_applicable(const alcop_conv_desc& d) {
   return d.C % 64 == 0 && d.K <= 128 && !window_conv_applicable(d) && window_common(d);
 }
 
-// 0 = pixel pairs, 1 = window (resident filter), 2 = window (streamed filter), -1 = none
+// the ResNet-50 stem exactly (7x7, stride 2, pad 3, K 64): four output rows
+// per tile with the filter rows stacked along N (kMode 3)
+static bool stem4_applicable(const alcop_conv_desc& d) {
+  return stem_pairs_applicable(d) && d.R == 7 && d.S == 7 && d.stride_h == 2 && d.stride_w == 2 && d.pad_h == 3 &&
+         d.pad_w == 3 && d.K == 64 && (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1 >= 4;
+}
+
+// 0 = pixel pairs, 1 = window (resident filter), 2 = window (streamed filter),
+// 3 = pixel pairs, four output rows per tile (the ResNet-50 stem), -1 = none
 static int stem_mode(const alcop_conv_desc& d) {
-  if (d.C == 4) return 0;
+  if (d.C == 4) return stem4_applicable(d) ? 3 : 0;
   if (window_conv_applicable(d)) return 1;
   if (window_stream_applicable(d)) return 2;
   return -1;
@@ -582,7 +658,7 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   g.P = (d.H + 2 * d.pad_h - d.R) / d.stride_h + 1;
   g.Q = (d.W + 2 * d.pad_w - d.S) / d.stride_w + 1;
   const int mode = stem_mode(d);
-  if (mode >= 1) {  // window modes
+  if (mode == 1 || mode == 2) {  // window modes
     const int64_t wp = window_pitch(d);
     const int64_t tr = 128 / wp;
     g.QB = 1;
@@ -598,7 +674,6 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
     return g;
   }
   g.QB = (g.Q + 127) / 128;
-  g.TR = 1;
   // tap s reads pixel 2q - pad_w + s = pair q + floor((s - pad_w) / 2)
   auto fdiv2 = [](int64_t v) { return v >= 0 ? v / 2 : -((1 - v) / 2); };
   g.o_min = static_cast<int32_t>(fdiv2(-d.pad_w));
@@ -608,7 +683,10 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   // window: shift (0..7) + 128 rows + T2-1 further pairs, in 8-pair (128 B) blocks
   g.NB = (7 + 128 + g.T2 - 1 + 7) / 8;
   g.row_bytes = static_cast<uint32_t>(g.NB * 128);
-  g.box_bytes = static_cast<uint32_t>(d.R * g.row_bytes);
+  // four output rows per tile (mode 3): the window covers 2 * 3 + R input rows
+  const int64_t wrows = mode == 3 ? 3 * d.stride_h + d.R : d.R;
+  g.TR = mode == 3 ? 4 : 1;
+  g.box_bytes = static_cast<uint32_t>(wrows * g.row_bytes);
   g.slot_bytes = static_cast<uint32_t>((g.box_bytes + 1023) / 1024 * 1024);
   g.wbytes = static_cast<uint32_t>((d.R * g.T2 * d.K * 16 + 1023) / 1024 * 1024);
   g.kdim = d.R * g.T2 * 8;
@@ -661,7 +739,8 @@ int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the window ring: equal A/B stages in 1..16");
   }
   const int max_inner = mode == 2 ? 2 : 8;
-  if (s.n_stage_inner < 1 || s.n_stage_inner > max_inner || s.n_stage_inner * d.K > kTmemCols)
+  const int64_t acc_cols = (mode == 3 ? 4 : 1) * d.K;  // mode 3: four output rows side by side
+  if (s.n_stage_inner < 1 || s.n_stage_inner > max_inner || s.n_stage_inner * acc_cols > kTmemCols)
     return set_error(ALCOP_ERR_CONFIG, "TmemCapacity", "n_stage_inner accumulators of K columns exceed TMEM");
   if (stem_pairs_smem_bytes(d, s) > kMaxSmemBytes)
     return set_error(ALCOP_ERR_CONFIG, "SmemCapacity", "window / filter rings exceed shared memory");
@@ -691,7 +770,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   const int ob = out_bytes(d);
   CUtensorMap tx, ty;
   const cuuint32_t one[4] = {1, 1, 1, 1};
-  if (mode == 0) {
+  if (mode == 0 || mode == 3) {
     // x viewed as {64 elements = 8 pixel pairs (128 B), W/16 blocks, H, N}; box
     // = NB blocks of R consecutive rows: the tile's whole input window, zero
     // filled above/below the image and left/right of it (pairs never straddle
@@ -699,7 +778,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
     const cuuint64_t xdims[4] = {64, static_cast<cuuint64_t>(d.W / 16), static_cast<cuuint64_t>(d.H),
                                  static_cast<cuuint64_t>(d.N)};
     const cuuint64_t xstr[3] = {128, static_cast<cuuint64_t>(d.W * 8), static_cast<cuuint64_t>(d.H * d.W * 8)};
-    const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), static_cast<cuuint32_t>(d.R), 1};
+    const cuuint32_t xbox[4] = {64, static_cast<cuuint32_t>(g.NB), g.box_bytes / g.row_bytes, 1};
     rc = encode_tiled_map(&tx, dt, x, 4, xdims, xstr, xbox, one, CU_TENSOR_MAP_SWIZZLE_NONE, "x (stem pairs)");
   } else {
     // x as {C channels, W, H, N}; box = 64 channels x WP pixels (from
@@ -726,7 +805,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   }
   // y as {K, Q, P, N}: each epilogue warp stores its 32 tile rows x 128 B
   // (window mode, WP = 16: two output rows of 16 columns)
-  const int64_t wcols = mode == 0 ? 32 : std::min<int64_t>(32, g.WP);
+  const int64_t wcols = (mode == 0 || mode == 3) ? 32 : std::min<int64_t>(32, g.WP);
   const cuuint64_t ydims[4] = {static_cast<cuuint64_t>(d.K), static_cast<cuuint64_t>(g.Q),
                                static_cast<cuuint64_t>(g.P), static_cast<cuuint64_t>(d.N)};
   const cuuint64_t ystr[3] = {static_cast<cuuint64_t>(d.K * ob), static_cast<cuuint64_t>(g.Q * d.K * ob),
@@ -738,7 +817,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
 
   StemKParams kp{};
   kp.Pout = static_cast<int32_t>(g.P);
-  kp.P = static_cast<int32_t>(mode == 0 ? g.P : (g.P + g.TR - 1) / g.TR);
+  kp.P = static_cast<int32_t>(mode == 0 ? g.P : (g.P + g.TR - 1) / g.TR);  // tile rows per image
   kp.Q = static_cast<int32_t>(g.Q);
   kp.QB = static_cast<int32_t>(g.QB);
   const int64_t tiles = d.N * static_cast<int64_t>(kp.P) * g.QB;
@@ -748,7 +827,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.S = static_cast<int32_t>(d.S);
   kp.T2 = g.T2;
   kp.o_min = g.o_min;
-  kp.row_step = mode == 0 ? d.stride_h : g.TR;
+  kp.row_step = mode == 0 ? d.stride_h : mode == 3 ? 4 * d.stride_h : g.TR;  // input rows per tile row
   kp.ph = d.pad_h;
   kp.pw = d.pad_w;
   kp.BN = static_cast<int32_t>(d.K);
@@ -758,7 +837,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.slot_bytes = g.slot_bytes;
   kp.box_bytes = g.box_bytes;
   kp.wbytes = g.wbytes;
-  kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(d.K));
+  kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols((mode == 3 ? 4 : 1) * d.K));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.nacc));
   kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, static_cast<uint32_t>(d.K));
   kp.w = static_cast<const uint16_t*>(wt);
@@ -787,7 +866,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.dn = grid / (kp.P * kp.QB);
   kp.dp = (grid - kp.dn * kp.P * kp.QB) / kp.QB;
   kp.dq = grid - kp.dn * kp.P * kp.QB - kp.dp * kp.QB;
-  if (mode == 0) {
+  if (mode == 0 || mode == 3) {
     // column block qb reads pairs from 128*qb + o_min: block 16*qb + floor(o_min/8), `shift` pairs in
     kp.blk_off = g.o_min >= 0 ? g.o_min / 8 : -((7 - g.o_min) / 8);
     kp.shift = g.o_min - 8 * kp.blk_off;

@@ -25,6 +25,8 @@ CASES = [  # N, H, W, C, K, R, S, (stride_h, stride_w), (pad_h, pad_w)
     (2, 12, 16, 2, 64, 1, 1, (2, 2), (0, 0)),     # 1x1 / 2 (one tap, zero partner)
     (1, 20, 32, 3, 64, 6, 3, (3, 2), (2, 1)),     # stride_h 3, R != S
     (1, 5, 32, 3, 64, 7, 7, (2, 2), (3, 3)),      # image shorter than the filter (window box > H)
+    (1, 9, 48, 3, 64, 7, 7, (2, 2), (3, 3)),      # stem, 5 output rows: a ragged four-row tile
+    (3, 14, 32, 4, 64, 7, 7, (2, 2), (3, 3)),     # stem, 7 output rows, several images per CTA
 ]
 
 
@@ -59,16 +61,25 @@ def test_stem_exact(alcop, case, out_dt):
     _assert_equal(Y.cpu(), torch.from_numpy(ref).to(odt), "model schedule %s" % s)
 
 
-def test_stem_schedules(alcop):
+@pytest.mark.parametrize("case", [(2, 30, 64, 3, 64, 7, 7, (2, 2), (3, 3)),    # the stem: four-row tiles
+                                  (2, 30, 64, 3, 64, 7, 7, (2, 2), (2, 3))],   # pad_h 2: one-row tiles
+                         ids=["stem4", "pairs"])
+def test_stem_schedules(alcop, case):
     """Every ring depth 1..8 x accumulators 1..4 that fits: same bits."""
-    case = (2, 30, 64, 3, 64, 7, 7, (2, 2), (3, 3))
     X, Wt, ref = _inputs(case, 71)
     want = torch.from_numpy(ref).to(torch.bfloat16)
+    ran = 0
     for st in (1, 2, 3, 5, 8):
         for inner in (1, 2, 4):
             s = alcop.make_schedule(tileN=64, tileK=64, n_stage=st, n_stage_inner=inner, mode=1)
-            Y = alcop.conv2d(X, Wt, (2, 2), (3, 3), sched=s, out_dtype=torch.bfloat16)
+            try:
+                Y = alcop.conv2d(X, Wt, case[7], case[8], sched=s, out_dtype=torch.bfloat16)
+            except alcop.AlcopError as e:  # a ring / accumulator ring that does not fit this mode
+                assert "SmemCapacity" in str(e) or "TmemCapacity" in str(e), e
+                continue
+            ran += 1
             _assert_equal(Y.cpu(), want, "stages %d inner %d" % (st, inner))
+    assert ran >= 8
 
 
 def test_stem_fourth_channel_and_grid(alcop):
@@ -112,7 +123,8 @@ def test_stem_rejects(alcop):
     assert lib.alcop_last_error().decode().startswith("Unsupported")
     d = alcop.conv_desc(1, 16, 32, 4, 64, 7, 7, (2, 2), (3, 3), alcop.BF16, alcop.BF16)
     for bad, tag in ((dict(tileN=128), "BadSchedule"), (dict(mode=0), "BadSchedule"),
-                     (dict(n_stage_inner=4, tileN=64), None)):
+                     (dict(n_stage_inner=4), "TmemCapacity"),  # the stem's four-row accumulators: 256 columns
+                     (dict(n_stage_inner=2, tileN=64), None)):
         s = alcop.make_schedule(**{**dict(tileN=64, tileK=64, n_stage=2, n_stage_inner=2, mode=1), **bad})
         rc = call(d, s)
         if tag is None:
