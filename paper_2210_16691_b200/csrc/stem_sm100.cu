@@ -1,6 +1,10 @@
-// stem_sm100.cu — the small-channel, stride-2 "stem" convolution (ResNet-50
-// conv1: 7x7, stride 2, 3 -> 64 channels on 224x224 images) as a pipelined
-// load-and-use kernel whose A operand is never expanded.
+// stem_sm100.cu — the window conv kernel: convolutions whose pipelined chunk
+// is the tile's input window, loaded once by one TMA box, with every filter
+// tap an MMA descriptor into it (the A operand is never expanded).  Modes:
+// 0 / 3 the small-channel stride-2 stem (ResNet-50 conv1, 7x7/2, 3 -> 64) on
+// pixel pairs (3: four output rows per tile), 1 C = 64 stride-1 convs with the
+// filter resident, 2 wider stride-1 convs with the filter streamed through its
+// own ring.  The pair mode is described first:
 //
 // The implicit-GEMM view of conv1 has K = R*S*C = 147 with C = 3: the generic
 // kernel pads every filter tap to 8 channels and gathers an im2col tile per

@@ -18,10 +18,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2210_16691_b200", "libalcop.so")
 # (substring of the demangled name, what the bench runs it for)
 PRODUCTION = [
-    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 32, false, false, true>",
+    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 32, false, false, true, false>",
      "CTA-pair GEMM, 256 x 512 tile (two N = 256 MMAs per k-step): the C5 squares (headline)"),
-    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 64, false, false, false>",
+    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 64, false, false, false, false>",
      "CTA-pair GEMM (cta_group::2): BERT QKV / FFN1 / FFN2"),
+    ("alcop_pipelined_gemm_pair_kernel<__nv_bfloat16, 64, false, false, false, true>",
+     "CTA-pair implicit-GEMM conv (im2col loads, cta_group::2): ResNet-50 l3 / l4 layers"),
     ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 0, false, 4>",
      "single-CTA GEMM: BERT FFN2 / O, attention PV, config-1 class"),
     ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 0, false, 8>",
@@ -33,8 +35,10 @@ PRODUCTION = [
     ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 3, false, 4>",
      "implicit-GEMM conv, stem (ResNet-50 conv1, halo-padded NHWC8)"),
     ("alcop_chain_gemm_kernel<__nv_bfloat16, 64>", "several GEMMs in one persistent launch (alcop_gemm_chain)"),
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 3, 7, 2>",
+     "resident-filter conv, pixel pairs, four output rows per tile: the ResNet-50 stem (C = 4, 7x7/2)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 0, 7, 2>",
-     "resident-filter conv, pixel-pair mode: the ResNet-50 stem (C = 4, 7x7/2)"),
+     "resident-filter conv, pixel-pair mode, one output row per tile (other C = 4 stride-2 shapes)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 1, 3, 3>",
      "resident-filter conv, window mode: 3x3 stride-1 C = 64 (ResNet-50 l1 3x3)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 2, 0, 0>",
