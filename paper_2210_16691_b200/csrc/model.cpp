@@ -99,7 +99,8 @@ extern "C" void alcop_hw_default_b200(alcop_hw* hw) {
   hw->clockGHz = 1.9;
   hw->tIssue = 384.5;       // per-chunk producer/consumer floor (barrier hops + issue)
   hw->tIssuePerBox = 9.71;
-  hw->tLaunch = 1139.9;
+  hw->tLaunch = 5500;  // launch + ramp of one kernel in back-to-back graphs (BERT GEMMs, round 2; was 1140, fitted
+                       // to the round-1 sweep; outside the power bound, so picks are unchanged)
   hw->tTile = 38.38;
   hw->overlapDRAM = 0.20;
   hw->tPair = 3716;
@@ -175,7 +176,11 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   out->tThreadblk = out->tInit + out->tMainLoop + out->tEpilogue;
   const double sm = out->tSmemLoad + body + (cg == 2 ? hw->tPair : 0.0);
   const double dram = static_cast<double>(out->bytesWorkset + w->M * w->N * ob * w->batch) / hw->bwDRAM;
-  out->tKernel = hw->tLaunch + std::max(sm, dram) + hw->overlapDRAM * std::min(sm, dram);
+  // the launch / ramp of one kernel (grid start, tensor-map fetch, first fill
+  // under the previous kernel's PDL tail) is paid in either regime: it sits
+  // outside the power bound, so it shifts every schedule of a shape alike
+  const double tBody = std::max(sm, dram) + hw->overlapDRAM * std::min(sm, dram);
+  out->tKernel = hw->tLaunch + tBody;
 
   // Power-capped regime (not in the reference's model): L2 -> SM bytes are
   // exact (every tile loads its A rows and B columns for every chunk); HBM
@@ -203,7 +208,7 @@ extern "C" int alcop_predict(const alcop_gemm_desc* w, const alcop_schedule* s, 
   const double flops = 2.0 * static_cast<double>(w->M) * w->N * w->K * w->batch;
   const double tPowerS = hw->tCapFlop * flops + hw->tCapL2Byte * out->bytesL2 + hw->tCapDramByte * dramEst;
   out->tPower = tPowerS * hw->clockGHz * 1e9;
-  out->tKernel = std::max(out->tKernel, out->tPower);
+  out->tKernel = hw->tLaunch + std::max(tBody, out->tPower);
   out->seconds = out->tKernel / (hw->clockGHz * 1e9);
   return ALCOP_OK;
 }
