@@ -86,7 +86,7 @@ struct StemKParams {
   // filter ring (n_stage_smem_B slots of TB x BN x 128 B)
   int32_t CB, TB, nbc, sB;
   uint32_t b_slot_bytes;
-  int32_t skip;                 // measurement only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
+  int32_t skip;                 // -DSTEM_PROBE builds only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
 };
 
 template <typename OutT>
@@ -849,11 +849,16 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   int lwp = 0;
   while ((1 << lwp) < g.WP) ++lwp;
   kp.lwp = lwp;
+#ifdef STEM_PROBE
+  // measurement builds only (-DSTEM_PROBE, tools/stem_skip_probe.py): switch parts of the pipeline off
   static const int skip_env = [] {
     const char* e = std::getenv("ALCOP_STEM_SKIP");
     return e ? std::atoi(e) : 0;
   }();
   kp.skip = skip_env;
+#else
+  kp.skip = 0;
+#endif
   kp.dual = stem_dual(d, s) ? 1 : 0;
   kp.stage_warps = kp.dual ? 8 : 4;
   if (mode == 2) {

@@ -5,7 +5,7 @@ C oracle's (fp32-accumulate, OpenMP on all cores) — measured on a bounded
 sample and extrapolated by the per-MMA cost (labelled), except C1 which runs
 whole.  C4 (conv) has no reference CPU path: only the oracle's direct conv.
 
-    python tools/cpu_configs.py [--out profiles/cpu_configs_r01.json] [--bench profiles/bench_r01.json]
+    python tools/cpu_configs.py [--out profiles/cpu_configs_r02.json] [--bench profiles/bench_r02.json]
 
 Test/measurement infrastructure: executes oracle/ only as the baseline.
 """
@@ -95,8 +95,8 @@ def oracle_conv(H, C, K, R, st, pd, nimg):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "cpu_configs_r01.json"))
-    ap.add_argument("--bench", default=os.path.join(ROOT, "profiles", "bench_r01.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "cpu_configs_r02.json"))
+    ap.add_argument("--bench", default=os.path.join(ROOT, "profiles", "bench_r02.json"))
     ap.add_argument("--ref-rows", type=int, default=64)
     args = ap.parse_args()
     coracle.build()
@@ -121,8 +121,9 @@ def main():
     for name, M, N, K in bench.BERT_GEMMS:
         e = {"flops": 2.0 * M * N * K, "reference": ref_gemm(M, N, K, 1, args.ref_rows),
              "oracle": oracle_gemm(M, N, K, 1, 256)}
-        if name in gpu.get("per_gemm", {}):
-            e["gpu_us"] = round(gpu["per_gemm"][name]["ms"] * 1e3, 2)
+        per_gemm = gpu.get("per_gemm") or gpu.get("bert_layer", {}).get("per_gemm", {})  # r01 / r02 line layout
+        if name in per_gemm:
+            e["gpu_us"] = round(per_gemm[name]["ms"] * 1e3, 2)
         cfg["C2_" + name] = e
 
     # C3: attention BMMs, batch*heads 192
@@ -157,6 +158,8 @@ def main():
         g = gpu.get("large_square_m_sharded", {}).get("sizes", {}).get(str(n))
         if g:
             e["gpu_us"] = round(e["flops"] / (g["tflops_aggregate"] * 1e12) * 1e6, 1)
+        elif str(n) in gpu.get("per_square", {}):  # r02 line: the headline squares, each timed alone
+            e["gpu_us"] = round(gpu["per_square"][str(n)]["ms"] * 1e3, 1)
         cfg["C5_%d" % n] = e
 
     for e in cfg.values():

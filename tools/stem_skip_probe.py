@@ -1,7 +1,10 @@
 """Stem kernel (csrc/stem_sm100.cu) with parts of its pipeline switched off
 (ALCOP_STEM_SKIP bits: 1 no MMA, 2 no window load, 4 no store), to find
 which stage sets the per-tile time.  Measurement only: skipped runs produce
-wrong outputs.  Usage: python tools/stem_skip_probe.py <skip> [batch]"""
+wrong outputs, so the switches exist only in a probe build:
+    ALCOP_BUILD_LIB=$PWD/paper_2210_16691_b200/libalcop_probe.so ALCOP_NVCC_EXTRA=-DSTEM_PROBE \
+        python -m paper_2210_16691_b200._build
+    ALCOP_LIB=paper_2210_16691_b200/libalcop_probe.so ALCOP_STEM_SKIP=<bits> python tools/stem_skip_probe.py <bits>"""
 import json
 import os
 import sys
