@@ -1045,8 +1045,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       const uint32_t b_group = !wide ? 0u : p.b_mn_major ? 2u * BK * 128u / 16u : 128u * kBoxK * 2u / 16u;
       const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
       const uint32_t idesc = p.idesc;
+#ifdef GEMM_TRACE
+      // measurement build only (-DGEMM_TRACE): CTA 0's MMA thread, clock64 per chunk
+      // (after the full wait, after the chunk's MMAs + commit were issued)
+      unsigned long long gtr[96];
+      int gtn = 0, gchunk = 0;
+#endif
       auto mma_seg = [&](int k, int cb, int ce) {
         const int acc = k % p.tacc;
+#ifdef GEMM_TRACE
+        if (blockIdx.x == 0 && gtn < 96) gtr[gtn++] = clock64() | (1ull << 62);  // tile start marker
+#endif
         mbar_wait(smem_u32(&tempty[acc]), ((k / p.tacc) & 1) ^ 1);  // both CTAs drained it
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
@@ -1054,6 +1063,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         for (int v = cb; v < ce; ++v) {
           const uint32_t slot = ca.slot, par = (ca.phase >> slot) & 1u;
           mbar_wait(smem_u32(&full[slot]), par);  // consumer_wait: both CTAs' halves landed
+#ifdef GEMM_TRACE
+          if (blockIdx.x == 0 && gtn < 96) gtr[gtn++] = clock64();
+#endif
           ca.phase ^= 1u << slot;
           if (lane == 0) chunkstamp<kDebug>(p, 1, ca.count++);
           tc_fence_after();
@@ -1069,6 +1081,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, idesc, acc_flag);
                 if constexpr (wide) umma_f16_ss_pair(d_tmem + 256, ad + a_off, bd + b_group + b_off, idesc, acc_flag);
               } umma_commit_pair_multicast(smem_u32(&empty[slot]), 0x3));  // consumer_release in both CTAs
+#ifdef GEMM_TRACE
+          if (blockIdx.x == 0 && gtn < 96) gtr[gtn++] = clock64();
+#endif
           ca.advance(p.sA);
         }
         ISSUE(umma_commit_pair_multicast(smem_u32(&tfull[acc]), 0x3));
@@ -1085,6 +1100,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         }
       };
       for_each_seg([&](int k, int, int cb, int ce) { mma_seg(k, cb, ce); });
+#ifdef GEMM_TRACE
+      if (blockIdx.x == 0 && lane == 0)
+        for (int i = 0; i < gtn; ++i) printf("T %d %llu\n", i, gtr[i]);
+#endif
     }
     __syncwarp();
   } else if (warp < 6) {
