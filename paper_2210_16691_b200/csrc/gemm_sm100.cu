@@ -1057,6 +1057,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         if (blockIdx.x == 0 && gtn < 96) gtr[gtn++] = clock64() | (1ull << 62);  // tile start marker
 #endif
         mbar_wait(smem_u32(&tempty[acc]), ((k / p.tacc) & 1) ^ 1);  // both CTAs drained it
+#ifdef GEMM_TRACE
+        if (blockIdx.x == 0 && gtn < 96) gtr[gtn++] = clock64() | (1ull << 61);  // accumulator free
+#endif
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.acc_stride;
         if (wrap) ca.slot = 0;
@@ -1201,6 +1204,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       };
       for (int c = 0; c < nchunks; ++c) {
         uint32_t w[32];
+        epistamp<kDebug>(p, warp, lane, c, 0);
         if constexpr (sizeof(OutT) == 4) {
           tmem_ld_32x32b_x32(t_addr + c * 32, w);
           tmem_wait_ld();
@@ -1225,6 +1229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
+        epistamp<kDebug>(p, warp, lane, c, 1);
         const uint32_t sbuf = stage_base + buf * 4096;
         if (lane == 0) {
           if (p.stage_bufs == 2)
@@ -1233,6 +1238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             bulk_wait_group_read<0>();
         }
         __syncwarp();
+        epistamp<kDebug>(p, warp, lane, c, 2);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
@@ -1243,6 +1249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           tma_store_3d(&tmC, sbuf, tc.nb * p.BN + c * kChunkCols, tc.mb * (2 * kTileM) + row0, tc.b);
           bulk_commit_group();
         }
+        epistamp<kDebug>(p, warp, lane, c, 3);
         buf ^= p.stage_bufs - 1;
       }
     });

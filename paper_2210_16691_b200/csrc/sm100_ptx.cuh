@@ -151,8 +151,15 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Arrive on a barrier in the peer CTA.  Release at CTA scope: the hand-offs
+// this carries (an accumulator drained by tcgen05.ld + wait::ld + the tcgen05
+// before-sync fence, a ring slot nobody wrote) publish no generic-proxy
+// writes to the peer.  The .release.cluster form compiles to MEMBAR.ALL.GPU,
+// which waits for the warp's outstanding global traffic: ~1000-1300 clk per
+// tile in the pair epilogue, the per-tile limit of short-K pair GEMMs
+// (tools/gemm_trace.py).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load whose completion is signalled on the pair leader's mbarrier
 __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
