@@ -87,6 +87,7 @@ struct StemKParams {
   int32_t CB, TB, nbc, sB;
   uint32_t b_slot_bytes;
   int32_t skip;                 // -DSTEM_PROBE builds only (ALCOP_STEM_SKIP): 1 no MMA, 2 no window load, 4 no store
+  int32_t bn_cta;               // filter rows staged per CTA: BN, or BN / 2 on a CTA pair (window modes)
 };
 
 template <typename OutT>
@@ -109,8 +110,7 @@ __device__ __forceinline__ uint32_t pack2s<__half>(uint32_t a, uint32_t b) {
 // clk per tile in the MMA warp).
 struct StemCursor {
   int n, p, qb;
-  __device__ __forceinline__ void start(const StemKParams& k) {
-    const int t = static_cast<int>(blockIdx.x);
+  __device__ __forceinline__ void start(const StemKParams& k, int t) {
     const int per_img = k.P * k.QB;
     n = t / per_img;
     const int rem = t - n * per_img;
@@ -128,10 +128,21 @@ struct StemCursor {
   }
 };
 
+// one tcgen05.mma: this CTA's (cta_group::1) or the CTA pair's (cta_group::2,
+// M = 256: A rows 0-127 from the leader's shared memory, 128-255 from the
+// peer's at the same address; B's N/2-row halves from each)
+template <bool kPair>
+__device__ __forceinline__ void stem_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (kPair)
+    ptx::umma_f16_ss_pair(d, a, b, idesc, acc);
+  else
+    ptx::umma_f16_ss(d, a, b, idesc, acc);
+}
+
 // Issue one tile's MMAs (one elected thread).  kR/kKS (pairs) or kR/kS
 // (window) fixed at compile time unroll the whole tile (immediate descriptor
 // offsets); 0 = run-time loops.
-template <int kMode, int kR, int kKS>
+template <int kMode, int kR, int kKS, bool kPair = false>
 __device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_tmem, uint32_t a0, uint32_t wsm) {
   using namespace ptx;
   if constexpr (kMode == 0) {
@@ -205,7 +216,7 @@ __device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_
     const uint64_t ad = make_smem_desc(a0, 16u, 1024u, kLayoutSW128);
     const uint64_t bd = make_smem_desc(wsm, 16u, 1024u, kLayoutSW128);
     const uint64_t a_row16 = (128u << p.lwp) >> 4;  // one window row
-    const uint64_t b_tap16 = (static_cast<uint32_t>(p.BN) * 128u) >> 4;
+    const uint64_t b_tap16 = (static_cast<uint32_t>(p.bn_cta) * 128u) >> 4;
     if constexpr (kR > 0) {
 #pragma unroll
       for (int r = 0; r < kR; ++r)
@@ -213,20 +224,29 @@ __device__ __forceinline__ void stem_tile_mmas(const StemKParams& p, uint32_t d_
         for (int s = 0; s < kKS; ++s)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            umma_f16_ss(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * kKS + s) * b_tap16 + 2 * u, p.idesc,
-                        (r > 0 || s > 0 || u > 0) ? 1u : 0u);
+            stem_mma<kPair>(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * kKS + s) * b_tap16 + 2 * u, p.idesc,
+                            (r > 0 || s > 0 || u > 0) ? 1u : 0u);
     } else {
       for (int r = 0; r < p.R; ++r)
         for (int s = 0; s < p.S; ++s)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            umma_f16_ss(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * p.S + s) * b_tap16 + 2 * u, p.idesc,
-                        (r > 0 || s > 0 || u > 0) ? 1u : 0u);
+            stem_mma<kPair>(d_tmem, ad + r * a_row16 + s * 8 + 2 * u, bd + (r * p.S + s) * b_tap16 + 2 * u, p.idesc,
+                            (r > 0 || s > 0 || u > 0) ? 1u : 0u);
     }
   }
 }
 
-template <typename OutT, int kMode, int kR, int kKS>
+// kPair (window modes 1, 2): a cluster of two CTAs computes a 256-pixel tile
+// with tcgen05.mma.cta_group::2 — each CTA loads the window of its own TR
+// output rows (tile rows 2u, 2u+1 of the pair tile u) and stages half of the
+// filter rows (bn_cta = BN / 2), so per 128 output pixels the MMAs read half
+// the filter bytes from each SM's shared memory (the port both the MMA operand
+// reads and the TMA fills share, ~128 B/clk).  Both CTAs' loads complete on
+// the leader's barriers, the leader's MMA warps issue for the pair, their
+// commits multicast the releases to both CTAs, and each CTA's epilogue drains
+// its own TMEM and hands the accumulator back on the leader's barrier.
+template <typename OutT, int kMode, int kR, int kKS, bool kPair = false>
 __global__ void __launch_bounds__(kStemThreads, 1)
     alcop_stem_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                            const __grid_constant__ CUtensorMap tmW, const StemKParams p) {
@@ -249,6 +269,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmY);
@@ -262,7 +284,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
       for (int i = 0; i < p.nacc; ++i) {
         mbar_init(smem_u32(&tfull[i]), 1);
-        mbar_init(smem_u32(&tempty[i]), 4);
+        mbar_init(smem_u32(&tempty[i]), kPair ? 8 : 4);  // 4 epilogue warps (x 2 CTAs)
       }
       for (int i = 0; i < p.sB; ++i) {
         mbar_init(smem_u32(&bfull[i]), 1);
@@ -271,9 +293,15 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       fence_barrier_init();
     }
     __syncwarp();
-    tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
-    tmem_relinquish();
+    if constexpr (kPair) {
+      tmem_alloc_pair(smem_u32(tmem_slot), p.tmem_cols);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
+      tmem_relinquish();
+    }
   }
+  if constexpr (kPair) cluster_sync();  // both CTAs' barriers initialised before any remote arrive / complete_tx
   // PDL: setup overlapped the previous kernel's tail; global data from here on
   grid_dependency_wait();
   grid_launch_dependents();
@@ -327,42 +355,59 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   } else if constexpr (kMode == 1) {
     // B operand per tap t = (r, s): BN filter rows x 64 channels (128 B),
     // 128B-swizzled K-major ([t][n][128 B], 16-byte chunk c of row n at c ^ (n & 7))
-    const int rows = p.R * p.S * p.BN;
+    // (a CTA pair: filters rank * bn_cta .. + bn_cta - 1 in each CTA)
+    const int rows = p.R * p.S * p.bn_cta;
     for (int idx = threadIdx.x; idx < rows * 8; idx += blockDim.x) {
       const int row = idx >> 3, c = idx & 7;
-      const int t = row / p.BN, n = row - t * p.BN;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.w + (static_cast<int64_t>(n) * p.R * p.S + t) * 64) + c);
+      const int t = row / p.bn_cta, n = row - t * p.bn_cta;
+      const int64_t f = static_cast<int64_t>(rank) * p.bn_cta + n;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.w + (f * p.R * p.S + t) * 64) + c);
       st_shared_v4(wsm + static_cast<uint32_t>(row) * 128u + ((c ^ (n & 7)) << 4), v.x, v.y, v.z, v.w);
     }
   }
   fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor cores
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // the leader's MMAs read the peer's filter half
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int grid = gridDim.x;
-  const int my_tiles = (p.num_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
+  // the work unit: a CTA, or a CTA pair (cluster) walking pair tiles
+  const int grid = kPair ? static_cast<int>(gridDim.x) >> 1 : static_cast<int>(gridDim.x);
+  const int unit = kPair ? static_cast<int>(blockIdx.x) >> 1 : static_cast<int>(blockIdx.x);
+  const int my_tiles = (p.num_tiles - unit + grid - 1) / grid;
 
   if (warp == 0) {
     // ======================= producer (TMA) =======================
     // the whole warp walks the loop (coordinates stay on the uniform
     // datapath), one elected lane issues
+    // (a CTA pair: each CTA loads its own tile row's window and filter half,
+    // completing on the leader's barriers, which the leader arms with both
+    // CTAs' bytes; each waits on its own empty barriers, which the leader's
+    // commits multicast)
     int slot = 0, bslot = 0;
     uint32_t phase = 0, bphase = 0;
     StemCursor cur;
-    cur.start(p);
+    cur.start(p, unit);
     for (int tl = 0; tl < my_tiles; ++tl, cur.advance(p)) {
+      const int prow = kPair ? 2 * cur.p + static_cast<int>(rank) : cur.p;  // this CTA's tile row
       for (int cb = 0; cb < (kMode == 2 ? p.CB : 1); ++cb) {
         mbar_wait(smem_u32(&empty[slot]), ((phase >> slot) & 1u) ^ 1u);  // producer_acquire (window)
         phase ^= 1u << slot;
         if (elect_one()) {
           if (p.skip & 2) {
-            mbar_arrive(smem_u32(&full[slot]));
+            if (leader) mbar_arrive(smem_u32(&full[slot]));
+          } else if constexpr (kPair) {
+            const uint32_t fb = smem_u32(&full[slot]);
+            if (leader) mbar_arrive_expect_tx(fb, 2 * p.box_bytes);        // producer_commit (both windows)
+            tma_load_4d_pair(ring + slot * p.slot_bytes, &tmX, mapa_shared(fb, 0), cb * 64, cur.qb * 16 + p.blk_off,
+                             prow * p.row_step - p.ph, cur.n);
           } else {
             mbar_arrive_expect_tx(smem_u32(&full[slot]), p.box_bytes);      // producer_commit
             tma_load_4d(ring + slot * p.slot_bytes, &tmX, smem_u32(&full[slot]), cb * 64, cur.qb * 16 + p.blk_off,
-                        cur.p * p.row_step - p.ph, cur.n);
+                        prow * p.row_step - p.ph, cur.n);
           }
         }
         __syncwarp();
@@ -373,10 +418,16 @@ __global__ void __launch_bounds__(kStemThreads, 1)
             mbar_wait(smem_u32(&bempty[bslot]), ((bphase >> bslot) & 1u) ^ 1u);
             bphase ^= 1u << bslot;
             if (elect_one()) {
-              mbar_arrive_expect_tx(smem_u32(&bfull[bslot]), p.TB * p.BN * 128u);
-              for (int t = 0; t < p.TB; ++t)
-                tma_load_3d(ringB + bslot * p.b_slot_bytes + t * p.BN * 128u, &tmW, smem_u32(&bfull[bslot]),
-                            (j * p.TB + t) * p.CB * 64 + cb * 64, 0, 0);
+              const uint32_t bb = smem_u32(&bfull[bslot]);
+              if (leader) mbar_arrive_expect_tx(bb, p.TB * p.BN * 128u);  // both halves: TB x BN rows
+              for (int t = 0; t < p.TB; ++t) {
+                const uint32_t dst = ringB + bslot * p.b_slot_bytes + t * p.bn_cta * 128u;
+                const int col = (j * p.TB + t) * p.CB * 64 + cb * 64;
+                if constexpr (kPair)
+                  tma_load_3d_pair(dst, &tmW, mapa_shared(bb, 0), col, static_cast<int>(rank) * p.bn_cta, 0);
+                else
+                  tma_load_3d(dst, &tmW, bb, col, 0, 0);
+              }
             }
             __syncwarp();
             bslot = bslot + 1 == p.sB ? 0 : bslot + 1;
@@ -395,13 +446,22 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     // tcgen05.commit tracks only the MMAs it issued.
     const int first = warp == 6 ? 1 : 0;
     const int step = p.dual ? 2 : 1;
-    if constexpr (kMode == 2) {
+    // a commit releasing a barrier in this CTA, or in both CTAs of the pair
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (kPair)
+        umma_commit_pair_multicast(smem_u32(bar), 0x3);
+      else
+        umma_commit(smem_u32(bar));
+    };
+    if (kPair && !leader) {
+      // the peer CTA issues nothing: the leader's MMAs cover both
+    } else if constexpr (kMode == 2) {
       // one issuing warp (the rings carry several chunks per tile in order)
       if (warp == 1) {
         int slot = 0, bslot = 0, acc = 0;
         uint32_t phase = 0, bphase = 0, acc_phase = 0;
         const uint64_t a_row16 = (128u << p.lwp) >> 4;
-        const uint64_t b_tap16 = (static_cast<uint32_t>(p.BN) * 128u) >> 4;
+        const uint64_t b_tap16 = (static_cast<uint32_t>(p.bn_cta) * 128u) >> 4;
         for (int tl = 0; tl < my_tiles; ++tl) {
           mbar_wait(smem_u32(&tempty[acc]), ((acc_phase >> acc) & 1u) ^ 1u);
           acc_phase ^= 1u << acc;
@@ -422,16 +482,16 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                 for (int t = 0; t < p.TB; ++t) {
 #pragma unroll
                   for (int u = 0; u < 4; ++u)
-                    umma_f16_ss(d_tmem, ad + rr * a_row16 + ss * 8 + 2 * u, bd + t * b_tap16 + 2 * u, p.idesc,
-                                (cb > 0 || j > 0 || t > 0 || u > 0) ? 1u : 0u);
+                    stem_mma<kPair>(d_tmem, ad + rr * a_row16 + ss * 8 + 2 * u, bd + t * b_tap16 + 2 * u, p.idesc,
+                                    (cb > 0 || j > 0 || t > 0 || u > 0) ? 1u : 0u);
                   if (++ss == p.S) {
                     ss = 0;
                     ++rr;
                   }
                 }
-                umma_commit(smem_u32(&bempty[bslot]));                     // consumer_release (filter chunk)
-                if (j == p.nbc - 1) umma_commit(smem_u32(&empty[slot]));   // consumer_release (window)
-                if (j == p.nbc - 1 && cb == p.CB - 1) umma_commit(smem_u32(&tfull[acc]));
+                commit(&bempty[bslot]);                     // consumer_release (filter chunk)
+                if (j == p.nbc - 1) commit(&empty[slot]);   // consumer_release (window)
+                if (j == p.nbc - 1 && cb == p.CB - 1) commit(&tfull[acc]);
               }
               __syncwarp();
               sx += p.TB;
@@ -459,10 +519,11 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           if (!(p.skip & 1))
-            stem_tile_mmas<kMode, kR, kKS>(p, tmem_base + acc * p.acc_stride,
-                                           ring + slot * p.slot_bytes + static_cast<uint32_t>(p.shift) * 16u, wsm);
-          umma_commit(smem_u32(&empty[slot]));  // consumer_release: the window slot is free once these retire
-          umma_commit(smem_u32(&tfull[acc]));   // accumulator ready
+            stem_tile_mmas<kMode, kR, kKS, kPair>(p, tmem_base + acc * p.acc_stride,
+                                                  ring + slot * p.slot_bytes + static_cast<uint32_t>(p.shift) * 16u,
+                                                  wsm);
+          commit(&empty[slot]);  // consumer_release: the window slot is free once these retire
+          commit(&tfull[acc]);   // accumulator ready
         }
         __syncwarp();
         slot += step;
@@ -490,7 +551,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     int acc = first % p.nacc;
     uint32_t acc_phase = 0;
     StemCursor cur;
-    cur.start(p);
+    cur.start(p, unit);
     if (first) cur.advance(p);
     // this warp's first output (column, row-in-tile) of the tile
     const int m0 = q * 32;
@@ -507,7 +568,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       for (int ic = 0; ic < kSub * nchunks; ++ic) {
         const int k = kSub == 1 ? 0 : ic / nchunks, c = kSub == 1 ? ic : ic - k * nchunks;
         const uint32_t ta = t_addr + k * p.BN;
-        const int op = kMode == 0 ? cur.p : kMode == 3 ? cur.p * 4 + k : cur.p * p.row_step + row0;  // output row
+        const int prow = kPair ? 2 * cur.p + static_cast<int>(rank) : cur.p;  // this CTA's tile row
+        const int op = kMode == 0 ? prow : kMode == 3 ? prow * 4 + k : prow * p.row_step + row0;  // output row
         const bool rows_live = oq < p.Q && op < p.Pout;
         uint32_t w[32];
         if constexpr (sizeof(OutT) == 4) {
@@ -527,7 +589,12 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         if (ic == kSub * nchunks - 1) {  // this warp's TMEM reads of the accumulator are done
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+          if (lane == 0) {
+            if constexpr (kPair)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's barrier
+            else
+              mbar_arrive(smem_u32(&tempty[acc]));
+          }
         }
         if (!rows_live || (p.skip & 4)) continue;  // tile rows past the image (the M=128 tile overhangs it)
         const uint32_t sbuf = stage_base + buf * kStemStaging;
@@ -558,20 +625,29 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // no CTA leaves while its peer may still signal it or read its shared memory
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+    if constexpr (kPair)
+      tmem_dealloc_pair(tmem_base, p.tmem_cols);
+    else
+      tmem_dealloc(tmem_base, p.tmem_cols);
   }
 }
 
 template <typename OutT>
 int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const CUtensorMap& tw, const StemKParams& kp,
-                      int mode, int grid, int smem, cudaStream_t st) {
-  auto kern = mode == 3   ? alcop_stem_conv_kernel<OutT, 3, 7, 2>
+                      int mode, bool pair, int grid, int smem, cudaStream_t st) {
+  const bool r3 = kp.R == 3 && kp.S == 3;
+  auto kern = pair ? (mode == 2 ? alcop_stem_conv_kernel<OutT, 2, 0, 0, true>
+                      : r3      ? alcop_stem_conv_kernel<OutT, 1, 3, 3, true>
+                                : alcop_stem_conv_kernel<OutT, 1, 0, 0, true>)
+              : mode == 3 ? alcop_stem_conv_kernel<OutT, 3, 7, 2>
               : mode == 2 ? alcop_stem_conv_kernel<OutT, 2, 0, 0>
-              : mode == 1 ? (kp.R == 3 && kp.S == 3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3>
-                                                    : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
+              : mode == 1 ? (r3 ? alcop_stem_conv_kernel<OutT, 1, 3, 3> : alcop_stem_conv_kernel<OutT, 1, 0, 0>)
                           : (kp.R == 7 && kp.T2 == 4 ? alcop_stem_conv_kernel<OutT, 0, 7, 2>
                                                      : alcop_stem_conv_kernel<OutT, 0, 0, 0>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -581,11 +657,15 @@ int launch_stem_typed(const CUtensorMap& tx, const CUtensorMap& ty, const CUtens
   cfg.blockDim = dim3(kStemThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // CTA pairs (window modes, cta_group 2)
+  attr[1].val.clusterDim.x = pair ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pair ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, kern, tx, ty, tw, kp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
@@ -697,9 +777,18 @@ StemGeometry stem_pairs_geometry(const alcop_conv_desc& d) {
   return g;
 }
 
+// filter rows staged per CTA: all K, or K / 2 on a CTA pair
+static int64_t filter_rows_cta(const alcop_conv_desc& d, const alcop_schedule& s) {
+  return s.cta_group == 2 ? d.K / 2 : d.K;
+}
 // streamed filter: taps per filter chunk (tileK = 64 x taps), ring of n_stage_smem_B chunks
 static int64_t stream_b_slot_bytes(const alcop_conv_desc& d, const alcop_schedule& s) {
-  return stem_mode(d) == 2 ? (s.tileK / 64) * d.K * 128 : 0;
+  return stem_mode(d) == 2 ? (s.tileK / 64) * filter_rows_cta(d, s) * 128 : 0;
+}
+// the resident filter (window mode 1): this CTA's rows of every tap
+static int64_t resident_filter_bytes(const alcop_conv_desc& d, const alcop_schedule& s, const StemGeometry& g) {
+  if (stem_mode(d) != 1) return g.wbytes;
+  return (d.R * d.S * filter_rows_cta(d, s) * 128 + 1023) / 1024 * 1024;
 }
 static bool stem_dual(const alcop_conv_desc& d, const alcop_schedule& s) {
   return stem_mode(d) != 2 && s.n_stage_smem_A % 2 == 0 && s.n_stage_inner % 2 == 0;
@@ -711,8 +800,8 @@ static int64_t stem_smem_bytes_bufs(const alcop_conv_desc& d, const alcop_schedu
   const int64_t sB = streamed ? s.n_stage_smem_B : 0;
   const int64_t bars = 8 * (2 * s.n_stage_smem_A + 2 * s.n_stage_inner + 2 * sB) + 16;
   const int warps = stem_dual(d, s) ? 8 : 4;
-  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + sB * stream_b_slot_bytes(d, s) + g.wbytes +
-         warps * bufs * kStemStaging + bars;
+  return 1024 + s.n_stage_smem_A * static_cast<int64_t>(g.slot_bytes) + sB * stream_b_slot_bytes(d, s) +
+         resident_filter_bytes(d, s, g) + warps * bufs * kStemStaging + bars;
 }
 
 // two staging buffers per epilogue warp when they fit, else one
@@ -729,13 +818,18 @@ int validate_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s) {
   if (mode < 0)
     return set_error(ALCOP_ERR_CONFIG, "Unsupported", "not a shape of the resident-filter / window conv kernel");
   const bool tk_ok = s.tileK == 64 || (mode == 2 && s.tileK == 64 * d.S);
-  if (s.tileM != kTileM || !tk_ok || s.tileN != d.K)
+  const bool window = mode == 1 || mode == 2;
+  if (s.cta_group != 1 && !(s.cta_group == 2 && window && d.K % 32 == 0))
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the window conv kernel's tile is 128 output pixels x all K filters (tileM 128, tileN = K, "
-                     "tileK 64; streamed filter: tileK 64 or 64 x S = taps per filter chunk)");
-  if (s.cta_group != 1 || s.stream_k != 0 || s.mode != ALCOP_MODE_FUSED)
+                     "the window conv kernel runs one CTA per tile, or a CTA pair per 256-pixel tile in the window "
+                     "modes (cta_group 2, K % 32 == 0)");
+  if (s.tileM != kTileM * s.cta_group || !tk_ok || s.tileN != d.K)
     return set_error(ALCOP_ERR_CONFIG, "BadSchedule",
-                     "the window conv kernel runs one CTA per tile (FUSED, cta_group 1)");
+                     "the window conv kernel's tile is 128 output pixels (256 on a CTA pair) x all K filters "
+                     "(tileM 128 x cta_group, tileN = K, tileK 64; streamed filter: tileK 64 or 64 x S = taps per "
+                     "filter chunk)");
+  if (s.stream_k != 0 || s.mode != ALCOP_MODE_FUSED)
+    return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "the window conv kernel runs whole tiles (FUSED, no stream-K)");
   if (mode == 2) {
     if (s.n_stage_smem_A < 1 || s.n_stage_smem_A > 4 || s.n_stage_smem_B < 1 || s.n_stage_smem_B > kMaxStages)
       return set_error(ALCOP_ERR_CONFIG, "BadSchedule", "streamed filter: window stages 1..4, filter stages 1..16");
@@ -798,12 +892,15 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   if (rc) return rc;
   // streamed filter: w viewed as [K rows, R*S*C columns]; box = 64 channels of
   // one tap x all K filters (128B-swizzled, K-major B)
+  // (a CTA pair: each CTA's box is its K / 2 filters)
+  const bool pair = s.cta_group == 2;
+  const int64_t bn_cta = filter_rows_cta(d, s);
   CUtensorMap tw = tx;
   if (mode == 2) {
     const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(d.R * d.S * d.C), static_cast<cuuint64_t>(d.K), 1};
     const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(d.R * d.S * d.C * 2),
                                 static_cast<cuuint64_t>(d.K * d.R * d.S * d.C * 2)};
-    const cuuint32_t wbox[3] = {64, static_cast<cuuint32_t>(d.K), 1};
+    const cuuint32_t wbox[3] = {64, static_cast<cuuint32_t>(bn_cta), 1};
     rc = encode_tiled_map(&tw, dt, wt, 3, wdims, wstr, wbox, one, CU_TENSOR_MAP_SWIZZLE_128B, "w (window)");
     if (rc) return rc;
   }
@@ -822,6 +919,7 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   StemKParams kp{};
   kp.Pout = static_cast<int32_t>(g.P);
   kp.P = static_cast<int32_t>(mode == 0 ? g.P : (g.P + g.TR - 1) / g.TR);  // tile rows per image
+  if (pair) kp.P = (kp.P + 1) / 2;  // pair tiles: tile rows 2u (leader) and 2u + 1 (peer)
   kp.Q = static_cast<int32_t>(g.Q);
   kp.QB = static_cast<int32_t>(g.QB);
   const int64_t tiles = d.N * static_cast<int64_t>(kp.P) * g.QB;
@@ -840,10 +938,12 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   kp.row_bytes = g.row_bytes;
   kp.slot_bytes = g.slot_bytes;
   kp.box_bytes = g.box_bytes;
-  kp.wbytes = g.wbytes;
+  kp.wbytes = static_cast<uint32_t>(resident_filter_bytes(d, s, g));
+  kp.bn_cta = static_cast<int32_t>(bn_cta);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols((mode == 3 ? 4 : 1) * d.K));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.nacc));
-  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM, static_cast<uint32_t>(d.K));
+  kp.idesc = ptx::make_idesc_f16(d.in_dtype == ALCOP_BF16 ? 1u : 0u, 0u, kTileM * (pair ? 2u : 1u),
+                                 static_cast<uint32_t>(d.K));
   kp.w = static_cast<const uint16_t*>(wt);
   kp.stage_bufs = stem_staging_bufs(d, s);
   int lwp = 0;
@@ -870,7 +970,9 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   }
   const int sms = device_sm_count();
   if (sms <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
-  int grid = s.num_ctas > 0 ? s.num_ctas : sms;
+  // work units (CTAs, or CTA pairs) walking the tiles
+  int grid = (s.num_ctas > 0 ? s.num_ctas : sms) / (pair ? 2 : 1);
+  if (grid < 1) grid = 1;
   if (grid > kp.num_tiles) grid = kp.num_tiles;
   kp.dn = grid / (kp.P * kp.QB);
   kp.dp = (grid - kp.dn * kp.P * kp.QB) / kp.QB;
@@ -885,10 +987,11 @@ int launch_conv2d_stem_pairs(const alcop_conv_desc& d, const alcop_schedule& s, 
   }
   const int smem = static_cast<int>(stem_pairs_smem_bytes(d, s));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int ctas = grid * (pair ? 2 : 1);
   switch (d.out_dtype) {
-    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, tw, kp, mode, grid, smem, st);
-    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, tw, kp, mode, grid, smem, st);
-    default: return launch_stem_typed<__half>(tx, ty, tw, kp, mode, grid, smem, st);
+    case ALCOP_F32: return launch_stem_typed<float>(tx, ty, tw, kp, mode, pair, ctas, smem, st);
+    case ALCOP_BF16: return launch_stem_typed<__nv_bfloat16>(tx, ty, tw, kp, mode, pair, ctas, smem, st);
+    default: return launch_stem_typed<__half>(tx, ty, tw, kp, mode, pair, ctas, smem, st);
   }
 }
 

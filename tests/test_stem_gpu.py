@@ -220,3 +220,58 @@ def test_window_stream_exact(alcop, case, out_dt):
             assert "SmemCapacity" in str(e) or "BadSchedule" in str(e), (s, e)  # a ring too deep for this K
             continue
         _assert_equal(Y.cpu(), want, "streamed %s" % s)
+
+
+# ----------------------------------------------------------------------------
+# Window modes on CTA pairs (cta_group 2): a 256-pixel tile = the two CTAs'
+# TR-row windows, one tcgen05.mma.cta_group::2 (M = 256) per k-step issued by
+# the leader, each CTA staging half of the filter rows (resident or streamed).
+# Odd tile-row counts leave the last pair's peer rows outside the image.
+@pytest.mark.parametrize("case", WINDOW_CASES, ids=lambda c: "x".join(map(str, c[:7])) + "_p%d%d" % c[8])
+def test_window_pairs_exact(alcop, case):
+    X, Wt, ref = _inputs(case, 95)
+    _, _, _, _, K, _, _, st, pd = case
+    ran = 0
+    for out_dt in ("f32", "bf16"):
+        odt = torch.float32 if out_dt == "f32" else torch.bfloat16
+        want = torch.from_numpy(ref).to(odt)
+        for stages, inner in ((2, 2), (3, 1), (4, 4), (1, 2)):
+            s = alcop.make_schedule(tileN=K, tileK=64, n_stage=stages, n_stage_inner=inner, mode=1, cta_group=2)
+            try:
+                Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=odt)
+            except alcop.AlcopError as e:
+                assert "SmemCapacity" in str(e) or "TmemCapacity" in str(e), (s, e)
+                continue
+            ran += 1
+            _assert_equal(Y.cpu(), want, "window pair %s" % s)
+    assert ran >= 4
+
+
+def test_window_pairs_small_grid(alcop):
+    """Two clusters walking every pair tile of three images (the cursor's
+    carries across images), resident filter and streamed filter."""
+    for case, sched in (((3, 28, 28, 64, 64, 3, 3, (1, 1), (1, 1)),
+                         dict(tileN=64, tileK=64, n_stage=2, n_stage_inner=2)),
+                        ((3, 28, 28, 128, 128, 3, 3, (1, 1), (1, 1)),
+                         dict(tileN=128, tileK=64, n_stage=2, n_stage_B=3, n_stage_inner=2))):
+        X, Wt, ref = _inputs(case, 97)
+        s = alcop.make_schedule(cta_group=2, **sched)
+        s.num_ctas = 4
+        Y = alcop.conv2d(X, Wt, (1, 1), (1, 1), sched=s, out_dtype=torch.float32)
+        _assert_equal(Y.cpu(), torch.from_numpy(ref), "pair grid 4 %s" % (case[:7],))
+
+
+@pytest.mark.parametrize("case", STREAM_CASES, ids=lambda c: "x".join(map(str, c[:7])))
+def test_window_stream_pairs_exact(alcop, case):
+    X, Wt, ref = _inputs(case, 103)
+    _, _, _, C, K, R, S, st, pd = case
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    # unequal A / B rings or an S-tap filter chunk: only the streamed-filter kernel accepts them
+    for tk, sa, sb in ((64, 1, 2), (64 * S, 2, 1), (64, 2, 4), (64 * S, 1, 2)):
+        s = alcop.make_schedule(tileN=K, tileK=tk, n_stage=sa, n_stage_B=sb, n_stage_inner=2, cta_group=2)
+        try:
+            Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=torch.bfloat16)
+        except alcop.AlcopError as e:
+            assert "SmemCapacity" in str(e), (s, e)
+            continue
+        _assert_equal(Y.cpu(), want, "streamed pair %s" % s)
