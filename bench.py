@@ -960,12 +960,14 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
         # the resident-filter kernels: ring depth x accumulators; 1x1 stride-1 layers: CTA-pair tiles too)
         gview = workloads.conv_gemm_desc(alcop, L, nloc)
         cands = []
+        # (the window modes also on CTA pairs: 256-pixel tiles, half the filter per SM)
         if L.stem or L.window:
-            cands = [alcop.make_schedule(tileN=L.K, tileK=64, n_stage=stg, n_stage_inner=inn)
-                     for stg in (8, 6, 4, 3, 2) for inn in (1, 2, 4)]
+            cands = [alcop.make_schedule(tileN=L.K, tileK=64, n_stage=stg, n_stage_inner=inn, cta_group=cg)
+                     for cg in ((1,) if L.stem else (1, 2)) for stg in (8, 6, 4, 3, 2) for inn in (1, 2, 3, 4)]
         if L.stream:  # window + streamed filter: taps per filter chunk x window ring x filter ring
-            cands = [alcop.make_schedule(tileN=L.K, tileK=tk, n_stage=sa, n_stage_B=sb, n_stage_inner=2)
-                     for tk in (64, 64 * L.R) for sa in (1, 2, 3) for sb in (2, 3, 4, 6)]
+            cands = [alcop.make_schedule(tileN=L.K, tileK=tk, n_stage=sa, n_stage_B=sb, n_stage_inner=2,
+                                         cta_group=cg)
+                     for cg in (1, 2) for tk in (64, 64 * L.R) for sa in (1, 2, 3, 4) for sb in (2, 3, 4, 6)]
         if not (L.stem or L.window):  # + the implicit-GEMM (im2col) kernel's space
             for tn in (64, 128, 192, 256):
                 pairs = L.gemm or (L.Cs % 64 == 0 and not L.halo and L.gemm_k() >= 512)  # CTA pairs in the space

@@ -268,13 +268,21 @@ extern "C" int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* h
 //   with one accumulator the epilogue serialises behind the MMAs;
 //   T_main = pipeline_latency(T_load, T_use, tiles per SM, n_stage, 1)
 // — the paper's stage formula with the window as the pipelined chunk.
+//   Window modes also pay the shared-memory port (~128 B/clk per SM, shared by
+//   the MMAs' operand reads and the TMA fills; tools/stem_skip_probe.py): per
+//   k-step 4 KB of A plus this SM's B rows (K, or K / 2 on a CTA pair, which
+//   is what the pair buys).
 static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, const alcop_schedule& s,
                               const alcop_hw& hw) {
+  constexpr double kSmemPort = 128.0;  // bytes / clk / SM
   const bool window = g.WP > 0;
   const bool streamed = window && g.wbytes == 0;  // window with the filter streamed per channel block
   const int64_t tr = g.TR > 0 ? g.TR : 1;          // output rows per tile (stem, four-row mode: 4)
+  const double cg = s.cta_group == 2 ? 2.0 : 1.0;
+  const double bn_cta = d.K / cg;                  // filter rows each SM stages and reads
   const double tiles = static_cast<double>(d.N * ((g.P + tr - 1) / tr) * g.QB);
-  const double per_sm = std::ceil(tiles / hw.numSM);
+  // 128-pixel tiles per SM (a pair walks pair tiles: its two SMs one half each)
+  const double per_sm = std::ceil(tiles / cg / (hw.numSM / cg));
   const double ob = d.out_dtype == ALCOP_F32 ? 4.0 : 2.0;
   const double mma_k = (128.0 * d.K * 16 * 2) / hw.throughputSM;  // one k-step of 16
   const double out_bytes = static_cast<double>(d.N * g.P * g.Q) * d.K * ob;
@@ -287,8 +295,9 @@ static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, c
     // chunks (the A ring one window per channel block)
     const double tb = static_cast<double>(s.tileK / 64);
     const double chunks = static_cast<double>(d.C / 64) * (d.R * d.S) / tb;
-    const double use = std::max({tb * 4 * mma_k, (tb * d.K * 128 + g.box_bytes * tb / (d.R * d.S)) / hw.bwSmem,
-                                 hbm_tile / chunks, hw.tIssue});
+    const double fill = tb * bn_cta * 128 + g.box_bytes * tb / (d.R * d.S);
+    const double port = (tb * 4 * (4096.0 + bn_cta * 32) + fill) / kSmemPort;
+    const double use = std::max({tb * 4 * mma_k, fill / hw.bwSmem, port, hbm_tile / chunks, hw.tIssue});
     double main = model::pipeline_latency(hw.latLLCRead, use, static_cast<int64_t>(per_sm * chunks),
                                           s.n_stage_smem_B, 1);
     if (s.n_stage_smem_A == 1) main += per_sm * (d.C / 64) * 0.5 * hw.latLLCRead;  // window refill bubble
@@ -299,7 +308,8 @@ static double stem_pairs_time(const alcop_conv_desc& d, const StemGeometry& g, c
       window ? static_cast<double>(d.R * d.S * 4) : static_cast<double>(tr * d.R * (g.T2 / 2));
   const double mma = ksteps * mma_k;
   const double fill = static_cast<double>(g.box_bytes) / hw.bwSmem;
-  double use = std::max({mma, fill, hbm_tile, hw.tIssue});
+  const double port = window ? (ksteps * (4096.0 + bn_cta * 32) + g.box_bytes) / kSmemPort : 0.0;
+  double use = std::max({mma, fill, port, hbm_tile, hw.tIssue});
   if (s.n_stage_inner == 1) use = std::max(use, mma + epi);
   // pair modes: one issuing warp serialises its per-tile barrier waits and
   // commits (~500 clk, tools/stem_trace.py) with the tile's MMAs; two (even
@@ -321,6 +331,7 @@ static int choose_stem_pairs(const alcop_conv_desc& d, const alcop_hw& hw, alcop
   const bool streamed = d.C != 4 && window_stream_applicable(d);
   double best = 1e300;
   bool found = false;
+  for (int cg = 1; cg <= (d.C == 4 ? 1 : 2); ++cg)
   for (int tk : {64, static_cast<int>(64 * d.S)}) {
     if (tk != 64 && !streamed) continue;
     for (int sa = streamed ? 4 : 8; sa >= 1; --sa)
@@ -328,6 +339,8 @@ static int choose_stem_pairs(const alcop_conv_desc& d, const alcop_hw& hw, alcop
         for (int inner = 4; inner >= 1; --inner) {
           alcop_schedule s;
           alcop_schedule_default(&s);
+          s.cta_group = cg;
+          s.tileM = 128 * cg;
           s.tileN = static_cast<int32_t>(d.K);
           s.tileK = tk;
           s.n_stage_smem_A = sa;

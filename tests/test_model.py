@@ -140,7 +140,8 @@ def test_power_regime_picks_the_wide_pair_tile_for_squares(alcop):
 def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
     """alcop_choose_conv_schedule (C ABI) returns a launchable conv schedule
     for all 23 ResNet-50 layers: the GEMM space for 1x1 stride-1 layers, the
-    window kernels' spaces (stem, window, streamed filter), else the im2col
+    window kernels' spaces (stem; window and streamed filter, CTA pairs
+    included), else the im2col
     kernel's (tileK 64, equal stages, CTA pairs only for C % 64 == 0 and
     K >= 512, within the 4-epilogue-warp shared memory)."""
     from paper_2210_16691_b200 import workloads as W
@@ -154,13 +155,14 @@ def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
             assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448
             continue
         if L.stream:  # window + streamed filter: tileK = 64 x taps per filter chunk, own A / B rings
-            assert s.tileN == L.K and s.tileK in (64, 64 * L.R) and s.cta_group == 1, s
+            assert s.tileN == L.K and s.tileK in (64, 64 * L.R) and s.tileM == 128 * s.cta_group, s
             continue
         assert s.tileK == 64 and s.n_stage_smem_A == s.n_stage_smem_B, L.name
-        assert s.cta_group == 1 or (L.Cs % 64 == 0 and L.gemm_k() >= 512), L.name  # pairs: 64-ch im2col, K >= 512
-        if L.stem or L.window:  # the resident-filter kernel: tile = 128 output pixels x all K filters
-            assert s.tileN == L.K and 1 <= s.n_stage_inner <= 8, s
+        if L.stem or L.window:  # the window kernel: tile = 128 output pixels (256 on a CTA pair) x all K filters
+            assert s.tileN == L.K and 1 <= s.n_stage_inner <= 8 and s.tileM == 128 * s.cta_group, s
+            assert s.cta_group == 1 or not L.stem, s  # the stem modes run one CTA per tile
             continue
+        assert s.cta_group == 1 or (L.Cs % 64 == 0 and L.gemm_k() >= 512), L.name  # pairs: 64-ch im2col, K >= 512
         g = W.conv_gemm_desc(alcop, L, 256)
         alcop.validate(g, s)
         assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448
