@@ -296,6 +296,9 @@ int alcop_set_stream_k_workspace(void* workspace, int64_t bytes);
  *    chunk, n_stage_smem_A = window ring 1..4, n_stage_smem_B = filter ring,
  *    n_stage_inner 1..2): window mode with the filter streamed through its
  *    own ring;
+ *    both window modes also run on CTA pairs (cta_group 2, tileM 256,
+ *    K % 32 == 0): a 256-pixel tile = the two CTAs' windows, each CTA staging
+ *    half of the filter rows;
  *  - 1x1, stride 1, no padding: the GEMM kernels ([N*H*W, C] x [K, C]^T),
  *    any GEMM schedule incl. CTA pairs;
  *  - otherwise C % 8 == 0: the implicit-GEMM kernel with TMA im2col loads
