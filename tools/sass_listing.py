@@ -35,14 +35,18 @@ PRODUCTION = [
     ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 3, false, 4>",
      "implicit-GEMM conv, stem (ResNet-50 conv1, halo-padded NHWC8)"),
     ("alcop_chain_gemm_kernel<__nv_bfloat16, 64>", "several GEMMs in one persistent launch (alcop_gemm_chain)"),
-    ("alcop_stem_conv_kernel<__nv_bfloat16, 3, 7, 2>",
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 3, 7, 2, false>",
      "resident-filter conv, pixel pairs, four output rows per tile: the ResNet-50 stem (C = 4, 7x7/2)"),
-    ("alcop_stem_conv_kernel<__nv_bfloat16, 0, 7, 2>",
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 0, 7, 2, false>",
      "resident-filter conv, pixel-pair mode, one output row per tile (other C = 4 stride-2 shapes)"),
-    ("alcop_stem_conv_kernel<__nv_bfloat16, 1, 3, 3>",
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 1, 3, 3, false>",
      "resident-filter conv, window mode: 3x3 stride-1 C = 64 (ResNet-50 l1 3x3)"),
-    ("alcop_stem_conv_kernel<__nv_bfloat16, 2, 0, 0>",
-     "window conv with a streamed filter (separate A / B rings): C > 64, K <= 128 (ResNet-50 l2 3x3)"),
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 2, 0, 0, false>",
+     "window conv with a streamed filter (separate A / B rings): C > 64, K <= 128"),
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 1, 3, 3, true>",
+     "window conv on CTA pairs (cta_group::2, M = 256): ResNet-50 l1 3x3"),
+    ("alcop_stem_conv_kernel<__nv_bfloat16, 2, 0, 0, true>",
+     "window conv, streamed filter, on CTA pairs: ResNet-50 l2 3x3"),
 ]
 KEYS = ("UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UTMAPF", "UTMACMDFLUSH", "SYNCS", "UTCATOMSWS",
         "UTCBAR", "ELECT", "FENCE", "ACQBULK", "MEMBAR")
