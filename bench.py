@@ -970,7 +970,7 @@ def conv_block(args, torch, alcop, dev, rank, world, ranks, parity, attainable):
                      for cg in (1, 2) for tk in (64, 64 * L.R) for sa in (1, 2, 3, 4) for sb in (2, 3, 4, 6)]
         if not (L.stem or L.window):  # + the implicit-GEMM (im2col) kernel's space
             for tn in (64, 128, 192, 256):
-                pairs = L.gemm or (L.Cs % 64 == 0 and not L.halo and L.gemm_k() >= 512)  # CTA pairs in the space
+                pairs = L.gemm or (L.Cs % 64 == 0 and not L.halo)  # CTA pairs in the space
                 for cg in ((1, 2) if pairs else (1,)):
                     if cg == 2 and tn == 64:
                         continue

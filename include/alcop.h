@@ -352,7 +352,8 @@ int alcop_choose_schedule(const alcop_gemm_desc* w, const alcop_hw* hw, alcop_sc
  * own per-tile model: MMA, window fill, the SM's share of the HBM stream,
  * pipeline_latency over the windows), the GEMM space for 1x1 stride-1 convs,
  * else the implicit-GEMM kernel's space (tileK 64, equal stages; CTA pairs
- * when C % 64 == 0 and R*S*C >= 512) ranked on the conv's GEMM view. */
+ * when C % 64 == 0) ranked on the conv's GEMM view; the window modes'
+ * space includes CTA pairs. */
 int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_hw* hw, alcop_schedule* out);
 
 /* One measured candidate of the model-assisted tuner. */

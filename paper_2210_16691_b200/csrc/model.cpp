@@ -390,12 +390,11 @@ extern "C" int alcop_choose_conv_schedule(const alcop_conv_desc* d, const alcop_
   g.b_layout = ALCOP_B_NK;
   double best = 1e300;
   bool found = false;
-  // CTA pairs run the 64-channel im2col path (C % 64 == 0, no halo layout).
-  // They need >= 8 chunks per tile to amortise the pair's per-tile handshake
-  // and epilogue, which the GEMM-view model does not see: on the ResNet-50
-  // layers with K = R*S*C >= 512 pairs measured 5-9 % faster, on the stride-2
-  // downsample with K = 256 1.24x slower (tools/conv_pair_probe.py)
-  const int max_cg = (d->C % 64 == 0 && !d->x_halo && g.K >= 512) ? 2 : 1;
+  // CTA pairs run the 64-channel im2col path (C % 64 == 0, no halo layout):
+  // with the pair's hand-off at CTA scope they measured faster at every K of
+  // the ResNet-50 layers, the K = 256 downsample included (818 -> 921 TFLOP/s;
+  // before that fix 1.24x slower there, tools/conv_pair_probe.py)
+  const int max_cg = (d->C % 64 == 0 && !d->x_halo) ? 2 : 1;
   for (int cg = 1; cg <= max_cg; ++cg)
   for (int tN : {64, 128, 192, 256})
     for (int st = 8; st >= 1; --st)

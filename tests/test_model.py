@@ -142,8 +142,8 @@ def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
     for all 23 ResNet-50 layers: the GEMM space for 1x1 stride-1 layers, the
     window kernels' spaces (stem; window and streamed filter, CTA pairs
     included), else the im2col
-    kernel's (tileK 64, equal stages, CTA pairs only for C % 64 == 0 and
-    K >= 512, within the 4-epilogue-warp shared memory)."""
+    kernel's (tileK 64, equal stages, CTA pairs only for C % 64 == 0,
+    within the 4-epilogue-warp shared memory)."""
     from paper_2210_16691_b200 import workloads as W
     import ctypes
     lib = alcop.load_library()
@@ -162,7 +162,7 @@ def test_choose_conv_schedule_is_valid_for_every_resnet_layer(alcop):
             assert s.tileN == L.K and 1 <= s.n_stage_inner <= 8 and s.tileM == 128 * s.cta_group, s
             assert s.cta_group == 1 or not L.stem, s  # the stem modes run one CTA per tile
             continue
-        assert s.cta_group == 1 or (L.Cs % 64 == 0 and L.gemm_k() >= 512), L.name  # pairs: 64-ch im2col, K >= 512
+        assert s.cta_group == 1 or (L.Cs % 64 == 0 and not L.halo), L.name  # pairs: the 64-channel im2col path
         g = W.conv_gemm_desc(alcop, L, 256)
         alcop.validate(g, s)
         assert lib.alcop_smem_bytes(ctypes.byref(g), ctypes.byref(s)) <= 232448
