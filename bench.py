@@ -593,7 +593,8 @@ def main_gpu(args, rank, world, local_rank):
     torch.cuda.empty_cache()
 
     # model pick vs a swept set (BASELINE: "analytical-model config vs exhaustive tuning"): every
-    # candidate (the pick among them) timed in two shuffled round-robin passes, best of the two
+    # candidate (the pick among them) timed in two shuffled round-robin passes, best of the two, then
+    # the shortlist re-timed (median of three rounds)
     if not args.quick:
         import random
         sweep = {}
@@ -628,8 +629,22 @@ def main_gpu(args, rank, world, local_rank):
                 for k, s in order:
                     times[k].append(time_graph(lambda i, s=s, it=it: hl.launch(it, sched=s),
                                                iters=6 if n <= 8192 else 2, warmup=1))
-            best_k = min(times, key=lambda k: min(times[k]))
-            best_ms, pick_ms = ranks.max(min(times[best_k])), ranks.max(min(times[pick_key]))
+            # the quick passes (2-6 launches per sample) only shortlist: the GPU's clock drifts with its
+            # power state, so the three fastest and the pick are re-timed in three round-robin rounds
+            # (longer samples, median) and compared on those
+            short = sorted(times, key=lambda k: min(times[k]))[:3]
+            if pick_key not in short:
+                short.append(pick_key)
+            sched_of = dict(cands)
+            final = {k: [] for k in short}
+            for _ in range(3):
+                for k in short:  # ~0.2 s per sample: the power-capped regime the headline step runs in
+                    reps = int(min(400, max(6, 0.2e3 / max(min(times[k]), 1e-3))))
+                    final[k].append(time_graph(lambda i, s=sched_of[k], it=it: hl.launch(it, sched=s),
+                                               iters=reps, warmup=2))
+            med = {k: statistics.median(v) for k, v in final.items()}
+            best_k = min(med, key=lambda k: med[k])
+            best_ms, pick_ms = ranks.max(med[best_k]), ranks.max(med[pick_key])
             sweep[str(n)] = {"candidates": len(cands),
                              "best_swept": {"tflops": round(square_flops(n) / (best_ms * 1e-3) / 1e12, 1),
                                             "tileN": best_k[0], "tileK": best_k[1], "cta_group": best_k[2],
@@ -637,7 +652,9 @@ def main_gpu(args, rank, world, local_rank):
                              "model_pick": {"tflops": round(square_flops(n) / (pick_ms * 1e-3) / 1e12, 1),
                                             "tileN": pick_key[0], "tileK": pick_key[1], "cta_group": pick_key[2],
                                             "n_stage": pick_key[3]},
-                             "model_pick_over_best_time": round(pick_ms / best_ms, 3)}
+                             "model_pick_over_best_time": round(pick_ms / best_ms, 3),
+                             "timing": "shortlist (3 fastest of two quick passes + the pick): median of 3 "
+                                       "round-robin rounds of ~0.2 s samples (sustained), CUDA graphs"}
         extra["c5_model_pick_vs_sweep"] = sweep
         torch.cuda.empty_cache()
 
