@@ -820,8 +820,9 @@ def bert_block(args, torch, alcop, lib, dev, rank, world, ranks, peaks, parity, 
     chain = {}
     for label, dep in (("row_block_dependencies", [0] + [1] * (len(gemms) - 1)), ("independent", None)):
         best = None
-        for tn, tk, st in ((192, 64, 5), (256, 64, 4), (128, 128, 3)):
-            cs_ = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st)
+        for tn, tk, st, cg in ((192, 64, 5, 1), (256, 64, 4, 1), (128, 128, 3, 1), (256, 64, 6, 2), (256, 128, 3, 2),
+                               (128, 64, 7, 2)):
+            cs_ = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg)
             ms = time_graph(lambda i: alcop.gemm_chain(csets[i % 4], cs_, dep=dep, workspace=cws), iters=40,
                             reps_per_graph=4)
             if best is None or ms < best[0]:

@@ -106,10 +106,12 @@ typedef struct {
  * The GEMMs run as ONE flattened (problem, tile, chunk) stream through the
  * same smem ring and TMEM accumulator ring, so nothing drains between them
  * (the holistic pipeline one level up: the last tile's epilogue of GEMM p
- * overlaps GEMM p+1's main loop).  dep[p] = 1: row block mb (128 rows) of
+ * overlaps GEMM p+1's main loop).  dep[p] = 1: row block mb (one tile row) of
  * A_p is read only after every tile of row block mb of C_{p-1} is stored
  * (requires M_p == M_{p-1}); dep[0] must be 0.  All GEMMs share the schedule
- * (cta_group 1, FUSED, equal A/B stages), dtypes and B layout; batch 1.
+ * (FUSED, equal A/B stages; cta_group 1, or 2 = CTA pairs with 256-row
+ * blocks and tileN % 128 == 0 for B[K,N], % 32 for B[N,K]), dtypes and B
+ * layout; batch 1.
  * workspace: device memory of alcop_gemm_chain_workspace_bytes() bytes
  * (row-block counters, zeroed on `stream` by the call). */
 #define ALCOP_CHAIN_MAX 4

@@ -410,9 +410,14 @@ int alcop_gemm_chain(const alcop_chain* ch, const alcop_schedule* s, void* works
   clear_error();
   if (ch->n < 1 || ch->n > ALCOP_CHAIN_MAX)
     return set_error(ALCOP_ERR_CONFIG, "BadWorkload", "chain length must be 1..ALCOP_CHAIN_MAX");
-  if (s->cta_group != 1 || s->mode != ALCOP_MODE_FUSED || s->n_stage_smem_A != s->n_stage_smem_B)
-    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the chain runs cta_group 1, FUSED, equal A/B stages");
+  if (s->mode != ALCOP_MODE_FUSED || s->n_stage_smem_A != s->n_stage_smem_B || s->stream_k)
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported", "the chain runs FUSED, equal A/B stages, whole tiles");
   const alcop_gemm_desc& w0 = ch->desc[0];
+  // CTA pairs: each CTA stages half of the tile's B columns — whole 64-column
+  // atoms for B[K,N], 16-row groups for B[N,K]
+  if (s->cta_group == 2 && (s->tileN % (w0.b_layout == ALCOP_B_KN ? 128 : 32) != 0))
+    return set_error(ALCOP_ERR_CONFIG, "Unsupported",
+                     "a chain on CTA pairs needs tileN % 128 == 0 (B[K,N]) or tileN % 32 == 0 (B[N,K])");
   for (int i = 0; i < ch->n; ++i) {
     const alcop_gemm_desc& w = ch->desc[i];
     if (!ch->A[i] || !ch->B[i] || !ch->C[i]) return set_error(ALCOP_ERR_CONFIG, "NullArgument", "NULL operand");

@@ -51,8 +51,9 @@ struct ChainProblem {
 
 struct ChainKParams {
   int32_t n, total_tiles, max_key, BN, sA, tacc, b_mn_major, stage_bufs, max_mb;
+  int32_t bn_cta;     // B columns (rows, K-major) each CTA stages: BN, or BN / 2 on a CTA pair
   uint32_t idesc, a_stage_bytes, b_stage_bytes, acc_stride, tmem_cols;
-  int32_t* counters;  // [n][max_mb] row-block completion counters (4 per stored tile)
+  int32_t* counters;  // [n][max_mb] row-block completion counters (4 per stored tile and CTA)
   ChainProblem prob[kMaxProblems];
 };
 
@@ -108,7 +109,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <typename OutT, int BK>
+// kPair: the chain on CTA pairs (cta_group::2, 256-row tiles): each CTA loads
+// its 128 rows of A and half of B's tile columns, both CTAs' copies complete
+// on the leader's full barrier, the leader issues M = 256 MMAs and multicasts
+// the releases, each CTA drains its own TMEM; the row-block counters count
+// 256-row blocks (4 epilogue warps x 2 CTAs per stored tile).
+template <typename OutT, int BK, bool kPair = false>
 __global__ void __launch_bounds__(kChainThreads, 1)
     alcop_chain_gemm_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ ChainKParams p) {
   using namespace ptx;
@@ -133,6 +139,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  constexpr int kRows = kPair ? 2 * kTileM : kTileM;  // output rows per tile
+  constexpr int kPubs = kPair ? 8 : 4;                 // counter increments per stored tile
   if (warp == 0 && elect_one()) {
     for (int i = 0; i < p.n; ++i) {
       prefetch_tmap(&maps.a[i]);
@@ -148,38 +158,48 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(smem_u32(&tfull[i]), 1);
-        mbar_init(smem_u32(&tempty[i]), 4);
+        mbar_init(smem_u32(&tempty[i]), kPair ? 8 : 4);  // 4 epilogue warps (x 2 CTAs)
       }
       fence_barrier_init();
     }
     __syncwarp();
-    tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
-    tmem_relinquish();
+    if constexpr (kPair) {
+      tmem_alloc_pair(smem_u32(tmem_slot), p.tmem_cols);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(smem_u32(tmem_slot), p.tmem_cols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive / complete_tx
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   grid_dependency_wait();
   grid_launch_dependents();
 
-  const int grid = gridDim.x;
-  const int my_tiles = (p.total_tiles - static_cast<int>(blockIdx.x) + grid - 1) / grid;
+  // work units: CTAs, or CTA pairs walking the pair tiles
+  const int grid = kPair ? static_cast<int>(gridDim.x) >> 1 : static_cast<int>(gridDim.x);
+  const int unit = kPair ? static_cast<int>(blockIdx.x) >> 1 : static_cast<int>(blockIdx.x);
+  const int my_tiles = (p.total_tiles - unit + grid - 1) / grid;
 
   if (warp == 0) {
     // ======================= producer (TMA), one flattened stream =======================
     uint32_t phase = 0;
     int slot = 0;
-    const uint32_t bytes = p.a_stage_bytes + p.b_stage_bytes;
+    const uint32_t bytes = (kPair ? 2u : 1u) * (p.a_stage_bytes + p.b_stage_bytes);  // (both CTAs' halves)
     for (int tl = 0; tl < my_tiles; ++tl) {
-      const ChainTile ct = chain_tile(p, static_cast<int>(blockIdx.x) + tl * grid);
+      const ChainTile ct = chain_tile(p, unit + tl * grid);
       const CUtensorMap* ta = &maps.a[ct.p];
       const CUtensorMap* tb = &maps.b[ct.p];
       if (p.prob[ct.p].dep) {
         // A row block mb of GEMM p is C row block mb of GEMM p-1: wait for its
         // num_n tiles (4 epilogue warps each), then order the TMA reads after
         const int32_t* cnt = p.counters + (ct.p - 1) * p.max_mb + ct.mb;
-        const int target = 4 * p.prob[ct.p - 1].num_n;
+        const int target = kPubs * p.prob[ct.p - 1].num_n;
         if (elect_one()) {
           long long t0 = 0;
           while (ld_acquire(cnt) < target) {
@@ -196,27 +216,33 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         phase ^= 1u << slot;
         const uint32_t fb = smem_u32(&full[slot]);
         if (elect_one()) {
-          mbar_arrive_expect_tx(fb, bytes);  // producer_commit
+          // a CTA pair: this CTA's 128 rows of A and its half of the tile's B
+          // columns, completing on the leader's barrier (armed by the leader)
+          auto ld = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+            if constexpr (kPair)
+              tma_load_3d_pair(dst, m, mapa_shared(fb, 0), c0, c1, 0);
+            else
+              tma_load_3d(dst, m, fb, c0, c1, 0);
+          };
+          if (leader) mbar_arrive_expect_tx(fb, bytes);  // producer_commit
+          const int row0 = ct.mb * kRows + static_cast<int>(rank) * kTileM;
+          const int n0 = ct.nb * p.BN + static_cast<int>(rank) * p.bn_cta;
 #pragma unroll
-          for (int a = 0; a < kKAtoms; ++a)
-            tma_load_3d(ringA + slot * p.a_stage_bytes + a * (kTileM * 128), ta, fb, c * BK + a * kBoxK,
-                        ct.mb * kTileM, 0);
+          for (int a = 0; a < kKAtoms; ++a) ld(ringA + slot * p.a_stage_bytes + a * (kTileM * 128), ta, c * BK + a * kBoxK, row0);
           const uint32_t dst = ringB + slot * p.b_stage_bytes;
           if (p.b_mn_major) {
-            for (int a = 0; a < (p.BN >> 6); ++a)
-              tma_load_3d(dst + a * (BK * 128), tb, fb, ct.nb * p.BN + a * 64, c * BK, 0);
+            for (int a = 0; a < (p.bn_cta >> 6); ++a) ld(dst + a * (BK * 128), tb, n0 + a * 64, c * BK);
           } else {
 #pragma unroll
-            for (int a = 0; a < kKAtoms; ++a)
-              tma_load_3d(dst + a * (p.BN * 128), tb, fb, c * BK + a * kBoxK, ct.nb * p.BN, 0);
+            for (int a = 0; a < kKAtoms; ++a) ld(dst + a * (p.bn_cta * 128), tb, c * BK + a * kBoxK, n0);
           }
         }
         __syncwarp();
         slot = (slot + 1 == p.sA) ? 0 : slot + 1;
       }
     }
-  } else if (warp == 1) {
-    // ======================= MMA issuer =======================
+  } else if (warp == 1 && leader) {
+    // ======================= MMA issuer (a CTA pair: the leader's, for both) =======================
     uint32_t phase = 0;
     int slot = 0;
     const uint64_t adesc0 = make_smem_desc(ringA, 16, kKSbo, kKLayout);
@@ -229,11 +255,17 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     } else {
       bdesc0 = make_smem_desc(ringB, 16, kKSbo, kKLayout);
       b_small = 2;
-      b_big = static_cast<uint32_t>(p.BN) * 128 / 16;
+      b_big = static_cast<uint32_t>(p.bn_cta) * 128 / 16;
     }
     const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (kPair)
+        umma_commit_pair_multicast(smem_u32(bar), 0x3);  // both CTAs' barriers
+      else
+        umma_commit(smem_u32(bar));
+    };
     for (int tl = 0; tl < my_tiles; ++tl) {
-      const int E = chain_tile(p, static_cast<int>(blockIdx.x) + tl * grid).E;
+      const int E = chain_tile(p, unit + tl * grid).E;
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tempty[acc]), ((tl / p.tacc) & 1) ^ 1);
       tc_fence_after();
@@ -249,17 +281,20 @@ __global__ void __launch_bounds__(kChainThreads, 1)
           for (int u = 0; u < kSteps; ++u) {
             const uint32_t a_off = BK >= 64 ? (u >> 2) * (kTileM * 128 / 16) + (u & 3) * 2 : u * 2;
             const uint32_t b_off = (u >> 2) * b_big + (u & 3) * b_small;
-            umma_f16_ss(d_tmem, ad + a_off, bd + b_off, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
+            if constexpr (kPair)
+              umma_f16_ss_pair(d_tmem, ad + a_off, bd + b_off, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
+            else
+              umma_f16_ss(d_tmem, ad + a_off, bd + b_off, p.idesc, (v > 0 || u > 0) ? 1u : 0u);
           }
-          umma_commit(smem_u32(&empty[slot]));  // consumer_release
+          commit(&empty[slot]);  // consumer_release
         }
         __syncwarp();
         slot = (slot + 1 == p.sA) ? 0 : slot + 1;
       }
-      if (elect_one()) umma_commit(smem_u32(&tfull[acc]));  // accumulator ready
+      if (elect_one()) commit(&tfull[acc]);  // accumulator ready
       __syncwarp();
     }
-  } else {
+  } else if (warp >= 2) {
     // ======================= epilogue (warps 2-5) =======================
     const int q = warp & 3;
     const uint32_t stage_base = staging + (warp - 2) * p.stage_bufs * 4096;
@@ -267,7 +302,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const int nchunks = p.BN / kChunkCols;
     int buf = 0;
     for (int tl = 0; tl < my_tiles; ++tl) {
-      const ChainTile ct = chain_tile(p, static_cast<int>(blockIdx.x) + tl * grid);
+      const ChainTile ct = chain_tile(p, unit + tl * grid);
       const CUtensorMap* tcm = &maps.c[ct.p];
       const int acc = tl % p.tacc;
       mbar_wait(smem_u32(&tfull[acc]), (tl / p.tacc) & 1);
@@ -292,7 +327,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (c == nchunks - 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+          if (lane == 0) {
+            if constexpr (kPair)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's barrier
+            else
+              mbar_arrive(smem_u32(&tempty[acc]));
+          }
         }
         const uint32_t sbuf = stage_base + buf * 4096;
         if (lane == 0) {
@@ -309,7 +349,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(tcm, sbuf, ct.nb * p.BN + c * kChunkCols, ct.mb * kTileM + q * 32, 0);
+          tma_store_3d(tcm, sbuf, ct.nb * p.BN + c * kChunkCols,
+                       ct.mb * kRows + static_cast<int>(rank) * kTileM + q * 32, 0);
           bulk_commit_group();
         }
         buf ^= p.stage_bufs - 1;
@@ -331,16 +372,23 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // no CTA leaves while its peer may still signal it or read its shared memory
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+    if constexpr (kPair)
+      tmem_dealloc_pair(tmem_base, p.tmem_cols);
+    else
+      tmem_dealloc(tmem_base, p.tmem_cols);
   }
 }
 
 template <typename OutT, int BK>
-int launch_chain_typed(const ChainMaps& maps, const ChainKParams& kp, int grid, int smem, cudaStream_t st) {
-  auto kern = alcop_chain_gemm_kernel<OutT, BK>;
+int launch_chain_typed(const ChainMaps& maps, const ChainKParams& kp, bool pair, int grid, int smem,
+                       cudaStream_t st) {
+  auto kern = pair ? alcop_chain_gemm_kernel<OutT, BK, true> : alcop_chain_gemm_kernel<OutT, BK, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   cudaLaunchConfig_t cfg{};
@@ -348,11 +396,15 @@ int launch_chain_typed(const ChainMaps& maps, const ChainKParams& kp, int grid, 
   cfg.blockDim = dim3(kChainThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // CTA pairs (cta_group 2)
+  attr[1].val.clusterDim.x = pair ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pair ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, kern, maps, kp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
@@ -381,14 +433,17 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
   const cuuint32_t es[3] = {1, 1, 1};
   ChainMaps maps;
   ChainKParams kp{};
+  const bool pair = s.cta_group == 2;
+  const int rows = kTileM * (pair ? 2 : 1);  // output rows per tile
   kp.n = ch.n;
   kp.BN = BN;
+  kp.bn_cta = pair ? BN / 2 : BN;
   kp.sA = s.n_stage_smem_A;
   kp.tacc = s.n_stage_inner;
   kp.b_mn_major = w0.b_layout == ALCOP_B_KN ? 1 : 0;
-  kp.idesc = ptx::make_idesc_f16(w0.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, kTileM, BN);
+  kp.idesc = ptx::make_idesc_f16(w0.in_dtype == ALCOP_BF16 ? 1u : 0u, kp.b_mn_major, static_cast<uint32_t>(rows), BN);
   kp.a_stage_bytes = static_cast<uint32_t>(kTileM * BK * 2);
-  kp.b_stage_bytes = static_cast<uint32_t>(BN * BK * 2);
+  kp.b_stage_bytes = static_cast<uint32_t>(kp.bn_cta * BK * 2);
   kp.acc_stride = static_cast<uint32_t>(round_up_pow2_cols(BN));
   kp.tmem_cols = static_cast<uint32_t>(round_up_pow2_cols(kp.acc_stride * kp.tacc));
   kp.max_mb = static_cast<int32_t>(chain_max_row_blocks(&ch));
@@ -415,7 +470,7 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
     } else {
       const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w.K), static_cast<cuuint64_t>(w.N), 1};
       const cuuint64_t str[2] = {static_cast<cuuint64_t>(ldb * 2), static_cast<cuuint64_t>(ldb * 2 * w.N)};
-      const cuuint32_t box[3] = {kbox, static_cast<cuuint32_t>(BN), 1};
+      const cuuint32_t box[3] = {kbox, static_cast<cuuint32_t>(kp.bn_cta), 1};
       rc = encode_tiled_map(&maps.b[i], dt, ch.B[i], 3, dims, str, box, es, kswz, "chain B");
     }
     if (rc) return rc;
@@ -427,7 +482,7 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
     }
     if (rc) return rc;
     ChainProblem& pr = kp.prob[i];
-    pr.num_m = static_cast<int32_t>((w.M + kTileM - 1) / kTileM);
+    pr.num_m = static_cast<int32_t>((w.M + rows - 1) / rows);
     pr.num_n = static_cast<int32_t>((w.N + BN - 1) / BN);
     pr.E = static_cast<int32_t>((w.K + BK - 1) / BK);
     pr.tiles = pr.num_m * pr.num_n;
@@ -435,7 +490,8 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
     tiles += pr.tiles;
   }
   kp.total_tiles = tiles;
-  int grid = s.num_ctas > 0 ? s.num_ctas : device_sm_count();
+  // work units: CTAs, or CTA pairs
+  int grid = (s.num_ctas > 0 ? s.num_ctas : device_sm_count()) / (pair ? 2 : 1);
   if (grid <= 0) return set_error(ALCOP_ERR_CUDA, "CudaError", "no CUDA device");
   if (grid > tiles) grid = tiles;
   for (int i = 0, begin = 0; i < ch.n; ++i) {  // first global tile of each problem (chain_tile)
@@ -447,18 +503,19 @@ int launch_chain(const alcop_chain& ch, const alcop_schedule& s, void* workspace
   const int smem = static_cast<int>(gemm_smem_bytes_epi(wsm, s, 4));
   kp.stage_bufs = gemm_staging_bufs_epi(wsm, s, 4);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int ctas = grid * (pair ? 2 : 1);
   cudaError_t e = cudaMemsetAsync(workspace, 0, sizeof(int32_t) * kp.max_mb * ch.n, st);
   if (e != cudaSuccess) return set_error(ALCOP_ERR_CUDA, "CudaError", cudaGetErrorString(e));
   switch (w0.out_dtype * 4 + (BK == 32 ? 0 : BK == 64 ? 1 : 2)) {
-    case ALCOP_F32 * 4 + 0: return launch_chain_typed<float, 32>(maps, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 1: return launch_chain_typed<float, 64>(maps, kp, grid, smem, st);
-    case ALCOP_F32 * 4 + 2: return launch_chain_typed<float, 128>(maps, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 0: return launch_chain_typed<__nv_bfloat16, 32>(maps, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 1: return launch_chain_typed<__nv_bfloat16, 64>(maps, kp, grid, smem, st);
-    case ALCOP_BF16 * 4 + 2: return launch_chain_typed<__nv_bfloat16, 128>(maps, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 0: return launch_chain_typed<__half, 32>(maps, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 1: return launch_chain_typed<__half, 64>(maps, kp, grid, smem, st);
-    case ALCOP_F16 * 4 + 2: return launch_chain_typed<__half, 128>(maps, kp, grid, smem, st);
+    case ALCOP_F32 * 4 + 0: return launch_chain_typed<float, 32>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_F32 * 4 + 1: return launch_chain_typed<float, 64>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_F32 * 4 + 2: return launch_chain_typed<float, 128>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_BF16 * 4 + 0: return launch_chain_typed<__nv_bfloat16, 32>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_BF16 * 4 + 1: return launch_chain_typed<__nv_bfloat16, 64>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_BF16 * 4 + 2: return launch_chain_typed<__nv_bfloat16, 128>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_F16 * 4 + 0: return launch_chain_typed<__half, 32>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_F16 * 4 + 1: return launch_chain_typed<__half, 64>(maps, kp, pair, ctas, smem, st);
+    case ALCOP_F16 * 4 + 2: return launch_chain_typed<__half, 128>(maps, kp, pair, ctas, smem, st);
   }
   return set_error(ALCOP_ERR_CONFIG, "BadDtype", "unsupported output dtype");
 }

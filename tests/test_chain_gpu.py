@@ -19,8 +19,9 @@ def _bf16_round(x):
     return torch.from_numpy(np.asarray(x, dtype=np.float64)).to(torch.float32).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("tileN,tileK,st", [(192, 64, 5), (256, 64, 4), (128, 128, 3), (64, 32, 6)])
-def test_chain_independent_exact(alcop, tileN, tileK, st):
+@pytest.mark.parametrize("tileN,tileK,st,cg", [(192, 64, 5, 1), (256, 64, 4, 1), (128, 128, 3, 1), (64, 32, 6, 1),
+                                               (256, 64, 6, 2), (128, 64, 7, 2), (256, 128, 3, 2)])
+def test_chain_independent_exact(alcop, tileN, tileK, st, cg):
     shapes = [(512, 384, 256), (384, 192, 640), (640, 576, 128), (256, 128, 64)]
     gemms, want = [], []
     for i, (M, N, K) in enumerate(shapes):
@@ -28,7 +29,7 @@ def test_chain_independent_exact(alcop, tileN, tileK, st):
         want.append(torch.from_numpy((a.astype(np.int64) @ b.astype(np.int64)).astype(np.float64)).float())
         gemms.append((torch.from_numpy(a).to(torch.bfloat16).cuda(), torch.from_numpy(b).to(torch.bfloat16).cuda(),
                       torch.zeros((M, N), dtype=torch.float32, device="cuda")))
-    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st)
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, cta_group=cg)
     alcop.gemm_chain(gemms, s)
     torch.cuda.synchronize()
     for (A, B, C), w in zip(gemms, want):
@@ -37,7 +38,8 @@ def test_chain_independent_exact(alcop, tileN, tileK, st):
 
 @pytest.mark.parametrize("M", [4096, 1000])
 @pytest.mark.parametrize("layout", [0, 1], ids=["KN", "NK"])
-def test_chain_dependent_exact(alcop, M, layout):
+@pytest.mark.parametrize("cg", [1, 2], ids=["cta", "pair"])
+def test_chain_dependent_exact(alcop, M, layout, cg):
     """X @ W0 -> C0 (bf16) -> C0 @ W1 -> C1 -> C1 @ W2 -> C2: each A_p is the
     previous C buffer.  Integer data: every fp32 sum is exact; the bf16
     output rounding is reproduced on the host."""
@@ -52,7 +54,8 @@ def test_chain_dependent_exact(alcop, M, layout):
         t = torch.from_numpy(w).to(torch.bfloat16)
         Ws.append((t if layout == 0 else t.t().contiguous()).cuda())
     gemms = [(X, Ws[0], Cs[0]), (Cs[0], Ws[1], Cs[1]), (Cs[1], Ws[2], Cs[2])]
-    s = alcop.make_schedule(tileN=64, tileK=64, n_stage=4)
+    # (CTA pairs: 256-row blocks, half of the 128 tile columns per CTA; M = 1000: a ragged last pair tile)
+    s = alcop.make_schedule(tileN=64 * cg, tileK=64, n_stage=4, cta_group=cg)
     for _ in range(3):  # repeated launches: stale counters or early reads would show
         for c in Cs:
             c.zero_()
@@ -71,3 +74,13 @@ def test_chain_rejects_bad_dependency(alcop):
     s = alcop.make_schedule(tileN=64, tileK=64, n_stage=2)
     with pytest.raises(alcop.AlcopError):
         alcop.gemm_chain([(a, b, a.new_zeros((256, 64))), (c[:, :64].contiguous(), b, c)], s, dep=[0, 1])
+
+
+def test_chain_pair_rejects_split_atoms(alcop):
+    """A chain on CTA pairs with B[K,N] stages whole 64-column atoms per CTA:
+    tileN 192 (96 columns per CTA) is named, not run."""
+    a = torch.zeros((256, 64), dtype=torch.bfloat16, device="cuda")
+    b = torch.zeros((64, 192), dtype=torch.bfloat16, device="cuda")
+    s = alcop.make_schedule(tileN=192, tileK=64, n_stage=4, cta_group=2)
+    with pytest.raises(alcop.AlcopError, match="Unsupported"):
+        alcop.gemm_chain([(a, b, a.new_zeros((256, 192)))], s)
