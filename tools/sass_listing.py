@@ -34,7 +34,8 @@ PRODUCTION = [
      "implicit-GEMM conv, 8-channel im2col boxes (small C)"),
     ("alcop_pipelined_gemm_kernel<__nv_bfloat16, 64, true, false, 3, false, 4>",
      "implicit-GEMM conv, stem (ResNet-50 conv1, halo-padded NHWC8)"),
-    ("alcop_chain_gemm_kernel<__nv_bfloat16, 64>", "several GEMMs in one persistent launch (alcop_gemm_chain)"),
+    ("alcop_chain_gemm_kernel<__nv_bfloat16, 64, false>", "several GEMMs in one persistent launch (alcop_gemm_chain)"),
+    ("alcop_chain_gemm_kernel<__nv_bfloat16, 64, true>", "alcop_gemm_chain on CTA pairs (the BERT layer as one launch)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 3, 7, 2, false>",
      "resident-filter conv, pixel pairs, four output rows per tile: the ResNet-50 stem (C = 4, 7x7/2)"),
     ("alcop_stem_conv_kernel<__nv_bfloat16, 0, 7, 2, false>",
