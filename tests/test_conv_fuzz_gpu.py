@@ -2,8 +2,9 @@
 alcop_conv2d routes to (stem pixel pairs, window with a resident or streamed
 filter on one CTA or a CTA pair, 1x1 on the GEMM kernels, im2col on one CTA or
 a pair, the small-channel im2col) x the chooser's pick and random schedules of
-that class, bit-exact against the oracle's direct convolution on the
-reference's integer inputs.  A random schedule may be rejected — then only
+that class, with bf16 or fp16 inputs and fp32 / bf16 / fp16 outputs,
+bit-exact against the oracle's direct convolution on the reference's integer
+inputs (16-bit outputs compared as RNE bit patterns).  A random schedule may be rejected — then only
 with a configuration error naming a rule tag, never a crash or wrong bits."""
 import numpy as np
 import pytest
@@ -75,26 +76,29 @@ def test_conv_fuzz(alcop, seed):
     N, H, W, C, K, R, S, st, pd = _shape(rng, cls)
     if (H + 2 * pd[0] - R) < 0 or (W + 2 * pd[1] - S) < 0:
         pytest.skip("empty output")
+    in_dt = ("bf16", "f16")[int(rng.integers(0, 2))]
+    out_dt = ("f32", "bf16", "f16")[int(rng.integers(0, 3))]
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}
     x = random_tensor(N * H * W * C, 500 + seed).reshape(N, H, W, C)
     w = random_tensor(K * R * S * C, 700 + seed).reshape(K, R, S, C)
-    ref = coracle.conv2d(coracle.to_dtype(x.astype(np.float32), "bf16"), coracle.to_dtype(w.astype(np.float32), "bf16"),
-                         st, pd, "bf16", "f32")
-    X = torch.from_numpy(x).to(torch.bfloat16).cuda()
-    Wt = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    ref = coracle.conv2d(coracle.to_dtype(x.astype(np.float32), in_dt), coracle.to_dtype(w.astype(np.float32), in_dt),
+                         st, pd, in_dt, out_dt)
+    X = torch.from_numpy(x).to(tdt[in_dt]).cuda()
+    Wt = torch.from_numpy(w).to(tdt[in_dt]).cuda()
     scheds = [None] + _random_schedules(alcop, rng, cls, K, S)
     ran = 0
     for s in scheds:
         try:
-            Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=torch.float32)
+            Y = alcop.conv2d(X, Wt, st, pd, sched=s, out_dtype=tdt[out_dt])
         except alcop.AlcopError as e:
             assert s is not None and any(t in str(e) for t in TAGS), (cls, (N, H, W, C, K, R, S, st, pd), s, e)
             continue
         torch.cuda.synchronize()
-        got = Y.cpu().numpy()
+        got = Y.cpu().numpy() if out_dt == "f32" else Y.cpu().view(torch.int16).numpy().view(np.uint16)
         if not np.array_equal(got, ref):
             bad = np.argwhere(got != ref)
-            raise AssertionError("%s %s %s: %d mismatches, first at %s: got %s want %s" % (
-                cls, (N, H, W, C, K, R, S, st, pd), s, len(bad), bad[0].tolist(), got[tuple(bad[0])],
+            raise AssertionError("%s %s %s->%s %s: %d mismatches, first at %s: got %s want %s" % (
+                cls, (N, H, W, C, K, R, S, st, pd), in_dt, out_dt, s, len(bad), bad[0].tolist(), got[tuple(bad[0])],
                 ref[tuple(bad[0])]))
         ran += 1
     assert ran >= 1  # the chooser's pick always runs
