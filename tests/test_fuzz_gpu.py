@@ -36,7 +36,10 @@ def _case(i):
 
 @pytest.mark.parametrize("i", range(CASES))
 def test_fuzz_exact(alcop, i):
-    c = _case(i)
+    _run_case(alcop, _case(i), i)
+
+
+def _run_case(alcop, c, i):
     in_dt = torch.float16 if c["out"] == "f16" else torch.bfloat16
     out_dt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[c["out"]]
     s = alcop.make_schedule(tileN=c["tileN"], tileK=c["tileK"], n_stage=c["st"], n_stage_inner=c["inner"],
@@ -64,3 +67,21 @@ def test_fuzz_exact(alcop, i):
     if not torch.equal(got, ref):
         bad = int((got.float() != ref.float()).sum())
         raise AssertionError("case %s: %d mismatches" % (c, bad))
+
+
+def _pair_case(i):
+    """CTA-pair schedules only, the 256 x 512 tile included (one 512-column
+    TMEM accumulator: inner 1), larger ragged shapes."""
+    r = random.Random(5000 + i)
+    tileN = r.choice([128, 192, 256, 512, 512])
+    tileK = r.choice([32, 64, 128])
+    st = r.randint(1, 8)
+    inner = 1 if (tileN == 512 or st == 1) else r.choice([1, 2])
+    return dict(cg=2, tileN=tileN, tileK=tileK, st=st, inner=inner, mode=r.choice([0, 1]), layout=r.choice([0, 1]),
+                out=r.choice(["f32", "bf16", "f16"]), batch=r.choice([1, 1, 2]), M=r.randint(1, 1300),
+                N=r.randint(1, 1100) // 8 * 8 + 8, K=r.randint(1, 900) // 8 * 8 + 8)
+
+
+@pytest.mark.parametrize("i", range(40))
+def test_fuzz_pairs_exact(alcop, i):
+    _run_case(alcop, _pair_case(i), 100 + i)
