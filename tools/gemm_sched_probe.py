@@ -1,6 +1,6 @@
 """Time one GEMM shape under a list of schedules (measurement tool).
 
-python tools/gemm_sched_probe.py M N K tn,tk,stages,cta_group[,inner[,num_ctas]] ...
+python tools/gemm_sched_probe.py M N K tn,tk,stages,cta_group[,inner[,num_ctas[,stream_k]]] ...
 
 Rotating inputs (> 2x L2), CUDA graphs, three round-robin rounds, median;
 prints TFLOP/s per schedule and the model's / the tuner's pick for context."""
@@ -22,6 +22,9 @@ for spec in sys.argv[4:]:
     s = alcop.make_schedule(tileN=tn, tileK=tk, n_stage=st, cta_group=cg, n_stage_inner=v[4] if len(v) > 4 else 2)
     if len(v) > 5:
         s.num_ctas = v[5]
+    if len(v) > 6 and v[6]:
+        s.stream_k = 1
+        alcop.set_stream_k_workspace(256 << 20)  # caller-owned stream-K workspace
     scheds[spec] = s
 scheds["model_pick"] = alcop.choose_schedule(alcop.gemm_desc(M, N, K))
 rot = Rotating(lambda i: ((torch.rand(M, K, device="cuda") - 0.5).to(torch.bfloat16),
