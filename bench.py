@@ -580,6 +580,12 @@ def main_gpu(args, rank, world, local_rank):
         except Exception:
             traffic = None
     step_ms = ms_total / args.steps
+    # the model predicts the sustained (power-capped) regime the step runs in; a square timed alone in a
+    # short graph runs between burst and sustained, so its model_err above is not the model's own bar
+    pred_step = sum(per_sq[k]["model_pred_ms"] for k in per_sq)
+    extra["model_step"] = {"pred_ms": round(pred_step, 4), "measured_ms": round(step_ms, 4),
+                           "err": round((pred_step - step_ms) / step_ms, 3),
+                           "what": "alcop_predict (sustained regime) summed over the step's squares vs the timed step"}
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
                 "kernel": "%s (square %d: %dx%dx%d per GPU, %s)"
