@@ -84,3 +84,45 @@ def test_chain_pair_rejects_split_atoms(alcop):
     s = alcop.make_schedule(tileN=192, tileK=64, n_stage=4, cta_group=2)
     with pytest.raises(alcop.AlcopError, match="Unsupported"):
         alcop.gemm_chain([(a, b, a.new_zeros((256, 192)))], s)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_chain_fuzz(alcop, seed):
+    """Seeded chains: 2-4 GEMMs, random ragged M (shared when dependent) / N / K, a real data chain (A_p IS
+    C_{p-1}) where dep[p] = 1, one CTA or a CTA pair per tile, both B layouts; bit-exact against the
+    host chain with the same bf16 roundings."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(2, 5))
+    cg = int(rng.integers(1, 3))
+    layout = int(rng.integers(0, 2))
+    tileN = int(rng.choice([128, 256])) if cg == 2 else int(rng.choice([64, 128, 192, 256]))
+    tileK = int(rng.choice([32, 64, 128]))
+    st = int(rng.integers(2, 6))
+    M = int(rng.integers(1, 1300))
+    dep = [0] + [int(rng.integers(0, 2)) for _ in range(n - 1)]
+    dims = [int(rng.integers(1, 40)) * 8 for _ in range(n + 1)]  # K_0, N_0 = K_1 (when chained), ...
+    gemms, refs = [], []
+    prev_c, prev_ref = None, None
+    for p in range(n):
+        K, N = dims[p], dims[p + 1]
+        if dep[p]:
+            A, a = prev_c, prev_ref  # the previous C buffer is this A (K = N_{p-1})
+        else:
+            a = rng.integers(-2, 3, size=(M, K)).astype(np.float64)
+            A = torch.from_numpy(a).to(torch.bfloat16).cuda()
+        w = rng.integers(-2, 3, size=(K, N)).astype(np.float64)
+        Wt = torch.from_numpy(w).to(torch.bfloat16)
+        C = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+        ref = _bf16_round(a @ w).double().numpy()
+        gemms.append((A, (Wt if layout == 0 else Wt.t().contiguous()).cuda(), C))
+        refs.append(ref)
+        prev_c, prev_ref = C, ref
+    s = alcop.make_schedule(tileN=tileN, tileK=tileK, n_stage=st, cta_group=cg)
+    try:
+        alcop.gemm_chain(gemms, s, dep=dep, b_layout=alcop.B_KN if layout == 0 else alcop.B_NK)
+    except alcop.AlcopError as e:
+        assert any(t in str(e) for t in ("SmemCapacity", "BadTile", "Unsupported", "BadStages")), (s, e)
+        pytest.skip("schedule invalid for this chain: %s" % e)
+    torch.cuda.synchronize()
+    for p, ((_, _, C), ref) in enumerate(zip(gemms, refs)):
+        assert torch.equal(C.cpu(), _bf16_round(ref)), "chain %s dep %s, GEMM %d, %s" % (dims, dep, p, s)
