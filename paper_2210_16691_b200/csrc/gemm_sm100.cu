@@ -451,11 +451,20 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
       };
       // joint ring: both buffers' copies of a chunk under one barrier pair
       // kRole: 0 = commit + A, 1 = B, 2 = both (single producer)
+#ifdef GEMM_TRACE
+      // measurement build only (-DGEMM_TRACE): CTA 0's producer, clock64 after each
+      // acquire and after each chunk's TMA issue
+      unsigned long long ptr_[64];
+      int ptn_ = 0;
+#endif
       auto load_joint = [&](int tl, int chunk, auto role) {
         constexpr int kRole = decltype(role)::value;
         const uint32_t slot = ra.slot;
         const uint32_t par = ((ra.phase >> slot) & 1u) ^ 1u;
         mbar_wait(smem_u32(&emptyA[slot]), par);
+#ifdef GEMM_TRACE
+        if (blockIdx.x == 0 && warp == 0 && ptn_ < 64) ptr_[ptn_++] = clock64();
+#endif
         ra.phase ^= 1u << slot;
         if (lane == 0) chunkstamp<kDebug>(p, 0, ra.count);
         ++ra.count;
@@ -467,6 +476,9 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
         } if constexpr (kRole != 0) issue_b(slot, fb, chunk);
               log_event<kDebug>(p, 0, nev, 0, 0, tl, slot, chunk, par, ra.count, ra.count, -1, -1);
               log_event<kDebug>(p, 0, nev, 0, 1, tl, slot, chunk, par, ra.count, ra.count, -1, -1));
+#ifdef GEMM_TRACE
+        if (blockIdx.x == 0 && warp == 0 && ptn_ < 64) ptr_[ptn_++] = clock64() | (1ull << 62);
+#endif
         ra.advance(p.sA);
       };
 
@@ -525,6 +537,10 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
         }
       }
       if (kDebug && ra.count == 1) stamp<kDebug>(p, 2);
+#ifdef GEMM_TRACE
+      if (blockIdx.x == 0 && warp == 0 && lane == 0)
+        for (int i = 0; i < ptn_; ++i) printf("P %d %llu\n", i, ptr_[i]);
+#endif
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -551,9 +567,16 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
       const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
       const uint32_t idesc = p.idesc;
       // consumer_wait of one buffer
+#ifdef GEMM_TRACE
+      unsigned long long ctr_[64];
+      int ctn_ = 0;
+#endif
       auto cwait = [&](RingCursor& r, uint64_t* full, int buf, int tl, int chunk) -> uint32_t {
         const uint32_t slot = r.slot, par = (r.phase >> slot) & 1u;
         mbar_wait(smem_u32(&full[slot]), par);
+#ifdef GEMM_TRACE
+        if (blockIdx.x == 0 && ctn_ < 64) ctr_[ctn_++] = clock64();
+#endif
         r.phase ^= 1u << slot;
         ++r.count;
         if constexpr (kDebug) ISSUE(log_event<kDebug>(p, 1, nev, 1, buf, tl, slot, chunk, par, -1, -1, r.count, r.released));
@@ -636,6 +659,10 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
           }
         }
       }
+#ifdef GEMM_TRACE
+      if (blockIdx.x == 0 && lane == 0)
+        for (int i = 0; i < ctn_; ++i) printf("C %d %llu\n", i, ctr_[i]);
+#endif
     }
     __syncwarp();
   } else if (kPreOp && warp >= 6) {
