@@ -65,7 +65,7 @@ struct GemmKParams {
   int32_t conv_stem5;                      // stem A map is the 5-D strided view (stored H % stride_h == 0)
   int32_t conv_sh, conv_sw, conv_ph, conv_pw;
   // atom-stacked view of A: one 4-D TMA box brings the BK/64 K atoms of a
-  // chunk instead of one instruction per atom (BK = 128 only; b_view unused)
+  // chunk instead of one instruction per atom (A: BK = 128; B: B[K,N] on one CTA, BN >= 128)
   int32_t a_view, b_view;
   // CTA pair, B[K,N] with BN/2 % 64 != 0 (BN 192: halves of 96 columns): load
   // each half as two 128B-swizzled 64-column atoms (over-fetching 32 columns
@@ -421,9 +421,13 @@ __global__ void __launch_bounds__(kPreOp ? kThreadsPreOp
         if (kConv == 3) {
           tma_load_3d(dst, &tmB, fb, 0, chunk, tc.nb * p.BN);  // filter row `chunk`: S*C taps, zero-filled to 64
         } else if (p.b_mn_major) {
-          // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}
-          for (int a = 0; a < (p.BN >> 6); ++a)
-            tma_load_3d(dst + a * (BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * BK, tc.b);
+          // B[K,N] row-major: BN/64 atoms of (BK rows x 128 B), box {64 N, BK K}; with the atom-stacked
+          // view {64, K, N/64} one box of BN/64 atoms
+          if (p.b_view)
+            tma_load_4d(dst, &tmB, fb, 0, chunk * BK, tc.nb * (p.BN >> 6), tc.b);
+          else
+            for (int a = 0; a < (p.BN >> 6); ++a)
+              tma_load_3d(dst + a * (BK * 128), &tmB, fb, tc.nb * p.BN + a * 64, chunk * BK, tc.b);
         } else {
           // B[N,K] row-major: K-major like A with BN rows
 #pragma unroll
@@ -1566,9 +1570,10 @@ int launch_gemm(const alcop_gemm_desc& w, const alcop_schedule& s, const void* A
   const bool b_pad = pair_b_pad(w, s);
   const int b_atom = (w.b_layout == ALCOP_B_KN && ((BN / cg) & 63) != 0 && !b_pad) ? 32 : 64;  // pair BN 192: SW64 halves
   const bool a_view = views_on && BK > 64 && w.K % 64 == 0 && w.pre_op == 0;
-  // B keeps one box per 64-column atom: a runtime view branch in the
-  // producer's B issue measured 4 % slower on the conv/GEMM main loop
-  const bool b_view = false;
+  // B[K,N] on one CTA: the atom-stacked view loads a chunk's BN/64 atoms in one box (the single producer
+  // issues 2 TMA instructions per chunk instead of 1 + BN/64)
+  const bool b_view = views_on && cg == 1 && w.b_layout == ALCOP_B_KN && w.pre_op == 0 && BN % 64 == 0 &&
+                      BN >= 128 && w.N % 64 == 0 && BK >= 64;
   int rc;
   if (a_view) {
     const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(w.M), static_cast<cuuint64_t>(w.K / 64),
